@@ -927,7 +927,9 @@ int or_align(const double* IA, const double* WA, const double* IB, const double*
         break;
       }
       const WSys s = build_system(jets, hd, n);
-      if (rank_deficient(s.H, out->spectrum)) {
+      double spectrum[6];
+      if (rank_deficient(s.H, spectrum)) {
+        memcpy(out->spectrum, spectrum, sizeof(spectrum));
         status = RGBID_E_DEGENERATE;
         break;
       }

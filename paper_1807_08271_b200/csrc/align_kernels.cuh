@@ -1,0 +1,112 @@
+// Device data layout + kernel declarations of the B200 alignment path.
+//
+// One "slot" = one independent alignment of a batch (config 5) or the single
+// alignment of rgbid_align (batch of 1).  Every kernel takes the slot array and
+// a per-level LevelInfo; grid.y (or grid.x for per-slot kernels) indexes slots.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "hd_math.cuh"
+
+namespace rgbid_b200 {
+
+constexpr int kMaxLevels = 6;       // GPU supports levels <= 6 (80x60 at level 3 for VGA)
+constexpr int kMaxSample = 19200;   // src/alignment.cpp:47
+constexpr int kTPB = 256;           // warp/residual/normal-equation kernels
+constexpr int kTdistThreads = 1024; // Student-t kernel
+constexpr int kNPart = 28;          // 21 (lower H) + 6 (b) + 1 (cost)
+constexpr int kTraceMax = 64;
+
+// K1 tiling of level l: tile = (level row, segment of tx level pixels).
+// Full-res pixels per tile = tx * 4^l <= 2048 (smem staging of the warp).
+__host__ __device__ inline int k1_tx(int l) {
+  const int a = 256 >> l, b = 2048 >> (2 * l);
+  const int m = a < b ? a : b;
+  return m < 1 ? 1 : m;
+}
+
+struct LevelInfo {
+  int level;
+  int w, h;          // level image size (w0 >> l, h0 >> l)
+  int tx, nseg;      // K1 tiling
+  int ntiles;        // K1 tiles = h * nseg
+  int ntiles3;       // K3 tiles of kTPB consecutive pixels
+  double fx, fy, cx, cy;
+  double Kinv[9];    // level K^-1 (host m3_inv, bit-identical to the oracle)
+};
+
+struct SlotIO {
+  const double* IA[kMaxLevels];  // A pyramid (level 0 = frame A)
+  const double* WA[kMaxLevels];
+  const double* IB;              // frame B, level 0
+  const double* WB;
+  double* fIA;                   // bilateral-filtered A (covariance pass)
+  double* fWA;
+  double* ib;                    // warped B at the current level (level-size maps)
+  double* wb;
+  double* resI;                  // residuals compacted per K1 tile (row-major ranks)
+  double* resW;
+  int* cntI;                     // per K1 tile counts
+  int* cntW;
+  double* part;                  // K3 partial sums [ntiles3][kNPart]
+};
+
+struct SlotState {
+  double R[9], t[3];   // current T_AB
+  WarpMats wm;         // warp matrices of the current T_AB (full resolution)
+  int status;          // rgbid_status
+  int done_level;      // level whose loop broke on ||xi|| < eps (-1 = none)
+  int iters[kMaxLevels];
+  double cost[kMaxLevels];
+  rgbid_tdist tI, tW;        // current iteration, as estimated (tI.nu not yet maxed)
+  rgbid_tdist finI, finW;    // last level-0 iteration (tI.nu maxed), AlignmentResult::tdist_*
+  long long nI, nW;          // jets / depth jets of the current iteration
+  double H[36];              // last normal matrix (error payload / trace)
+  double cov[36];
+  int cov_degenerate;
+  int total_iters;
+  int trace_n;
+};
+
+// phase 0 = IRLS level loop, phase 1 = filtered-Hessian covariance pass
+__device__ __forceinline__ bool slot_active(const SlotState& s, int level, int phase) {
+  return s.status == RGBID_OK && (phase == 1 || s.done_level != level);
+}
+
+struct AlignLaunch {
+  SlotIO* io;          // device array [nslots]
+  SlotState* st;       // device array [nslots]
+  rgbid_iter_trace* trace;  // device [kTraceMax] (slot 0) or nullptr
+  int nslots;
+  int w0, h0;
+  double eps;
+  double lambda_n_min;
+};
+
+// Kernel launchers (align_kernels.cu); all asynchronous on `stream`.
+void launch_warp_residuals(const AlignLaunch& a, const LevelInfo& li, int phase, cudaStream_t s);
+void launch_tdist(const AlignLaunch& a, const LevelInfo& li, int phase, cudaStream_t s);
+void launch_normal_equations(const AlignLaunch& a, const LevelInfo& li, int phase, cudaStream_t s);
+void launch_solve(const AlignLaunch& a, const LevelInfo& li, const LevelInfo& li0, cudaStream_t s);
+void launch_covariance(const AlignLaunch& a, const LevelInfo& li, cudaStream_t s);
+void launch_downsample2(const double* I, const double* W, int w, int h, double* oI, double* oW,
+                        cudaStream_t s);
+void launch_bilateral_pair(const AlignLaunch& a, double ss, double sr_i, double sr_w,
+                           cudaStream_t s);
+void launch_bilateral(const double* img, int w, int h, double ss, double sr, double* out,
+                      cudaStream_t s);
+void launch_warp_maps(const double* IB, const double* WB, int wb, int hb, const double* WA, int w,
+                      int h, const WarpMats& m, double* oI, double* oW, double* omx, double* omy,
+                      cudaStream_t s);
+int tdist_smem_bytes(int ntiles);
+int init_kernel_attributes();
+
+// per-launch counter (all library kernels go through launchers that bump it)
+extern thread_local long long* g_launch_counter;
+inline void count_launch() {
+  if (g_launch_counter) ++*g_launch_counter;
+}
+
+}  // namespace rgbid_b200

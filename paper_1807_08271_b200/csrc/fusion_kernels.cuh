@@ -1,0 +1,46 @@
+// Fusion / covisibility / registration / synthetic-input kernels (fusion_kernels.cu).
+#pragma once
+#include <cuda_runtime.h>
+
+#include "hd_math.cuh"
+
+namespace rgbid_b200 {
+
+struct FuseFrame {  // one frame of integrate_frame: its W map + warp matrices of T_kf_frame
+  const double* W;
+  WarpMats wm;
+};
+
+struct CovisDir {  // one direction of count_visible
+  const double* WA;
+  const double* WB;
+  double Rt[9], tt[3];
+};
+
+struct RegisterMats {  // forward_register host-side setup (src/warping.cpp:22-25)
+  double Rt_AB[9];
+  double tt[3];
+};
+
+struct SynthView {
+  int w, h;
+  M3 Kinv, R;
+  double t[3], n[3], d;
+  double tex_scale;
+  double noise_i, noise_w;
+  unsigned long long seed;
+  int occluder;
+};
+
+void launch_integrate(const FuseFrame* frames_dev, int k, double* kfW, double* kfC, int w, int h,
+                      double sigma_w, cudaStream_t s);
+void launch_covisibility(const CovisDir& d0, const CovisDir& d1, int w, int h, double sigma_w,
+                         unsigned long long* counts_dev, cudaStream_t s);
+void launch_correct_depth(const double* Wm, int w, int h, const rgbid_depth_intrinsics& d,
+                          const rgbid_intrinsics& K, int spatial, double* out, cudaStream_t s);
+void launch_forward_register(const double* WA, int w, int h, const RegisterMats& r,
+                             unsigned long long* inter, int iw, int ih, int wb, int hb,
+                             double* out, cudaStream_t s);
+void launch_render(const SynthView& v, double* I, double* W, cudaStream_t s);
+
+}  // namespace rgbid_b200

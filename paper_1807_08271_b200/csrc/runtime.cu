@@ -1,0 +1,986 @@
+// Host runtime of librgbid_b200.so: contexts, device frames, the on-device
+// alignment driver and every C-ABI entry point of include/rgbid_b200.h.
+//
+// The level/iteration loop of align (src/alignment.cpp:372-404) is issued as a
+// fixed sequence of kernel launches on the ctx stream; convergence breaks and
+// degenerate throws are per-slot flags evaluated on the device (SlotState), so
+// the host never waits inside an alignment.  The launch sequence of a given
+// (batch size, levels, iterations) is captured once into a CUDA graph and
+// replayed.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/rgbid_b200.h"
+#include "align_kernels.cuh"
+#include "fusion_kernels.cuh"
+
+using namespace rgbid_b200;
+
+struct rgbid_frame {
+  int w = 0, h = 0;
+  double* I = nullptr;  // level 0
+  double* W = nullptr;
+  double* pyr = nullptr;  // levels 1..kMaxLevels-1, I and W interleaved per level
+  double* pI[kMaxLevels] = {};
+  double* pW[kMaxLevels] = {};
+  int pyr_levels = 0;  // levels currently valid (0 = none built)
+};
+
+namespace {
+
+struct CachedGraph {
+  cudaGraphExec_t exec = nullptr;
+  long long launches = 0;  // kernel launches per replay
+};
+
+}  // namespace
+
+struct rgbid_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::string err;
+  long long launches = 0;
+  // slot workspace
+  int cap_slots = 0, cap_w = 0, cap_h = 0;
+  double* ws_f64 = nullptr;
+  int* ws_i32 = nullptr;
+  SlotIO* d_io = nullptr;
+  SlotState* d_st = nullptr;
+  rgbid_iter_trace* d_trace = nullptr;
+  std::vector<SlotIO> h_io;
+  std::vector<SlotState> h_st;
+  SlotState* h_st_pinned = nullptr;
+  std::vector<rgbid_iter_trace> last_trace;
+  // graph cache for the align launch sequence
+  std::map<std::string, CachedGraph> graphs;
+  bool use_graphs = true;
+  // scratch device buffers for the one-shot host APIs
+  std::map<std::string, std::pair<void*, size_t>> scratch;
+  rgbid_frame* tmpA = nullptr;
+  rgbid_frame* tmpB = nullptr;
+};
+
+namespace {
+
+struct LaunchScope {  // routes count_launch() to this ctx
+  explicit LaunchScope(rgbid_ctx* c) { g_launch_counter = &c->launches; }
+  ~LaunchScope() { g_launch_counter = nullptr; }
+};
+
+#define CK(expr)                                                        \
+  do {                                                                  \
+    cudaError_t e_ = (expr);                                            \
+    if (e_ != cudaSuccess) {                                            \
+      ctx->err = std::string(#expr) + ": " + cudaGetErrorString(e_);    \
+      return e_ == cudaErrorMemoryAllocation ? RGBID_E_OOM : RGBID_E_CUDA; \
+    }                                                                   \
+  } while (0)
+
+int check_launch(rgbid_ctx* ctx) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    ctx->err = std::string("kernel launch: ") + cudaGetErrorString(e);
+    return RGBID_E_CUDA;
+  }
+  return RGBID_OK;
+}
+
+template <typename T>
+int scratch_buf(rgbid_ctx* ctx, const char* name, size_t count, T** out) {
+  auto& e = ctx->scratch[name];
+  const size_t bytes = count * sizeof(T);
+  if (e.second < bytes) {
+    if (e.first) cudaFree(e.first);
+    e.first = nullptr;
+    e.second = 0;
+    CK(cudaMalloc(&e.first, bytes));
+    e.second = bytes;
+  }
+  *out = static_cast<T*>(e.first);
+  return RGBID_OK;
+}
+
+rgbid_align_config default_config() {
+  rgbid_align_config c;
+  std::memset(&c, 0, sizeof(c));
+  c.levels = 3;
+  c.n_iterations = 3;
+  c.iterations[0] = 10;
+  c.iterations[1] = 5;
+  c.iterations[2] = 4;
+  c.convergence_eps = 1e-6;
+  c.lambda_n_min = 0.1;
+  c.bilateral_sigma_space = 2.0;
+  c.bilateral_sigma_intensity = 0.05;
+  c.bilateral_sigma_depth = 0.02;
+  return c;
+}
+
+int level_iters(const rgbid_align_config& c, int level) {
+  return level < c.n_iterations ? c.iterations[level] : 5;  // src/alignment.cpp:373-374
+}
+
+// build_pyramid intrinsics — src/alignment.cpp:18-25
+void level_intrinsics(const rgbid_intrinsics& K0, int level, rgbid_intrinsics* out) {
+  rgbid_intrinsics k = K0;
+  for (int l = 0; l < level; ++l) {
+    k.fx /= 2.0;
+    k.fy /= 2.0;
+    k.cx = (k.cx - 0.5) / 2.0;
+    k.cy = (k.cy - 0.5) / 2.0;
+    k.width /= 2;
+    k.height /= 2;
+  }
+  *out = k;
+}
+
+LevelInfo make_level(const rgbid_intrinsics& K0, int w0, int h0, int level) {
+  LevelInfo li;
+  std::memset(&li, 0, sizeof(li));
+  li.level = level;
+  li.w = w0 >> level;
+  li.h = h0 >> level;
+  li.tx = k1_tx(level);
+  li.nseg = (li.w + li.tx - 1) / li.tx;
+  li.ntiles = li.nseg * li.h;
+  li.ntiles3 = (li.w * li.h + kTPB - 1) / kTPB;
+  rgbid_intrinsics k;
+  level_intrinsics(K0, level, &k);
+  li.fx = k.fx;
+  li.fy = k.fy;
+  li.cx = k.cx;
+  li.cy = k.cy;
+  const M3 Ki = m3_inv(K_mat(k.fx, k.fy, k.cx, k.cy));
+  for (int i = 0; i < 9; ++i) li.Kinv[i] = Ki.m[i / 3][i % 3];
+  return li;
+}
+
+PoseD pose_of(const rgbid_pose* p) {
+  if (!p) {
+    PoseD I;
+    std::memset(&I, 0, sizeof(I));
+    I.R.m[0][0] = I.R.m[1][1] = I.R.m[2][2] = 1.0;
+    return I;
+  }
+  return pose_from(p->R, p->t);
+}
+
+// Per-slot workspace: ib, wb, resI, resW, fIA, fWA (N doubles each) + part; cntI/cntW ints.
+size_t slot_f64(int w, int h) {
+  const size_t N = (size_t)w * h;
+  const size_t part = (size_t)((N + kTPB - 1) / kTPB) * kNPart;
+  return 6 * N + part;
+}
+size_t slot_i32(int w, int h) {
+  size_t mx = 0;
+  for (int l = 0; l < kMaxLevels; ++l) {
+    if ((w >> l) < 1 || (h >> l) < 1) break;
+    const int tx = k1_tx(l);
+    mx = std::max(mx, (size_t)(((w >> l) + tx - 1) / tx) * (size_t)(h >> l));
+  }
+  return 2 * mx;
+}
+
+int ensure_workspace(rgbid_ctx* ctx, int nslots, int w, int h) {
+  if (nslots <= ctx->cap_slots && w * h <= ctx->cap_w * ctx->cap_h && w == ctx->cap_w &&
+      h == ctx->cap_h)
+    return RGBID_OK;
+  if (ctx->ws_f64) cudaFree(ctx->ws_f64);
+  if (ctx->ws_i32) cudaFree(ctx->ws_i32);
+  if (ctx->d_io) cudaFree(ctx->d_io);
+  if (ctx->d_st) cudaFree(ctx->d_st);
+  if (ctx->h_st_pinned) cudaFreeHost(ctx->h_st_pinned);
+  ctx->ws_f64 = nullptr;
+  ctx->ws_i32 = nullptr;
+  ctx->d_io = nullptr;
+  ctx->d_st = nullptr;
+  ctx->h_st_pinned = nullptr;
+  ctx->cap_slots = 0;
+  for (auto& g : ctx->graphs) cudaGraphExecDestroy(g.second.exec);
+  ctx->graphs.clear();
+  CK(cudaMalloc(&ctx->ws_f64, sizeof(double) * slot_f64(w, h) * nslots));
+  CK(cudaMalloc(&ctx->ws_i32, sizeof(int) * slot_i32(w, h) * nslots));
+  CK(cudaMalloc(&ctx->d_io, sizeof(SlotIO) * nslots));
+  CK(cudaMalloc(&ctx->d_st, sizeof(SlotState) * nslots));
+  CK(cudaMallocHost(&ctx->h_st_pinned, sizeof(SlotState) * nslots));
+  if (!ctx->d_trace) CK(cudaMalloc(&ctx->d_trace, sizeof(rgbid_iter_trace) * kTraceMax));
+  ctx->cap_slots = nslots;
+  ctx->cap_w = w;
+  ctx->cap_h = h;
+  ctx->h_io.resize(nslots);
+  ctx->h_st.resize(nslots);
+  return RGBID_OK;
+}
+
+int frame_ensure_pyramid(rgbid_ctx* ctx, rgbid_frame* f, int levels) {
+  if (f->pyr_levels >= levels) return RGBID_OK;
+  if (!f->pyr) {
+    size_t tot = 0;
+    for (int l = 1; l < kMaxLevels; ++l) tot += 2 * (size_t)(f->w >> l) * (f->h >> l);
+    if (tot == 0) tot = 1;
+    CK(cudaMalloc(&f->pyr, sizeof(double) * tot));
+    size_t off = 0;
+    for (int l = 1; l < kMaxLevels; ++l) {
+      const size_t n = (size_t)(f->w >> l) * (f->h >> l);
+      f->pI[l] = f->pyr + off;
+      f->pW[l] = f->pyr + off + n;
+      off += 2 * n;
+    }
+  }
+  f->pI[0] = f->I;
+  f->pW[0] = f->W;
+  for (int l = std::max(1, f->pyr_levels); l < levels; ++l)
+    launch_downsample2(f->pI[l - 1], f->pW[l - 1], f->w >> (l - 1), f->h >> (l - 1), f->pI[l],
+                       f->pW[l], ctx->stream);
+  f->pyr_levels = levels;
+  return check_launch(ctx);
+}
+
+// Host Jacobi eigenvalues (spectrum payload of DegenerateAlignmentError only).
+void spectrum_of(const double H[36], long long n_jets, double out[6]) {
+  if (n_jets < 6) {
+    for (int i = 0; i < 6; ++i) out[i] = 0.0;
+    return;
+  }
+  bool bad = false;
+  for (int i = 0; i < 6; ++i)
+    if (H[i * 6 + i] <= 0.0) bad = true;
+  if (bad) {
+    for (int i = 0; i < 6; ++i) out[i] = H[i * 6 + i];
+    return;
+  }
+  double s[6], a[6][6];
+  for (int i = 0; i < 6; ++i) s[i] = 1.0 / std::sqrt(H[i * 6 + i]);
+  for (int i = 0; i < 6; ++i)
+    for (int j = 0; j < 6; ++j) a[i][j] = (s[i] * H[i * 6 + j]) * s[j];
+  for (int sweep = 0; sweep < 100; ++sweep) {
+    double off = 0.0;
+    for (int i = 0; i < 6; ++i)
+      for (int j = i + 1; j < 6; ++j) off += a[i][j] * a[i][j];
+    if (off == 0.0) break;
+    for (int p = 0; p < 6; ++p)
+      for (int q = p + 1; q < 6; ++q) {
+        if (a[p][q] == 0.0) continue;
+        const double th = (a[q][q] - a[p][p]) / (2.0 * a[p][q]);
+        const double t = (th >= 0 ? 1.0 : -1.0) / (std::fabs(th) + std::sqrt(th * th + 1.0));
+        const double c = 1.0 / std::sqrt(t * t + 1.0), sn = t * c;
+        for (int k = 0; k < 6; ++k) {
+          const double kp = a[k][p], kq = a[k][q];
+          a[k][p] = c * kp - sn * kq;
+          a[k][q] = sn * kp + c * kq;
+        }
+        for (int k = 0; k < 6; ++k) {
+          const double pk = a[p][k], qk = a[q][k];
+          a[p][k] = c * pk - sn * qk;
+          a[q][k] = sn * pk + c * qk;
+        }
+      }
+  }
+  for (int i = 0; i < 6; ++i) out[i] = a[i][i];
+  std::sort(out, out + 6);
+}
+
+int validate_cfg(const rgbid_align_config& c, int w, int h) {
+  if (c.levels < 1 || c.levels > kMaxLevels) return RGBID_E_ARG;
+  if (c.n_iterations < 0 || c.n_iterations > RGBID_MAX_LEVELS) return RGBID_E_ARG;
+  if ((w >> (c.levels - 1)) < 1 || (h >> (c.levels - 1)) < 1) return RGBID_E_ARG;
+  return RGBID_OK;
+}
+
+// Enqueue the whole align (all levels + covariance pass) for ctx->cap slots.
+void enqueue_align(rgbid_ctx* ctx, const AlignLaunch& a, const rgbid_intrinsics& K,
+                   const rgbid_align_config& cfg) {
+  const LevelInfo li0 = make_level(K, a.w0, a.h0, 0);
+  for (int level = cfg.levels - 1; level >= 0; --level) {
+    const LevelInfo li = make_level(K, a.w0, a.h0, level);
+    const int iters = level_iters(cfg, level);
+    for (int it = 0; it < iters; ++it) {
+      launch_warp_residuals(a, li, 0, ctx->stream);
+      launch_tdist(a, li, 0, ctx->stream);
+      launch_normal_equations(a, li, 0, ctx->stream);
+      launch_solve(a, li, li0, ctx->stream);
+    }
+  }
+  // filtered_hessian_covariance — src/alignment.cpp:406-407, 411-436
+  launch_bilateral_pair(a, cfg.bilateral_sigma_space, cfg.bilateral_sigma_intensity,
+                        cfg.bilateral_sigma_depth, ctx->stream);
+  launch_warp_residuals(a, li0, 1, ctx->stream);
+  launch_tdist(a, li0, 1, ctx->stream);
+  launch_normal_equations(a, li0, 1, ctx->stream);
+  launch_covariance(a, li0, ctx->stream);
+}
+
+// Run n alignments (n <= cap) whose frames are given; fills results.
+int run_align_slots(rgbid_ctx* ctx, int n, const rgbid_frame* const* fa,
+                    const rgbid_frame* const* fb, const rgbid_intrinsics& K,
+                    const rgbid_pose* inits, const rgbid_align_config& cfg,
+                    rgbid_align_result* results, bool want_trace) {
+  const int w = fa[0]->w, h = fa[0]->h;
+  int rc = ensure_workspace(ctx, std::max(n, ctx->cap_slots), w, h);
+  if (rc) return rc;
+  for (int i = 0; i < n; ++i) {
+    rc = frame_ensure_pyramid(ctx, const_cast<rgbid_frame*>(fa[i]), cfg.levels);
+    if (rc) return rc;
+  }
+  const size_t N = (size_t)w * h;
+  const size_t sf = slot_f64(w, h), si = slot_i32(w, h);
+  const LevelInfo li0 = make_level(K, w, h, 0);
+  const int nslots = n;
+  for (int i = 0; i < nslots; ++i) {
+    SlotIO& o = ctx->h_io[i];
+    std::memset(&o, 0, sizeof(o));
+    for (int l = 0; l < kMaxLevels; ++l) {
+      o.IA[l] = fa[i]->pI[l];
+      o.WA[l] = fa[i]->pW[l];
+    }
+    o.IA[0] = fa[i]->I;
+    o.WA[0] = fa[i]->W;
+    o.IB = fb[i]->I;
+    o.WB = fb[i]->W;
+    double* base = ctx->ws_f64 + sf * i;
+    o.ib = base;
+    o.wb = base + N;
+    o.resI = base + 2 * N;
+    o.resW = base + 3 * N;
+    o.fIA = base + 4 * N;
+    o.fWA = base + 5 * N;
+    o.part = base + 6 * N;
+    o.cntI = ctx->ws_i32 + si * i;
+    o.cntW = o.cntI + si / 2;
+    SlotState& s = ctx->h_st_pinned[i];
+    std::memset(&s, 0, sizeof(s));
+    const PoseD T = pose_of(inits ? &inits[i] : nullptr);
+    pose_to(T, s.R, s.t);
+    s.wm = warp_mats(T, li0.fx, li0.fy, li0.cx, li0.cy);
+    s.status = RGBID_OK;
+    s.done_level = -1;
+  }
+  CK(cudaMemcpyAsync(ctx->d_io, ctx->h_io.data(), sizeof(SlotIO) * nslots, cudaMemcpyHostToDevice,
+                     ctx->stream));
+  CK(cudaMemcpyAsync(ctx->d_st, ctx->h_st_pinned, sizeof(SlotState) * nslots,
+                     cudaMemcpyHostToDevice, ctx->stream));
+  AlignLaunch a;
+  a.io = ctx->d_io;
+  a.st = ctx->d_st;
+  a.trace = want_trace ? ctx->d_trace : nullptr;
+  a.nslots = nslots;
+  a.w0 = w;
+  a.h0 = h;
+  a.eps = cfg.convergence_eps;
+  a.lambda_n_min = cfg.lambda_n_min;
+
+  // every value baked into the launch sequence is part of the graph key
+  struct {
+    int nslots, trace, levels, w, h;
+    int iters[kMaxLevels];
+    double p[9];
+  } kb;
+  std::memset(&kb, 0, sizeof(kb));
+  kb.nslots = nslots;
+  kb.trace = want_trace;
+  kb.levels = cfg.levels;
+  kb.w = w;
+  kb.h = h;
+  for (int l = 0; l < cfg.levels; ++l) kb.iters[l] = level_iters(cfg, l);
+  const double p[9] = {cfg.convergence_eps, cfg.lambda_n_min, cfg.bilateral_sigma_space,
+                       cfg.bilateral_sigma_intensity, cfg.bilateral_sigma_depth, K.fx, K.fy, K.cx,
+                       K.cy};
+  std::memcpy(kb.p, p, sizeof(p));
+  const std::string key(reinterpret_cast<const char*>(&kb), sizeof(kb));
+  if (ctx->use_graphs) {
+    auto it = ctx->graphs.find(key);
+    if (it == ctx->graphs.end()) {
+      cudaGraph_t g;
+      CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+      const long long before = ctx->launches;
+      enqueue_align(ctx, a, K, cfg);
+      CachedGraph cg;
+      cg.launches = ctx->launches - before;
+      ctx->launches = before;
+      CK(cudaStreamEndCapture(ctx->stream, &g));
+      CK(cudaGraphInstantiate(&cg.exec, g, 0));
+      cudaGraphDestroy(g);
+      it = ctx->graphs.emplace(key, cg).first;
+    }
+    CK(cudaGraphLaunch(it->second.exec, ctx->stream));
+    ctx->launches += it->second.launches;
+  } else {
+    enqueue_align(ctx, a, K, cfg);
+  }
+  rc = check_launch(ctx);
+  if (rc) return rc;
+  CK(cudaMemcpyAsync(ctx->h_st_pinned, ctx->d_st, sizeof(SlotState) * nslots,
+                     cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (want_trace) {
+    ctx->last_trace.resize(kTraceMax);
+    CK(cudaMemcpy(ctx->last_trace.data(), ctx->d_trace, sizeof(rgbid_iter_trace) * kTraceMax,
+                  cudaMemcpyDeviceToHost));
+    ctx->last_trace.resize(std::min(ctx->h_st_pinned[0].trace_n, kTraceMax));
+  }
+  for (int i = 0; i < nslots; ++i) {
+    const SlotState& s = ctx->h_st_pinned[i];
+    rgbid_align_result& r = results[i];
+    std::memset(&r, 0, sizeof(r));
+    r.status = s.status;
+    if (s.status == RGBID_E_DEGENERATE) {
+      spectrum_of(s.H, s.nI, r.spectrum);
+      continue;
+    }
+    std::memcpy(r.T_AB.R, s.R, sizeof(s.R));
+    std::memcpy(r.T_AB.t, s.t, sizeof(s.t));
+    std::memcpy(r.cov, s.cov, sizeof(s.cov));
+    r.converged = 1;
+    r.cov_degenerate = s.cov_degenerate;
+    r.n_levels = cfg.levels;
+    for (int k = 0; k < cfg.levels; ++k) {
+      const int level = cfg.levels - 1 - k;
+      r.level_log[k].level = level;
+      r.level_log[k].iterations = s.iters[level];
+      r.level_log[k].final_cost = s.cost[level];
+    }
+    r.tdist_intensity = s.finI;
+    r.tdist_depth = s.finW;
+    r.total_iterations = s.total_iters;
+  }
+  return RGBID_OK;
+}
+
+int frame_from_host(rgbid_ctx* ctx, rgbid_frame** slot, int w, int h, const double* I,
+                    const double* W) {
+  if (*slot && ((*slot)->w != w || (*slot)->h != h)) {
+    rgbid_frame_destroy(ctx, *slot);
+    *slot = nullptr;
+  }
+  if (!*slot) {
+    int rc = rgbid_frame_create(ctx, w, h, slot);
+    if (rc) return rc;
+  }
+  return rgbid_frame_upload(ctx, *slot, I, W);
+}
+
+}  // namespace
+
+// ===========================================================================
+extern "C" {
+
+const char* rgbid_version(void) { return "rgbid_b200 0.1 (sm_100a)"; }
+
+const char* rgbid_status_string(int s) {
+  switch (s) {
+    case RGBID_OK: return "ok";
+    case RGBID_E_DEGENERATE: return "degenerate alignment: under-constrained scene";
+    case RGBID_E_CUDA: return "CUDA error";
+    case RGBID_E_ARG: return "invalid argument";
+    case RGBID_E_OOM: return "out of device memory";
+    default: return "unknown";
+  }
+}
+
+int rgbid_ctx_create(int device, rgbid_ctx** out) {
+  if (!out) return RGBID_E_ARG;
+  *out = nullptr;
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || device < 0 || device >= n) return RGBID_E_CUDA;
+  cudaDeviceProp p;
+  if (cudaGetDeviceProperties(&p, device) != cudaSuccess) return RGBID_E_CUDA;
+  if (p.major < 10) return RGBID_E_CUDA;  // sm_100a binary only
+  if (cudaSetDevice(device) != cudaSuccess) return RGBID_E_CUDA;
+  cudaGetLastError();
+  rgbid_ctx* ctx = new rgbid_ctx();
+  ctx->device = device;
+  if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
+    delete ctx;
+    return RGBID_E_CUDA;
+  }
+  if (init_kernel_attributes() != 0) {
+    delete ctx;
+    return RGBID_E_CUDA;
+  }
+  const char* g = std::getenv("RGBID_NO_GRAPHS");
+  ctx->use_graphs = !(g && g[0] == '1');
+  *out = ctx;
+  return RGBID_OK;
+}
+
+int rgbid_ctx_destroy(rgbid_ctx* ctx) {
+  if (!ctx) return RGBID_E_ARG;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  for (auto& g : ctx->graphs) cudaGraphExecDestroy(g.second.exec);
+  for (auto& s : ctx->scratch)
+    if (s.second.first) cudaFree(s.second.first);
+  if (ctx->tmpA) rgbid_frame_destroy(ctx, ctx->tmpA);
+  if (ctx->tmpB) rgbid_frame_destroy(ctx, ctx->tmpB);
+  cudaFree(ctx->ws_f64);
+  cudaFree(ctx->ws_i32);
+  cudaFree(ctx->d_io);
+  cudaFree(ctx->d_st);
+  cudaFree(ctx->d_trace);
+  if (ctx->h_st_pinned) cudaFreeHost(ctx->h_st_pinned);
+  cudaStreamDestroy(ctx->stream);
+  delete ctx;
+  return RGBID_OK;
+}
+
+const char* rgbid_ctx_last_error(rgbid_ctx* ctx) { return ctx ? ctx->err.c_str() : ""; }
+long long rgbid_ctx_kernel_launches(rgbid_ctx* ctx) { return ctx ? ctx->launches : 0; }
+int rgbid_ctx_synchronize(rgbid_ctx* ctx) {
+  if (!ctx) return RGBID_E_ARG;
+  CK(cudaStreamSynchronize(ctx->stream));
+  return RGBID_OK;
+}
+void* rgbid_ctx_stream(rgbid_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
+
+int rgbid_frame_create(rgbid_ctx* ctx, int w, int h, rgbid_frame** out) {
+  if (!ctx || !out || w <= 0 || h <= 0) return RGBID_E_ARG;
+  cudaSetDevice(ctx->device);
+  rgbid_frame* f = new rgbid_frame();
+  f->w = w;
+  f->h = h;
+  const size_t N = (size_t)w * h;
+  cudaError_t e = cudaMalloc(&f->I, sizeof(double) * 2 * N);
+  if (e != cudaSuccess) {
+    delete f;
+    ctx->err = cudaGetErrorString(e);
+    return RGBID_E_OOM;
+  }
+  f->W = f->I + N;
+  f->pI[0] = f->I;
+  f->pW[0] = f->W;
+  *out = f;
+  return RGBID_OK;
+}
+
+int rgbid_frame_upload(rgbid_ctx* ctx, rgbid_frame* f, const double* I, const double* W) {
+  if (!ctx || !f || !W) return RGBID_E_ARG;
+  const size_t N = (size_t)f->w * f->h;
+  if (I)
+    CK(cudaMemcpyAsync(f->I, I, sizeof(double) * N, cudaMemcpyHostToDevice, ctx->stream));
+  else
+    CK(cudaMemsetAsync(f->I, 0xff, sizeof(double) * N, ctx->stream));  // NaN holes
+  CK(cudaMemcpyAsync(f->W, W, sizeof(double) * N, cudaMemcpyHostToDevice, ctx->stream));
+  f->pyr_levels = 0;
+  CK(cudaStreamSynchronize(ctx->stream));
+  return RGBID_OK;
+}
+
+int rgbid_frame_download(rgbid_ctx* ctx, const rgbid_frame* f, double* I, double* W) {
+  if (!ctx || !f) return RGBID_E_ARG;
+  const size_t N = (size_t)f->w * f->h;
+  if (I) CK(cudaMemcpyAsync(I, f->I, sizeof(double) * N, cudaMemcpyDeviceToHost, ctx->stream));
+  if (W) CK(cudaMemcpyAsync(W, f->W, sizeof(double) * N, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return RGBID_OK;
+}
+
+int rgbid_frame_device_ptrs(rgbid_frame* f, double** I_dev, double** W_dev) {
+  if (!f) return RGBID_E_ARG;
+  if (I_dev) *I_dev = f->I;
+  if (W_dev) *W_dev = f->W;
+  f->pyr_levels = 0;  // caller may write through these pointers
+  return RGBID_OK;
+}
+
+int rgbid_frame_destroy(rgbid_ctx* ctx, rgbid_frame* f) {
+  (void)ctx;
+  if (!f) return RGBID_E_ARG;
+  cudaFree(f->I);
+  if (f->pyr) cudaFree(f->pyr);
+  delete f;
+  return RGBID_OK;
+}
+
+int rgbid_build_pyramid(rgbid_ctx* ctx, const double* I, const double* W, int w, int h,
+                        const rgbid_intrinsics* K, int levels, double** out_I, double** out_W,
+                        rgbid_intrinsics* K_out) {
+  if (!ctx || !W || !K || levels < 1 || levels > kMaxLevels) return RGBID_E_ARG;
+  LaunchScope ls(ctx);
+  int rc = frame_from_host(ctx, &ctx->tmpA, w, h, I, W);
+  if (rc) return rc;
+  rgbid_frame* f = ctx->tmpA;
+  rc = frame_ensure_pyramid(ctx, f, levels);
+  if (rc) return rc;
+  for (int l = 0; l < levels; ++l) {
+    const size_t n = (size_t)(w >> l) * (h >> l);
+    if (out_I && out_I[l])
+      CK(cudaMemcpyAsync(out_I[l], f->pI[l], sizeof(double) * n, cudaMemcpyDeviceToHost,
+                         ctx->stream));
+    if (out_W && out_W[l])
+      CK(cudaMemcpyAsync(out_W[l], f->pW[l], sizeof(double) * n, cudaMemcpyDeviceToHost,
+                         ctx->stream));
+    if (K_out) level_intrinsics(*K, l, &K_out[l]);
+  }
+  CK(cudaStreamSynchronize(ctx->stream));
+  return RGBID_OK;
+}
+
+int rgbid_inverse_geometric_warp(rgbid_ctx* ctx, const double* I_B, const double* W_B, int wb,
+                                 int hb, const double* W_A, int w, int h, const rgbid_pose* T_AB,
+                                 const rgbid_intrinsics* K, double* oI, double* oW, double* omx,
+                                 double* omy) {
+  if (!ctx || !W_B || !W_A || !T_AB || !K) return RGBID_E_ARG;
+  LaunchScope ls(ctx);
+  const size_t NB = (size_t)wb * hb, N = (size_t)w * h;
+  double *dB, *dA, *dO;
+  int rc = scratch_buf(ctx, "warp_in", 2 * NB + N, &dB);
+  if (rc) return rc;
+  rc = scratch_buf(ctx, "warp_out", 4 * N, &dO);
+  if (rc) return rc;
+  dA = dB + 2 * NB;
+  if (I_B)
+    CK(cudaMemcpyAsync(dB, I_B, sizeof(double) * NB, cudaMemcpyHostToDevice, ctx->stream));
+  else
+    CK(cudaMemsetAsync(dB, 0xff, sizeof(double) * NB, ctx->stream));
+  CK(cudaMemcpyAsync(dB + NB, W_B, sizeof(double) * NB, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(dA, W_A, sizeof(double) * N, cudaMemcpyHostToDevice, ctx->stream));
+  const WarpMats m = warp_mats(pose_of(T_AB), K->fx, K->fy, K->cx, K->cy);
+  launch_warp_maps(dB, dB + NB, wb, hb, dA, w, h, m, dO, dO + N, dO + 2 * N, dO + 3 * N,
+                   ctx->stream);
+  rc = check_launch(ctx);
+  if (rc) return rc;
+  double* outs[4] = {oI, oW, omx, omy};
+  for (int k = 0; k < 4; ++k)
+    if (outs[k])
+      CK(cudaMemcpyAsync(outs[k], dO + k * N, sizeof(double) * N, cudaMemcpyDeviceToHost,
+                         ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return RGBID_OK;
+}
+
+int rgbid_align(rgbid_ctx* ctx, const rgbid_frame* a, const rgbid_frame* b,
+                const rgbid_intrinsics* K, const rgbid_pose* init, const rgbid_align_config* cfg,
+                rgbid_align_result* result) {
+  if (!ctx || !a || !b || !K || !result) return RGBID_E_ARG;
+  if (a->w != b->w || a->h != b->h) return RGBID_E_ARG;
+  const rgbid_align_config c = cfg ? *cfg : default_config();
+  if (validate_cfg(c, a->w, a->h)) return RGBID_E_ARG;
+  LaunchScope ls(ctx);
+  cudaSetDevice(ctx->device);
+  int rc = run_align_slots(ctx, 1, &a, &b, *K, init, c, result, true);
+  if (rc) return rc;
+  return result->status;
+}
+
+int rgbid_align_host(rgbid_ctx* ctx, const double* IA, const double* WA, const double* IB,
+                     const double* WB, int w, int h, const rgbid_intrinsics* K,
+                     const rgbid_pose* init, const rgbid_align_config* cfg,
+                     rgbid_align_result* result) {
+  if (!ctx) return RGBID_E_ARG;
+  int rc = frame_from_host(ctx, &ctx->tmpA, w, h, IA, WA);
+  if (rc) return rc;
+  rc = frame_from_host(ctx, &ctx->tmpB, w, h, IB, WB);
+  if (rc) return rc;
+  return rgbid_align(ctx, ctx->tmpA, ctx->tmpB, K, init, cfg, result);
+}
+
+int rgbid_last_align_trace(rgbid_ctx* ctx, rgbid_iter_trace* out, int max_entries, int* n) {
+  if (!ctx || !n) return RGBID_E_ARG;
+  const int m = std::min<int>(max_entries, (int)ctx->last_trace.size());
+  if (out && m > 0) std::memcpy(out, ctx->last_trace.data(), sizeof(rgbid_iter_trace) * m);
+  *n = m;
+  return RGBID_OK;
+}
+
+int rgbid_align_batch(rgbid_ctx* ctx, int n, const rgbid_frame* const* a,
+                      const rgbid_frame* const* b, const rgbid_intrinsics* K,
+                      const rgbid_pose* inits, const rgbid_align_config* cfg,
+                      rgbid_align_result* results) {
+  if (!ctx || n < 0 || (n > 0 && (!a || !b || !K || !results))) return RGBID_E_ARG;
+  if (n == 0) return RGBID_OK;
+  const rgbid_align_config c = cfg ? *cfg : default_config();
+  for (int i = 0; i < n; ++i)
+    if (!a[i] || !b[i] || a[i]->w != a[0]->w || a[i]->h != a[0]->h || b[i]->w != a[0]->w ||
+        b[i]->h != a[0]->h)
+      return RGBID_E_ARG;
+  if (validate_cfg(c, a[0]->w, a[0]->h)) return RGBID_E_ARG;
+  LaunchScope ls(ctx);
+  cudaSetDevice(ctx->device);
+  // chunk so the slot workspace stays bounded (~15 MB per VGA slot)
+  const char* env = std::getenv("RGBID_BATCH_SLOTS");
+  int chunk = env ? std::max(1, atoi(env)) : 128;
+  for (int i0 = 0; i0 < n; i0 += chunk) {
+    const int m = std::min(chunk, n - i0);
+    const int rc = run_align_slots(ctx, m, a + i0, b + i0, *K, inits ? inits + i0 : nullptr, c,
+                                   results + i0, i0 == 0);
+    if (rc) return rc;
+  }
+  return RGBID_OK;
+}
+
+int rgbid_align_batch_host(rgbid_ctx* ctx, int n, const double* const* IA,
+                           const double* const* WA, const double* const* IB,
+                           const double* const* WB, int w, int h, const rgbid_intrinsics* K,
+                           const rgbid_pose* inits, const rgbid_align_config* cfg, int chunk,
+                           rgbid_align_result* results) {
+  if (!ctx || n < 0 || !K || (n > 0 && (!IA || !WA || !IB || !WB || !results)))
+    return RGBID_E_ARG;
+  if (chunk <= 0) chunk = 64;
+  LaunchScope ls(ctx);
+  std::vector<rgbid_frame*> fa, fb;
+  auto cleanup = [&]() {
+    for (auto* f : fa) rgbid_frame_destroy(ctx, f);
+    for (auto* f : fb) rgbid_frame_destroy(ctx, f);
+  };
+  for (int i = 0; i < std::min(chunk, n); ++i) {
+    rgbid_frame *x, *y;
+    int rc = rgbid_frame_create(ctx, w, h, &x);
+    if (rc) return cleanup(), rc;
+    fa.push_back(x);
+    rc = rgbid_frame_create(ctx, w, h, &y);
+    if (rc) return cleanup(), rc;
+    fb.push_back(y);
+  }
+  const size_t N = (size_t)w * h;
+  for (int i0 = 0; i0 < n; i0 += chunk) {
+    const int m = std::min(chunk, n - i0);
+    for (int i = 0; i < m; ++i) {
+      cudaMemcpyAsync(fa[i]->I, IA[i0 + i], sizeof(double) * N, cudaMemcpyHostToDevice, ctx->stream);
+      cudaMemcpyAsync(fa[i]->W, WA[i0 + i], sizeof(double) * N, cudaMemcpyHostToDevice, ctx->stream);
+      cudaMemcpyAsync(fb[i]->I, IB[i0 + i], sizeof(double) * N, cudaMemcpyHostToDevice, ctx->stream);
+      cudaMemcpyAsync(fb[i]->W, WB[i0 + i], sizeof(double) * N, cudaMemcpyHostToDevice, ctx->stream);
+      fa[i]->pyr_levels = 0;
+    }
+    const rgbid_align_config c = cfg ? *cfg : default_config();
+    if (validate_cfg(c, w, h)) return cleanup(), RGBID_E_ARG;
+    const int rc = run_align_slots(ctx, m, fa.data(), fb.data(), *K, inits ? inits + i0 : nullptr,
+                                   c, results + i0, i0 == 0);
+    if (rc) return cleanup(), rc;
+  }
+  cleanup();
+  return RGBID_OK;
+}
+
+int rgbid_filtered_hessian_covariance(rgbid_ctx* ctx, const rgbid_frame* a, const rgbid_frame* b,
+                                      const rgbid_intrinsics* K, const rgbid_pose* T_AB,
+                                      const rgbid_align_config* cfg, double* cov36,
+                                      int* degenerate) {
+  if (!ctx || !a || !b || !K || !T_AB || !cov36) return RGBID_E_ARG;
+  rgbid_align_config c = cfg ? *cfg : default_config();
+  // zero iterations at every level: only the covariance pass runs at T_AB
+  c.levels = 1;
+  c.n_iterations = 1;
+  c.iterations[0] = 0;
+  rgbid_align_result r;
+  LaunchScope ls(ctx);
+  int rc = run_align_slots(ctx, 1, &a, &b, *K, T_AB, c, &r, false);
+  if (rc) return rc;
+  std::memcpy(cov36, r.cov, sizeof(r.cov));
+  if (degenerate) *degenerate = r.cov_degenerate;
+  return RGBID_OK;
+}
+
+int rgbid_bilateral_filter(rgbid_ctx* ctx, const double* img, int w, int h, double ss, double sr,
+                           double* out) {
+  if (!ctx || !img || !out || w <= 0 || h <= 0) return RGBID_E_ARG;
+  LaunchScope ls(ctx);
+  const size_t N = (size_t)w * h;
+  double* d;
+  int rc = scratch_buf(ctx, "bilateral", 2 * N, &d);
+  if (rc) return rc;
+  CK(cudaMemcpyAsync(d, img, sizeof(double) * N, cudaMemcpyHostToDevice, ctx->stream));
+  launch_bilateral(d, w, h, ss, sr, d + N, ctx->stream);
+  rc = check_launch(ctx);
+  if (rc) return rc;
+  CK(cudaMemcpyAsync(out, d + N, sizeof(double) * N, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return RGBID_OK;
+}
+
+int rgbid_integrate_frame(rgbid_ctx* ctx, double* kf_W, double* kf_C, const double* frame_I,
+                          const double* frame_W, int w, int h, const rgbid_pose* T,
+                          const rgbid_intrinsics* K, double sigma_w) {
+  (void)frame_I;  // the warped intensity is never used by the reference (src/fusion.cpp:70-71)
+  if (!ctx || !kf_W || !kf_C || !frame_W || !T || !K) return RGBID_E_ARG;
+  LaunchScope ls(ctx);
+  const size_t N = (size_t)w * h;
+  double* d;
+  int rc = scratch_buf(ctx, "integrate", 3 * N, &d);
+  if (rc) return rc;
+  FuseFrame* df;
+  rc = scratch_buf(ctx, "integrate_frames", 1, &df);
+  if (rc) return rc;
+  CK(cudaMemcpyAsync(d, kf_W, sizeof(double) * N, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(d + N, kf_C, sizeof(double) * N, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(d + 2 * N, frame_W, sizeof(double) * N, cudaMemcpyHostToDevice, ctx->stream));
+  FuseFrame f;
+  f.W = d + 2 * N;
+  f.wm = warp_mats(pose_of(T), K->fx, K->fy, K->cx, K->cy);
+  CK(cudaMemcpyAsync(df, &f, sizeof(f), cudaMemcpyHostToDevice, ctx->stream));
+  launch_integrate(df, 1, d, d + N, w, h, sigma_w, ctx->stream);
+  rc = check_launch(ctx);
+  if (rc) return rc;
+  CK(cudaMemcpyAsync(kf_W, d, sizeof(double) * N, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(kf_C, d + N, sizeof(double) * N, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return RGBID_OK;
+}
+
+int rgbid_integrate_frames(rgbid_ctx* ctx, rgbid_frame* kf, double* kf_C_dev, int k,
+                           const rgbid_frame* const* frames, const rgbid_pose* T,
+                           const rgbid_intrinsics* K, double sigma_w) {
+  if (!ctx || !kf || !kf_C_dev || k < 0 || (k > 0 && (!frames || !T)) || !K) return RGBID_E_ARG;
+  if (k == 0) return RGBID_OK;
+  LaunchScope ls(ctx);
+  std::vector<FuseFrame> hf(k);
+  for (int i = 0; i < k; ++i) {
+    if (frames[i]->w != kf->w || frames[i]->h != kf->h) return RGBID_E_ARG;
+    hf[i].W = frames[i]->W;
+    hf[i].wm = warp_mats(pose_of(&T[i]), K->fx, K->fy, K->cx, K->cy);
+  }
+  FuseFrame* df;
+  int rc = scratch_buf(ctx, "integrate_frames", k, &df);
+  if (rc) return rc;
+  CK(cudaMemcpyAsync(df, hf.data(), sizeof(FuseFrame) * k, cudaMemcpyHostToDevice, ctx->stream));
+  launch_integrate(df, k, kf->W, kf_C_dev, kf->w, kf->h, sigma_w, ctx->stream);
+  kf->pyr_levels = 0;
+  rc = check_launch(ctx);
+  if (rc) return rc;
+  CK(cudaStreamSynchronize(ctx->stream));
+  return RGBID_OK;
+}
+
+int rgbid_covisibility_ratio(rgbid_ctx* ctx, const rgbid_frame* a, const rgbid_frame* b,
+                             const rgbid_pose* T_BA, const rgbid_intrinsics* K, double sigma_w,
+                             double* ratio, int* empty, long long* counts) {
+  if (!ctx || !a || !b || !T_BA || !K || !ratio) return RGBID_E_ARG;
+  if (a->w != b->w || a->h != b->h) return RGBID_E_ARG;
+  LaunchScope ls(ctx);
+  const M3 Km = K_mat(K->fx, K->fy, K->cx, K->cy), Kinv = m3_inv(Km);
+  auto dir = [&](const rgbid_frame* A, const rgbid_frame* B, const PoseD& T) {
+    CovisDir d;
+    d.WA = A->W;
+    d.WB = B->W;
+    const M3 Rt = m3_mul(m3_mul(Km, T.R), Kinv);
+    const V3 tt = m3_mulv(Km, T.t);
+    for (int i = 0; i < 9; ++i) d.Rt[i] = Rt.m[i / 3][i % 3];
+    for (int i = 0; i < 3; ++i) d.tt[i] = tt.v[i];
+    return d;
+  };
+  const PoseD T = pose_of(T_BA);
+  const CovisDir d0 = dir(a, b, T), d1 = dir(b, a, pose_inverse(T));
+  unsigned long long* dc;
+  int rc = scratch_buf(ctx, "covis", 4, &dc);
+  if (rc) return rc;
+  launch_covisibility(d0, d1, a->w, a->h, sigma_w, dc, ctx->stream);
+  rc = check_launch(ctx);
+  if (rc) return rc;
+  unsigned long long hc[4];
+  CK(cudaMemcpyAsync(hc, dc, sizeof(hc), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (counts)
+    for (int i = 0; i < 4; ++i) counts[i] = (long long)hc[i];
+  // covisibility_ratio — src/fusion.cpp:56-66
+  *ratio = 0.0;
+  int e = 0;
+  if (hc[0] == 0 || hc[2] == 0) {
+    e = 1;
+  } else {
+    *ratio = dmin_std((double)hc[1] / (double)hc[0], (double)hc[3] / (double)hc[2]);
+  }
+  if (empty) *empty = e;
+  return RGBID_OK;
+}
+
+int rgbid_correct_inverse_depth(rgbid_ctx* ctx, const double* Wm, int w, int h,
+                                const rgbid_depth_intrinsics* d, const rgbid_intrinsics* K,
+                                int spatial, double* out) {
+  if (!ctx || !Wm || !d || !K || !out) return RGBID_E_ARG;
+  LaunchScope ls(ctx);
+  const size_t N = (size_t)w * h;
+  double* dd;
+  int rc = scratch_buf(ctx, "correct", 2 * N, &dd);
+  if (rc) return rc;
+  CK(cudaMemcpyAsync(dd, Wm, sizeof(double) * N, cudaMemcpyHostToDevice, ctx->stream));
+  launch_correct_depth(dd, w, h, *d, *K, spatial, dd + N, ctx->stream);
+  rc = check_launch(ctx);
+  if (rc) return rc;
+  CK(cudaMemcpyAsync(out, dd + N, sizeof(double) * N, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return RGBID_OK;
+}
+
+int rgbid_forward_register(rgbid_ctx* ctx, const double* WA, int w, int h, const rgbid_pose* T_BA,
+                           const rgbid_intrinsics* KA, const rgbid_intrinsics* KB, double* out) {
+  if (!ctx || !WA || !T_BA || !KA || !KB || !out) return RGBID_E_ARG;
+  LaunchScope ls(ctx);
+  // host setup — src/warping.cpp:22-25
+  const PoseD T = pose_of(T_BA), Tab = pose_inverse(T);
+  const M3 KAm = K_mat(KA->fx, KA->fy, KA->cx, KA->cy), KBm = K_mat(KB->fx, KB->fy, KB->cx, KB->cy);
+  const M3 Rt_BA = m3_mul(m3_mul(KBm, T.R), m3_inv(KAm));
+  const M3 Rt_AB = m3_inv(Rt_BA);
+  const V3 tt = m3_mulv(KAm, Tab.t);
+  RegisterMats r;
+  for (int i = 0; i < 9; ++i) r.Rt_AB[i] = Rt_AB.m[i / 3][i % 3];
+  for (int i = 0; i < 3; ++i) r.tt[i] = tt.v[i];
+  const int iw = std::max(w, KB->width), ih = std::max(h, KB->height);
+  const size_t N = (size_t)w * h, NB = (size_t)KB->width * KB->height;
+  double* d;
+  unsigned long long* inter;
+  int rc = scratch_buf(ctx, "register", N + NB, &d);
+  if (rc) return rc;
+  rc = scratch_buf(ctx, "register_inter", (size_t)iw * ih, &inter);
+  if (rc) return rc;
+  CK(cudaMemcpyAsync(d, WA, sizeof(double) * N, cudaMemcpyHostToDevice, ctx->stream));
+  launch_forward_register(d, w, h, r, inter, iw, ih, KB->width, KB->height, d + N, ctx->stream);
+  rc = check_launch(ctx);
+  if (rc) return rc;
+  CK(cudaMemcpyAsync(out, d + N, sizeof(double) * NB, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return RGBID_OK;
+}
+
+int rgbid_synth_pair_device(rgbid_ctx* ctx, rgbid_frame* a, rgbid_frame* b,
+                            const rgbid_intrinsics* K, uint32_t pair_seed, int variant,
+                            rgbid_pose* T_AB_truth) {
+  if (!ctx || !a || !b || !K) return RGBID_E_ARG;
+  LaunchScope ls(ctx);
+  // Pair geometry: A at a small random pose, B = A * random_pose(seed, 3 mm, 0.02 rad)
+  rgbid_pose pa, pab;
+  rgbid_synth_random_pose(5000u + pair_seed, 0, 0.01, 0.01, &pa);
+  rgbid_synth_random_pose(1000u + pair_seed, 0, 0.003, 0.02, &pab);
+  const PoseD TA = pose_of(&pa), TAB = pose_of(&pab);
+  const PoseD TB = pose_compose(TA, TAB);
+  if (T_AB_truth) pose_to(TAB, T_AB_truth->R, T_AB_truth->t);
+  double n[3] = {0.2, -0.15, 1.0};
+  const double nn = std::sqrt(red3(n[0] * n[0], n[1] * n[1], n[2] * n[2]));
+  for (double& v : n) v /= nn;
+  auto view = [&](const PoseD& T, int noisy, unsigned long long seed) {
+    SynthView v;
+    v.w = a->w;
+    v.h = a->h;
+    v.Kinv = m3_inv(K_mat(K->fx, K->fy, K->cx, K->cy));
+    v.R = T.R;
+    for (int i = 0; i < 3; ++i) {
+      v.t[i] = T.t.v[i];
+      v.n[i] = n[i];
+    }
+    v.d = -2.0;
+    v.tex_scale = a->w / 80.0;
+    v.noise_i = noisy ? 0.005 : 0.0;
+    v.noise_w = noisy ? 0.002 : 0.0;
+    v.seed = seed;
+    v.occluder = 0;
+    return v;
+  };
+  SynthView va = view(TA, variant, 2u * pair_seed + 1), vb = view(TB, variant, 2u * pair_seed + 2);
+  vb.occluder = variant ? 1 : 0;
+  launch_render(va, a->I, a->W, ctx->stream);
+  launch_render(vb, b->I, b->W, ctx->stream);
+  a->pyr_levels = 0;
+  b->pyr_levels = 0;
+  int rc = check_launch(ctx);
+  if (rc) return rc;
+  CK(cudaStreamSynchronize(ctx->stream));
+  return RGBID_OK;
+}
+
+}  // extern "C"

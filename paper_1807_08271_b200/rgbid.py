@@ -1,0 +1,670 @@
+"""Python mirror of the reference's front-end API (namespace ``rgbid``), backed by
+the CUDA library through the C-ABI (include/rgbid_b200.h).
+
+Names, argument meaning and error behaviour follow the reference headers:
+``inc/alignment.hpp`` (align, build_pyramid, filtered_hessian_covariance,
+bilateral_filter, DegenerateAlignmentError), ``inc/warping.hpp``
+(inverse_geometric_warp, forward_register), ``inc/fusion.hpp`` (make_keyframe,
+covisibility_ratio, integrate_frame, FrameBuffer, drain_buffer_step) and
+``inc/camera.hpp`` (Intrinsics, DepthIntrinsics, correct_inverse_depth).
+Images are float64 numpy arrays (row-major, NaN holes).  Every compute call
+runs on the GPU; there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import threading
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from . import abi
+from .abi import dptr
+
+# --------------------------------------------------------------------------- types
+
+
+@dataclass
+class Intrinsics:
+    """inc/camera.hpp:16-41"""
+    fx: float = 0.0
+    fy: float = 0.0
+    cx: float = 0.0
+    cy: float = 0.0
+    k: tuple = (0.0, 0.0, 0.0, 0.0, 0.0)
+    width: int = 0
+    height: int = 0
+
+    def K(self) -> np.ndarray:
+        return np.array([[self.fx, 0, self.cx], [0, self.fy, self.cy], [0, 0, 1.0]])
+
+    def scaled(self, s: float) -> "Intrinsics":
+        return Intrinsics(self.fx * s, self.fy * s, self.cx * s, self.cy * s, tuple(self.k),
+                          int(self.width * s), int(self.height * s))
+
+    def to_c(self) -> abi.Intrinsics_t:
+        c = abi.Intrinsics_t()
+        c.fx, c.fy, c.cx, c.cy = self.fx, self.fy, self.cx, self.cy
+        for i in range(5):
+            c.k[i] = self.k[i]
+        c.width, c.height = int(self.width), int(self.height)
+        return c
+
+    @staticmethod
+    def from_c(c) -> "Intrinsics":
+        return Intrinsics(c.fx, c.fy, c.cx, c.cy, tuple(c.k), c.width, c.height)
+
+
+def simple_intrinsics(w: int = 80, h: int = 60, f: float = 60.0) -> Intrinsics:
+    """tests/synthetic.hpp:13-21"""
+    return Intrinsics(f, f, (w - 1) / 2.0, (h - 1) / 2.0, (0.0,) * 5, w, h)
+
+
+class Pose:
+    """inc/geometry.hpp:22-39: X_A = R X_B + t."""
+
+    __slots__ = ("R", "t")
+
+    def __init__(self, R=None, t=None):
+        self.R = np.eye(3) if R is None else np.array(R, dtype=np.float64).reshape(3, 3)
+        self.t = np.zeros(3) if t is None else np.array(t, dtype=np.float64).reshape(3)
+
+    def __mul__(self, o):
+        if isinstance(o, Pose):
+            return Pose(self.R @ o.R, self.R @ o.t + self.t)
+        return self.R @ np.asarray(o, dtype=np.float64) + self.t
+
+    def inverse(self) -> "Pose":
+        return Pose(self.R.T, -(self.R.T @ self.t))
+
+    def matrix(self) -> np.ndarray:
+        m = np.eye(4)
+        m[:3, :3] = self.R
+        m[:3, 3] = self.t
+        return m
+
+    def to_c(self) -> abi.Pose_t:
+        c = abi.Pose_t()
+        for i in range(9):
+            c.R[i] = float(self.R.reshape(9)[i])
+        for i in range(3):
+            c.t[i] = float(self.t[i])
+        return c
+
+    @staticmethod
+    def from_c(c) -> "Pose":
+        return Pose(np.array(c.R[:]).reshape(3, 3), np.array(c.t[:]))
+
+    def __repr__(self):
+        return f"Pose(R={self.R.tolist()}, t={self.t.tolist()})"
+
+
+def so3_exp(theta) -> np.ndarray:
+    """src/geometry.cpp:15-28 (host-side helper)."""
+    th = np.asarray(theta, dtype=np.float64)
+    angle = float(np.sqrt(th @ th))
+    K = np.array([[0, -th[2], th[1]], [th[2], 0, -th[0]], [-th[1], th[0], 0]])
+    if angle < 1e-4:
+        a, b = 1.0 - angle * angle / 6.0, 0.5 - angle * angle / 24.0
+    else:
+        a, b = np.sin(angle) / angle, (1.0 - np.cos(angle)) / (angle * angle)
+    return np.eye(3) + a * K + b * K @ K
+
+
+def so3_log(R) -> np.ndarray:
+    """src/geometry.cpp:30-54 (host-side helper for tests)."""
+    R = np.asarray(R)
+    c = min(1.0, max(-1.0, (np.trace(R) - 1.0) / 2.0))
+    angle = np.arccos(c)
+    w = np.array([R[2, 1] - R[1, 2], R[0, 2] - R[2, 0], R[1, 0] - R[0, 1]])
+    if angle < 1e-4:
+        return w / 2.0
+    if np.pi - angle < 1e-6:
+        A = (R + np.eye(3)) / 2.0
+        k = int(np.argmax(np.diag(A)))
+        axis = A[:, k] / np.sqrt(A[k, k])
+        axis /= np.linalg.norm(axis)
+        if axis @ w < 0:
+            axis = -axis
+        return angle * axis
+    return angle * w / np.linalg.norm(w)
+
+
+def se3_exp(xi) -> Pose:
+    """Decoupled SE(3) exp, src/geometry.cpp:56."""
+    xi = np.asarray(xi, dtype=np.float64)
+    return Pose(so3_exp(xi[3:]), xi[:3])
+
+
+@dataclass
+class FrameData:
+    """inc/alignment.hpp:14-18"""
+    intensity: np.ndarray
+    inverse_depth: np.ndarray
+
+    def __post_init__(self):
+        self.intensity = np.ascontiguousarray(self.intensity, dtype=np.float64)
+        self.inverse_depth = np.ascontiguousarray(self.inverse_depth, dtype=np.float64)
+
+    @property
+    def width(self) -> int:
+        return self.inverse_depth.shape[1]
+
+    @property
+    def height(self) -> int:
+        return self.inverse_depth.shape[0]
+
+    def copy(self) -> "FrameData":
+        return FrameData(self.intensity.copy(), self.inverse_depth.copy())
+
+
+@dataclass
+class Pyramid:
+    levels: List[FrameData]
+    intrinsics: List[Intrinsics]
+
+
+@dataclass
+class TDistParams:
+    mu: float = 0.0
+    sigma: float = 1.0
+    nu: float = 5.0
+
+
+@dataclass
+class LevelLog:
+    level: int = 0
+    iterations: int = 0
+    final_cost: float = 0.0
+
+
+@dataclass
+class AlignmentConfig:
+    """inc/alignment.hpp:88-96"""
+    levels: int = 3
+    iterations: List[int] = field(default_factory=lambda: [10, 5, 4])
+    convergence_eps: float = 1e-6
+    lambda_n_min: float = 0.1
+    bilateral_sigma_space: float = 2.0
+    bilateral_sigma_intensity: float = 0.05
+    bilateral_sigma_depth: float = 0.02
+
+    def to_c(self) -> abi.AlignConfig_t:
+        c = abi.AlignConfig_t()
+        c.levels = self.levels
+        c.n_iterations = len(self.iterations)
+        for i, v in enumerate(self.iterations[: abi.MAX_LEVELS]):
+            c.iterations[i] = int(v)
+        c.convergence_eps = self.convergence_eps
+        c.lambda_n_min = self.lambda_n_min
+        c.bilateral_sigma_space = self.bilateral_sigma_space
+        c.bilateral_sigma_intensity = self.bilateral_sigma_intensity
+        c.bilateral_sigma_depth = self.bilateral_sigma_depth
+        return c
+
+
+@dataclass
+class AlignmentResult:
+    """inc/alignment.hpp:72-80"""
+    T_AB: Pose
+    cov: np.ndarray
+    converged: bool
+    cov_degenerate: bool
+    level_log: List[LevelLog]
+    tdist_intensity: TDistParams
+    tdist_depth: TDistParams
+    total_iterations: int = 0
+
+    @staticmethod
+    def from_c(r) -> "AlignmentResult":
+        return AlignmentResult(
+            Pose.from_c(r.T_AB), np.array(r.cov[:]).reshape(6, 6), bool(r.converged),
+            bool(r.cov_degenerate),
+            [LevelLog(l.level, l.iterations, l.final_cost) for l in r.level_log[: r.n_levels]],
+            TDistParams(r.tdist_intensity.mu, r.tdist_intensity.sigma, r.tdist_intensity.nu),
+            TDistParams(r.tdist_depth.mu, r.tdist_depth.sigma, r.tdist_depth.nu),
+            r.total_iterations)
+
+
+class DegenerateAlignmentError(RuntimeError):
+    """inc/alignment.hpp:82-86"""
+
+    def __init__(self, spectrum):
+        super().__init__("degenerate alignment: under-constrained scene")
+        self.spectrum = np.asarray(spectrum, dtype=np.float64)
+
+
+class CudaError(RuntimeError):
+    pass
+
+
+def t_weight(x: float, nu: float) -> float:
+    """inc/alignment.hpp:35"""
+    return (nu + 1.0) / (nu + x * x)
+
+
+# --------------------------------------------------------------------------- context
+
+
+class Context:
+    """One rgbid_ctx (CUDA stream + workspaces) — one per host thread, like the
+    reference's two-thread front-end/back-end model."""
+
+    def __init__(self, device: int = 0):
+        self.lib = abi.lib()
+        self.h = C.c_void_p()
+        rc = self.lib.rgbid_ctx_create(device, C.byref(self.h))
+        if rc != abi.OK:
+            raise CudaError(f"rgbid_ctx_create(device={device}) failed: "
+                            f"{self.lib.rgbid_status_string(rc).decode()} (a B200 / sm_100 GPU is required)")
+        self.device = device
+
+    def check(self, rc: int, what: str):
+        if rc == abi.OK:
+            return
+        msg = self.lib.rgbid_ctx_last_error(self.h).decode()
+        if rc == abi.E_ARG:
+            raise ValueError(f"{what}: invalid argument")
+        raise CudaError(f"{what}: {self.lib.rgbid_status_string(rc).decode()} {msg}")
+
+    @property
+    def kernel_launches(self) -> int:
+        return int(self.lib.rgbid_ctx_kernel_launches(self.h))
+
+    def synchronize(self):
+        self.check(self.lib.rgbid_ctx_synchronize(self.h), "synchronize")
+
+    def close(self):
+        if self.h:
+            self.lib.rgbid_ctx_destroy(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_tls = threading.local()
+
+
+def default_context() -> Context:
+    ctx = getattr(_tls, "ctx", None)
+    if ctx is None:
+        ctx = Context(0)
+        _tls.ctx = ctx
+    return ctx
+
+
+class DeviceFrame:
+    """A FrameData resident in HBM (rgbid_frame); its pyramid is cached."""
+
+    def __init__(self, width: int, height: int, ctx: Optional[Context] = None):
+        self.ctx = ctx or default_context()
+        self.h = C.c_void_p()
+        self.width, self.height = width, height
+        self.ctx.check(self.ctx.lib.rgbid_frame_create(self.ctx.h, width, height, C.byref(self.h)),
+                       "frame_create")
+
+    @staticmethod
+    def from_frame(f: FrameData, ctx: Optional[Context] = None) -> "DeviceFrame":
+        d = DeviceFrame(f.width, f.height, ctx)
+        d.upload(f)
+        return d
+
+    def upload(self, f: FrameData):
+        self.ctx.check(self.ctx.lib.rgbid_frame_upload(self.ctx.h, self.h, dptr(f.intensity),
+                                                       dptr(f.inverse_depth)), "frame_upload")
+
+    def download(self) -> FrameData:
+        I = np.empty((self.height, self.width))
+        W = np.empty((self.height, self.width))
+        self.ctx.check(self.ctx.lib.rgbid_frame_download(self.ctx.h, self.h, dptr(I), dptr(W)),
+                       "frame_download")
+        return FrameData(I, W)
+
+    def device_ptrs(self):
+        I, W = abi.DP(), abi.DP()
+        self.ctx.lib.rgbid_frame_device_ptrs(self.h, C.byref(I), C.byref(W))
+        return C.cast(I, C.c_void_p).value, C.cast(W, C.c_void_p).value
+
+    def close(self):
+        if self.h:
+            self.ctx.lib.rgbid_frame_destroy(self.ctx.h, self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+# --------------------------------------------------------------------------- entry points
+
+
+def build_pyramid(frame: FrameData, K: Intrinsics, levels: int,
+                  ctx: Optional[Context] = None) -> Pyramid:
+    """src/alignment.cpp:9-30"""
+    ctx = ctx or default_context()
+    h, w = frame.inverse_depth.shape
+    sizes = [(h, w)]
+    for _ in range(1, levels):
+        sizes.append((sizes[-1][0] // 2, sizes[-1][1] // 2))
+    oI = [np.empty(s) for s in sizes]
+    oW = [np.empty(s) for s in sizes]
+    Ks = (abi.Intrinsics_t * levels)()
+    ctx.check(ctx.lib.rgbid_build_pyramid(ctx.h, dptr(frame.intensity), dptr(frame.inverse_depth),
+                                          w, h, C.byref(K.to_c()), levels, abi.dptr_array(oI),
+                                          abi.dptr_array(oW), Ks), "build_pyramid")
+    return Pyramid([FrameData(a, b) for a, b in zip(oI, oW)], [Intrinsics.from_c(k) for k in Ks])
+
+
+@dataclass
+class WarpedFrame:
+    """inc/warping.hpp:27-36"""
+    intensity: np.ndarray
+    inverse_depth: np.ndarray
+    map_x: np.ndarray
+    map_y: np.ndarray
+
+
+def inverse_geometric_warp(I_B, W_B, W_A, T_AB: Pose, K: Intrinsics,
+                           ctx: Optional[Context] = None) -> WarpedFrame:
+    """src/warping.cpp:76-114"""
+    ctx = ctx or default_context()
+    I_B = np.ascontiguousarray(I_B, dtype=np.float64)
+    W_B = np.ascontiguousarray(W_B, dtype=np.float64)
+    W_A = np.ascontiguousarray(W_A, dtype=np.float64)
+    hb, wb = W_B.shape
+    h, w = W_A.shape
+    out = [np.empty((h, w)) for _ in range(4)]
+    ctx.check(ctx.lib.rgbid_inverse_geometric_warp(ctx.h, dptr(I_B), dptr(W_B), wb, hb, dptr(W_A),
+                                                   w, h, C.byref(T_AB.to_c()), C.byref(K.to_c()),
+                                                   *[dptr(o) for o in out]),
+              "inverse_geometric_warp")
+    return WarpedFrame(*out)
+
+
+def _result_or_raise(r) -> AlignmentResult:
+    if r.status == abi.E_DEGENERATE:
+        raise DegenerateAlignmentError(list(r.spectrum))
+    return AlignmentResult.from_c(r)
+
+
+def align(frame_a, frame_b, K: Intrinsics, init: Optional[Pose] = None,
+          config: Optional[AlignmentConfig] = None, ctx: Optional[Context] = None,
+          trace: bool = False):
+    """src/alignment.cpp:367-409.  frame_a/frame_b: FrameData or DeviceFrame.
+    Raises DegenerateAlignmentError like the reference.  With trace=True also
+    returns the per-iteration records (rgbid_iter_trace)."""
+    ctx = ctx or default_context()
+    cfg = (config or AlignmentConfig()).to_c()
+    res = abi.AlignResult_t()
+    init_c = (init or Pose()).to_c()
+    if isinstance(frame_a, DeviceFrame):
+        rc = ctx.lib.rgbid_align(ctx.h, frame_a.h, frame_b.h, C.byref(K.to_c()), C.byref(init_c),
+                                 C.byref(cfg), C.byref(res))
+    else:
+        h, w = frame_a.inverse_depth.shape
+        rc = ctx.lib.rgbid_align_host(ctx.h, dptr(frame_a.intensity), dptr(frame_a.inverse_depth),
+                                      dptr(frame_b.intensity), dptr(frame_b.inverse_depth), w, h,
+                                      C.byref(K.to_c()), C.byref(init_c), C.byref(cfg),
+                                      C.byref(res))
+    if rc not in (abi.OK, abi.E_DEGENERATE):
+        ctx.check(rc, "align")
+    if trace:
+        tr = (abi.IterTrace_t * 64)()
+        n = C.c_int(0)
+        ctx.lib.rgbid_last_align_trace(ctx.h, tr, 64, C.byref(n))
+        records = list(tr)[: n.value]
+        if res.status == abi.E_DEGENERATE:
+            return None, records, list(res.spectrum)
+        return AlignmentResult.from_c(res), records
+    return _result_or_raise(res)
+
+
+def align_batch(frames_a: Sequence[DeviceFrame], frames_b: Sequence[DeviceFrame], K: Intrinsics,
+                inits: Optional[Sequence[Pose]] = None, config: Optional[AlignmentConfig] = None,
+                ctx: Optional[Context] = None):
+    """Batched independent alignments (config 5).  Returns the raw C results
+    (status per pair; see _result_or_raise)."""
+    ctx = ctx or default_context()
+    n = len(frames_a)
+    A = (C.c_void_p * n)(*[f.h.value for f in frames_a])
+    B = (C.c_void_p * n)(*[f.h.value for f in frames_b])
+    ini = (abi.Pose_t * n)(*[p.to_c() for p in inits]) if inits is not None else None
+    res = (abi.AlignResult_t * n)()
+    cfg = (config or AlignmentConfig()).to_c()
+    ctx.check(ctx.lib.rgbid_align_batch(ctx.h, n, A, B, C.byref(K.to_c()), ini, C.byref(cfg), res),
+              "align_batch")
+    return list(res)
+
+
+def filtered_hessian_covariance(frame_a, frame_b, K: Intrinsics, T_AB: Pose,
+                                config: Optional[AlignmentConfig] = None,
+                                ctx: Optional[Context] = None):
+    """src/alignment.cpp:411-436 -> (cov 6x6, degenerate)"""
+    ctx = ctx or default_context()
+    fa = frame_a if isinstance(frame_a, DeviceFrame) else DeviceFrame.from_frame(frame_a, ctx)
+    fb = frame_b if isinstance(frame_b, DeviceFrame) else DeviceFrame.from_frame(frame_b, ctx)
+    cov = np.empty(36)
+    deg = C.c_int(0)
+    ctx.check(ctx.lib.rgbid_filtered_hessian_covariance(
+        ctx.h, fa.h, fb.h, C.byref(K.to_c()), C.byref(T_AB.to_c()),
+        C.byref((config or AlignmentConfig()).to_c()), dptr(cov), C.byref(deg)),
+        "filtered_hessian_covariance")
+    return cov.reshape(6, 6), bool(deg.value)
+
+
+def bilateral_filter(img, sigma_space: float, sigma_range: float,
+                     ctx: Optional[Context] = None) -> np.ndarray:
+    """src/alignment.cpp:252-277"""
+    ctx = ctx or default_context()
+    img = np.ascontiguousarray(img, dtype=np.float64)
+    h, w = img.shape
+    out = np.empty_like(img)
+    ctx.check(ctx.lib.rgbid_bilateral_filter(ctx.h, dptr(img), w, h, sigma_space, sigma_range,
+                                             dptr(out)), "bilateral_filter")
+    return out
+
+
+# --------------------------------------------------------------------------- fusion
+
+
+@dataclass
+class Keyframe:
+    """inc/fusion.hpp:15-22"""
+    intensity: np.ndarray
+    inverse_depth: np.ndarray
+    weight: np.ndarray
+    T_W_kf: Pose
+    id: int = 0
+    timestamp: float = 0.0
+
+
+def make_keyframe(frame: FrameData, T_W_kf: Pose, id: int, timestamp: float) -> Keyframe:
+    """src/fusion.cpp:7-16 (C = 1 everywhere, holes included)"""
+    return Keyframe(frame.intensity.copy(), frame.inverse_depth.copy(),
+                    np.ones_like(frame.inverse_depth), T_W_kf, id, timestamp)
+
+
+@dataclass
+class CovisibilityResult:
+    ratio: float = 0.0
+    empty_frame: bool = False
+    counts: tuple = ()
+
+
+def covisibility_ratio(frame_a, frame_b, T_BA: Pose, K: Intrinsics, sigma_w: float,
+                       ctx: Optional[Context] = None) -> CovisibilityResult:
+    """src/fusion.cpp:52-66"""
+    ctx = ctx or default_context()
+    fa = frame_a if isinstance(frame_a, DeviceFrame) else DeviceFrame.from_frame(frame_a, ctx)
+    fb = frame_b if isinstance(frame_b, DeviceFrame) else DeviceFrame.from_frame(frame_b, ctx)
+    ratio = C.c_double(0.0)
+    empty = C.c_int(0)
+    counts = (C.c_longlong * 4)()
+    ctx.check(ctx.lib.rgbid_covisibility_ratio(ctx.h, fa.h, fb.h, C.byref(T_BA.to_c()),
+                                               C.byref(K.to_c()), sigma_w, C.byref(ratio),
+                                               C.byref(empty), counts), "covisibility_ratio")
+    return CovisibilityResult(ratio.value, bool(empty.value), tuple(counts))
+
+
+def should_switch_keyframe(ratio: float, threshold: float = 0.7) -> bool:
+    return ratio < threshold
+
+
+def should_switch_reference(ratio: float, threshold: float = 0.9) -> bool:
+    return ratio < threshold
+
+
+def integrate_frame(kf: Keyframe, frame: FrameData, T_kf_frame: Pose, K: Intrinsics,
+                    sigma_w: float, ctx: Optional[Context] = None) -> None:
+    """src/fusion.cpp:68-95 — updates kf.inverse_depth and kf.weight in place."""
+    ctx = ctx or default_context()
+    h, w = kf.inverse_depth.shape
+    for name in ("inverse_depth", "weight"):
+        a = getattr(kf, name)
+        if not (a.flags["C_CONTIGUOUS"] and a.dtype == np.float64):
+            setattr(kf, name, np.ascontiguousarray(a, dtype=np.float64))
+    ctx.check(ctx.lib.rgbid_integrate_frame(ctx.h, dptr(kf.inverse_depth), dptr(kf.weight),
+                                            dptr(frame.intensity), dptr(frame.inverse_depth), w, h,
+                                            C.byref(T_kf_frame.to_c()), C.byref(K.to_c()),
+                                            sigma_w), "integrate_frame")
+
+
+@dataclass
+class BufferedFrame:
+    frame: FrameData
+    T_W_frame: Pose
+    timestamp: float = 0.0
+
+
+class FrameBuffer:
+    """inc/fusion.hpp:56-74, src/fusion.cpp:97-111 (host bookkeeping)."""
+
+    def __init__(self, capacity: int = 30):
+        self.capacity = capacity
+        self.frames: List[BufferedFrame] = []
+
+    def push(self, f: BufferedFrame):
+        if len(self.frames) >= self.capacity:
+            self.frames.pop(0)
+        self.frames.append(f)
+
+    def empty(self) -> bool:
+        return not self.frames
+
+    def size(self) -> int:
+        return len(self.frames)
+
+    def clear(self):
+        self.frames.clear()
+
+    def pop_closest(self, timestamp: float) -> Optional[BufferedFrame]:
+        if not self.frames:
+            return None
+        best, best_dt = 0, abs(self.frames[0].timestamp - timestamp)
+        for i in range(1, len(self.frames)):
+            dt = abs(self.frames[i].timestamp - timestamp)
+            if dt < best_dt:
+                best, best_dt = i, dt
+        return self.frames.pop(best)
+
+
+def drain_buffer_step(kf: Keyframe, buffer: FrameBuffer, K: Intrinsics, sigma_w: float,
+                      ctx: Optional[Context] = None) -> None:
+    """src/fusion.cpp:113-118"""
+    f = buffer.pop_closest(kf.timestamp)
+    if f is None:
+        return
+    integrate_frame(kf, f.frame, kf.T_W_kf.inverse() * f.T_W_frame, K, sigma_w, ctx)
+
+
+# --------------------------------------------------------------------------- depth camera
+
+
+@dataclass
+class DepthIntrinsics:
+    """inc/camera.hpp:45-51"""
+    beta0: float = 0.0
+    beta1: float = 1.0
+    q0: tuple = (0.0,) * 9
+    q1: tuple = (1.0,) + (0.0,) * 8
+    p0: tuple = (4.0, 4.0)
+
+    def to_c(self) -> abi.DepthIntrinsics_t:
+        c = abi.DepthIntrinsics_t()
+        c.beta0, c.beta1 = self.beta0, self.beta1
+        for i in range(9):
+            c.q0[i], c.q1[i] = self.q0[i], self.q1[i]
+        c.p0[0], c.p0[1] = self.p0
+        return c
+
+
+def correct_inverse_depth(W_m, dintr: DepthIntrinsics, intr: Intrinsics, spatial: bool,
+                          ctx: Optional[Context] = None) -> np.ndarray:
+    """src/camera.cpp:62-81"""
+    ctx = ctx or default_context()
+    W_m = np.ascontiguousarray(W_m, dtype=np.float64)
+    h, w = W_m.shape
+    out = np.empty_like(W_m)
+    ctx.check(ctx.lib.rgbid_correct_inverse_depth(ctx.h, dptr(W_m), w, h, C.byref(dintr.to_c()),
+                                                  C.byref(intr.to_c()), int(spatial), dptr(out)),
+              "correct_inverse_depth")
+    return out
+
+
+def forward_register(W_A, T_BA: Pose, K_A: Intrinsics, K_B: Intrinsics,
+                     ctx: Optional[Context] = None) -> np.ndarray:
+    """src/warping.cpp:20-74"""
+    ctx = ctx or default_context()
+    W_A = np.ascontiguousarray(W_A, dtype=np.float64)
+    h, w = W_A.shape
+    out = np.empty((K_B.height, K_B.width))
+    ctx.check(ctx.lib.rgbid_forward_register(ctx.h, dptr(W_A), w, h, C.byref(T_BA.to_c()),
+                                             C.byref(K_A.to_c()), C.byref(K_B.to_c()), dptr(out)),
+              "forward_register")
+    return out
+
+
+# --------------------------------------------------------------------------- synthetic inputs
+
+
+def render_plane(K: Intrinsics, T_WC: Pose, n=(0.0, 0.0, 1.0), d: float = -2.0,
+                 tex_scale: float = 1.0) -> FrameData:
+    """tests/synthetic.hpp:31-50 (bit-identical to the reference fixture at tex_scale=1)."""
+    L = abi.lib()
+    I = np.empty((K.height, K.width))
+    W = np.empty((K.height, K.width))
+    nn = np.ascontiguousarray(n, dtype=np.float64)
+    L.rgbid_synth_render_plane(C.byref(K.to_c()), C.byref(T_WC.to_c()), dptr(nn), d, tex_scale,
+                               dptr(I), dptr(W))
+    return FrameData(I, W)
+
+
+def random_pose(seed: int, t_scale: float = 1.0, angle_scale: float = 1.0, skip: int = 0) -> Pose:
+    """random_pose(std::mt19937(seed)) of tests/synthetic.hpp:52-59 (after `skip` draws)."""
+    out = abi.Pose_t()
+    abi.lib().rgbid_synth_random_pose(seed, skip, t_scale, angle_scale, C.byref(out))
+    return Pose.from_c(out)
+
+
+def add_noise(frame: FrameData, seed: int, sigma_i: float, sigma_w: float) -> FrameData:
+    f = frame.copy()
+    h, w = f.inverse_depth.shape
+    abi.lib().rgbid_synth_add_noise(dptr(f.intensity), dptr(f.inverse_depth), w, h, seed, sigma_i,
+                                    sigma_w)
+    return f
+
+
+def synth_pair_device(a: DeviceFrame, b: DeviceFrame, K: Intrinsics, pair_seed: int,
+                      variant: int) -> Pose:
+    """Device-rendered benchmark pair; returns the ground-truth T_AB."""
+    T = abi.Pose_t()
+    a.ctx.check(a.ctx.lib.rgbid_synth_pair_device(a.ctx.h, a.h, b.h, C.byref(K.to_c()), pair_seed,
+                                                  variant, C.byref(T)), "synth_pair_device")
+    return Pose.from_c(T)
