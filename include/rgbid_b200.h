@@ -129,6 +129,14 @@ long long rgbid_ctx_kernel_launches(rgbid_ctx* ctx);
 int rgbid_ctx_synchronize(rgbid_ctx* ctx);
 /* stream used by ctx (cudaStream_t, as void*) */
 void* rgbid_ctx_stream(rgbid_ctx* ctx);
+/* Per-kernel CUDA-event timing of every library launch (graphs are bypassed
+ * while enabled).  kernel_stats writes {"name": [launches, total_ms], ...} JSON
+ * and returns the buffer size needed. */
+int rgbid_ctx_set_profiling(rgbid_ctx* ctx, int enable);
+int rgbid_ctx_reset_stats(rgbid_ctx* ctx);
+int rgbid_ctx_kernel_stats(rgbid_ctx* ctx, char* buf, int cap);
+/* bytes this ctx copied host->device / device->host since the last reset */
+int rgbid_ctx_transfer_bytes(rgbid_ctx* ctx, long long* h2d, long long* d2h);
 
 /* ---- device frames ------------------------------------------------------ */
 /* FrameData (inc/alignment.hpp:14-18) uploaded once; I may be NULL (depth only). */
@@ -138,6 +146,8 @@ int rgbid_frame_download(rgbid_ctx* ctx, const rgbid_frame* f, double* I, double
 /* device pointers of the frame's level-0 maps (for zero-copy producers) */
 int rgbid_frame_device_ptrs(rgbid_frame* f, double** I_dev, double** W_dev);
 int rgbid_frame_destroy(rgbid_ctx* ctx, rgbid_frame* f);
+/* mark the cached pyramid stale (the producer wrote new maps in place) */
+int rgbid_frame_invalidate(rgbid_frame* f);
 
 /* ---- hot-path entry points (reference signatures noted) ---------------- */
 

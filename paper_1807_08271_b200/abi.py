@@ -89,11 +89,16 @@ EXPORTS = [
     ("rgbid_ctx_kernel_launches", C.c_longlong, [VP]),
     ("rgbid_ctx_synchronize", C.c_int, [VP]),
     ("rgbid_ctx_stream", VP, [VP]),
+    ("rgbid_ctx_set_profiling", C.c_int, [VP, C.c_int]),
+    ("rgbid_ctx_reset_stats", C.c_int, [VP]),
+    ("rgbid_ctx_kernel_stats", C.c_int, [VP, C.c_char_p, C.c_int]),
+    ("rgbid_ctx_transfer_bytes", C.c_int, [VP, C.POINTER(C.c_longlong), C.POINTER(C.c_longlong)]),
     ("rgbid_frame_create", C.c_int, [VP, C.c_int, C.c_int, C.POINTER(VP)]),
     ("rgbid_frame_upload", C.c_int, [VP, VP, DP, DP]),
     ("rgbid_frame_download", C.c_int, [VP, VP, DP, DP]),
     ("rgbid_frame_device_ptrs", C.c_int, [VP, C.POINTER(DP), C.POINTER(DP)]),
     ("rgbid_frame_destroy", C.c_int, [VP, VP]),
+    ("rgbid_frame_invalidate", C.c_int, [VP]),
     ("rgbid_build_pyramid", C.c_int, [VP, DP, DP, C.c_int, C.c_int, C.POINTER(Intrinsics_t),
                                       C.c_int, C.POINTER(DP), C.POINTER(DP),
                                       C.POINTER(Intrinsics_t)]),

@@ -25,6 +25,31 @@
 namespace rgbid_b200 {
 
 thread_local long long* g_launch_counter = nullptr;
+thread_local Profiler* g_profiler = nullptr;
+
+cudaEvent_t Profiler::get() {
+  if (!pool.empty()) {
+    cudaEvent_t e = pool.back();
+    pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+KScope::KScope(const char* n, cudaStream_t s) : name(n), stream(s) {
+  if (g_launch_counter) ++*g_launch_counter;
+  if (g_profiler && g_profiler->enabled) {
+    cudaEvent_t start = g_profiler->get();
+    stop = g_profiler->get();
+    cudaEventRecord(start, s);
+    g_profiler->pending.push_back(KernelRecord{n, start, stop});
+  }
+}
+KScope::~KScope() {
+  if (stop) cudaEventRecord(stop, stream);
+}
 
 __device__ __forceinline__ bool valid(double v) { return isfinite(v); }
 
@@ -251,6 +276,7 @@ __global__ void __launch_bounds__(kTPB) k_warp_residuals(const SlotIO* __restric
 }
 
 void launch_warp_residuals(const AlignLaunch& a, const LevelInfo& li, int phase, cudaStream_t s) {
+  KScope ks_("warp_residuals", s);
   dim3 grid(li.ntiles, a.nslots);
   switch (li.level) {
     case 0: k_warp_residuals<0><<<grid, kTPB, 0, s>>>(a.io, a.st, li, a.w0, a.h0, phase); break;
@@ -261,7 +287,6 @@ void launch_warp_residuals(const AlignLaunch& a, const LevelInfo& li, int phase,
     case 5: k_warp_residuals<5><<<grid, kTPB, 0, s>>>(a.io, a.st, li, a.w0, a.h0, phase); break;
     default: return;
   }
-  count_launch();
 }
 
 // ---------------------------------------------------------------------------
@@ -506,8 +531,8 @@ __global__ void __launch_bounds__(kTdistThreads) k_tdist(const SlotIO* __restric
 
 void launch_tdist(const AlignLaunch& a, const LevelInfo& li, int phase, cudaStream_t s) {
   const int smem = tdist_smem_bytes(li.ntiles);  // <= 200 KB for ntiles <= 11000
+  KScope ks_("tdist", s);
   k_tdist<<<dim3(2, a.nslots), kTdistThreads, smem, s>>>(a.io, a.st, li, phase);
-  count_launch();
 }
 
 // ---------------------------------------------------------------------------
@@ -656,8 +681,8 @@ __global__ void __launch_bounds__(kTPB) k_normal_eq(const SlotIO* __restrict__ i
 }
 
 void launch_normal_equations(const AlignLaunch& a, const LevelInfo& li, int phase, cudaStream_t s) {
+  KScope ks_("normal_eq", s);
   k_normal_eq<<<dim3(li.ntiles3, a.nslots), kTPB, 0, s>>>(a.io, a.st, li, phase, a.lambda_n_min);
-  count_launch();
 }
 
 // fixed-order reduction of the per-tile partials into H (full, mirrored), b, cost
@@ -778,14 +803,14 @@ __global__ void __launch_bounds__(kTPB) k_covariance(const SlotIO* __restrict__ 
 }
 
 void launch_covariance(const AlignLaunch& a, const LevelInfo& li, cudaStream_t s) {
+  KScope ks_("covariance", s);
   k_covariance<<<a.nslots, kTPB, 0, s>>>(a.io, a.st, li.ntiles3);
-  count_launch();
 }
 
 void launch_solve(const AlignLaunch& a, const LevelInfo& li, const LevelInfo& li0, cudaStream_t s) {
+  KScope ks_("solve", s);
   k_solve<<<a.nslots, kTPB, 0, s>>>(a.io, a.st, a.trace, li, a.w0, a.h0, li0.fx, li0.fy, li0.cx,
                                     li0.cy, a.eps);
-  count_launch();
 }
 
 // ---------------------------------------------------------------------------
@@ -805,8 +830,8 @@ void launch_downsample2(const double* I, const double* W, int w, int h, double* 
                         cudaStream_t s) {
   const int n = (w / 2) * (h / 2);
   if (n <= 0) return;
+  KScope ks_("pyramid_downsample2", s);
   k_downsample2<<<(n + 255) / 256, 256, 0, s>>>(I, W, w, h, oI, oW);
-  count_launch();
 }
 
 // bilateral_filter — src/alignment.cpp:252-277
@@ -839,8 +864,8 @@ __global__ void k_bilateral(const double* __restrict__ img, int w, int h, double
 void launch_bilateral(const double* img, int w, int h, double ss, double sr, double* out,
                       cudaStream_t s) {
   const double inv2ss = 1.0 / (2.0 * ss * ss), inv2sr = 1.0 / (2.0 * sr * sr);
+  KScope ks_("bilateral", s);
   k_bilateral<<<(w * h + 255) / 256, 256, 0, s>>>(img, w, h, inv2ss, inv2sr, out);
-  count_launch();
 }
 
 // both filtered maps of every active slot (covariance pass input)
@@ -861,9 +886,9 @@ void launch_bilateral_pair(const AlignLaunch& a, double ss, double sr_i, double 
   const double inv2ss = 1.0 / (2.0 * ss * ss);
   const double ii = 1.0 / (2.0 * sr_i * sr_i), iw = 1.0 / (2.0 * sr_w * sr_w);
   const int n = a.w0 * a.h0;
+  KScope ks_("bilateral_slots", s);
   k_bilateral_slots<<<dim3((n + 255) / 256, a.nslots), 256, 0, s>>>(a.io, a.st, a.w0, a.h0,
                                                                      inv2ss, ii, iw);
-  count_launch();
 }
 
 // inverse_geometric_warp producing all four WarpedFrame maps (drop-in + tests)
@@ -884,8 +909,8 @@ __global__ void k_warp_maps(const double* __restrict__ IB, const double* __restr
 void launch_warp_maps(const double* IB, const double* WB, int wb, int hb, const double* WA, int w,
                       int h, const WarpMats& m, double* oI, double* oW, double* omx, double* omy,
                       cudaStream_t s) {
+  KScope ks_("warp_maps", s);
   k_warp_maps<<<(w * h + 255) / 256, 256, 0, s>>>(IB, WB, wb, hb, WA, w, h, m, oI, oW, omx, omy);
-  count_launch();
 }
 
 }  // namespace rgbid_b200

@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <vector>
 
 #include "hd_math.cuh"
 
@@ -103,10 +104,27 @@ void launch_warp_maps(const double* IB, const double* WB, int wb, int hb, const 
 int tdist_smem_bytes(int ntiles);
 int init_kernel_attributes();
 
-// per-launch counter (all library kernels go through launchers that bump it)
+// Launch accounting + optional per-kernel CUDA-event timing.  Every library
+// kernel launch is wrapped in a KScope (launchers below); the owning ctx routes
+// the counters through these thread-locals for the duration of an API call.
+struct KernelRecord {
+  const char* name;
+  cudaEvent_t start, stop;
+};
+struct Profiler {
+  bool enabled = false;
+  std::vector<KernelRecord> pending;  // events recorded, not yet read back
+  std::vector<cudaEvent_t> pool;
+  cudaEvent_t get();
+};
 extern thread_local long long* g_launch_counter;
-inline void count_launch() {
-  if (g_launch_counter) ++*g_launch_counter;
-}
+extern thread_local Profiler* g_profiler;
+struct KScope {
+  KScope(const char* name, cudaStream_t s);
+  ~KScope();
+  const char* name;
+  cudaStream_t stream;
+  cudaEvent_t stop = nullptr;
+};
 
 }  // namespace rgbid_b200

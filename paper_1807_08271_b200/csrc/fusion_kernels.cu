@@ -78,8 +78,8 @@ __global__ void __launch_bounds__(256) k_integrate(const FuseFrame* __restrict__
 
 void launch_integrate(const FuseFrame* frames_dev, int k, double* kfW, double* kfC, int w, int h,
                       double sigma_w, cudaStream_t s) {
+  KScope ks_("integrate", s);
   k_integrate<<<(w * h + 255) / 256, 256, 0, s>>>(frames_dev, k, kfW, kfC, w, h, sigma_w);
-  count_launch();
 }
 
 // ---------------------------------------------------------------------------
@@ -136,9 +136,9 @@ __global__ void __launch_bounds__(256) k_covisibility(CovisDir d0, CovisDir d1, 
 void launch_covisibility(const CovisDir& d0, const CovisDir& d1, int w, int h, double sigma_w,
                          unsigned long long* counts_dev, cudaStream_t s) {
   cudaMemsetAsync(counts_dev, 0, 4 * sizeof(unsigned long long), s);
+  KScope ks_("covisibility", s);
   k_covisibility<<<dim3((w * h + 255) / 256, 2), 256, 0, s>>>(d0, d1, w, h, 3.0 * sigma_w,
                                                               counts_dev);
-  count_launch();
 }
 
 // ---------------------------------------------------------------------------
@@ -175,9 +175,9 @@ __global__ void k_correct_depth(const double* __restrict__ Wm, int w, int h,
 
 void launch_correct_depth(const double* Wm, int w, int h, const rgbid_depth_intrinsics& d,
                           const rgbid_intrinsics& K, int spatial, double* out, cudaStream_t s) {
+  KScope ks_("correct_depth", s);
   k_correct_depth<<<(w * h + 255) / 256, 256, 0, s>>>(Wm, w, h, d, K.fx, K.fy, K.cx, K.cy, spatial,
                                                       out);
-  count_launch();
 }
 
 // ---------------------------------------------------------------------------
@@ -237,10 +237,12 @@ void launch_forward_register(const double* WA, int w, int h, const RegisterMats&
                              unsigned long long* inter, int iw, int ih, int wb, int hb,
                              double* out, cudaStream_t s) {
   cudaMemsetAsync(inter, 0, sizeof(unsigned long long) * (size_t)iw * ih, s);
-  k_splat<<<(w * h + 255) / 256, 256, 0, s>>>(WA, w, h, r, inter, iw, ih);
+  {
+    KScope ks_("register_splat", s);
+    k_splat<<<(w * h + 255) / 256, 256, 0, s>>>(WA, w, h, r, inter, iw, ih);
+  }
+  KScope ks_("register_gather", s);
   k_gather_register<<<(wb * hb + 255) / 256, 256, 0, s>>>(inter, iw, ih, r, wb, hb, out);
-  count_launch();
-  count_launch();
 }
 
 // ---------------------------------------------------------------------------
@@ -292,8 +294,8 @@ __global__ void k_render(SynthView v, double* __restrict__ I, double* __restrict
 }
 
 void launch_render(const SynthView& v, double* I, double* W, cudaStream_t s) {
+  KScope ks_("synth_render", s);
   k_render<<<(v.w * v.h + 255) / 256, 256, 0, s>>>(v, I, W);
-  count_launch();
 }
 
 }  // namespace rgbid_b200

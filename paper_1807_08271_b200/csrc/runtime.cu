@@ -66,14 +66,53 @@ struct rgbid_ctx {
   std::map<std::string, std::pair<void*, size_t>> scratch;
   rgbid_frame* tmpA = nullptr;
   rgbid_frame* tmpB = nullptr;
+  // profiling (per-kernel CUDA-event times) and host<->device byte counters
+  Profiler prof;
+  std::map<std::string, std::pair<long long, double>> kstats;  // name -> (launches, ms)
+  long long h2d_bytes = 0, d2h_bytes = 0;
 };
 
 namespace {
 
-struct LaunchScope {  // routes count_launch() to this ctx
-  explicit LaunchScope(rgbid_ctx* c) { g_launch_counter = &c->launches; }
-  ~LaunchScope() { g_launch_counter = nullptr; }
+// Reads back the per-kernel events recorded while profiling (after a sync).
+void flush_profile(rgbid_ctx* ctx) {
+  for (auto& r : ctx->prof.pending) {
+    float ms = 0.f;
+    if (cudaEventSynchronize(r.stop) == cudaSuccess && cudaEventElapsedTime(&ms, r.start, r.stop) == cudaSuccess) {
+      auto& e = ctx->kstats[r.name];
+      e.first += 1;
+      e.second += ms;
+    }
+    ctx->prof.pool.push_back(r.start);
+    ctx->prof.pool.push_back(r.stop);
+  }
+  ctx->prof.pending.clear();
+}
+
+struct LaunchScope {  // routes launch accounting / profiling to this ctx
+  explicit LaunchScope(rgbid_ctx* c) : ctx(c) {
+    g_launch_counter = &c->launches;
+    g_profiler = &c->prof;
+  }
+  ~LaunchScope() {
+    if (!ctx->prof.pending.empty()) flush_profile(ctx);
+    g_launch_counter = nullptr;
+    g_profiler = nullptr;
+  }
+  rgbid_ctx* ctx;
 };
+
+// host<->device copies on the ctx stream, counted for the e2e byte report
+#define H2D(dst, src, bytes)                                                              \
+  do {                                                                                    \
+    CK(cudaMemcpyAsync((dst), (src), (bytes), cudaMemcpyHostToDevice, ctx->stream)); \
+    ctx->h2d_bytes += (long long)(bytes);                                                 \
+  } while (0)
+#define D2H(dst, src, bytes)                                                              \
+  do {                                                                                    \
+    CK(cudaMemcpyAsync((dst), (src), (bytes), cudaMemcpyDeviceToHost, ctx->stream)); \
+    ctx->d2h_bytes += (long long)(bytes);                                                 \
+  } while (0)
 
 #define CK(expr)                                                        \
   do {                                                                  \
@@ -363,10 +402,8 @@ int run_align_slots(rgbid_ctx* ctx, int n, const rgbid_frame* const* fa,
     s.status = RGBID_OK;
     s.done_level = -1;
   }
-  CK(cudaMemcpyAsync(ctx->d_io, ctx->h_io.data(), sizeof(SlotIO) * nslots, cudaMemcpyHostToDevice,
-                     ctx->stream));
-  CK(cudaMemcpyAsync(ctx->d_st, ctx->h_st_pinned, sizeof(SlotState) * nslots,
-                     cudaMemcpyHostToDevice, ctx->stream));
+  H2D(ctx->d_io, ctx->h_io.data(), sizeof(SlotIO) * nslots);
+  H2D(ctx->d_st, ctx->h_st_pinned, sizeof(SlotState) * nslots);
   AlignLaunch a;
   a.io = ctx->d_io;
   a.st = ctx->d_st;
@@ -395,7 +432,7 @@ int run_align_slots(rgbid_ctx* ctx, int n, const rgbid_frame* const* fa,
                        K.cy};
   std::memcpy(kb.p, p, sizeof(p));
   const std::string key(reinterpret_cast<const char*>(&kb), sizeof(kb));
-  if (ctx->use_graphs) {
+  if (ctx->use_graphs && !ctx->prof.enabled) {
     auto it = ctx->graphs.find(key);
     if (it == ctx->graphs.end()) {
       cudaGraph_t g;
@@ -417,8 +454,7 @@ int run_align_slots(rgbid_ctx* ctx, int n, const rgbid_frame* const* fa,
   }
   rc = check_launch(ctx);
   if (rc) return rc;
-  CK(cudaMemcpyAsync(ctx->h_st_pinned, ctx->d_st, sizeof(SlotState) * nslots,
-                     cudaMemcpyDeviceToHost, ctx->stream));
+  D2H(ctx->h_st_pinned, ctx->d_st, sizeof(SlotState) * nslots);
   CK(cudaStreamSynchronize(ctx->stream));
   if (want_trace) {
     ctx->last_trace.resize(kTraceMax);
@@ -564,10 +600,10 @@ int rgbid_frame_upload(rgbid_ctx* ctx, rgbid_frame* f, const double* I, const do
   if (!ctx || !f || !W) return RGBID_E_ARG;
   const size_t N = (size_t)f->w * f->h;
   if (I)
-    CK(cudaMemcpyAsync(f->I, I, sizeof(double) * N, cudaMemcpyHostToDevice, ctx->stream));
+    H2D(f->I, I, sizeof(double) * N);
   else
     CK(cudaMemsetAsync(f->I, 0xff, sizeof(double) * N, ctx->stream));  // NaN holes
-  CK(cudaMemcpyAsync(f->W, W, sizeof(double) * N, cudaMemcpyHostToDevice, ctx->stream));
+  H2D(f->W, W, sizeof(double) * N);
   f->pyr_levels = 0;
   CK(cudaStreamSynchronize(ctx->stream));
   return RGBID_OK;
@@ -576,8 +612,8 @@ int rgbid_frame_upload(rgbid_ctx* ctx, rgbid_frame* f, const double* I, const do
 int rgbid_frame_download(rgbid_ctx* ctx, const rgbid_frame* f, double* I, double* W) {
   if (!ctx || !f) return RGBID_E_ARG;
   const size_t N = (size_t)f->w * f->h;
-  if (I) CK(cudaMemcpyAsync(I, f->I, sizeof(double) * N, cudaMemcpyDeviceToHost, ctx->stream));
-  if (W) CK(cudaMemcpyAsync(W, f->W, sizeof(double) * N, cudaMemcpyDeviceToHost, ctx->stream));
+  if (I) D2H(I, f->I, sizeof(double) * N);
+  if (W) D2H(W, f->W, sizeof(double) * N);
   CK(cudaStreamSynchronize(ctx->stream));
   return RGBID_OK;
 }
@@ -612,11 +648,9 @@ int rgbid_build_pyramid(rgbid_ctx* ctx, const double* I, const double* W, int w,
   for (int l = 0; l < levels; ++l) {
     const size_t n = (size_t)(w >> l) * (h >> l);
     if (out_I && out_I[l])
-      CK(cudaMemcpyAsync(out_I[l], f->pI[l], sizeof(double) * n, cudaMemcpyDeviceToHost,
-                         ctx->stream));
+      D2H(out_I[l], f->pI[l], sizeof(double) * n);
     if (out_W && out_W[l])
-      CK(cudaMemcpyAsync(out_W[l], f->pW[l], sizeof(double) * n, cudaMemcpyDeviceToHost,
-                         ctx->stream));
+      D2H(out_W[l], f->pW[l], sizeof(double) * n);
     if (K_out) level_intrinsics(*K, l, &K_out[l]);
   }
   CK(cudaStreamSynchronize(ctx->stream));
@@ -637,11 +671,11 @@ int rgbid_inverse_geometric_warp(rgbid_ctx* ctx, const double* I_B, const double
   if (rc) return rc;
   dA = dB + 2 * NB;
   if (I_B)
-    CK(cudaMemcpyAsync(dB, I_B, sizeof(double) * NB, cudaMemcpyHostToDevice, ctx->stream));
+    H2D(dB, I_B, sizeof(double) * NB);
   else
     CK(cudaMemsetAsync(dB, 0xff, sizeof(double) * NB, ctx->stream));
-  CK(cudaMemcpyAsync(dB + NB, W_B, sizeof(double) * NB, cudaMemcpyHostToDevice, ctx->stream));
-  CK(cudaMemcpyAsync(dA, W_A, sizeof(double) * N, cudaMemcpyHostToDevice, ctx->stream));
+  H2D(dB + NB, W_B, sizeof(double) * NB);
+  H2D(dA, W_A, sizeof(double) * N);
   const WarpMats m = warp_mats(pose_of(T_AB), K->fx, K->fy, K->cx, K->cy);
   launch_warp_maps(dB, dB + NB, wb, hb, dA, w, h, m, dO, dO + N, dO + 2 * N, dO + 3 * N,
                    ctx->stream);
@@ -650,8 +684,7 @@ int rgbid_inverse_geometric_warp(rgbid_ctx* ctx, const double* I_B, const double
   double* outs[4] = {oI, oW, omx, omy};
   for (int k = 0; k < 4; ++k)
     if (outs[k])
-      CK(cudaMemcpyAsync(outs[k], dO + k * N, sizeof(double) * N, cudaMemcpyDeviceToHost,
-                         ctx->stream));
+      D2H(outs[k], dO + k * N, sizeof(double) * N);
   CK(cudaStreamSynchronize(ctx->stream));
   return RGBID_OK;
 }
@@ -743,10 +776,10 @@ int rgbid_align_batch_host(rgbid_ctx* ctx, int n, const double* const* IA,
   for (int i0 = 0; i0 < n; i0 += chunk) {
     const int m = std::min(chunk, n - i0);
     for (int i = 0; i < m; ++i) {
-      cudaMemcpyAsync(fa[i]->I, IA[i0 + i], sizeof(double) * N, cudaMemcpyHostToDevice, ctx->stream);
-      cudaMemcpyAsync(fa[i]->W, WA[i0 + i], sizeof(double) * N, cudaMemcpyHostToDevice, ctx->stream);
-      cudaMemcpyAsync(fb[i]->I, IB[i0 + i], sizeof(double) * N, cudaMemcpyHostToDevice, ctx->stream);
-      cudaMemcpyAsync(fb[i]->W, WB[i0 + i], sizeof(double) * N, cudaMemcpyHostToDevice, ctx->stream);
+      H2D(fa[i]->I, IA[i0 + i], sizeof(double) * N);
+      H2D(fa[i]->W, WA[i0 + i], sizeof(double) * N);
+      H2D(fb[i]->I, IB[i0 + i], sizeof(double) * N);
+      H2D(fb[i]->W, WB[i0 + i], sizeof(double) * N);
       fa[i]->pyr_levels = 0;
     }
     const rgbid_align_config c = cfg ? *cfg : default_config();
@@ -786,11 +819,11 @@ int rgbid_bilateral_filter(rgbid_ctx* ctx, const double* img, int w, int h, doub
   double* d;
   int rc = scratch_buf(ctx, "bilateral", 2 * N, &d);
   if (rc) return rc;
-  CK(cudaMemcpyAsync(d, img, sizeof(double) * N, cudaMemcpyHostToDevice, ctx->stream));
+  H2D(d, img, sizeof(double) * N);
   launch_bilateral(d, w, h, ss, sr, d + N, ctx->stream);
   rc = check_launch(ctx);
   if (rc) return rc;
-  CK(cudaMemcpyAsync(out, d + N, sizeof(double) * N, cudaMemcpyDeviceToHost, ctx->stream));
+  D2H(out, d + N, sizeof(double) * N);
   CK(cudaStreamSynchronize(ctx->stream));
   return RGBID_OK;
 }
@@ -808,18 +841,18 @@ int rgbid_integrate_frame(rgbid_ctx* ctx, double* kf_W, double* kf_C, const doub
   FuseFrame* df;
   rc = scratch_buf(ctx, "integrate_frames", 1, &df);
   if (rc) return rc;
-  CK(cudaMemcpyAsync(d, kf_W, sizeof(double) * N, cudaMemcpyHostToDevice, ctx->stream));
-  CK(cudaMemcpyAsync(d + N, kf_C, sizeof(double) * N, cudaMemcpyHostToDevice, ctx->stream));
-  CK(cudaMemcpyAsync(d + 2 * N, frame_W, sizeof(double) * N, cudaMemcpyHostToDevice, ctx->stream));
+  H2D(d, kf_W, sizeof(double) * N);
+  H2D(d + N, kf_C, sizeof(double) * N);
+  H2D(d + 2 * N, frame_W, sizeof(double) * N);
   FuseFrame f;
   f.W = d + 2 * N;
   f.wm = warp_mats(pose_of(T), K->fx, K->fy, K->cx, K->cy);
-  CK(cudaMemcpyAsync(df, &f, sizeof(f), cudaMemcpyHostToDevice, ctx->stream));
+  H2D(df, &f, sizeof(f));
   launch_integrate(df, 1, d, d + N, w, h, sigma_w, ctx->stream);
   rc = check_launch(ctx);
   if (rc) return rc;
-  CK(cudaMemcpyAsync(kf_W, d, sizeof(double) * N, cudaMemcpyDeviceToHost, ctx->stream));
-  CK(cudaMemcpyAsync(kf_C, d + N, sizeof(double) * N, cudaMemcpyDeviceToHost, ctx->stream));
+  D2H(kf_W, d, sizeof(double) * N);
+  D2H(kf_C, d + N, sizeof(double) * N);
   CK(cudaStreamSynchronize(ctx->stream));
   return RGBID_OK;
 }
@@ -839,7 +872,7 @@ int rgbid_integrate_frames(rgbid_ctx* ctx, rgbid_frame* kf, double* kf_C_dev, in
   FuseFrame* df;
   int rc = scratch_buf(ctx, "integrate_frames", k, &df);
   if (rc) return rc;
-  CK(cudaMemcpyAsync(df, hf.data(), sizeof(FuseFrame) * k, cudaMemcpyHostToDevice, ctx->stream));
+  H2D(df, hf.data(), sizeof(FuseFrame) * k);
   launch_integrate(df, k, kf->W, kf_C_dev, kf->w, kf->h, sigma_w, ctx->stream);
   kf->pyr_levels = 0;
   rc = check_launch(ctx);
@@ -874,7 +907,7 @@ int rgbid_covisibility_ratio(rgbid_ctx* ctx, const rgbid_frame* a, const rgbid_f
   rc = check_launch(ctx);
   if (rc) return rc;
   unsigned long long hc[4];
-  CK(cudaMemcpyAsync(hc, dc, sizeof(hc), cudaMemcpyDeviceToHost, ctx->stream));
+  D2H(hc, dc, sizeof(hc));
   CK(cudaStreamSynchronize(ctx->stream));
   if (counts)
     for (int i = 0; i < 4; ++i) counts[i] = (long long)hc[i];
@@ -899,11 +932,11 @@ int rgbid_correct_inverse_depth(rgbid_ctx* ctx, const double* Wm, int w, int h,
   double* dd;
   int rc = scratch_buf(ctx, "correct", 2 * N, &dd);
   if (rc) return rc;
-  CK(cudaMemcpyAsync(dd, Wm, sizeof(double) * N, cudaMemcpyHostToDevice, ctx->stream));
+  H2D(dd, Wm, sizeof(double) * N);
   launch_correct_depth(dd, w, h, *d, *K, spatial, dd + N, ctx->stream);
   rc = check_launch(ctx);
   if (rc) return rc;
-  CK(cudaMemcpyAsync(out, dd + N, sizeof(double) * N, cudaMemcpyDeviceToHost, ctx->stream));
+  D2H(out, dd + N, sizeof(double) * N);
   CK(cudaStreamSynchronize(ctx->stream));
   return RGBID_OK;
 }
@@ -929,11 +962,11 @@ int rgbid_forward_register(rgbid_ctx* ctx, const double* WA, int w, int h, const
   if (rc) return rc;
   rc = scratch_buf(ctx, "register_inter", (size_t)iw * ih, &inter);
   if (rc) return rc;
-  CK(cudaMemcpyAsync(d, WA, sizeof(double) * N, cudaMemcpyHostToDevice, ctx->stream));
+  H2D(d, WA, sizeof(double) * N);
   launch_forward_register(d, w, h, r, inter, iw, ih, KB->width, KB->height, d + N, ctx->stream);
   rc = check_launch(ctx);
   if (rc) return rc;
-  CK(cudaMemcpyAsync(out, d + N, sizeof(double) * NB, cudaMemcpyDeviceToHost, ctx->stream));
+  D2H(out, d + N, sizeof(double) * NB);
   CK(cudaStreamSynchronize(ctx->stream));
   return RGBID_OK;
 }
@@ -980,6 +1013,51 @@ int rgbid_synth_pair_device(rgbid_ctx* ctx, rgbid_frame* a, rgbid_frame* b,
   int rc = check_launch(ctx);
   if (rc) return rc;
   CK(cudaStreamSynchronize(ctx->stream));
+  return RGBID_OK;
+}
+
+int rgbid_ctx_set_profiling(rgbid_ctx* ctx, int enable) {
+  if (!ctx) return RGBID_E_ARG;
+  ctx->prof.enabled = enable != 0;
+  return RGBID_OK;
+}
+
+int rgbid_ctx_reset_stats(rgbid_ctx* ctx) {
+  if (!ctx) return RGBID_E_ARG;
+  ctx->kstats.clear();
+  ctx->h2d_bytes = ctx->d2h_bytes = 0;
+  return RGBID_OK;
+}
+
+int rgbid_ctx_kernel_stats(rgbid_ctx* ctx, char* buf, int cap) {
+  if (!ctx) return -1;
+  std::string js = "{";
+  bool first = true;
+  for (auto& e : ctx->kstats) {
+    char tmp[256];
+    std::snprintf(tmp, sizeof(tmp), "%s\"%s\": [%lld, %.6f]", first ? "" : ", ", e.first.c_str(),
+                  e.second.first, e.second.second);
+    js += tmp;
+    first = false;
+  }
+  js += "}";
+  if (buf && cap > 0) {
+    std::strncpy(buf, js.c_str(), cap - 1);
+    buf[cap - 1] = 0;
+  }
+  return (int)js.size() + 1;
+}
+
+int rgbid_ctx_transfer_bytes(rgbid_ctx* ctx, long long* h2d, long long* d2h) {
+  if (!ctx) return RGBID_E_ARG;
+  if (h2d) *h2d = ctx->h2d_bytes;
+  if (d2h) *d2h = ctx->d2h_bytes;
+  return RGBID_OK;
+}
+
+int rgbid_frame_invalidate(rgbid_frame* f) {
+  if (!f) return RGBID_E_ARG;
+  f->pyr_levels = 0;
   return RGBID_OK;
 }
 

@@ -272,6 +272,28 @@ class Context:
     def kernel_launches(self) -> int:
         return int(self.lib.rgbid_ctx_kernel_launches(self.h))
 
+    def set_profiling(self, enable: bool):
+        self.check(self.lib.rgbid_ctx_set_profiling(self.h, int(enable)), "set_profiling")
+
+    def reset_stats(self):
+        self.check(self.lib.rgbid_ctx_reset_stats(self.h), "reset_stats")
+
+    def kernel_stats(self) -> dict:
+        import json
+        n = self.lib.rgbid_ctx_kernel_stats(self.h, None, 0)
+        buf = C.create_string_buffer(n)
+        self.lib.rgbid_ctx_kernel_stats(self.h, buf, n)
+        return {k: (int(v[0]), float(v[1])) for k, v in json.loads(buf.value.decode()).items()}
+
+    def transfer_bytes(self):
+        a, b = C.c_longlong(0), C.c_longlong(0)
+        self.lib.rgbid_ctx_transfer_bytes(self.h, C.byref(a), C.byref(b))
+        return a.value, b.value
+
+    @property
+    def stream_ptr(self) -> int:
+        return int(self.lib.rgbid_ctx_stream(self.h) or 0)
+
     def synchronize(self):
         self.check(self.lib.rgbid_ctx_synchronize(self.h), "synchronize")
 
@@ -324,6 +346,9 @@ class DeviceFrame:
         self.ctx.check(self.ctx.lib.rgbid_frame_download(self.ctx.h, self.h, dptr(I), dptr(W)),
                        "frame_download")
         return FrameData(I, W)
+
+    def invalidate(self):
+        self.ctx.lib.rgbid_frame_invalidate(self.h)
 
     def device_ptrs(self):
         I, W = abi.DP(), abi.DP()
