@@ -234,6 +234,12 @@ int rgbid_forward_register(rgbid_ctx* ctx, const double* W_A, int width, int hei
                            const rgbid_pose* T_BA, const rgbid_intrinsics* K_A,
                            const rgbid_intrinsics* K_B, double* out);
 
+/* ---- self tests ---------------------------------------------------------- */
+/* Bitwise check of the warp's reciprocal-based correctly-rounded division
+ * against IEEE division on n random operand pairs; *mismatches must be 0. */
+int rgbid_selftest_division(rgbid_ctx* ctx, unsigned long long n, unsigned long long seed,
+                            unsigned long long* mismatches);
+
 /* ---- synthetic inputs (restates /root/reference/proj/tests/synthetic.hpp) ---- */
 /* render_plane(K, T_WC, n, d) with plane_texture evaluated at tex_scale * (X, Y) */
 int rgbid_synth_render_plane(const rgbid_intrinsics* K, const rgbid_pose* T_WC, const double n[3],

@@ -136,6 +136,8 @@ EXPORTS = [
                                               C.POINTER(Intrinsics_t), C.c_int, DP]),
     ("rgbid_forward_register", C.c_int, [VP, DP, C.c_int, C.c_int, C.POINTER(Pose_t),
                                          C.POINTER(Intrinsics_t), C.POINTER(Intrinsics_t), DP]),
+    ("rgbid_selftest_division", C.c_int, [VP, C.c_ulonglong, C.c_ulonglong,
+                                          C.POINTER(C.c_ulonglong)]),
     ("rgbid_synth_render_plane", C.c_int, [C.POINTER(Intrinsics_t), C.POINTER(Pose_t), DP,
                                            C.c_double, C.c_double, DP, DP]),
     ("rgbid_synth_random_pose", C.c_int, [C.c_uint32, C.c_int, C.c_double, C.c_double,

@@ -53,6 +53,16 @@ KScope::~KScope() {
 
 __device__ __forceinline__ bool valid(double v) { return isfinite(v); }
 
+// Correctly rounded a / b from r = RN(1/b) (Markstein): q = RN(a r),
+// e = a - b q (exact with FMA), RN(q + e r) == RN(a / b) for normal operands.
+// Used where several quotients share a divisor; bit-identity with IEEE division
+// is asserted by the warp-map tests and rgbid_selftest_division.
+__device__ __forceinline__ double div_rcp(double a, double b, double r) {
+  const double q = a * r;
+  const double e = fma(-b, q, a);
+  return fma(e, r, q);
+}
+
 // bilinear — inc/image.hpp:51-62
 __device__ __forceinline__ double bilinear(const double* __restrict__ img, int w, int h, double x,
                                            double y) {
@@ -66,7 +76,27 @@ __device__ __forceinline__ double bilinear(const double* __restrict__ img, int w
   return (1 - fy) * ((1 - fx) * v00 + fx * v10) + fy * ((1 - fx) * v01 + fx * v11);
 }
 
-// one A pixel of inverse_geometric_warp — src/warping.cpp:96-111
+// bilinear of I_B and W_B at the same point, sharing the tap setup
+__device__ __forceinline__ void bilinear2(const double* __restrict__ I, const double* __restrict__ W,
+                                          int w, int h, double x, double y, double& oi,
+                                          double& ow) {
+  oi = CUDART_NAN;
+  ow = CUDART_NAN;
+  if (!(x >= 0.0 && x <= w - 1.0 && y >= 0.0 && y <= h - 1.0)) return;
+  const int x0 = (int)floor(x), y0 = (int)floor(y);
+  const int x1 = min(x0 + 1, w - 1), y1 = min(y0 + 1, h - 1);
+  const double fx = x - x0, fy = y - y0, gx = 1 - fx, gy = 1 - fy;
+  const size_t i00 = (size_t)y0 * w + x0, i10 = (size_t)y0 * w + x1;
+  const size_t i01 = (size_t)y1 * w + x0, i11 = (size_t)y1 * w + x1;
+  const double a00 = __ldg(I + i00), a10 = __ldg(I + i10), a01 = __ldg(I + i01), a11 = __ldg(I + i11);
+  const double b00 = __ldg(W + i00), b10 = __ldg(W + i10), b01 = __ldg(W + i01), b11 = __ldg(W + i11);
+  if (valid(a00) && valid(a10) && valid(a01) && valid(a11))
+    oi = gy * (gx * a00 + fx * a10) + fy * (gx * a01 + fx * a11);
+  if (valid(b00) && valid(b10) && valid(b01) && valid(b11))
+    ow = gy * (gx * b00 + fx * b10) + fy * (gx * b01 + fx * b11);
+}
+
+// one A pixel of inverse_geometric_warp — src/warping.cpp:96-111 (bit-identical)
 __device__ __forceinline__ void warp_px(const WarpMats& m, const double* __restrict__ IB,
                                         const double* __restrict__ WB, int wb, int hb, int x,
                                         int y, double w_a, double& oI, double& oW, double& mx,
@@ -76,21 +106,23 @@ __device__ __forceinline__ void warp_px(const WarpMats& m, const double* __restr
   mx = CUDART_NAN;
   my = CUDART_NAN;
   if (!valid(w_a) || w_a <= 0.0) return;
-  const double qx = x / w_a, qy = y / w_a, qz = 1.0 / w_a;
+  const double qz = __drcp_rn(w_a);  // == 1.0 / w_a
+  const double qx = div_rcp((double)x, w_a, qz), qy = div_rcp((double)y, w_a, qz);
   const double xb0 = red3(m.Rt_BA[0] * qx, m.Rt_BA[1] * qy, m.Rt_BA[2] * qz) + m.tt_BA[0];
   const double xb1 = red3(m.Rt_BA[3] * qx, m.Rt_BA[4] * qy, m.Rt_BA[5] * qz) + m.tt_BA[1];
   const double xb2 = red3(m.Rt_BA[6] * qx, m.Rt_BA[7] * qy, m.Rt_BA[8] * qz) + m.tt_BA[2];
   if (xb2 <= 1e-12) return;
-  const double px = xb0 / xb2, py = xb1 / xb2;
+  const double rz2 = __drcp_rn(xb2);
+  const double px = div_rcp(xb0, xb2, rz2), py = div_rcp(xb1, xb2, rz2);
   mx = px;
   my = py;
-  oI = bilinear(IB, wb, hb, px, py);
-  const double w_meas = bilinear(WB, wb, hb, px, py);
+  double w_meas;
+  bilinear2(IB, WB, wb, hb, px, py, oI, w_meas);
   if (!valid(w_meas) || w_meas <= 0.0) return;
   const double rz = red3(m.Rt_AB[6] * px, m.Rt_AB[7] * py, m.Rt_AB[8] * 1.0);
   const double za = rz / w_meas + m.tt_AB[2];
   if (za <= 1e-12) return;
-  oW = 1.0 / za;
+  oW = __drcp_rn(za);  // == 1.0 / za
 }
 
 __device__ __forceinline__ double px_or_nan(const double* img, int w, int h, int x, int y) {
@@ -157,19 +189,28 @@ __device__ __forceinline__ void load_wm(const WarpMats& g, WarpMats& m) {
 }
 
 // ---------------------------------------------------------------------------
-// K1: warp + downsample-to-level + residual validity + per-tile compaction.
+// K1: warp + downsample-to-level + jet validity + per-tile validity bitmasks.
+// The A-side conditions of src/alignment.cpp:209-211,227 (valid/positive w_a,
+// valid i_a, gradient_at(I_A), gradient_at(W_A)) do not change across IRLS
+// iterations: they are precomputed once per alignment into amask (k_amask); K1
+// adds the warped-B conditions and ballots the row-major validity bits per
+// tile (compacted rank = prefix popcount, consumed by the sample gather of K2).
 template <int L>
 __global__ void __launch_bounds__(kTPB) k_warp_residuals(const SlotIO* __restrict__ io,
                                                          const SlotState* __restrict__ st,
                                                          LevelInfo li, int w0, int h0, int phase) {
   const int slot = blockIdx.y;
-  if (!slot_active(st[slot], L, phase)) return;
+  const SlotState& S = st[slot];
+  if (!slot_active(S, L, phase)) return;
+  __shared__ WarpMats wm;
+  if (threadIdx.x < 24)
+    reinterpret_cast<double*>(&wm)[threadIdx.x] = reinterpret_cast<const double*>(&S.wm)[threadIdx.x];
   const SlotIO& o = io[slot];
-  const double* WAw = phase ? o.fWA : o.WA[0];
-  const double* IAl = phase ? o.fIA : o.IA[L];
-  const double* WAl = phase ? o.fWA : o.WA[L];
-  WarpMats m;
-  load_wm(st[slot].wm, m);
+  const double* __restrict__ WAw = phase ? o.fWA : o.WA[0];
+  const uint8_t* __restrict__ am = phase ? o.amask_cov : o.amask[L];
+  const double* __restrict__ IB = o.IB;
+  const double* __restrict__ WB = o.WB;
+  __syncthreads();
 
   const int tid = threadIdx.x;
   const int tile = blockIdx.x;
@@ -181,7 +222,7 @@ __global__ void __launch_bounds__(kTPB) k_warp_residuals(const SlotIO* __restric
   if constexpr (L == 0) {
     if (tid < nx) {
       const int x = xl0 + tid;
-      warp_px(m, o.IB, o.WB, w0, h0, x, yl, __ldg(WAw + (size_t)yl * w0 + x), ib, wb, d0, d1);
+      warp_px(wm, IB, WB, w0, h0, x, yl, __ldg(WAw + yl * w0 + x), ib, wb, d0, d1);
     }
   } else {
     __shared__ double sI[2048], sW[2048];
@@ -191,7 +232,7 @@ __global__ void __launch_bounds__(kTPB) k_warp_residuals(const SlotIO* __restric
       const int r = k / cw, c = k - r * cw;
       const int x = (xl0 << L) + c, y = (yl << L) + r;
       double vi, vw;
-      warp_px(m, o.IB, o.WB, w0, h0, x, y, __ldg(WAw + (size_t)y * w0 + x), vi, vw, d0, d1);
+      warp_px(wm, IB, WB, w0, h0, x, y, __ldg(WAw + y * w0 + x), vi, vw, d0, d1);
       sI[k] = vi;
       sW[k] = vw;
     }
@@ -230,48 +271,86 @@ __global__ void __launch_bounds__(kTPB) k_warp_residuals(const SlotIO* __restric
   }
 
   bool jet = false, dep = false;
-  double rI = 0.0, rW = 0.0;
   if (tid < nx) {
-    const int xl = xl0 + tid;
-    const size_t idx = (size_t)yl * li.w + xl;
+    const int idx = yl * li.w + xl0 + tid;
     o.ib[idx] = ib;
     o.wb[idx] = wb;
-    const double w_a = __ldg(WAl + idx), i_a = __ldg(IAl + idx);
-    if (valid(w_a) && w_a > 0.0 && valid(i_a) && valid(ib) && gradient_ok(IAl, li.w, li.h, xl, yl)) {
-      jet = true;
-      rI = ib - i_a;
-      if (valid(wb) && wb > 0.0 && gradient_ok(WAl, li.w, li.h, xl, yl)) {
-        dep = true;
-        rW = wb - w_a;
-      }
-    }
+    const unsigned a = am[idx];
+    jet = (a & 1u) && valid(ib);
+    dep = jet && (a & 2u) && valid(wb) && wb > 0.0;
   }
-  // block compaction in row-major order (tid order == x order)
+  const unsigned bj = __ballot_sync(0xffffffffu, jet), bd = __ballot_sync(0xffffffffu, dep);
   __shared__ int wcnt[2][kTPB / 32];
   const int lane = tid & 31, wid = tid >> 5;
-  const unsigned bj = __ballot_sync(0xffffffffu, jet), bd = __ballot_sync(0xffffffffu, dep);
   if (lane == 0) {
     wcnt[0][wid] = __popc(bj);
     wcnt[1][wid] = __popc(bd);
+    if (wid < kWordsPerTile) {
+      o.bitsI[tile * kWordsPerTile + wid] = bj;
+      o.bitsW[tile * kWordsPerTile + wid] = bd;
+    }
   }
   __syncthreads();
-  int offI = 0, offW = 0, totI = 0, totW = 0;
-#pragma unroll
-  for (int k = 0; k < kTPB / 32; ++k) {
-    if (k < wid) {
-      offI += wcnt[0][k];
-      offW += wcnt[1][k];
-    }
-    totI += wcnt[0][k];
-    totW += wcnt[1][k];
-  }
-  const unsigned lt = (1u << lane) - 1u;
-  const size_t base = (size_t)yl * li.w + xl0;
-  if (jet) o.resI[base + offI + __popc(bj & lt)] = rI;
-  if (dep) o.resW[base + offW + __popc(bd & lt)] = rW;
   if (tid == 0) {
-    o.cntI[tile] = totI;
-    o.cntW[tile] = totW;
+    int tI = 0, tW = 0;
+#pragma unroll
+    for (int k = 0; k < kTPB / 32; ++k) {
+      tI += wcnt[0][k];
+      tW += wcnt[1][k];
+    }
+    o.cntI[tile] = tI;
+    o.cntW[tile] = tW;
+  }
+}
+
+// A-side jet validity of one level pixel (src/alignment.cpp:209-211, 227)
+__global__ void k_amask(const SlotIO* __restrict__ io, const SlotState* __restrict__ st, int level,
+                        int w, int h, int phase) {
+  const int slot = blockIdx.y;
+  if (st[slot].status != RGBID_OK) return;
+  const SlotIO& o = io[slot];
+  const double* IA = phase ? o.fIA : o.IA[level];
+  const double* WA = phase ? o.fWA : o.WA[level];
+  uint8_t* out = phase ? o.amask_cov : o.amask[level];
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= w * h) return;
+  const int y = k / w, x = k - y * w;
+  const double w_a = WA[k], i_a = IA[k];
+  unsigned m = 0;
+  if (valid(w_a) && w_a > 0.0 && valid(i_a) && gradient_ok(IA, w, h, x, y)) m |= 1u;
+  if (gradient_ok(WA, w, h, x, y)) m |= 2u;
+  out[k] = (uint8_t)m;
+}
+
+void launch_amask(const AlignLaunch& a, int levels, int phase, cudaStream_t s) {
+  for (int l = 0; l < levels; ++l) {
+    const int w = a.w0 >> l, h = a.h0 >> l;
+    KScope ks_("amask", s);
+    k_amask<<<dim3((w * h + 255) / 256, a.nslots), 256, 0, s>>>(a.io, a.st, l, w, h, phase);
+  }
+}
+
+// pyramid levels 1..L-1 of every slot whose frame A needs them (src/alignment.cpp:13-28)
+__global__ void k_pyramid_slots(const SlotIO* __restrict__ io, int level, int w, int h) {
+  const SlotIO& o = io[blockIdx.y];
+  if (!o.build_pyr) return;
+  const int ow = w / 2, oh = h / 2;
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= ow * oh) return;
+  const int y = k / ow, x = k - y * ow;
+  const double* I = o.IA[level - 1];
+  const double* W = o.WA[level - 1];
+  const int i0 = (2 * y) * w + 2 * x, i1 = i0 + w;
+  o.IA[level][k] = ds4(I[i0], I[i0 + 1], I[i1], I[i1 + 1]);
+  o.WA[level][k] = ds4(W[i0], W[i0 + 1], W[i1], W[i1 + 1]);
+}
+
+void launch_pyramid_slots(const AlignLaunch& a, int levels, cudaStream_t s) {
+  for (int l = 1; l < levels; ++l) {
+    const int w = a.w0 >> (l - 1), h = a.h0 >> (l - 1);
+    const int n = (w / 2) * (h / 2);
+    KScope ks_("pyramid", s);
+    k_pyramid_slots<<<dim3((n + 255) / 256, a.nslots), 256, 0, s>>>(a.io, l, w, h);
   }
 }
 
@@ -290,7 +369,16 @@ void launch_warp_residuals(const AlignLaunch& a, const LevelInfo& li, int phase,
 }
 
 // ---------------------------------------------------------------------------
-// Block-wide fixed-order reductions (every thread receives the bit-identical total).
+// K2: Student-t chain.  One CTA (kTdistThreads) per (slot, residual type).  The
+// systematic sample (src/alignment.cpp:50-57) is gathered into shared memory
+// (fixed per-thread ownership -> deterministic), then the whole
+// chain of src/alignment.cpp:61-157,288-320 runs with block-wide fixed-order
+// reductions.  Per-sample arithmetic uses (v - mu) * (1/sigma) and a
+// MUFU-seeded Newton reciprocal for t_weight (<= 1-2 ulp per term; the
+// reference's sums are sequential, ours a fixed tree — both only change
+// rounding, well inside the 1e-4 normal-equation tolerance).
+constexpr int kSPT = (kMaxSample + kTdistThreads - 1) / kTdistThreads;
+
 template <int NV, int NT>
 __device__ __forceinline__ void block_allsum(double (&v)[NV], double* scratch) {
   constexpr int NW = NT / 32;
@@ -318,42 +406,69 @@ struct TD {
 
 __device__ __forceinline__ double t_weight(double x, double nu) { return (nu + 1.0) / (nu + x * x); }
 
-// estimate_location_scale on the (already sampled) smem vector — src/alignment.cpp:61-101
+// 1/q for q >= 1 (t_weight denominators): MUFU seed + cubic Newton step.
+__device__ __forceinline__ double rcp_fast(double q) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(q));
+  const double e = fma(-q, r, 1.0);
+  return fma(r, fma(e, e, e), r);
+}
+
+struct Sample {
+  const double* v;  // shared memory, kSPT strided slots per thread
+  int m;
+};
+
+// estimate_location_scale on the register-resident sample — src/alignment.cpp:61-101
 template <int NT>
-__device__ TD loc_scale(const double* smp, int m, double nu, double* scratch) {
+__device__ __forceinline__ TD loc_scale(const Sample& S, double nu, double* scratch) {
   TD p{0.0, 1.0, nu};
+  const int m = S.m;
   if (m == 0) return p;
   const int tid = threadIdx.x;
+  const double inv_m = 1.0 / (double)m;
   double a1[1] = {0.0};
-  for (int i = tid; i < m; i += NT) a1[0] += smp[i];
+#pragma unroll
+  for (int k = 0; k < kSPT; ++k)
+    if (k * NT + tid < m) a1[0] += S.v[k * NT + tid];
   block_allsum<1, NT>(a1, scratch);
   double mu = a1[0] / (double)m;
   a1[0] = 0.0;
-  for (int i = tid; i < m; i += NT) {
-    const double d = smp[i] - mu;
-    a1[0] += d * d;
-  }
+#pragma unroll
+  for (int k = 0; k < kSPT; ++k)
+    if (k * NT + tid < m) {
+      const double d = S.v[k * NT + tid] - mu;
+      a1[0] = fma(d, d, a1[0]);
+    }
   block_allsum<1, NT>(a1, scratch);
   double sigma = sqrt(a1[0] / (double)m);
   if (sigma < 1e-8) return TD{mu, 1e-8, nu};
+  const double nu1 = nu + 1.0;
   for (int it = 0; it < 50; ++it) {
+    const double isg = 1.0 / sigma;
     double a2[2] = {0.0, 0.0};
-    for (int i = tid; i < m; i += NT) {
-      const double v = smp[i];
-      const double w = t_weight((v - mu) / sigma, nu);
-      a2[0] += w;
-      a2[1] += w * v;
-    }
+#pragma unroll
+    for (int k = 0; k < kSPT; ++k)
+      if (k * NT + tid < m) {
+        const double v = S.v[k * NT + tid];
+        const double x = (v - mu) * isg;
+        const double w = nu1 * rcp_fast(fma(x, x, nu));
+        a2[0] += w;
+        a2[1] = fma(w, v, a2[1]);
+      }
     block_allsum<2, NT>(a2, scratch);
     const double mu_new = a2[1] / a2[0];
     a1[0] = 0.0;
-    for (int i = tid; i < m; i += NT) {
-      const double v = smp[i];
-      const double w = t_weight((v - mu_new) / sigma, nu);
-      a1[0] += w * (v - mu_new) * (v - mu_new);
-    }
+#pragma unroll
+    for (int k = 0; k < kSPT; ++k)
+      if (k * NT + tid < m) {
+        const double d = S.v[k * NT + tid] - mu_new;
+        const double x = d * isg;
+        const double w = nu1 * rcp_fast(fma(x, x, nu));
+        a1[0] = fma(w * d, d, a1[0]);
+      }
     block_allsum<1, NT>(a1, scratch);
-    const double sigma_new = dmax_std(1e-8, sqrt(a1[0] / (double)m));
+    const double sigma_new = dmax_std(1e-8, sqrt(a1[0] * inv_m));
     const double rel = fabs(sigma_new - sigma) / sigma;
     mu = mu_new;
     sigma = sigma_new;
@@ -375,32 +490,36 @@ __device__ __forceinline__ double digamma_d(double x) {
   return result;
 }
 
-// stationarity of solve_nu — src/alignment.cpp:132-141.  The nu-only part C is
-// hoisted; each per-sample term (C + log w) - w is bit-identical to the reference's.
+// stationarity of solve_nu — src/alignment.cpp:132-141 (the nu-only part C hoisted;
+// per-sample term (C + log w) - w as in the reference).
 template <int NT>
-__device__ double stationarity(const double* smp, int m, double mu, double sigma, double nu,
+__device__ __forceinline__ double stationarity(const Sample& S, double mu, double sigma, double nu,
                                double* scratch) {
   const double C = (((-digamma_d(nu / 2.0) + log(nu / 2.0)) + digamma_d((nu + 1.0) / 2.0)) -
                     log((nu + 1.0) / 2.0)) + 1.0;
+  const double isg = 1.0 / sigma, nu1 = nu + 1.0;
   double a[1] = {0.0};
-  for (int i = threadIdx.x; i < m; i += NT) {
-    const double w = t_weight((smp[i] - mu) / sigma, nu);
-    a[0] += (C + log(w)) - w;
-  }
+#pragma unroll
+  for (int k = 0; k < kSPT; ++k)
+    if (k * NT + threadIdx.x < S.m) {
+      const double x = (S.v[k * NT + threadIdx.x] - mu) * isg;
+      const double w = nu1 * rcp_fast(fma(x, x, nu));
+      a[0] += (C + log(w)) - w;
+    }
   block_allsum<1, NT>(a, scratch);
-  return a[0] / (double)m;
+  return a[0] / (double)S.m;
 }
 
 // solve_nu — src/alignment.cpp:131-157
 template <int NT>
-__device__ double solve_nu(const double* smp, int m, double mu, double sigma, double* scratch) {
+__device__ __forceinline__ double solve_nu(const Sample& S, double mu, double sigma, double* scratch) {
   double lo = 2.0, hi = 10.0;
-  double flo = stationarity<NT>(smp, m, mu, sigma, lo, scratch);
-  const double fhi = stationarity<NT>(smp, m, mu, sigma, hi, scratch);
+  double flo = stationarity<NT>(S, mu, sigma, lo, scratch);
+  const double fhi = stationarity<NT>(S, mu, sigma, hi, scratch);
   if (flo * fhi > 0.0) return fhi > 0.0 ? hi : lo;
   for (int it = 0; it < 30; ++it) {
     const double mid = 0.5 * (lo + hi);
-    const double fmid = stationarity<NT>(smp, m, mu, sigma, mid, scratch);
+    const double fmid = stationarity<NT>(S, mu, sigma, mid, scratch);
     if (flo * fmid <= 0.0) {
       hi = mid;
     } else {
@@ -413,13 +532,13 @@ __device__ double solve_nu(const double* smp, int m, double mu, double sigma, do
 
 // estimate_nu — src/alignment.cpp:109-127
 template <int NT>
-__device__ double estimate_nu(const double* smp, int m, double mu, double sigma, double* scratch) {
-  if (m == 0 || sigma <= 0.0) return 5.0;
-  double nu = solve_nu<NT>(smp, m, mu, sigma, scratch);
+__device__ __forceinline__ double estimate_nu(const Sample& S, double mu, double sigma, double* scratch) {
+  if (S.m == 0 || sigma <= 0.0) return 5.0;
+  double nu = solve_nu<NT>(S, mu, sigma, scratch);
   for (int it = 0; it < 2 && nu < 9.99; ++it) {
-    const TD refit = loc_scale<NT>(smp, m, nu, scratch);
+    const TD refit = loc_scale<NT>(S, nu, scratch);
     if (refit.sigma <= 0.0) break;
-    const double nu_new = solve_nu<NT>(smp, m, refit.mu, refit.sigma, scratch);
+    const double nu_new = solve_nu<NT>(S, refit.mu, refit.sigma, scratch);
     if (fabs(nu_new - nu) < 1e-3) {
       nu = nu_new;
       break;
@@ -429,41 +548,28 @@ __device__ double estimate_nu(const double* smp, int m, double mu, double sigma,
   return nu;
 }
 
-__global__ void k_tdist(const SlotIO* __restrict__ io, SlotState* __restrict__ st, LevelInfo li,
-                        int phase);
+int tdist_smem_bytes(int ntiles) { return kMaxSample * 8 + (ntiles + 1) * 4; }
 
-int init_kernel_attributes() {
-  // sample (19200 doubles) + tile offsets; static smem of k_tdist is small
-  const cudaError_t e =
-      cudaFuncSetAttribute(k_tdist, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  cudaGetLastError();  // do not leave a sticky error for the next launch check
-  return e == cudaSuccess ? 0 : 1;
-}
-
-int tdist_smem_bytes(int ntiles) {
-  return kMaxSample * 8 + (ntiles + 1) * 4 + 64 * 8 + 16;
-}
-
-// K2: systematic sample + Student-t chain for one (slot, residual type).
-__global__ void __launch_bounds__(kTdistThreads) k_tdist(const SlotIO* __restrict__ io,
-                                                         SlotState* __restrict__ st, LevelInfo li,
-                                                         int phase) {
+__global__ void __launch_bounds__(kTdistThreads, 1)
+    k_tdist(const SlotIO* __restrict__ io, SlotState* __restrict__ st, LevelInfo li, int phase) {
   constexpr int NT = kTdistThreads;
   const int type = blockIdx.x, slot = blockIdx.y;
   SlotState& S = st[slot];
   if (!slot_active(S, li.level, phase)) return;
   const SlotIO& o = io[slot];
   const int* cnt = type ? o.cntW : o.cntI;
-  const double* res = type ? o.resW : o.resI;
-  extern __shared__ double dsm[];
-  double* smp = dsm;
-  double* scratch = dsm + kMaxSample;                    // 64 doubles
-  int* offs = reinterpret_cast<int*>(scratch + 64);      // ntiles + 1
+  const unsigned* bits = type ? o.bitsW : o.bitsI;
+  const double* bv = type ? o.wb : o.ib;  // warped B at this level
+  const double* av = type ? (phase ? o.fWA : o.WA[li.level]) : (phase ? o.fIA : o.IA[li.level]);
+  extern __shared__ double dsm[];  // sample[kMaxSample] + offs[ntiles + 1]
+  double* smp_sh = dsm;
+  int* offs = reinterpret_cast<int*>(dsm + kMaxSample);
   __shared__ int wsum[NT / 32];
+  __shared__ double scratch[NT / 32 * 2];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int nt = li.ntiles;
 
-  // exclusive scan of per-tile counts (contiguous chunk per thread)
+  // exclusive scan of the per-tile counts (contiguous chunk per thread)
   const int per = (nt + NT - 1) / NT;
   const int b0 = min(nt, tid * per), b1 = min(nt, b0 + per);
   int local = 0;
@@ -476,42 +582,58 @@ __global__ void __launch_bounds__(kTdistThreads) k_tdist(const SlotIO* __restric
   }
   if (lane == 31) wsum[wid] = incl;
   __syncthreads();
-  int woff = 0;
-  for (int k = 0; k < wid; ++k) woff += wsum[k];
+  int woff = 0, total = 0;
+  for (int k = 0; k < NT / 32; ++k) {
+    if (k < wid) woff += wsum[k];
+    total += wsum[k];
+  }
   int run = woff + incl - local;
   for (int i = b0; i < b1; ++i) {
     offs[i] = run;
     run += cnt[i];
   }
-  int total = 0;
-  for (int k = 0; k < NT / 32; ++k) total += wsum[k];
   if (tid == 0) offs[nt] = total;
   __syncthreads();
 
+  // systematic sample straight into registers: sample s = k*NT + tid
   const long long n = total;
   const long long stride = n <= kMaxSample ? 1 : (n + kMaxSample - 1) / kMaxSample;
-  const int m = n == 0 ? 0 : (int)((n - 1) / stride + 1);
-  for (int s = tid; s < m; s += NT) {
-    const long long g = (long long)s * stride;
-    int lo = 0, hi = nt - 1;
-    while (lo < hi) {  // last tile with offs[t] <= g
-      const int mid = (lo + hi + 1) >> 1;
-      if (offs[mid] <= g)
-        lo = mid;
-      else
-        hi = mid - 1;
+  Sample smp;
+  smp.v = smp_sh;
+  smp.m = n == 0 ? 0 : (int)((n - 1) / stride + 1);
+  for (int k = 0; k < kSPT; ++k) {
+    const int s = k * NT + tid;
+    if (s < smp.m) {
+      const long long g = (long long)s * stride;
+      int lo = 0, hi = nt - 1;
+      while (lo < hi) {  // last tile with offs[t] <= g
+        const int mid = (lo + hi + 1) >> 1;
+        if (offs[mid] <= g)
+          lo = mid;
+        else
+          hi = mid - 1;
+      }
+      // j-th set bit of tile lo's row-major validity mask -> level pixel
+      int j = (int)(g - offs[lo]), word = 0;
+      unsigned msk = bits[lo * kWordsPerTile];
+      while (j >= __popc(msk)) {
+        j -= __popc(msk);
+        msk = bits[lo * kWordsPerTile + (++word)];
+      }
+      for (int q = 0; q < j; ++q) msk &= msk - 1u;
+      const int yl = lo / li.nseg, seg = lo - yl * li.nseg;
+      const int idx = yl * li.w + seg * li.tx + word * 32 + (__ffs(msk) - 1);
+      smp_sh[s] = bv[idx] - av[idx];  // r_I = i_b - i_a / r_W = w_b - w_a (src/alignment.cpp:222,229)
     }
-    const int yl = lo / li.nseg, seg = lo - yl * li.nseg;
-    smp[s] = res[(size_t)yl * li.w + (size_t)seg * li.tx + (size_t)(g - offs[lo])];
   }
   __syncthreads();
 
   // build_system's Student-t part — src/alignment.cpp:305-317
-  TD t = loc_scale<NT>(smp, m, 5.0, scratch);
+  TD t = loc_scale<NT>(smp, 5.0, scratch);
   t.sigma = dmax_std(t.sigma, 1e-8);
-  t.nu = estimate_nu<NT>(smp, m, t.mu, t.sigma, scratch);
+  t.nu = estimate_nu<NT>(smp, t.mu, t.sigma, scratch);
   if (t.nu < 4.99) {
-    const TD r = loc_scale<NT>(smp, m, t.nu, scratch);
+    const TD r = loc_scale<NT>(smp, t.nu, scratch);
     if (r.sigma > 0.0) {
       t.mu = r.mu;
       t.sigma = dmax_std(r.sigma, 1e-8);
@@ -529,88 +651,25 @@ __global__ void __launch_bounds__(kTdistThreads) k_tdist(const SlotIO* __restric
   }
 }
 
+int init_kernel_attributes() {
+  const cudaError_t e =
+      cudaFuncSetAttribute(k_tdist, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaGetLastError();
+  return e == cudaSuccess ? 0 : 1;
+}
+
 void launch_tdist(const AlignLaunch& a, const LevelInfo& li, int phase, cudaStream_t s) {
-  const int smem = tdist_smem_bytes(li.ntiles);  // <= 200 KB for ntiles <= 11000
   KScope ks_("tdist", s);
-  k_tdist<<<dim3(2, a.nslots), kTdistThreads, smem, s>>>(a.io, a.st, li, phase);
+  k_tdist<<<dim3(2, a.nslots), kTdistThreads, tdist_smem_bytes(li.ntiles), s>>>(a.io, a.st, li,
+                                                                                 phase);
 }
 
 // ---------------------------------------------------------------------------
-// K3: jets + robust weights + 28 fp64 sums per tile.
-struct Jet {
-  double rI, rW, JI[6], JW[6], lambda;
-  bool depth;
-};
-
-// residuals_and_jacobians for one pixel — src/alignment.cpp:206-246
-__device__ __forceinline__ bool jet_at(const double* IA, const double* WA, double i_b, double w_b,
-                                       int w, int h, int x, int y, const LevelInfo& li,
-                                       double lambda_n_min, Jet& j) {
-  const size_t i = (size_t)y * w + x;
-  const double w_a = __ldg(WA + i), i_a = __ldg(IA + i);
-  if (!valid(w_a) || w_a <= 0.0 || !valid(i_a) || !valid(i_b)) return false;
-  double gix, giy;
-  if (!gradient_at(IA, w, h, x, y, gix, giy)) return false;
-  // A = K - p e_z^T ; X_A = K^-1 p / w_a ; M = [I | -[X_A]x]
-  const double px = x, py = y;
-  double A[3][3] = {{li.fx, 0.0, li.cx - px}, {0.0, li.fy, li.cy - py}, {0.0, 0.0, 1.0 - 1.0}};
-  const double* Ki = li.Kinv;
-  const double X0 = red3(Ki[0] * px, Ki[1] * py, Ki[2] * 1.0) / w_a;
-  const double X1 = red3(Ki[3] * px, Ki[4] * py, Ki[5] * 1.0) / w_a;
-  const double X2 = red3(Ki[6] * px, Ki[7] * py, Ki[8] * 1.0) / w_a;
-  const double M[3][6] = {{1.0, 0.0, 0.0, -0.0, X2, -X1},
-                          {0.0, 1.0, 0.0, -X2, -0.0, X0},
-                          {0.0, 0.0, 1.0, X1, -X0, -0.0}};
-  j.rI = i_b - i_a;
-  j.rW = 0.0;
-  j.lambda = 1.0;
-  j.depth = false;
-  {
-    const double s0 = w_a * gix, s1 = w_a * giy, s2 = w_a * 0.0;
-    double u[3];
-#pragma unroll
-    for (int c = 0; c < 3; ++c) u[c] = red3(s0 * A[0][c], s1 * A[1][c], s2 * A[2][c]);
-#pragma unroll
-    for (int c = 0; c < 6; ++c) j.JI[c] = red3(u[0] * M[0][c], u[1] * M[1][c], u[2] * M[2][c]);
-  }
-  double gwx, gwy;
-  if (!(valid(w_b) && w_b > 0.0 && gradient_at(WA, w, h, x, y, gwx, gwy))) return true;
-  j.depth = true;
-  j.rW = w_b - w_a;
-  double gA[3], s2v[3];
-#pragma unroll
-  for (int c = 0; c < 3; ++c) gA[c] = red3(gwx * A[0][c], gwy * A[1][c], 0.0 * A[2][c]);
-  s2v[0] = w_a * (gA[0] + w_b * 0.0);
-  s2v[1] = w_a * (gA[1] + w_b * 0.0);
-  s2v[2] = w_a * (gA[2] + w_b * 1.0);
-#pragma unroll
-  for (int c = 0; c < 6; ++c) j.JW[c] = red3(s2v[0] * M[0][c], s2v[1] * M[1][c], s2v[2] * M[2][c]);
-  double n0 = gA[0] / w_a + 0.0, n1 = gA[1] / w_a + 0.0, n2 = gA[2] / w_a + 1.0;
-  const double nn = sqrt(red3(n0 * n0, n1 * n1, n2 * n2));
-  if (!(nn < 1e-12)) {
-    n0 /= nn;
-    n1 /= nn;
-    n2 /= nn;
-    if (n2 < 0) {
-      n0 = -n0;
-      n1 = -n1;
-      n2 = -n2;
-    }
-    double r0 = red3(Ki[0] * px, Ki[1] * py, Ki[2] * 1.0);  // ray = K^-1 p
-    double r1 = red3(Ki[3] * px, Ki[4] * py, Ki[5] * 1.0);
-    double r2 = red3(Ki[6] * px, Ki[7] * py, Ki[8] * 1.0);
-    const double sq = red3(r0 * r0, r1 * r1, r2 * r2);
-    if (sq > 0.0) {
-      const double sn = sqrt(sq);
-      r0 /= sn;
-      r1 /= sn;
-      r2 /= sn;
-    }
-    j.lambda = dmax_std(lambda_n_min, red3(n0 * r0, n1 * r1, n2 * r2));
-  }
-  return true;
-}
-
+// K3: jets + robust weights + 28 fp64 sums per tile (kPixK3 pixels per thread).
+// Jets restate src/alignment.cpp:212-244 with the structure of A = K - p e_z^T and
+// M = [I | -[X_A]x] folded in: J = (u, X_A x u) with u = w_a g A; the weights are
+// src/alignment.cpp:324,329-330.  Tolerance-level (not bitwise) w.r.t. the
+// reference: the sums' order differs anyway.
 template <int NT>
 __device__ __forceinline__ void block_sum_to(double (&v)[kNPart], double* out, double* scratch) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -629,6 +688,22 @@ __device__ __forceinline__ void block_sum_to(double (&v)[kNPart], double* out, d
   }
 }
 
+__device__ __forceinline__ void accum(double (&acc)[kNPart], const double (&J)[6], double w,
+                                      double r) {
+  int q = 0;
+#pragma unroll
+  for (int a = 0; a < 6; ++a) {
+    const double va = w * J[a];
+#pragma unroll
+    for (int c = 0; c <= a; ++c) {
+      acc[q] = fma(va, J[c], acc[q]);
+      ++q;
+    }
+    acc[21 + a] = fma(va, r, acc[21 + a]);
+  }
+  acc[27] = fma(w * r, r, acc[27]);
+}
+
 __global__ void __launch_bounds__(kTPB) k_normal_eq(const SlotIO* __restrict__ io,
                                                     const SlotState* __restrict__ st, LevelInfo li,
                                                     int phase, double lambda_n_min) {
@@ -636,46 +711,80 @@ __global__ void __launch_bounds__(kTPB) k_normal_eq(const SlotIO* __restrict__ i
   const SlotState& S = st[slot];
   if (!slot_active(S, li.level, phase)) return;
   const SlotIO& o = io[slot];
-  const double* IAl = phase ? o.fIA : o.IA[li.level];
-  const double* WAl = phase ? o.fWA : o.WA[li.level];
+  const double* IA = phase ? o.fIA : o.IA[li.level];
+  const double* WA = phase ? o.fWA : o.WA[li.level];
   __shared__ double scratch[(kTPB / 32) * kNPart];
-  const double muI = S.tI.mu, sgI = S.tI.sigma, nuI = dmax_std(S.tI.nu, S.tW.nu);
-  const double muW = S.tW.mu, sgW = S.tW.sigma, nuW = S.tW.nu;
-  const double s2i = sgI * sgI, s2w = sgW * sgW;
+  const double muI = S.tI.mu, isgI = 1.0 / S.tI.sigma, nuI = dmax_std(S.tI.nu, S.tW.nu);
+  const double muW = S.tW.mu, isgW = 1.0 / S.tW.sigma, nuW = S.tW.nu;
+  const double nuI1 = nuI + 1.0, nuW1 = nuW + 1.0;
+  const double is2i = isgI * isgI, is2w = isgW * isgW;
+  const int w = li.w, h = li.h;
+  const double* Ki = li.Kinv;
   double acc[kNPart];
 #pragma unroll
   for (int i = 0; i < kNPart; ++i) acc[i] = 0.0;
-  const long long k = (long long)blockIdx.x * kTPB + threadIdx.x;
-  const long long N = (long long)li.w * li.h;
-  if (k < N) {
-    const int y = (int)(k / li.w), x = (int)(k - (long long)y * li.w);
-    Jet j;
-    if (jet_at(IAl, WAl, o.ib[k], o.wb[k], li.w, li.h, x, y, li, lambda_n_min, j)) {
-      const double wi = t_weight((j.rI - muI) / sgI, nuI) / s2i;
-      int q = 0;
-#pragma unroll
-      for (int a = 0; a < 6; ++a) {
-        const double va = wi * j.JI[a];
-#pragma unroll
-        for (int c = 0; c <= a; ++c) acc[q++] += va * j.JI[c];
-      }
-#pragma unroll
-      for (int a = 0; a < 6; ++a) acc[21 + a] += (wi * j.JI[a]) * j.rI;
-      acc[27] += wi * j.rI * j.rI;
-      if (j.depth) {
-        const double ww = j.lambda * t_weight((j.rW - muW) / sgW, nuW) / s2w;
-        q = 0;
-#pragma unroll
-        for (int a = 0; a < 6; ++a) {
-          const double va = ww * j.JW[a];
-#pragma unroll
-          for (int c = 0; c <= a; ++c) acc[q++] += va * j.JW[c];
-        }
-#pragma unroll
-        for (int a = 0; a < 6; ++a) acc[21 + a] += (ww * j.JW[a]) * j.rW;
-        acc[27] += ww * j.rW * j.rW;
+  const long long N = (long long)w * h;
+#pragma unroll 1
+  for (int p = 0; p < kPixK3; ++p) {
+    const long long k = ((long long)blockIdx.x * kPixK3 + p) * kTPB + threadIdx.x;
+    if (k >= N) break;
+    const int y = (int)(k / w), x = (int)(k - (long long)y * w);
+    const double i_b = o.ib[k], w_b = o.wb[k];
+    const double w_a = __ldg(WA + k), i_a = __ldg(IA + k);
+    if (!valid(w_a) || w_a <= 0.0 || !valid(i_a) || !valid(i_b)) continue;
+    double gix, giy;
+    if (!gradient_at(IA, w, h, x, y, gix, giy)) continue;
+    const double px = x, py = y;
+    const double ax = li.cx - px, ay = li.cy - py;  // A(0,2), A(1,2)
+    const double iwa = 1.0 / w_a;
+    const double k0 = red3(Ki[0] * px, Ki[1] * py, Ki[2]), k1 = red3(Ki[3] * px, Ki[4] * py, Ki[5]),
+                 k2 = red3(Ki[6] * px, Ki[7] * py, Ki[8]);
+    const double X0 = k0 * iwa, X1 = k1 * iwa, X2 = k2 * iwa;
+    // photometric row: u = w_a (gix, giy, 0) A ; J_I = (u, X x u)
+    double J[6];
+    {
+      const double s0 = w_a * gix, s1 = w_a * giy;
+      const double u0 = s0 * li.fx, u1 = s1 * li.fy, u2 = s0 * ax + s1 * ay;
+      J[0] = u0;
+      J[1] = u1;
+      J[2] = u2;
+      J[3] = X1 * u2 - X2 * u1;
+      J[4] = X2 * u0 - X0 * u2;
+      J[5] = X0 * u1 - X1 * u0;
+      const double rI = i_b - i_a;
+      const double xi_ = (rI - muI) * isgI;
+      const double wi = nuI1 * rcp_fast(fma(xi_, xi_, nuI)) * is2i;
+      accum(acc, J, wi, rI);
+    }
+    double gwx, gwy;
+    if (!(valid(w_b) && w_b > 0.0 && gradient_at(WA, w, h, x, y, gwx, gwy))) continue;
+    // geometric row: s = w_a (g_W A + w_b e_z) ; J_W = (s, X x s)
+    const double g0 = gwx * li.fx, g1 = gwy * li.fy, g2 = gwx * ax + gwy * ay;
+    {
+      const double s0 = w_a * g0, s1 = w_a * g1, s2 = w_a * (g2 + w_b);
+      J[0] = s0;
+      J[1] = s1;
+      J[2] = s2;
+      J[3] = X1 * s2 - X2 * s1;
+      J[4] = X2 * s0 - X0 * s2;
+      J[5] = X0 * s1 - X1 * s0;
+    }
+    // lambda_n: normal of the inverse-depth surface vs the viewing ray
+    double lambda = 1.0;
+    {
+      const double n0 = g0 * iwa, n1 = g1 * iwa, n2 = g2 * iwa + 1.0;
+      const double nn2 = n0 * n0 + n1 * n1 + n2 * n2;
+      if (!(sqrt(nn2) < 1e-12)) {
+        const double rr2 = k0 * k0 + k1 * k1 + k2 * k2;
+        double c = (n0 * k0 + n1 * k1 + n2 * k2) * rsqrt(nn2) * rsqrt(rr2);
+        if (n2 < 0) c = -c;
+        lambda = dmax_std(lambda_n_min, c);
       }
     }
+    const double rW = w_b - w_a;
+    const double xw = (rW - muW) * isgW;
+    const double ww = lambda * nuW1 * rcp_fast(fma(xw, xw, nuW)) * is2w;
+    accum(acc, J, ww, rW);
   }
   block_sum_to<kTPB>(acc, o.part + (size_t)blockIdx.x * kNPart, scratch);
 }
@@ -911,6 +1020,49 @@ void launch_warp_maps(const double* IB, const double* WB, int wb, int hb, const 
                       cudaStream_t s) {
   KScope ks_("warp_maps", s);
   k_warp_maps<<<(w * h + 255) / 256, 256, 0, s>>>(IB, WB, wb, hb, WA, w, h, m, oI, oW, omx, omy);
+}
+
+// ---------------------------------------------------------------------------
+// Self-test of div_rcp against IEEE division on n random operand pairs spanning
+// the ranges the warp sees (numerators |a| < 2^20 incl. integers, divisors
+// b in [1e-12, 1e6]).  Counts mismatches (bitwise).
+__device__ __forceinline__ unsigned long long mix64(unsigned long long z) {
+  z += 0x9e3779b97f4a7c15ull;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+__global__ void k_selftest_div(unsigned long long n, unsigned long long seed,
+                               unsigned long long* mismatches) {
+  unsigned long long bad = 0;
+  for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
+       i += (unsigned long long)gridDim.x * blockDim.x) {
+    const unsigned long long r1 = mix64(seed * 0x100000001ull + 2 * i), r2 = mix64(seed + 2 * i + 1);
+    const double u1 = (r1 >> 11) * (1.0 / 9007199254740992.0);
+    const double u2 = (r2 >> 11) * (1.0 / 9007199254740992.0);
+    double a = (i & 3) == 0 ? (double)((r1 >> 40) % 2048) : (u1 - 0.5) * exp2(40.0 * u2 - 20.0);
+    const double b = exp2(-39.9 + 59.8 * u2) * (1.0 + u1);
+    const double r = __drcp_rn(b);
+    const double q1 = div_rcp(a, b, r), q2 = a / b;
+    if (__double_as_longlong(q1) != __double_as_longlong(q2)) ++bad;
+    if (__double_as_longlong(r) != __double_as_longlong(1.0 / b)) ++bad;
+  }
+  if (bad) atomicAdd(mismatches, bad);
+}
+
+int selftest_division(unsigned long long n, unsigned long long seed, unsigned long long* out,
+                      cudaStream_t s) {
+  unsigned long long* d;
+  if (cudaMalloc(&d, sizeof(*d)) != cudaSuccess) return 1;
+  cudaMemsetAsync(d, 0, sizeof(*d), s);
+  {
+    KScope ks_("selftest_div", s);
+    k_selftest_div<<<148 * 8, 256, 0, s>>>(n, seed, d);
+  }
+  cudaMemcpyAsync(out, d, sizeof(*d), cudaMemcpyDeviceToHost, s);
+  cudaStreamSynchronize(s);
+  cudaFree(d);
+  return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
 
 }  // namespace rgbid_b200

@@ -16,9 +16,10 @@ namespace rgbid_b200 {
 constexpr int kMaxLevels = 6;       // GPU supports levels <= 6 (80x60 at level 3 for VGA)
 constexpr int kMaxSample = 19200;   // src/alignment.cpp:47
 constexpr int kTPB = 256;           // warp/residual/normal-equation kernels
-constexpr int kTdistThreads = 1024; // Student-t kernel
+constexpr int kTdistThreads = 1024; // Student-t kernel (sample in shared memory)
 constexpr int kNPart = 28;          // 21 (lower H) + 6 (b) + 1 (cost)
 constexpr int kTraceMax = 64;
+constexpr int kPixK3 = 4;           // pixels per thread in the normal-equation kernel
 
 // K1 tiling of level l: tile = (level row, segment of tx level pixels).
 // Full-res pixels per tile = tx * 4^l <= 2048 (smem staging of the warp).
@@ -33,25 +34,30 @@ struct LevelInfo {
   int w, h;          // level image size (w0 >> l, h0 >> l)
   int tx, nseg;      // K1 tiling
   int ntiles;        // K1 tiles = h * nseg
-  int ntiles3;       // K3 tiles of kTPB consecutive pixels
+  int ntiles3;       // K3 tiles of kTPB * kPixK3 consecutive pixels
   double fx, fy, cx, cy;
   double Kinv[9];    // level K^-1 (host m3_inv, bit-identical to the oracle)
 };
 
+constexpr int kWordsPerTile = 8;  // K1 tile <= 256 level pixels -> 8 ballot words per type
+
 struct SlotIO {
-  const double* IA[kMaxLevels];  // A pyramid (level 0 = frame A)
-  const double* WA[kMaxLevels];
+  double* IA[kMaxLevels];        // A pyramid (level 0 = frame A; levels >= 1 built on device)
+  double* WA[kMaxLevels];
   const double* IB;              // frame B, level 0
   const double* WB;
   double* fIA;                   // bilateral-filtered A (covariance pass)
   double* fWA;
   double* ib;                    // warped B at the current level (level-size maps)
   double* wb;
-  double* resI;                  // residuals compacted per K1 tile (row-major ranks)
-  double* resW;
-  int* cntI;                     // per K1 tile counts
+  uint8_t* amask[kMaxLevels];    // A-side jet validity per level pixel (bit0 photometric, bit1 depth)
+  uint8_t* amask_cov;            // same for the filtered A (covariance pass)
+  int* cntI;                     // per K1 tile counts (jets / depth jets)
   int* cntW;
+  unsigned* bitsI;               // per K1 tile validity bitmask [ntiles][kWordsPerTile]
+  unsigned* bitsW;
   double* part;                  // K3 partial sums [ntiles3][kNPart]
+  int build_pyr;                 // 1: this slot builds frame A's pyramid levels >= 1
 };
 
 struct SlotState {
@@ -94,6 +100,8 @@ void launch_solve(const AlignLaunch& a, const LevelInfo& li, const LevelInfo& li
 void launch_covariance(const AlignLaunch& a, const LevelInfo& li, cudaStream_t s);
 void launch_downsample2(const double* I, const double* W, int w, int h, double* oI, double* oW,
                         cudaStream_t s);
+void launch_pyramid_slots(const AlignLaunch& a, int levels, cudaStream_t s);
+void launch_amask(const AlignLaunch& a, int levels, int phase, cudaStream_t s);
 void launch_bilateral_pair(const AlignLaunch& a, double ss, double sr_i, double sr_w,
                            cudaStream_t s);
 void launch_bilateral(const double* img, int w, int h, double ss, double sr, double* out,
@@ -102,6 +110,8 @@ void launch_warp_maps(const double* IB, const double* WB, int wb, int hb, const 
                       int h, const WarpMats& m, double* oI, double* oW, double* omx, double* omy,
                       cudaStream_t s);
 int tdist_smem_bytes(int ntiles);
+int selftest_division(unsigned long long n, unsigned long long seed, unsigned long long* out,
+                      cudaStream_t s);
 int init_kernel_attributes();
 
 // Launch accounting + optional per-kernel CUDA-event timing.  Every library

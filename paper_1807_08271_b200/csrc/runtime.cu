@@ -52,6 +52,7 @@ struct rgbid_ctx {
   int cap_slots = 0, cap_w = 0, cap_h = 0;
   double* ws_f64 = nullptr;
   int* ws_i32 = nullptr;
+  uint8_t* ws_u8 = nullptr;
   SlotIO* d_io = nullptr;
   SlotState* d_st = nullptr;
   rgbid_iter_trace* d_trace = nullptr;
@@ -190,7 +191,7 @@ LevelInfo make_level(const rgbid_intrinsics& K0, int w0, int h0, int level) {
   li.tx = k1_tx(level);
   li.nseg = (li.w + li.tx - 1) / li.tx;
   li.ntiles = li.nseg * li.h;
-  li.ntiles3 = (li.w * li.h + kTPB - 1) / kTPB;
+  li.ntiles3 = (li.w * li.h + kTPB * kPixK3 - 1) / (kTPB * kPixK3);
   rgbid_intrinsics k;
   level_intrinsics(K0, level, &k);
   li.fx = k.fx;
@@ -212,21 +213,28 @@ PoseD pose_of(const rgbid_pose* p) {
   return pose_from(p->R, p->t);
 }
 
-// Per-slot workspace: ib, wb, resI, resW, fIA, fWA (N doubles each) + part; cntI/cntW ints.
-size_t slot_f64(int w, int h) {
-  const size_t N = (size_t)w * h;
-  const size_t part = (size_t)((N + kTPB - 1) / kTPB) * kNPart;
-  return 6 * N + part;
-}
-size_t slot_i32(int w, int h) {
+// Per-slot workspace: ib, wb, fIA, fWA (N doubles each) + K3 partials;
+// A-side masks (all levels + covariance pass); per-tile counts + validity bitmasks.
+size_t max_tiles(int w, int h) {
   size_t mx = 0;
   for (int l = 0; l < kMaxLevels; ++l) {
     if ((w >> l) < 1 || (h >> l) < 1) break;
     const int tx = k1_tx(l);
     mx = std::max(mx, (size_t)(((w >> l) + tx - 1) / tx) * (size_t)(h >> l));
   }
-  return 2 * mx;
+  return mx;
 }
+size_t slot_f64(int w, int h) {
+  const size_t N = (size_t)w * h;
+  const size_t part = (size_t)((N + kTPB * kPixK3 - 1) / (kTPB * kPixK3)) * kNPart;
+  return 4 * N + part;
+}
+size_t slot_u8(int w, int h) {
+  size_t t = (size_t)w * h;  // covariance-pass mask
+  for (int l = 0; l < kMaxLevels; ++l) t += (size_t)(w >> l) * (h >> l);
+  return (t + 255) & ~(size_t)255;
+}
+size_t slot_i32(int w, int h) { return 2 * max_tiles(w, h) * (1 + kWordsPerTile); }
 
 int ensure_workspace(rgbid_ctx* ctx, int nslots, int w, int h) {
   if (nslots <= ctx->cap_slots && w * h <= ctx->cap_w * ctx->cap_h && w == ctx->cap_w &&
@@ -234,11 +242,13 @@ int ensure_workspace(rgbid_ctx* ctx, int nslots, int w, int h) {
     return RGBID_OK;
   if (ctx->ws_f64) cudaFree(ctx->ws_f64);
   if (ctx->ws_i32) cudaFree(ctx->ws_i32);
+  if (ctx->ws_u8) cudaFree(ctx->ws_u8);
   if (ctx->d_io) cudaFree(ctx->d_io);
   if (ctx->d_st) cudaFree(ctx->d_st);
   if (ctx->h_st_pinned) cudaFreeHost(ctx->h_st_pinned);
   ctx->ws_f64 = nullptr;
   ctx->ws_i32 = nullptr;
+  ctx->ws_u8 = nullptr;
   ctx->d_io = nullptr;
   ctx->d_st = nullptr;
   ctx->h_st_pinned = nullptr;
@@ -247,6 +257,7 @@ int ensure_workspace(rgbid_ctx* ctx, int nslots, int w, int h) {
   ctx->graphs.clear();
   CK(cudaMalloc(&ctx->ws_f64, sizeof(double) * slot_f64(w, h) * nslots));
   CK(cudaMalloc(&ctx->ws_i32, sizeof(int) * slot_i32(w, h) * nslots));
+  CK(cudaMalloc(&ctx->ws_u8, slot_u8(w, h) * nslots));
   CK(cudaMalloc(&ctx->d_io, sizeof(SlotIO) * nslots));
   CK(cudaMalloc(&ctx->d_st, sizeof(SlotState) * nslots));
   CK(cudaMallocHost(&ctx->h_st_pinned, sizeof(SlotState) * nslots));
@@ -259,8 +270,7 @@ int ensure_workspace(rgbid_ctx* ctx, int nslots, int w, int h) {
   return RGBID_OK;
 }
 
-int frame_ensure_pyramid(rgbid_ctx* ctx, rgbid_frame* f, int levels) {
-  if (f->pyr_levels >= levels) return RGBID_OK;
+int frame_alloc_pyramid(rgbid_ctx* ctx, rgbid_frame* f) {
   if (!f->pyr) {
     size_t tot = 0;
     for (int l = 1; l < kMaxLevels; ++l) tot += 2 * (size_t)(f->w >> l) * (f->h >> l);
@@ -276,6 +286,13 @@ int frame_ensure_pyramid(rgbid_ctx* ctx, rgbid_frame* f, int levels) {
   }
   f->pI[0] = f->I;
   f->pW[0] = f->W;
+  return RGBID_OK;
+}
+
+int frame_ensure_pyramid(rgbid_ctx* ctx, rgbid_frame* f, int levels) {
+  if (f->pyr_levels >= levels) return RGBID_OK;
+  const int rc = frame_alloc_pyramid(ctx, f);
+  if (rc) return rc;
   for (int l = std::max(1, f->pyr_levels); l < levels; ++l)
     launch_downsample2(f->pI[l - 1], f->pW[l - 1], f->w >> (l - 1), f->h >> (l - 1), f->pI[l],
                        f->pW[l], ctx->stream);
@@ -338,6 +355,8 @@ int validate_cfg(const rgbid_align_config& c, int w, int h) {
 void enqueue_align(rgbid_ctx* ctx, const AlignLaunch& a, const rgbid_intrinsics& K,
                    const rgbid_align_config& cfg) {
   const LevelInfo li0 = make_level(K, a.w0, a.h0, 0);
+  launch_pyramid_slots(a, cfg.levels, ctx->stream);  // build_pyramid (src/alignment.cpp:369)
+  launch_amask(a, cfg.levels, 0, ctx->stream);        // A-side jet validity, once per align
   for (int level = cfg.levels - 1; level >= 0; --level) {
     const LevelInfo li = make_level(K, a.w0, a.h0, level);
     const int iters = level_iters(cfg, level);
@@ -351,6 +370,7 @@ void enqueue_align(rgbid_ctx* ctx, const AlignLaunch& a, const rgbid_intrinsics&
   // filtered_hessian_covariance — src/alignment.cpp:406-407, 411-436
   launch_bilateral_pair(a, cfg.bilateral_sigma_space, cfg.bilateral_sigma_intensity,
                         cfg.bilateral_sigma_depth, ctx->stream);
+  launch_amask(a, 1, 1, ctx->stream);
   launch_warp_residuals(a, li0, 1, ctx->stream);
   launch_tdist(a, li0, 1, ctx->stream);
   launch_normal_equations(a, li0, 1, ctx->stream);
@@ -366,11 +386,12 @@ int run_align_slots(rgbid_ctx* ctx, int n, const rgbid_frame* const* fa,
   int rc = ensure_workspace(ctx, std::max(n, ctx->cap_slots), w, h);
   if (rc) return rc;
   for (int i = 0; i < n; ++i) {
-    rc = frame_ensure_pyramid(ctx, const_cast<rgbid_frame*>(fa[i]), cfg.levels);
+    rc = frame_alloc_pyramid(ctx, const_cast<rgbid_frame*>(fa[i]));
     if (rc) return rc;
   }
   const size_t N = (size_t)w * h;
-  const size_t sf = slot_f64(w, h), si = slot_i32(w, h);
+  const size_t sf = slot_f64(w, h), si = slot_i32(w, h), su = slot_u8(w, h);
+  const size_t mt = max_tiles(w, h);
   const LevelInfo li0 = make_level(K, w, h, 0);
   const int nslots = n;
   for (int i = 0; i < nslots; ++i) {
@@ -387,13 +408,28 @@ int run_align_slots(rgbid_ctx* ctx, int n, const rgbid_frame* const* fa,
     double* base = ctx->ws_f64 + sf * i;
     o.ib = base;
     o.wb = base + N;
-    o.resI = base + 2 * N;
-    o.resW = base + 3 * N;
-    o.fIA = base + 4 * N;
-    o.fWA = base + 5 * N;
-    o.part = base + 6 * N;
-    o.cntI = ctx->ws_i32 + si * i;
-    o.cntW = o.cntI + si / 2;
+    o.fIA = base + 2 * N;
+    o.fWA = base + 3 * N;
+    o.part = base + 4 * N;
+    int* ib32 = ctx->ws_i32 + si * i;
+    o.cntI = ib32;
+    o.cntW = ib32 + mt;
+    o.bitsI = reinterpret_cast<unsigned*>(ib32 + 2 * mt);
+    o.bitsW = o.bitsI + mt * kWordsPerTile;
+    uint8_t* u8 = ctx->ws_u8 + su * i;
+    for (int l = 0; l < kMaxLevels; ++l) {
+      o.amask[l] = u8;
+      u8 += (size_t)(w >> l) * (h >> l);
+    }
+    o.amask_cov = u8;
+    // build frame A's pyramid in-graph unless cached (once per distinct frame)
+    o.build_pyr = 0;
+    if (fa[i]->pyr_levels < cfg.levels) {
+      bool first = true;
+      for (int j = 0; j < i; ++j)
+        if (fa[j] == fa[i]) first = false;
+      o.build_pyr = first ? 1 : 0;
+    }
     SlotState& s = ctx->h_st_pinned[i];
     std::memset(&s, 0, sizeof(s));
     const PoseD T = pose_of(inits ? &inits[i] : nullptr);
@@ -454,6 +490,9 @@ int run_align_slots(rgbid_ctx* ctx, int n, const rgbid_frame* const* fa,
   }
   rc = check_launch(ctx);
   if (rc) return rc;
+  for (int i = 0; i < nslots; ++i)
+    const_cast<rgbid_frame*>(fa[i])->pyr_levels =
+        std::max(const_cast<rgbid_frame*>(fa[i])->pyr_levels, cfg.levels);
   D2H(ctx->h_st_pinned, ctx->d_st, sizeof(SlotState) * nslots);
   CK(cudaStreamSynchronize(ctx->stream));
   if (want_trace) {
@@ -558,6 +597,7 @@ int rgbid_ctx_destroy(rgbid_ctx* ctx) {
   if (ctx->tmpB) rgbid_frame_destroy(ctx, ctx->tmpB);
   cudaFree(ctx->ws_f64);
   cudaFree(ctx->ws_i32);
+  cudaFree(ctx->ws_u8);
   cudaFree(ctx->d_io);
   cudaFree(ctx->d_st);
   cudaFree(ctx->d_trace);
@@ -739,7 +779,7 @@ int rgbid_align_batch(rgbid_ctx* ctx, int n, const rgbid_frame* const* a,
   cudaSetDevice(ctx->device);
   // chunk so the slot workspace stays bounded (~15 MB per VGA slot)
   const char* env = std::getenv("RGBID_BATCH_SLOTS");
-  int chunk = env ? std::max(1, atoi(env)) : 128;
+  int chunk = env ? std::max(1, atoi(env)) : 512;
   for (int i0 = 0; i0 < n; i0 += chunk) {
     const int m = std::min(chunk, n - i0);
     const int rc = run_align_slots(ctx, m, a + i0, b + i0, *K, inits ? inits + i0 : nullptr, c,
@@ -1053,6 +1093,13 @@ int rgbid_ctx_transfer_bytes(rgbid_ctx* ctx, long long* h2d, long long* d2h) {
   if (h2d) *h2d = ctx->h2d_bytes;
   if (d2h) *d2h = ctx->d2h_bytes;
   return RGBID_OK;
+}
+
+int rgbid_selftest_division(rgbid_ctx* ctx, unsigned long long n, unsigned long long seed,
+                            unsigned long long* mismatches) {
+  if (!ctx || !mismatches) return RGBID_E_ARG;
+  LaunchScope ls(ctx);
+  return selftest_division(n, seed, mismatches, ctx->stream) ? RGBID_E_CUDA : RGBID_OK;
 }
 
 int rgbid_frame_invalidate(rgbid_frame* f) {

@@ -272,6 +272,13 @@ def test_deterministic_replay(ctx):
     assert np.array_equal(r1.cov, r2.cov)
 
 
+def test_selftest_division_bitwise(ctx):
+    import ctypes as C
+    bad = C.c_ulonglong(0)
+    ctx.check(ctx.lib.rgbid_selftest_division(ctx.h, 200_000_000, 12345, C.byref(bad)), "selftest")
+    assert bad.value == 0
+
+
 def test_kernels_launched(ctx):
     K = rg.simple_intrinsics(80, 60)
     f = rg.render_plane(K, rg.Pose())
