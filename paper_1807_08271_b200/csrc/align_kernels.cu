@@ -76,7 +76,16 @@ __device__ __forceinline__ double bilinear(const double* __restrict__ img, int w
   return (1 - fy) * ((1 - fx) * v00 + fx * v10) + fy * ((1 - fx) * v01 + fx * v11);
 }
 
-// bilinear of I_B and W_B at the same point, sharing the tap setup
+// bilinear of I_B and W_B at the same point, sharing the tap setup.
+// Fast path: the interpolation formula is evaluated directly; it is finite only
+// if all four taps are finite (NaN/inf taps propagate through the products and
+// sums, including 0 * inf), so the explicit tap checks of inc/image.hpp:59 are
+// only needed when the result is non-finite — then the reference's hole (NaN)
+// is returned if any tap is invalid, else the (overflowed) formula value.
+__device__ __forceinline__ double bilin_fix(double r, double a, double b, double c, double d) {
+  if (isfinite(r)) return r;
+  return (valid(a) && valid(b) && valid(c) && valid(d)) ? r : CUDART_NAN;
+}
 __device__ __forceinline__ void bilinear2(const double* __restrict__ I, const double* __restrict__ W,
                                           int w, int h, double x, double y, double& oi,
                                           double& ow) {
@@ -84,16 +93,16 @@ __device__ __forceinline__ void bilinear2(const double* __restrict__ I, const do
   ow = CUDART_NAN;
   if (!(x >= 0.0 && x <= w - 1.0 && y >= 0.0 && y <= h - 1.0)) return;
   const int x0 = (int)floor(x), y0 = (int)floor(y);
-  const int x1 = min(x0 + 1, w - 1), y1 = min(y0 + 1, h - 1);
+  const int dx = x0 + 1 < w ? 1 : 0;        // x1 = min(x0 + 1, w - 1)
+  const int dy = y0 + 1 < h ? w : 0;        // y1 = min(y0 + 1, h - 1)
   const double fx = x - x0, fy = y - y0, gx = 1 - fx, gy = 1 - fy;
-  const size_t i00 = (size_t)y0 * w + x0, i10 = (size_t)y0 * w + x1;
-  const size_t i01 = (size_t)y1 * w + x0, i11 = (size_t)y1 * w + x1;
-  const double a00 = __ldg(I + i00), a10 = __ldg(I + i10), a01 = __ldg(I + i01), a11 = __ldg(I + i11);
-  const double b00 = __ldg(W + i00), b10 = __ldg(W + i10), b01 = __ldg(W + i01), b11 = __ldg(W + i11);
-  if (valid(a00) && valid(a10) && valid(a01) && valid(a11))
-    oi = gy * (gx * a00 + fx * a10) + fy * (gx * a01 + fx * a11);
-  if (valid(b00) && valid(b10) && valid(b01) && valid(b11))
-    ow = gy * (gx * b00 + fx * b10) + fy * (gx * b01 + fx * b11);
+  const int i00 = y0 * w + x0;
+  const double a00 = __ldg(I + i00), a10 = __ldg(I + i00 + dx), a01 = __ldg(I + i00 + dy),
+               a11 = __ldg(I + i00 + dy + dx);
+  const double b00 = __ldg(W + i00), b10 = __ldg(W + i00 + dx), b01 = __ldg(W + i00 + dy),
+               b11 = __ldg(W + i00 + dy + dx);
+  oi = bilin_fix(gy * (gx * a00 + fx * a10) + fy * (gx * a01 + fx * a11), a00, a10, a01, a11);
+  ow = bilin_fix(gy * (gx * b00 + fx * b10) + fy * (gx * b01 + fx * b11), b00, b10, b01, b11);
 }
 
 // one A pixel of inverse_geometric_warp — src/warping.cpp:96-111 (bit-identical)
@@ -207,7 +216,7 @@ __global__ void __launch_bounds__(kTPB) k_warp_residuals(const SlotIO* __restric
     reinterpret_cast<double*>(&wm)[threadIdx.x] = reinterpret_cast<const double*>(&S.wm)[threadIdx.x];
   const SlotIO& o = io[slot];
   const double* __restrict__ WAw = phase ? o.fWA : o.WA[0];
-  const uint8_t* __restrict__ am = phase ? o.amask_cov : o.amask[L];
+  const uint8_t* __restrict__ am = o.amask[L];  // level-0 entries rebuilt for phase 1
   const double* __restrict__ IB = o.IB;
   const double* __restrict__ WB = o.WB;
   __syncthreads();
@@ -227,38 +236,43 @@ __global__ void __launch_bounds__(kTPB) k_warp_residuals(const SlotIO* __restric
   } else {
     __shared__ double sI[2048], sW[2048];
     int cw = nx << L, ch = 1 << L;
-    const int npx = cw * ch;
-    for (int k = tid; k < npx; k += kTPB) {
-      const int r = k / cw, c = k - r * cw;
-      const int x = (xl0 << L) + c, y = (yl << L) + r;
-      double vi, vw;
-      warp_px(wm, IB, WB, w0, h0, x, y, __ldg(WAw + y * w0 + x), vi, vw, d0, d1);
-      sI[k] = vi;
-      sW[k] = vw;
+    // full-res block: cw = nx * 2^L <= 256 columns (one per thread) x 2^L rows
+    if (tid < cw) {
+      const int x = (xl0 << L) + tid;
+#pragma unroll
+      for (int r = 0; r < (1 << L); ++r) {
+        const int y = (yl << L) + r;
+        double vi, vw;
+        warp_px(wm, IB, WB, w0, h0, x, y, __ldg(WAw + y * w0 + x), vi, vw, d0, d1);
+        sI[r * cw + tid] = vi;
+        sW[r * cw + tid] = vw;
+      }
     }
     __syncthreads();
 #pragma unroll
     for (int s = 0; s < L; ++s) {
-      const int ow = cw >> 1, oh = ch >> 1, nout = ow * oh;
-      double oi[2], owv[2];
+      // stage s: (cw x ch) -> (cw/2 x ch/2); thread tid owns output column tid
+      const int ow = cw >> 1;
+      constexpr int kMaxOh = 1 << (L - 1);
+      const int oh = ch >> 1;
+      double oi[kMaxOh], owv[kMaxOh];
+      if (tid < ow) {
 #pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        const int k = tid + q * kTPB;
-        if (k < nout) {
-          const int r = k / ow, c = k - r * ow;
-          const int i0 = (2 * r) * cw + 2 * c, i1 = i0 + cw;
-          oi[q] = ds4(sI[i0], sI[i0 + 1], sI[i1], sI[i1 + 1]);
-          owv[q] = ds4(sW[i0], sW[i0 + 1], sW[i1], sW[i1 + 1]);
-        }
+        for (int r = 0; r < kMaxOh; ++r)
+          if (r < oh) {
+            const int i0 = (2 * r) * cw + 2 * tid, i1 = i0 + cw;
+            oi[r] = ds4(sI[i0], sI[i0 + 1], sI[i1], sI[i1 + 1]);
+            owv[r] = ds4(sW[i0], sW[i0 + 1], sW[i1], sW[i1 + 1]);
+          }
       }
       __syncthreads();
+      if (tid < ow) {
 #pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        const int k = tid + q * kTPB;
-        if (k < nout) {
-          sI[k] = oi[q];
-          sW[k] = owv[q];
-        }
+        for (int r = 0; r < kMaxOh; ++r)
+          if (r < oh) {
+            sI[r * ow + tid] = oi[r];
+            sW[r * ow + tid] = owv[r];
+          }
       }
       __syncthreads();
       cw = ow;
@@ -303,30 +317,36 @@ __global__ void __launch_bounds__(kTPB) k_warp_residuals(const SlotIO* __restric
   }
 }
 
-// A-side jet validity of one level pixel (src/alignment.cpp:209-211, 227)
-__global__ void k_amask(const SlotIO* __restrict__ io, const SlotState* __restrict__ st, int level,
-                        int w, int h, int phase) {
+// A-side part of residuals_and_jacobians, constant over the IRLS iterations:
+// validity (src/alignment.cpp:209-211,227) and gradient_at of I_A and W_A
+// (src/alignment.cpp:165-191) per level pixel.  phase 1 = from the filtered A
+// into the level-0 slots (covariance pass, after the level loop).
+__global__ void k_prep_A(const SlotIO* __restrict__ io, const SlotState* __restrict__ st, int level,
+                         int w, int h, int phase) {
   const int slot = blockIdx.y;
   if (st[slot].status != RGBID_OK) return;
   const SlotIO& o = io[slot];
   const double* IA = phase ? o.fIA : o.IA[level];
   const double* WA = phase ? o.fWA : o.WA[level];
-  uint8_t* out = phase ? o.amask_cov : o.amask[level];
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= w * h) return;
   const int y = k / w, x = k - y * w;
   const double w_a = WA[k], i_a = IA[k];
+  double g[4] = {0.0, 0.0, 0.0, 0.0};
   unsigned m = 0;
-  if (valid(w_a) && w_a > 0.0 && valid(i_a) && gradient_ok(IA, w, h, x, y)) m |= 1u;
-  if (gradient_ok(WA, w, h, x, y)) m |= 2u;
-  out[k] = (uint8_t)m;
+  if (valid(w_a) && w_a > 0.0 && valid(i_a) && gradient_at(IA, w, h, x, y, g[0], g[1])) m |= 1u;
+  if (gradient_at(WA, w, h, x, y, g[2], g[3])) m |= 2u;
+  o.amask[level][k] = (uint8_t)m;
+  double2* gp = reinterpret_cast<double2*>(o.agrad[level] + 4 * (size_t)k);
+  gp[0] = make_double2(g[0], g[1]);
+  gp[1] = make_double2(g[2], g[3]);
 }
 
 void launch_amask(const AlignLaunch& a, int levels, int phase, cudaStream_t s) {
   for (int l = 0; l < levels; ++l) {
     const int w = a.w0 >> l, h = a.h0 >> l;
-    KScope ks_("amask", s);
-    k_amask<<<dim3((w * h + 255) / 256, a.nslots), 256, 0, s>>>(a.io, a.st, l, w, h, phase);
+    KScope ks_("prep_A", s);
+    k_prep_A<<<dim3((w * h + 255) / 256, a.nslots), 256, 0, s>>>(a.io, a.st, l, w, h, phase);
   }
 }
 
@@ -354,8 +374,14 @@ void launch_pyramid_slots(const AlignLaunch& a, int levels, cudaStream_t s) {
   }
 }
 
+static const char* kLevelNames[2][kMaxLevels] = {
+    {"warp_residuals_L0", "warp_residuals_L1", "warp_residuals_L2", "warp_residuals_L3",
+     "warp_residuals_L4", "warp_residuals_L5"},
+    {"warp_residuals_cov", "warp_residuals_cov", "warp_residuals_cov", "warp_residuals_cov",
+     "warp_residuals_cov", "warp_residuals_cov"}};
+
 void launch_warp_residuals(const AlignLaunch& a, const LevelInfo& li, int phase, cudaStream_t s) {
-  KScope ks_("warp_residuals", s);
+  KScope ks_(kLevelNames[phase ? 1 : 0][li.level], s);
   dim3 grid(li.ntiles, a.nslots);
   switch (li.level) {
     case 0: k_warp_residuals<0><<<grid, kTPB, 0, s>>>(a.io, a.st, li, a.w0, a.h0, phase); break;
@@ -379,9 +405,15 @@ void launch_warp_residuals(const AlignLaunch& a, const LevelInfo& li, int phase,
 // rounding, well inside the 1e-4 normal-equation tolerance).
 constexpr int kSPT = (kMaxSample + kTdistThreads - 1) / kTdistThreads;
 
+// Block-wide sum; every thread receives the bit-identical total.  The scratch
+// has two halves used alternately (the caller's parity flips per call), so one
+// barrier per reduction suffices: a half is rewritten only two calls later,
+// after every thread has passed the intervening barrier.
 template <int NV, int NT>
-__device__ __forceinline__ void block_allsum(double (&v)[NV], double* scratch) {
+__device__ __forceinline__ void block_allsum(double (&v)[NV], double* scratch2, int& parity) {
   constexpr int NW = NT / 32;
+  double* scratch = scratch2 + parity * (NW * 2);
+  parity ^= 1;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1)
@@ -397,7 +429,6 @@ __device__ __forceinline__ void block_allsum(double (&v)[NV], double* scratch) {
   for (int off = 16; off > 0; off >>= 1)
 #pragma unroll
     for (int i = 0; i < NV; ++i) v[i] += __shfl_xor_sync(0xffffffffu, v[i], off);
-  __syncthreads();
 }
 
 struct TD {
@@ -406,75 +437,106 @@ struct TD {
 
 __device__ __forceinline__ double t_weight(double x, double nu) { return (nu + 1.0) / (nu + x * x); }
 
-// 1/q for q >= 1 (t_weight denominators): MUFU seed + cubic Newton step.
+// 1/q for q >= 1 (t_weight denominators): MUFU seed + cubic Newton step (full precision).
 __device__ __forceinline__ double rcp_fast(double q) {
   double r;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(q));
   const double e = fma(-q, r, 1.0);
   return fma(r, fma(e, e, e), r);
 }
+// 1/q for normal positive q: MUFU seed + one quadratic Newton step (~1e-12 relative;
+// used only inside sums whose order already differs from the reference).
+__device__ __forceinline__ double rcp_q(double q) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(q));
+  return fma(r, fma(-q, r, 1.0), r);
+}
 
 struct Sample {
-  const double* v;  // shared memory, kSPT strided slots per thread
+  const double* v;  // shared memory; thread t owns v[t], v[t + NT], ...
+  double* scratch;  // 2 x (NT/32 x 2) doubles for block_allsum
+  int parity;
   int m;
+  int kfull;        // rounds where every thread owns a sample (m / NT)
+  // memo of the last estimate_location_scale(nu) call: same sample + same nu
+  // -> same result (e.g. the final refit repeating estimate_nu's, src/alignment.cpp:117,316)
+  double memo_nu;
+  TD memo;
 };
 
-// estimate_location_scale on the register-resident sample — src/alignment.cpp:61-101
+// sum over the thread's samples of f(v) into NACC accumulators (breaks the
+// add dependency chain); fixed assignment -> deterministic
+template <int NT, int NV, typename F>
+__device__ __forceinline__ void sample_sum(const Sample& S, double (&acc)[NV], F f) {
+  double a0[NV], a1[NV];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) a0[i] = a1[i] = 0.0;
+  const double* v = S.v + threadIdx.x;
+  int k = 0;
+#pragma unroll 2
+  for (; k + 1 < S.kfull; k += 2) {
+    f(v[k * NT], a0);
+    f(v[(k + 1) * NT], a1);
+  }
+  for (; k < kSPT; ++k)
+    if (k * NT + (int)threadIdx.x < S.m) f(v[k * NT], a0);
+#pragma unroll
+  for (int i = 0; i < NV; ++i) acc[i] = a0[i] + a1[i];
+}
+
+// estimate_location_scale on the shared-memory sample — src/alignment.cpp:61-101
 template <int NT>
-__device__ __forceinline__ TD loc_scale(const Sample& S, double nu, double* scratch) {
+__device__ __forceinline__ TD loc_scale(Sample& S, double nu, double* scratch) {
   TD p{0.0, 1.0, nu};
   const int m = S.m;
   if (m == 0) return p;
-  const int tid = threadIdx.x;
+  if (S.memo_nu == nu) return S.memo;
   const double inv_m = 1.0 / (double)m;
-  double a1[1] = {0.0};
-#pragma unroll
-  for (int k = 0; k < kSPT; ++k)
-    if (k * NT + tid < m) a1[0] += S.v[k * NT + tid];
-  block_allsum<1, NT>(a1, scratch);
-  double mu = a1[0] / (double)m;
-  a1[0] = 0.0;
-#pragma unroll
-  for (int k = 0; k < kSPT; ++k)
-    if (k * NT + tid < m) {
-      const double d = S.v[k * NT + tid] - mu;
-      a1[0] = fma(d, d, a1[0]);
-    }
-  block_allsum<1, NT>(a1, scratch);
+  double a1[1];
+  sample_sum<NT>(S, a1, [](double v, double (&a)[1]) { a[0] += v; });
+  block_allsum<1, NT>(a1, S.scratch, S.parity);
+  const double mu0 = a1[0] / (double)m;
+  sample_sum<NT>(S, a1, [mu0](double v, double (&a)[1]) {
+    const double d = v - mu0;
+    a[0] = fma(d, d, a[0]);
+  });
+  block_allsum<1, NT>(a1, S.scratch, S.parity);
+  double mu = mu0;
   double sigma = sqrt(a1[0] / (double)m);
-  if (sigma < 1e-8) return TD{mu, 1e-8, nu};
-  const double nu1 = nu + 1.0;
-  for (int it = 0; it < 50; ++it) {
-    const double isg = 1.0 / sigma;
-    double a2[2] = {0.0, 0.0};
-#pragma unroll
-    for (int k = 0; k < kSPT; ++k)
-      if (k * NT + tid < m) {
-        const double v = S.v[k * NT + tid];
-        const double x = (v - mu) * isg;
-        const double w = nu1 * rcp_fast(fma(x, x, nu));
-        a2[0] += w;
-        a2[1] = fma(w, v, a2[1]);
-      }
-    block_allsum<2, NT>(a2, scratch);
-    const double mu_new = a2[1] / a2[0];
-    a1[0] = 0.0;
-#pragma unroll
-    for (int k = 0; k < kSPT; ++k)
-      if (k * NT + tid < m) {
-        const double d = S.v[k * NT + tid] - mu_new;
-        const double x = d * isg;
-        const double w = nu1 * rcp_fast(fma(x, x, nu));
-        a1[0] = fma(w * d, d, a1[0]);
-      }
-    block_allsum<1, NT>(a1, scratch);
-    const double sigma_new = dmax_std(1e-8, sqrt(a1[0] * inv_m));
-    const double rel = fabs(sigma_new - sigma) / sigma;
-    mu = mu_new;
-    sigma = sigma_new;
-    if (rel < 1e-4) break;
+  TD out;
+  if (sigma < 1e-8) {
+    out = TD{mu, 1e-8, nu};
+  } else {
+    const double nu1 = nu + 1.0;
+    for (int it = 0; it < 50; ++it) {
+      // t_weight((v-mu)/sigma, nu) = (nu+1) s2 / (nu s2 + (v-mu)^2), s2 = sigma^2
+      const double s2 = sigma * sigma, c1 = nu * s2, c2 = nu1 * s2;
+      double a2[2];
+      sample_sum<NT>(S, a2, [mu, c1, c2](double v, double (&a)[2]) {
+        const double d = v - mu;
+        const double w = c2 * rcp_q(fma(d, d, c1));
+        a[0] += w;
+        a[1] = fma(w, v, a[1]);
+      });
+      block_allsum<2, NT>(a2, S.scratch, S.parity);
+      const double mu_new = a2[1] / a2[0];
+      sample_sum<NT>(S, a1, [mu_new, c1, c2](double v, double (&a)[1]) {
+        const double d = v - mu_new;
+        const double w = c2 * rcp_q(fma(d, d, c1));
+        a[0] = fma(w * d, d, a[0]);
+      });
+      block_allsum<1, NT>(a1, S.scratch, S.parity);
+      const double sigma_new = dmax_std(1e-8, sqrt(a1[0] * inv_m));
+      const double rel = fabs(sigma_new - sigma) / sigma;
+      mu = mu_new;
+      sigma = sigma_new;
+      if (rel < 1e-4) break;
+    }
+    out = TD{mu, dmax_std(sigma, 1e-8), nu};
   }
-  return TD{mu, dmax_std(sigma, 1e-8), nu};
+  S.memo_nu = nu;
+  S.memo = out;
+  return out;
 }
 
 // digamma — src/alignment.cpp:32-43
@@ -493,26 +555,24 @@ __device__ __forceinline__ double digamma_d(double x) {
 // stationarity of solve_nu — src/alignment.cpp:132-141 (the nu-only part C hoisted;
 // per-sample term (C + log w) - w as in the reference).
 template <int NT>
-__device__ __forceinline__ double stationarity(const Sample& S, double mu, double sigma, double nu,
-                               double* scratch) {
+__device__ __forceinline__ double stationarity(Sample& S, double mu, double sigma, double nu,
+                                               double* scratch) {
   const double C = (((-digamma_d(nu / 2.0) + log(nu / 2.0)) + digamma_d((nu + 1.0) / 2.0)) -
                     log((nu + 1.0) / 2.0)) + 1.0;
-  const double isg = 1.0 / sigma, nu1 = nu + 1.0;
-  double a[1] = {0.0};
-#pragma unroll
-  for (int k = 0; k < kSPT; ++k)
-    if (k * NT + threadIdx.x < S.m) {
-      const double x = (S.v[k * NT + threadIdx.x] - mu) * isg;
-      const double w = nu1 * rcp_fast(fma(x, x, nu));
-      a[0] += (C + log(w)) - w;
-    }
-  block_allsum<1, NT>(a, scratch);
+  const double s2 = sigma * sigma, c1 = nu * s2, c2 = (nu + 1.0) * s2;
+  double a[1];
+  sample_sum<NT>(S, a, [mu, c1, c2, C](double v, double (&acc)[1]) {
+    const double d = v - mu;
+    const double w = c2 * rcp_fast(fma(d, d, c1));
+    acc[0] += (C + log(w)) - w;
+  });
+  block_allsum<1, NT>(a, S.scratch, S.parity);
   return a[0] / (double)S.m;
 }
 
 // solve_nu — src/alignment.cpp:131-157
 template <int NT>
-__device__ __forceinline__ double solve_nu(const Sample& S, double mu, double sigma, double* scratch) {
+__device__ __forceinline__ double solve_nu(Sample& S, double mu, double sigma, double* scratch) {
   double lo = 2.0, hi = 10.0;
   double flo = stationarity<NT>(S, mu, sigma, lo, scratch);
   const double fhi = stationarity<NT>(S, mu, sigma, hi, scratch);
@@ -532,7 +592,7 @@ __device__ __forceinline__ double solve_nu(const Sample& S, double mu, double si
 
 // estimate_nu — src/alignment.cpp:109-127
 template <int NT>
-__device__ __forceinline__ double estimate_nu(const Sample& S, double mu, double sigma, double* scratch) {
+__device__ __forceinline__ double estimate_nu(Sample& S, double mu, double sigma, double* scratch) {
   if (S.m == 0 || sigma <= 0.0) return 5.0;
   double nu = solve_nu<NT>(S, mu, sigma, scratch);
   for (int it = 0; it < 2 && nu < 9.99; ++it) {
@@ -550,7 +610,7 @@ __device__ __forceinline__ double estimate_nu(const Sample& S, double mu, double
 
 int tdist_smem_bytes(int ntiles) { return kMaxSample * 8 + (ntiles + 1) * 4; }
 
-__global__ void __launch_bounds__(kTdistThreads, 1)
+__global__ void __launch_bounds__(kTdistThreads, 2)
     k_tdist(const SlotIO* __restrict__ io, SlotState* __restrict__ st, LevelInfo li, int phase) {
   constexpr int NT = kTdistThreads;
   const int type = blockIdx.x, slot = blockIdx.y;
@@ -565,7 +625,7 @@ __global__ void __launch_bounds__(kTdistThreads, 1)
   double* smp_sh = dsm;
   int* offs = reinterpret_cast<int*>(dsm + kMaxSample);
   __shared__ int wsum[NT / 32];
-  __shared__ double scratch[NT / 32 * 2];
+  __shared__ double scratch[NT / 32 * 2 * 2];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int nt = li.ntiles;
 
@@ -601,6 +661,10 @@ __global__ void __launch_bounds__(kTdistThreads, 1)
   Sample smp;
   smp.v = smp_sh;
   smp.m = n == 0 ? 0 : (int)((n - 1) / stride + 1);
+  smp.kfull = smp.m / NT;
+  smp.memo_nu = -1.0;
+  smp.scratch = scratch;
+  smp.parity = 0;
   for (int k = 0; k < kSPT; ++k) {
     const int s = k * NT + tid;
     if (s < smp.m) {
@@ -704,36 +768,41 @@ __device__ __forceinline__ void accum(double (&acc)[kNPart], const double (&J)[6
   acc[27] = fma(w * r, r, acc[27]);
 }
 
-__global__ void __launch_bounds__(kTPB) k_normal_eq(const SlotIO* __restrict__ io,
+__global__ void __launch_bounds__(kTPB, 2) k_normal_eq(const SlotIO* __restrict__ io,
                                                     const SlotState* __restrict__ st, LevelInfo li,
                                                     int phase, double lambda_n_min) {
   const int slot = blockIdx.y;
   const SlotState& S = st[slot];
   if (!slot_active(S, li.level, phase)) return;
   const SlotIO& o = io[slot];
-  const double* IA = phase ? o.fIA : o.IA[li.level];
-  const double* WA = phase ? o.fWA : o.WA[li.level];
+  const double* __restrict__ IA = phase ? o.fIA : o.IA[li.level];
+  const double* __restrict__ WA = phase ? o.fWA : o.WA[li.level];
+  const uint8_t* __restrict__ am = o.amask[li.level];
+  const double2* __restrict__ ag = reinterpret_cast<const double2*>(o.agrad[li.level]);
+  const double* __restrict__ ibp = o.ib;
+  const double* __restrict__ wbp = o.wb;
   __shared__ double scratch[(kTPB / 32) * kNPart];
   const double muI = S.tI.mu, isgI = 1.0 / S.tI.sigma, nuI = dmax_std(S.tI.nu, S.tW.nu);
   const double muW = S.tW.mu, isgW = 1.0 / S.tW.sigma, nuW = S.tW.nu;
   const double nuI1 = nuI + 1.0, nuW1 = nuW + 1.0;
   const double is2i = isgI * isgI, is2w = isgW * isgW;
-  const int w = li.w, h = li.h;
+  const int w = li.w;
   const double* Ki = li.Kinv;
   double acc[kNPart];
 #pragma unroll
   for (int i = 0; i < kNPart; ++i) acc[i] = 0.0;
-  const long long N = (long long)w * h;
+  const int N = li.w * li.h;
 #pragma unroll 1
   for (int p = 0; p < kPixK3; ++p) {
-    const long long k = ((long long)blockIdx.x * kPixK3 + p) * kTPB + threadIdx.x;
+    const int k = (blockIdx.x * kPixK3 + p) * kTPB + threadIdx.x;
     if (k >= N) break;
-    const int y = (int)(k / w), x = (int)(k - (long long)y * w);
-    const double i_b = o.ib[k], w_b = o.wb[k];
+    const unsigned a = am[k];
+    if (!(a & 1u)) continue;
+    const double i_b = ibp[k];
+    if (!valid(i_b)) continue;
     const double w_a = __ldg(WA + k), i_a = __ldg(IA + k);
-    if (!valid(w_a) || w_a <= 0.0 || !valid(i_a) || !valid(i_b)) continue;
-    double gix, giy;
-    if (!gradient_at(IA, w, h, x, y, gix, giy)) continue;
+    const double2 gI = __ldg(ag + 2 * k);
+    const int y = k / w, x = k - y * w;
     const double px = x, py = y;
     const double ax = li.cx - px, ay = li.cy - py;  // A(0,2), A(1,2)
     const double iwa = 1.0 / w_a;
@@ -743,7 +812,7 @@ __global__ void __launch_bounds__(kTPB) k_normal_eq(const SlotIO* __restrict__ i
     // photometric row: u = w_a (gix, giy, 0) A ; J_I = (u, X x u)
     double J[6];
     {
-      const double s0 = w_a * gix, s1 = w_a * giy;
+      const double s0 = w_a * gI.x, s1 = w_a * gI.y;
       const double u0 = s0 * li.fx, u1 = s1 * li.fy, u2 = s0 * ax + s1 * ay;
       J[0] = u0;
       J[1] = u1;
@@ -756,10 +825,11 @@ __global__ void __launch_bounds__(kTPB) k_normal_eq(const SlotIO* __restrict__ i
       const double wi = nuI1 * rcp_fast(fma(xi_, xi_, nuI)) * is2i;
       accum(acc, J, wi, rI);
     }
-    double gwx, gwy;
-    if (!(valid(w_b) && w_b > 0.0 && gradient_at(WA, w, h, x, y, gwx, gwy))) continue;
+    const double w_b = wbp[k];
+    if (!((a & 2u) && valid(w_b) && w_b > 0.0)) continue;
+    const double2 gW = __ldg(ag + 2 * k + 1);
     // geometric row: s = w_a (g_W A + w_b e_z) ; J_W = (s, X x s)
-    const double g0 = gwx * li.fx, g1 = gwy * li.fy, g2 = gwx * ax + gwy * ay;
+    const double g0 = gW.x * li.fx, g1 = gW.y * li.fy, g2 = gW.x * ax + gW.y * ay;
     {
       const double s0 = w_a * g0, s1 = w_a * g1, s2 = w_a * (g2 + w_b);
       J[0] = s0;
@@ -789,8 +859,11 @@ __global__ void __launch_bounds__(kTPB) k_normal_eq(const SlotIO* __restrict__ i
   block_sum_to<kTPB>(acc, o.part + (size_t)blockIdx.x * kNPart, scratch);
 }
 
+static const char* kNeNames[kMaxLevels] = {"normal_eq_L0", "normal_eq_L1", "normal_eq_L2",
+                                            "normal_eq_L3", "normal_eq_L4", "normal_eq_L5"};
+
 void launch_normal_equations(const AlignLaunch& a, const LevelInfo& li, int phase, cudaStream_t s) {
-  KScope ks_("normal_eq", s);
+  KScope ks_(phase ? "normal_eq_cov" : kNeNames[li.level], s);
   k_normal_eq<<<dim3(li.ntiles3, a.nslots), kTPB, 0, s>>>(a.io, a.st, li, phase, a.lambda_n_min);
 }
 

@@ -16,10 +16,10 @@ namespace rgbid_b200 {
 constexpr int kMaxLevels = 6;       // GPU supports levels <= 6 (80x60 at level 3 for VGA)
 constexpr int kMaxSample = 19200;   // src/alignment.cpp:47
 constexpr int kTPB = 256;           // warp/residual/normal-equation kernels
-constexpr int kTdistThreads = 1024; // Student-t kernel (sample in shared memory)
+constexpr int kTdistThreads = 512;  // Student-t kernel (sample in shared memory)
 constexpr int kNPart = 28;          // 21 (lower H) + 6 (b) + 1 (cost)
 constexpr int kTraceMax = 64;
-constexpr int kPixK3 = 4;           // pixels per thread in the normal-equation kernel
+constexpr int kPixK3 = 8;           // pixels per thread in the normal-equation kernel
 
 // K1 tiling of level l: tile = (level row, segment of tx level pixels).
 // Full-res pixels per tile = tx * 4^l <= 2048 (smem staging of the warp).
@@ -51,7 +51,9 @@ struct SlotIO {
   double* ib;                    // warped B at the current level (level-size maps)
   double* wb;
   uint8_t* amask[kMaxLevels];    // A-side jet validity per level pixel (bit0 photometric, bit1 depth)
-  uint8_t* amask_cov;            // same for the filtered A (covariance pass)
+  double* agrad[kMaxLevels];     // A-side gradients per level pixel {gI_x, gI_y, gW_x, gW_y}
+                                 // (level-0 entries are rebuilt from the filtered A for the
+                                 //  covariance pass)
   int* cntI;                     // per K1 tile counts (jets / depth jets)
   int* cntW;
   unsigned* bitsI;               // per K1 tile validity bitmask [ntiles][kWordsPerTile]

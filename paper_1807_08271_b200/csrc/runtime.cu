@@ -32,6 +32,8 @@ struct rgbid_frame {
   double* pI[kMaxLevels] = {};
   double* pW[kMaxLevels] = {};
   int pyr_levels = 0;  // levels currently valid (0 = none built)
+  int pyr_lane = -1;   // lane whose chunk (sequence pyr_seq) builds/built the pyramid
+  unsigned long long pyr_seq = 0;
 };
 
 namespace {
@@ -43,30 +45,46 @@ struct CachedGraph {
 
 }  // namespace
 
-struct rgbid_ctx {
-  int device = 0;
+// One execution lane of the alignment driver: a stream, a slot workspace and the
+// CUDA graphs captured on it.  Batches alternate chunks over the lanes so that
+// the FP64-bound Student-t kernels of one chunk overlap the memory/latency-bound
+// warp and normal-equation kernels of the other.
+struct Lane {
   cudaStream_t stream = nullptr;
-  std::string err;
-  long long launches = 0;
-  // slot workspace
+  cudaEvent_t done = nullptr;
   int cap_slots = 0, cap_w = 0, cap_h = 0;
   double* ws_f64 = nullptr;
   int* ws_i32 = nullptr;
   uint8_t* ws_u8 = nullptr;
   SlotIO* d_io = nullptr;
   SlotState* d_st = nullptr;
-  rgbid_iter_trace* d_trace = nullptr;
   std::vector<SlotIO> h_io;
-  std::vector<SlotState> h_st;
   SlotState* h_st_pinned = nullptr;
-  std::vector<rgbid_iter_trace> last_trace;
-  // graph cache for the align launch sequence
   std::map<std::string, CachedGraph> graphs;
+  // chunk in flight
+  int pend_n = 0;
+  rgbid_align_result* pend_results = nullptr;
+  int pend_levels = 0;
+  bool pend_trace = false;
+  unsigned long long seq = 0;  // chunks enqueued on this lane
+};
+constexpr int kLanes = 2;
+
+struct rgbid_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;  // == lanes[0].stream
+  std::string err;
+  long long launches = 0;
+  Lane lanes[kLanes];
+  rgbid_iter_trace* d_trace = nullptr;
+  std::vector<rgbid_iter_trace> last_trace;
   bool use_graphs = true;
   // scratch device buffers for the one-shot host APIs
   std::map<std::string, std::pair<void*, size_t>> scratch;
   rgbid_frame* tmpA = nullptr;
   rgbid_frame* tmpB = nullptr;
+  // device frames reused by rgbid_align_batch_host across calls ([lane][slot] A/B)
+  std::vector<rgbid_frame*> host_fa[2], host_fb[2];
   // profiling (per-kernel CUDA-event times) and host<->device byte counters
   Profiler prof;
   std::map<std::string, std::pair<long long, double>> kstats;  // name -> (launches, ms)
@@ -108,6 +126,16 @@ struct LaunchScope {  // routes launch accounting / profiling to this ctx
   do {                                                                                    \
     CK(cudaMemcpyAsync((dst), (src), (bytes), cudaMemcpyHostToDevice, ctx->stream)); \
     ctx->h2d_bytes += (long long)(bytes);                                                 \
+  } while (0)
+#define H2DS(st, dst, src, bytes)                                                         \
+  do {                                                                                    \
+    CK(cudaMemcpyAsync((dst), (src), (bytes), cudaMemcpyHostToDevice, (st)));             \
+    ctx->h2d_bytes += (long long)(bytes);                                                 \
+  } while (0)
+#define D2HS(st, dst, src, bytes)                                                         \
+  do {                                                                                    \
+    CK(cudaMemcpyAsync((dst), (src), (bytes), cudaMemcpyDeviceToHost, (st)));             \
+    ctx->d2h_bytes += (long long)(bytes);                                                 \
   } while (0)
 #define D2H(dst, src, bytes)                                                              \
   do {                                                                                    \
@@ -224,49 +252,51 @@ size_t max_tiles(int w, int h) {
   }
   return mx;
 }
+size_t pyr_pixels(int w, int h) {
+  size_t t = 0;
+  for (int l = 0; l < kMaxLevels; ++l) t += (size_t)(w >> l) * (h >> l);
+  return t;
+}
 size_t slot_f64(int w, int h) {
   const size_t N = (size_t)w * h;
   const size_t part = (size_t)((N + kTPB * kPixK3 - 1) / (kTPB * kPixK3)) * kNPart;
-  return 4 * N + part;
+  return 4 * N + 4 * pyr_pixels(w, h) + part;
 }
-size_t slot_u8(int w, int h) {
-  size_t t = (size_t)w * h;  // covariance-pass mask
-  for (int l = 0; l < kMaxLevels; ++l) t += (size_t)(w >> l) * (h >> l);
-  return (t + 255) & ~(size_t)255;
-}
+size_t slot_u8(int w, int h) { return (pyr_pixels(w, h) + 255) & ~(size_t)255; }
 size_t slot_i32(int w, int h) { return 2 * max_tiles(w, h) * (1 + kWordsPerTile); }
 
-int ensure_workspace(rgbid_ctx* ctx, int nslots, int w, int h) {
-  if (nslots <= ctx->cap_slots && w * h <= ctx->cap_w * ctx->cap_h && w == ctx->cap_w &&
-      h == ctx->cap_h)
-    return RGBID_OK;
-  if (ctx->ws_f64) cudaFree(ctx->ws_f64);
-  if (ctx->ws_i32) cudaFree(ctx->ws_i32);
-  if (ctx->ws_u8) cudaFree(ctx->ws_u8);
-  if (ctx->d_io) cudaFree(ctx->d_io);
-  if (ctx->d_st) cudaFree(ctx->d_st);
-  if (ctx->h_st_pinned) cudaFreeHost(ctx->h_st_pinned);
-  ctx->ws_f64 = nullptr;
-  ctx->ws_i32 = nullptr;
-  ctx->ws_u8 = nullptr;
-  ctx->d_io = nullptr;
-  ctx->d_st = nullptr;
-  ctx->h_st_pinned = nullptr;
-  ctx->cap_slots = 0;
-  for (auto& g : ctx->graphs) cudaGraphExecDestroy(g.second.exec);
-  ctx->graphs.clear();
-  CK(cudaMalloc(&ctx->ws_f64, sizeof(double) * slot_f64(w, h) * nslots));
-  CK(cudaMalloc(&ctx->ws_i32, sizeof(int) * slot_i32(w, h) * nslots));
-  CK(cudaMalloc(&ctx->ws_u8, slot_u8(w, h) * nslots));
-  CK(cudaMalloc(&ctx->d_io, sizeof(SlotIO) * nslots));
-  CK(cudaMalloc(&ctx->d_st, sizeof(SlotState) * nslots));
-  CK(cudaMallocHost(&ctx->h_st_pinned, sizeof(SlotState) * nslots));
+void free_lane_ws(Lane& L) {
+  if (L.ws_f64) cudaFree(L.ws_f64);
+  if (L.ws_i32) cudaFree(L.ws_i32);
+  if (L.ws_u8) cudaFree(L.ws_u8);
+  if (L.d_io) cudaFree(L.d_io);
+  if (L.d_st) cudaFree(L.d_st);
+  if (L.h_st_pinned) cudaFreeHost(L.h_st_pinned);
+  L.ws_f64 = nullptr;
+  L.ws_i32 = nullptr;
+  L.ws_u8 = nullptr;
+  L.d_io = nullptr;
+  L.d_st = nullptr;
+  L.h_st_pinned = nullptr;
+  L.cap_slots = 0;
+  for (auto& g : L.graphs) cudaGraphExecDestroy(g.second.exec);
+  L.graphs.clear();
+}
+
+int ensure_workspace(rgbid_ctx* ctx, Lane& L, int nslots, int w, int h) {
+  if (nslots <= L.cap_slots && w == L.cap_w && h == L.cap_h) return RGBID_OK;
+  free_lane_ws(L);
+  CK(cudaMalloc(&L.ws_f64, sizeof(double) * slot_f64(w, h) * nslots));
+  CK(cudaMalloc(&L.ws_i32, sizeof(int) * slot_i32(w, h) * nslots));
+  CK(cudaMalloc(&L.ws_u8, slot_u8(w, h) * nslots));
+  CK(cudaMalloc(&L.d_io, sizeof(SlotIO) * nslots));
+  CK(cudaMalloc(&L.d_st, sizeof(SlotState) * nslots));
+  CK(cudaMallocHost(&L.h_st_pinned, sizeof(SlotState) * nslots));
   if (!ctx->d_trace) CK(cudaMalloc(&ctx->d_trace, sizeof(rgbid_iter_trace) * kTraceMax));
-  ctx->cap_slots = nslots;
-  ctx->cap_w = w;
-  ctx->cap_h = h;
-  ctx->h_io.resize(nslots);
-  ctx->h_st.resize(nslots);
+  L.cap_slots = nslots;
+  L.cap_w = w;
+  L.cap_h = h;
+  L.h_io.resize(nslots);
   return RGBID_OK;
 }
 
@@ -352,38 +382,80 @@ int validate_cfg(const rgbid_align_config& c, int w, int h) {
 }
 
 // Enqueue the whole align (all levels + covariance pass) for ctx->cap slots.
-void enqueue_align(rgbid_ctx* ctx, const AlignLaunch& a, const rgbid_intrinsics& K,
+void enqueue_align(cudaStream_t stream, const AlignLaunch& a, const rgbid_intrinsics& K,
                    const rgbid_align_config& cfg) {
   const LevelInfo li0 = make_level(K, a.w0, a.h0, 0);
-  launch_pyramid_slots(a, cfg.levels, ctx->stream);  // build_pyramid (src/alignment.cpp:369)
-  launch_amask(a, cfg.levels, 0, ctx->stream);        // A-side jet validity, once per align
+  launch_pyramid_slots(a, cfg.levels, stream);  // build_pyramid (src/alignment.cpp:369)
+  launch_amask(a, cfg.levels, 0, stream);        // A-side jet validity, once per align
   for (int level = cfg.levels - 1; level >= 0; --level) {
     const LevelInfo li = make_level(K, a.w0, a.h0, level);
     const int iters = level_iters(cfg, level);
     for (int it = 0; it < iters; ++it) {
-      launch_warp_residuals(a, li, 0, ctx->stream);
-      launch_tdist(a, li, 0, ctx->stream);
-      launch_normal_equations(a, li, 0, ctx->stream);
-      launch_solve(a, li, li0, ctx->stream);
+      launch_warp_residuals(a, li, 0, stream);
+      launch_tdist(a, li, 0, stream);
+      launch_normal_equations(a, li, 0, stream);
+      launch_solve(a, li, li0, stream);
     }
   }
   // filtered_hessian_covariance — src/alignment.cpp:406-407, 411-436
   launch_bilateral_pair(a, cfg.bilateral_sigma_space, cfg.bilateral_sigma_intensity,
-                        cfg.bilateral_sigma_depth, ctx->stream);
-  launch_amask(a, 1, 1, ctx->stream);
-  launch_warp_residuals(a, li0, 1, ctx->stream);
-  launch_tdist(a, li0, 1, ctx->stream);
-  launch_normal_equations(a, li0, 1, ctx->stream);
-  launch_covariance(a, li0, ctx->stream);
+                        cfg.bilateral_sigma_depth, stream);
+  launch_amask(a, 1, 1, stream);
+  launch_warp_residuals(a, li0, 1, stream);
+  launch_tdist(a, li0, 1, stream);
+  launch_normal_equations(a, li0, 1, stream);
+  launch_covariance(a, li0, stream);
 }
 
-// Run n alignments (n <= cap) whose frames are given; fills results.
-int run_align_slots(rgbid_ctx* ctx, int n, const rgbid_frame* const* fa,
-                    const rgbid_frame* const* fb, const rgbid_intrinsics& K,
-                    const rgbid_pose* inits, const rgbid_align_config& cfg,
-                    rgbid_align_result* results, bool want_trace) {
+// Unpacks the SlotState records of a lane's finished chunk into results.
+int finish_chunk(rgbid_ctx* ctx, Lane& L) {
+  if (L.pend_n == 0) return RGBID_OK;
+  CK(cudaEventSynchronize(L.done));
+  if (L.pend_trace) {
+    ctx->last_trace.resize(kTraceMax);
+    CK(cudaMemcpy(ctx->last_trace.data(), ctx->d_trace, sizeof(rgbid_iter_trace) * kTraceMax,
+                  cudaMemcpyDeviceToHost));
+    ctx->last_trace.resize(std::min(L.h_st_pinned[0].trace_n, kTraceMax));
+  }
+  for (int i = 0; i < L.pend_n; ++i) {
+    const SlotState& s = L.h_st_pinned[i];
+    rgbid_align_result& r = L.pend_results[i];
+    std::memset(&r, 0, sizeof(r));
+    r.status = s.status;
+    if (s.status == RGBID_E_DEGENERATE) {
+      spectrum_of(s.H, s.nI, r.spectrum);
+      continue;
+    }
+    std::memcpy(r.T_AB.R, s.R, sizeof(s.R));
+    std::memcpy(r.T_AB.t, s.t, sizeof(s.t));
+    std::memcpy(r.cov, s.cov, sizeof(s.cov));
+    r.converged = 1;
+    r.cov_degenerate = s.cov_degenerate;
+    r.n_levels = L.pend_levels;
+    for (int k = 0; k < L.pend_levels; ++k) {
+      const int level = L.pend_levels - 1 - k;
+      r.level_log[k].level = level;
+      r.level_log[k].iterations = s.iters[level];
+      r.level_log[k].final_cost = s.cost[level];
+    }
+    r.tdist_intensity = s.finI;
+    r.tdist_depth = s.finW;
+    r.total_iterations = s.total_iters;
+  }
+  L.pend_n = 0;
+  return RGBID_OK;
+}
+
+// Enqueues n alignments (one chunk) on lane L: slot setup, H2D of the slot
+// records, the (cached) CUDA graph of the whole align, D2H of the results.
+int enqueue_chunk(rgbid_ctx* ctx, Lane& L, int n, const rgbid_frame* const* fa,
+                  const rgbid_frame* const* fb, const rgbid_intrinsics& K,
+                  const rgbid_pose* inits, const rgbid_align_config& cfg,
+                  rgbid_align_result* results, bool want_trace) {
+  int rc = finish_chunk(ctx, L);  // the lane's previous chunk owns h_st_pinned
+  if (rc) return rc;
   const int w = fa[0]->w, h = fa[0]->h;
-  int rc = ensure_workspace(ctx, std::max(n, ctx->cap_slots), w, h);
+  rc = ensure_workspace(ctx, L, std::max(n, L.cap_slots), w, h);
   if (rc) return rc;
   for (int i = 0; i < n; ++i) {
     rc = frame_alloc_pyramid(ctx, const_cast<rgbid_frame*>(fa[i]));
@@ -395,7 +467,7 @@ int run_align_slots(rgbid_ctx* ctx, int n, const rgbid_frame* const* fa,
   const LevelInfo li0 = make_level(K, w, h, 0);
   const int nslots = n;
   for (int i = 0; i < nslots; ++i) {
-    SlotIO& o = ctx->h_io[i];
+    SlotIO& o = L.h_io[i];
     std::memset(&o, 0, sizeof(o));
     for (int l = 0; l < kMaxLevels; ++l) {
       o.IA[l] = fa[i]->pI[l];
@@ -405,23 +477,27 @@ int run_align_slots(rgbid_ctx* ctx, int n, const rgbid_frame* const* fa,
     o.WA[0] = fa[i]->W;
     o.IB = fb[i]->I;
     o.WB = fb[i]->W;
-    double* base = ctx->ws_f64 + sf * i;
+    double* base = L.ws_f64 + sf * i;
     o.ib = base;
     o.wb = base + N;
     o.fIA = base + 2 * N;
     o.fWA = base + 3 * N;
-    o.part = base + 4 * N;
-    int* ib32 = ctx->ws_i32 + si * i;
+    double* g = base + 4 * N;
+    for (int l = 0; l < kMaxLevels; ++l) {
+      o.agrad[l] = g;
+      g += 4 * (size_t)(w >> l) * (h >> l);
+    }
+    o.part = g;
+    int* ib32 = L.ws_i32 + si * i;
     o.cntI = ib32;
     o.cntW = ib32 + mt;
     o.bitsI = reinterpret_cast<unsigned*>(ib32 + 2 * mt);
     o.bitsW = o.bitsI + mt * kWordsPerTile;
-    uint8_t* u8 = ctx->ws_u8 + su * i;
+    uint8_t* u8 = L.ws_u8 + su * i;
     for (int l = 0; l < kMaxLevels; ++l) {
       o.amask[l] = u8;
       u8 += (size_t)(w >> l) * (h >> l);
     }
-    o.amask_cov = u8;
     // build frame A's pyramid in-graph unless cached (once per distinct frame)
     o.build_pyr = 0;
     if (fa[i]->pyr_levels < cfg.levels) {
@@ -430,7 +506,7 @@ int run_align_slots(rgbid_ctx* ctx, int n, const rgbid_frame* const* fa,
         if (fa[j] == fa[i]) first = false;
       o.build_pyr = first ? 1 : 0;
     }
-    SlotState& s = ctx->h_st_pinned[i];
+    SlotState& s = L.h_st_pinned[i];
     std::memset(&s, 0, sizeof(s));
     const PoseD T = pose_of(inits ? &inits[i] : nullptr);
     pose_to(T, s.R, s.t);
@@ -438,11 +514,22 @@ int run_align_slots(rgbid_ctx* ctx, int n, const rgbid_frame* const* fa,
     s.status = RGBID_OK;
     s.done_level = -1;
   }
-  H2D(ctx->d_io, ctx->h_io.data(), sizeof(SlotIO) * nslots);
-  H2D(ctx->d_st, ctx->h_st_pinned, sizeof(SlotState) * nslots);
+  // frames whose pyramid another lane's in-flight chunk builds: wait for it
+  const int my = (int)(&L - ctx->lanes);
+  bool wait[kLanes] = {};
+  for (int i = 0; i < nslots; ++i) {
+    const int k = fa[i]->pyr_lane;
+    if (k >= 0 && k != my && ctx->lanes[k].pend_n > 0 && fa[i]->pyr_seq == ctx->lanes[k].seq)
+      wait[k] = true;
+  }
+  for (int k = 0; k < kLanes; ++k)
+    if (wait[k]) CK(cudaStreamWaitEvent(L.stream, ctx->lanes[k].done, 0));
+  L.seq += 1;
+  H2DS(L.stream, L.d_io, L.h_io.data(), sizeof(SlotIO) * nslots);
+  H2DS(L.stream, L.d_st, L.h_st_pinned, sizeof(SlotState) * nslots);
   AlignLaunch a;
-  a.io = ctx->d_io;
-  a.st = ctx->d_st;
+  a.io = L.d_io;
+  a.st = L.d_st;
   a.trace = want_trace ? ctx->d_trace : nullptr;
   a.nslots = nslots;
   a.w0 = w;
@@ -469,64 +556,53 @@ int run_align_slots(rgbid_ctx* ctx, int n, const rgbid_frame* const* fa,
   std::memcpy(kb.p, p, sizeof(p));
   const std::string key(reinterpret_cast<const char*>(&kb), sizeof(kb));
   if (ctx->use_graphs && !ctx->prof.enabled) {
-    auto it = ctx->graphs.find(key);
-    if (it == ctx->graphs.end()) {
+    auto it = L.graphs.find(key);
+    if (it == L.graphs.end()) {
       cudaGraph_t g;
-      CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+      CK(cudaStreamBeginCapture(L.stream, cudaStreamCaptureModeThreadLocal));
       const long long before = ctx->launches;
-      enqueue_align(ctx, a, K, cfg);
+      enqueue_align(L.stream, a, K, cfg);
       CachedGraph cg;
       cg.launches = ctx->launches - before;
       ctx->launches = before;
-      CK(cudaStreamEndCapture(ctx->stream, &g));
+      CK(cudaStreamEndCapture(L.stream, &g));
       CK(cudaGraphInstantiate(&cg.exec, g, 0));
       cudaGraphDestroy(g);
-      it = ctx->graphs.emplace(key, cg).first;
+      it = L.graphs.emplace(key, cg).first;
     }
-    CK(cudaGraphLaunch(it->second.exec, ctx->stream));
+    CK(cudaGraphLaunch(it->second.exec, L.stream));
     ctx->launches += it->second.launches;
   } else {
-    enqueue_align(ctx, a, K, cfg);
+    enqueue_align(L.stream, a, K, cfg);
   }
   rc = check_launch(ctx);
   if (rc) return rc;
-  for (int i = 0; i < nslots; ++i)
-    const_cast<rgbid_frame*>(fa[i])->pyr_levels =
-        std::max(const_cast<rgbid_frame*>(fa[i])->pyr_levels, cfg.levels);
-  D2H(ctx->h_st_pinned, ctx->d_st, sizeof(SlotState) * nslots);
-  CK(cudaStreamSynchronize(ctx->stream));
-  if (want_trace) {
-    ctx->last_trace.resize(kTraceMax);
-    CK(cudaMemcpy(ctx->last_trace.data(), ctx->d_trace, sizeof(rgbid_iter_trace) * kTraceMax,
-                  cudaMemcpyDeviceToHost));
-    ctx->last_trace.resize(std::min(ctx->h_st_pinned[0].trace_n, kTraceMax));
-  }
   for (int i = 0; i < nslots; ++i) {
-    const SlotState& s = ctx->h_st_pinned[i];
-    rgbid_align_result& r = results[i];
-    std::memset(&r, 0, sizeof(r));
-    r.status = s.status;
-    if (s.status == RGBID_E_DEGENERATE) {
-      spectrum_of(s.H, s.nI, r.spectrum);
-      continue;
+    rgbid_frame* f = const_cast<rgbid_frame*>(fa[i]);
+    if (L.h_io[i].build_pyr) {
+      f->pyr_lane = my;
+      f->pyr_seq = L.seq;
     }
-    std::memcpy(r.T_AB.R, s.R, sizeof(s.R));
-    std::memcpy(r.T_AB.t, s.t, sizeof(s.t));
-    std::memcpy(r.cov, s.cov, sizeof(s.cov));
-    r.converged = 1;
-    r.cov_degenerate = s.cov_degenerate;
-    r.n_levels = cfg.levels;
-    for (int k = 0; k < cfg.levels; ++k) {
-      const int level = cfg.levels - 1 - k;
-      r.level_log[k].level = level;
-      r.level_log[k].iterations = s.iters[level];
-      r.level_log[k].final_cost = s.cost[level];
-    }
-    r.tdist_intensity = s.finI;
-    r.tdist_depth = s.finW;
-    r.total_iterations = s.total_iters;
+    f->pyr_levels = std::max(f->pyr_levels, cfg.levels);
   }
+  D2HS(L.stream, L.h_st_pinned, L.d_st, sizeof(SlotState) * nslots);
+  CK(cudaEventRecord(L.done, L.stream));
+  L.pend_n = nslots;
+  L.pend_results = results;
+  L.pend_levels = cfg.levels;
+  L.pend_trace = want_trace;
   return RGBID_OK;
+}
+
+// n alignments on one lane, synchronous (single align / small batches)
+int run_align_slots(rgbid_ctx* ctx, int n, const rgbid_frame* const* fa,
+                    const rgbid_frame* const* fb, const rgbid_intrinsics& K,
+                    const rgbid_pose* inits, const rgbid_align_config& cfg,
+                    rgbid_align_result* results, bool want_trace) {
+  Lane& L = ctx->lanes[0];
+  int rc = enqueue_chunk(ctx, L, n, fa, fb, K, inits, cfg, results, want_trace);
+  if (rc) return rc;
+  return finish_chunk(ctx, L);
 }
 
 int frame_from_host(rgbid_ctx* ctx, rgbid_frame** slot, int w, int h, const double* I,
@@ -572,10 +648,14 @@ int rgbid_ctx_create(int device, rgbid_ctx** out) {
   cudaGetLastError();
   rgbid_ctx* ctx = new rgbid_ctx();
   ctx->device = device;
-  if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
-    delete ctx;
-    return RGBID_E_CUDA;
+  for (int k = 0; k < kLanes; ++k) {
+    if (cudaStreamCreateWithFlags(&ctx->lanes[k].stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ctx->lanes[k].done, cudaEventDisableTiming) != cudaSuccess) {
+      delete ctx;
+      return RGBID_E_CUDA;
+    }
   }
+  ctx->stream = ctx->lanes[0].stream;
   if (init_kernel_attributes() != 0) {
     delete ctx;
     return RGBID_E_CUDA;
@@ -590,19 +670,23 @@ int rgbid_ctx_destroy(rgbid_ctx* ctx) {
   if (!ctx) return RGBID_E_ARG;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
-  for (auto& g : ctx->graphs) cudaGraphExecDestroy(g.second.exec);
+  for (auto& L : ctx->lanes) {
+    cudaStreamSynchronize(L.stream);
+    free_lane_ws(L);
+  }
   for (auto& s : ctx->scratch)
     if (s.second.first) cudaFree(s.second.first);
+  for (int k = 0; k < 2; ++k) {
+    for (auto* f : ctx->host_fa[k]) rgbid_frame_destroy(ctx, f);
+    for (auto* f : ctx->host_fb[k]) rgbid_frame_destroy(ctx, f);
+  }
   if (ctx->tmpA) rgbid_frame_destroy(ctx, ctx->tmpA);
   if (ctx->tmpB) rgbid_frame_destroy(ctx, ctx->tmpB);
-  cudaFree(ctx->ws_f64);
-  cudaFree(ctx->ws_i32);
-  cudaFree(ctx->ws_u8);
-  cudaFree(ctx->d_io);
-  cudaFree(ctx->d_st);
   cudaFree(ctx->d_trace);
-  if (ctx->h_st_pinned) cudaFreeHost(ctx->h_st_pinned);
-  cudaStreamDestroy(ctx->stream);
+  for (auto& L : ctx->lanes) {
+    cudaEventDestroy(L.done);
+    cudaStreamDestroy(L.stream);
+  }
   delete ctx;
   return RGBID_OK;
 }
@@ -645,6 +729,7 @@ int rgbid_frame_upload(rgbid_ctx* ctx, rgbid_frame* f, const double* I, const do
     CK(cudaMemsetAsync(f->I, 0xff, sizeof(double) * N, ctx->stream));  // NaN holes
   H2D(f->W, W, sizeof(double) * N);
   f->pyr_levels = 0;
+  f->pyr_lane = -1;
   CK(cudaStreamSynchronize(ctx->stream));
   return RGBID_OK;
 }
@@ -663,6 +748,7 @@ int rgbid_frame_device_ptrs(rgbid_frame* f, double** I_dev, double** W_dev) {
   if (I_dev) *I_dev = f->I;
   if (W_dev) *W_dev = f->W;
   f->pyr_levels = 0;  // caller may write through these pointers
+  f->pyr_lane = -1;
   return RGBID_OK;
 }
 
@@ -780,12 +866,23 @@ int rgbid_align_batch(rgbid_ctx* ctx, int n, const rgbid_frame* const* a,
   // chunk so the slot workspace stays bounded (~15 MB per VGA slot)
   const char* env = std::getenv("RGBID_BATCH_SLOTS");
   int chunk = env ? std::max(1, atoi(env)) : 512;
-  for (int i0 = 0; i0 < n; i0 += chunk) {
+  // balanced chunks alternating over the lanes (chunk c+1 is prepared and
+  // enqueued while chunk c runs)
+  const int nch = (n + chunk - 1) / chunk;
+  chunk = (n + nch - 1) / nch;
+  const int lanes = ctx->prof.enabled ? 1 : kLanes;  // profiling: serialised kernel times
+  int lane = 0;
+  for (int i0 = 0; i0 < n; i0 += chunk, lane = (lane + 1) % lanes) {
     const int m = std::min(chunk, n - i0);
-    const int rc = run_align_slots(ctx, m, a + i0, b + i0, *K, inits ? inits + i0 : nullptr, c,
-                                   results + i0, i0 == 0);
+    const int rc = enqueue_chunk(ctx, ctx->lanes[lane], m, a + i0, b + i0, *K,
+                                 inits ? inits + i0 : nullptr, c, results + i0, i0 == 0);
     if (rc) return rc;
   }
+  for (auto& L : ctx->lanes) {
+    const int rc = finish_chunk(ctx, L);
+    if (rc) return rc;
+  }
+  CK(cudaStreamSynchronize(ctx->lanes[1].stream));
   return RGBID_OK;
 }
 
@@ -796,39 +893,60 @@ int rgbid_align_batch_host(rgbid_ctx* ctx, int n, const double* const* IA,
                            rgbid_align_result* results) {
   if (!ctx || n < 0 || !K || (n > 0 && (!IA || !WA || !IB || !WB || !results)))
     return RGBID_E_ARG;
-  if (chunk <= 0) chunk = 64;
+  if (n == 0) return RGBID_OK;
+  const rgbid_align_config c = cfg ? *cfg : default_config();
+  if (validate_cfg(c, w, h)) return RGBID_E_ARG;
+  if (chunk <= 0) chunk = 256;
+  chunk = std::min(chunk, n);
   LaunchScope ls(ctx);
-  std::vector<rgbid_frame*> fa, fb;
+  // per-lane device frames for one chunk (cached in ctx across calls); uploads go on
+  // the lane's stream, so the H2D of chunk c+1 overlaps the compute of chunk c
+  auto& fa = ctx->host_fa;
+  auto& fb = ctx->host_fb;
   auto cleanup = [&]() {
-    for (auto* f : fa) rgbid_frame_destroy(ctx, f);
-    for (auto* f : fb) rgbid_frame_destroy(ctx, f);
+    for (auto& L : ctx->lanes) cudaStreamSynchronize(L.stream);
   };
-  for (int i = 0; i < std::min(chunk, n); ++i) {
-    rgbid_frame *x, *y;
-    int rc = rgbid_frame_create(ctx, w, h, &x);
-    if (rc) return cleanup(), rc;
-    fa.push_back(x);
-    rc = rgbid_frame_create(ctx, w, h, &y);
-    if (rc) return cleanup(), rc;
-    fb.push_back(y);
-  }
-  const size_t N = (size_t)w * h;
-  for (int i0 = 0; i0 < n; i0 += chunk) {
-    const int m = std::min(chunk, n - i0);
-    for (int i = 0; i < m; ++i) {
-      H2D(fa[i]->I, IA[i0 + i], sizeof(double) * N);
-      H2D(fa[i]->W, WA[i0 + i], sizeof(double) * N);
-      H2D(fb[i]->I, IB[i0 + i], sizeof(double) * N);
-      H2D(fb[i]->W, WB[i0 + i], sizeof(double) * N);
-      fa[i]->pyr_levels = 0;
+  for (int k = 0; k < kLanes; ++k) {
+    if (!fa[k].empty() && (fa[k][0]->w != w || fa[k][0]->h != h)) {
+      cudaDeviceSynchronize();
+      for (auto* f : fa[k]) rgbid_frame_destroy(ctx, f);
+      for (auto* f : fb[k]) rgbid_frame_destroy(ctx, f);
+      fa[k].clear();
+      fb[k].clear();
     }
-    const rgbid_align_config c = cfg ? *cfg : default_config();
-    if (validate_cfg(c, w, h)) return cleanup(), RGBID_E_ARG;
-    const int rc = run_align_slots(ctx, m, fa.data(), fb.data(), *K, inits ? inits + i0 : nullptr,
-                                   c, results + i0, i0 == 0);
+    while ((int)fa[k].size() < chunk) {
+      rgbid_frame *x, *y;
+      int rc = rgbid_frame_create(ctx, w, h, &x);
+      if (rc) return cleanup(), rc;
+      fa[k].push_back(x);
+      rc = rgbid_frame_create(ctx, w, h, &y);
+      if (rc) return cleanup(), rc;
+      fb[k].push_back(y);
+    }
+  }
+  const size_t bytes = sizeof(double) * (size_t)w * h;
+  int lane = 0;
+  for (int i0 = 0; i0 < n; i0 += chunk, lane = (lane + 1) % kLanes) {
+    const int m = std::min(chunk, n - i0);
+    Lane& L = ctx->lanes[lane];
+    int rc = finish_chunk(ctx, L);  // frames of this lane are free again
+    if (rc) return cleanup(), rc;
+    for (int i = 0; i < m; ++i) {
+      H2DS(L.stream, fa[lane][i]->I, IA[i0 + i], bytes);
+      H2DS(L.stream, fa[lane][i]->W, WA[i0 + i], bytes);
+      H2DS(L.stream, fb[lane][i]->I, IB[i0 + i], bytes);
+      H2DS(L.stream, fb[lane][i]->W, WB[i0 + i], bytes);
+      fa[lane][i]->pyr_levels = 0;
+      fa[lane][i]->pyr_lane = -1;
+    }
+    rc = enqueue_chunk(ctx, L, m, fa[lane].data(), fb[lane].data(), *K,
+                       inits ? inits + i0 : nullptr, c, results + i0, i0 == 0);
     if (rc) return cleanup(), rc;
   }
-  cleanup();
+  for (auto& L : ctx->lanes) {
+    const int rc = finish_chunk(ctx, L);
+    if (rc) return cleanup(), rc;
+  }
   return RGBID_OK;
 }
 
@@ -1105,6 +1223,7 @@ int rgbid_selftest_division(rgbid_ctx* ctx, unsigned long long n, unsigned long 
 int rgbid_frame_invalidate(rgbid_frame* f) {
   if (!f) return RGBID_E_ARG;
   f->pyr_levels = 0;
+  f->pyr_lane = -1;
   return RGBID_OK;
 }
 
