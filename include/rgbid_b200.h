@@ -234,6 +234,27 @@ int rgbid_forward_register(rgbid_ctx* ctx, const double* W_A, int width, int hei
                            const rgbid_pose* T_BA, const rgbid_intrinsics* K_A,
                            const rgbid_intrinsics* K_B, double* out);
 
+/* ---- remaining drop-in entry points (not on the align hot path) --------- */
+/* inverse_warp's sampling (src/warping.cpp:8-18): out(i) = bilinear(src, map_x(i), map_y(i))
+ * for a coordinate map the caller evaluated from its f_w. */
+int rgbid_remap_bilinear(rgbid_ctx* ctx, const double* src, int width, int height,
+                         const double* map_x, const double* map_y, int out_width, int out_height,
+                         double* out);
+/* std::vector<PixelJet> residuals_and_jacobians(a, warped_b, K, lambda_n_min) —
+ * src/alignment.cpp:195-250.  jets: records {x, y, r_I, r_W, J_I[6], J_W[6], lambda_n}
+ * in row-major order; returns the jet count (negative rgbid_status on error). */
+long long rgbid_residuals_and_jacobians(rgbid_ctx* ctx, const double* I_A, const double* W_A,
+                                        const double* I_Bw, const double* W_Bw, int width,
+                                        int height, const rgbid_intrinsics* K,
+                                        double lambda_n_min, double* jets,
+                                        unsigned char* has_depth, long long cap);
+/* TDistParams estimate_location_scale(residuals, nu) — src/alignment.cpp:61-101 */
+int rgbid_estimate_location_scale(rgbid_ctx* ctx, const double* r, long long n, double nu,
+                                  rgbid_tdist* out);
+/* double estimate_nu(residuals, mu, sigma) — src/alignment.cpp:109-127 */
+int rgbid_estimate_nu(rgbid_ctx* ctx, const double* r, long long n, double mu, double sigma,
+                      double* nu);
+
 /* ---- self tests ---------------------------------------------------------- */
 /* Bitwise check of the warp's reciprocal-based correctly-rounded division
  * against IEEE division on n random operand pairs; *mismatches must be 0. */

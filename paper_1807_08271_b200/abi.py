@@ -136,6 +136,14 @@ EXPORTS = [
                                               C.POINTER(Intrinsics_t), C.c_int, DP]),
     ("rgbid_forward_register", C.c_int, [VP, DP, C.c_int, C.c_int, C.POINTER(Pose_t),
                                          C.POINTER(Intrinsics_t), C.POINTER(Intrinsics_t), DP]),
+    ("rgbid_remap_bilinear", C.c_int, [VP, DP, C.c_int, C.c_int, DP, DP, C.c_int, C.c_int, DP]),
+    ("rgbid_residuals_and_jacobians", C.c_longlong, [VP, DP, DP, DP, DP, C.c_int, C.c_int,
+                                                     C.POINTER(Intrinsics_t), C.c_double, DP,
+                                                     C.POINTER(C.c_ubyte), C.c_longlong]),
+    ("rgbid_estimate_location_scale", C.c_int, [VP, DP, C.c_longlong, C.c_double,
+                                                C.POINTER(TDist_t)]),
+    ("rgbid_estimate_nu", C.c_int, [VP, DP, C.c_longlong, C.c_double, C.c_double,
+                                    C.POINTER(C.c_double)]),
     ("rgbid_selftest_division", C.c_int, [VP, C.c_ulonglong, C.c_ulonglong,
                                           C.POINTER(C.c_ulonglong)]),
     ("rgbid_synth_render_plane", C.c_int, [C.POINTER(Intrinsics_t), C.POINTER(Pose_t), DP,

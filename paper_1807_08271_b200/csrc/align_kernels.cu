@@ -1096,6 +1096,117 @@ void launch_warp_maps(const double* IB, const double* WB, int wb, int hb, const 
 }
 
 // ---------------------------------------------------------------------------
+// Drop-in helpers (reference entry points that are not on the align hot path but
+// are part of the replaced sources).
+
+// inverse_warp's sampling step (src/warping.cpp:8-18) for a host-evaluated map
+__global__ void k_remap_bilinear(const double* __restrict__ src, int w, int h,
+                                 const double* __restrict__ mx, const double* __restrict__ my,
+                                 int n, double* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = bilinear(src, w, h, mx[i], my[i]);
+}
+void launch_remap_bilinear(const double* src, int w, int h, const double* mx, const double* my,
+                           int n, double* out, cudaStream_t s) {
+  KScope ks_("remap_bilinear", s);
+  k_remap_bilinear<<<(n + 255) / 256, 256, 0, s>>>(src, w, h, mx, my, n, out);
+}
+
+// residuals_and_jacobians per pixel (src/alignment.cpp:195-250): record
+// {x, y, r_I, r_W, J_I[6], J_W[6], lambda_n} + flag (0 none, 1 jet, 2 jet+depth)
+__global__ void k_jets(const double* __restrict__ IA, const double* __restrict__ WA,
+                       const double* __restrict__ IBw, const double* __restrict__ WBw, LevelInfo li,
+                       double lambda_n_min, double* __restrict__ rec, uint8_t* __restrict__ flag) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  const int w = li.w, h = li.h;
+  if (k >= w * h) return;
+  const int y = k / w, x = k - y * w;
+  flag[k] = 0;
+  const double w_a = WA[k], i_a = IA[k], i_b = IBw[k];
+  if (!valid(w_a) || w_a <= 0.0 || !valid(i_a) || !valid(i_b)) return;
+  double gix, giy;
+  if (!gradient_at(IA, w, h, x, y, gix, giy)) return;
+  const double* Ki = li.Kinv;
+  const double px = x, py = y, ax = li.cx - px, ay = li.cy - py;
+  const double k0 = red3(Ki[0] * px, Ki[1] * py, Ki[2]), k1 = red3(Ki[3] * px, Ki[4] * py, Ki[5]),
+               k2 = red3(Ki[6] * px, Ki[7] * py, Ki[8]);
+  const double X0 = k0 / w_a, X1 = k1 / w_a, X2 = k2 / w_a;
+  double* o = rec + (size_t)k * 17;
+  o[0] = x;
+  o[1] = y;
+  o[2] = i_b - i_a;
+  o[3] = 0.0;
+  {
+    const double s0 = w_a * gix, s1 = w_a * giy;
+    const double u0 = s0 * li.fx, u1 = s1 * li.fy, u2 = s0 * ax + s1 * ay;
+    o[4] = u0, o[5] = u1, o[6] = u2;
+    o[7] = X1 * u2 - X2 * u1, o[8] = X2 * u0 - X0 * u2, o[9] = X0 * u1 - X1 * u0;
+  }
+  for (int c = 10; c < 16; ++c) o[c] = 0.0;
+  o[16] = 1.0;
+  flag[k] = 1;
+  const double w_b = WBw[k];
+  double gwx, gwy;
+  if (!(valid(w_b) && w_b > 0.0 && gradient_at(WA, w, h, x, y, gwx, gwy))) return;
+  const double g0 = gwx * li.fx, g1 = gwy * li.fy, g2 = gwx * ax + gwy * ay;
+  const double s0 = w_a * g0, s1 = w_a * g1, s2 = w_a * (g2 + w_b);
+  o[3] = w_b - w_a;
+  o[10] = s0, o[11] = s1, o[12] = s2;
+  o[13] = X1 * s2 - X2 * s1, o[14] = X2 * s0 - X0 * s2, o[15] = X0 * s1 - X1 * s0;
+  const double n0 = g0 / w_a, n1 = g1 / w_a, n2 = g2 / w_a + 1.0;
+  const double nn = sqrt(n0 * n0 + n1 * n1 + n2 * n2);
+  double lambda = 1.0;
+  if (!(nn < 1e-12)) {
+    double c = (n0 * k0 + n1 * k1 + n2 * k2) / (nn * sqrt(k0 * k0 + k1 * k1 + k2 * k2));
+    if (n2 < 0) c = -c;
+    lambda = dmax_std(lambda_n_min, c);
+  }
+  o[16] = lambda;
+  flag[k] = 2;
+}
+void launch_jets(const double* IA, const double* WA, const double* IBw, const double* WBw,
+                 const LevelInfo& li, double lambda_n_min, double* rec, uint8_t* flag,
+                 cudaStream_t s) {
+  KScope ks_("jets", s);
+  k_jets<<<(li.w * li.h + 255) / 256, 256, 0, s>>>(IA, WA, IBw, WBw, li, lambda_n_min, rec, flag);
+}
+
+// estimate_location_scale (mode 0) / estimate_nu (mode 1) on a residual vector
+// (src/alignment.cpp:61-127): systematic sample into smem, then the same
+// device chain as k_tdist.
+__global__ void __launch_bounds__(kTdistThreads, 2)
+    k_tdist_vec(const double* __restrict__ r, long long n, int mode, double a, double b,
+                double* __restrict__ out) {
+  constexpr int NT = kTdistThreads;
+  extern __shared__ double dsm[];
+  __shared__ double scratch[NT / 32 * 2 * 2];
+  const long long stride = n <= kMaxSample ? 1 : (n + kMaxSample - 1) / kMaxSample;
+  Sample smp;
+  smp.v = dsm;
+  smp.m = n == 0 ? 0 : (int)((n - 1) / stride + 1);
+  smp.kfull = smp.m / NT;
+  smp.memo_nu = -1.0;
+  smp.scratch = scratch;
+  smp.parity = 0;
+  for (int s = threadIdx.x; s < smp.m; s += NT) dsm[s] = r[(long long)s * stride];
+  __syncthreads();
+  if (mode == 0) {
+    const TD t = loc_scale<NT>(smp, a, scratch);
+    if (threadIdx.x == 0) out[0] = t.mu, out[1] = t.sigma, out[2] = t.nu;
+  } else {
+    const double nu = estimate_nu<NT>(smp, a, b, scratch);
+    if (threadIdx.x == 0) out[0] = nu;
+  }
+}
+int launch_tdist_vec(const double* r, long long n, int mode, double a, double b, double* out,
+                     cudaStream_t s) {
+  cudaFuncSetAttribute(k_tdist_vec, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSample * 8);
+  KScope ks_("tdist_vec", s);
+  k_tdist_vec<<<1, kTdistThreads, kMaxSample * 8, s>>>(r, n, mode, a, b, out);
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
 // Self-test of div_rcp against IEEE division on n random operand pairs spanning
 // the ranges the warp sees (numerators |a| < 2^20 incl. integers, divisors
 // b in [1e-12, 1e6]).  Counts mismatches (bitwise).

@@ -112,6 +112,13 @@ void launch_warp_maps(const double* IB, const double* WB, int wb, int hb, const 
                       int h, const WarpMats& m, double* oI, double* oW, double* omx, double* omy,
                       cudaStream_t s);
 int tdist_smem_bytes(int ntiles);
+void launch_remap_bilinear(const double* src, int w, int h, const double* mx, const double* my,
+                           int n, double* out, cudaStream_t s);
+void launch_jets(const double* IA, const double* WA, const double* IBw, const double* WBw,
+                 const LevelInfo& li, double lambda_n_min, double* rec, uint8_t* flag,
+                 cudaStream_t s);
+int launch_tdist_vec(const double* r, long long n, int mode, double a, double b, double* out,
+                     cudaStream_t s);
 int selftest_division(unsigned long long n, unsigned long long seed, unsigned long long* out,
                       cudaStream_t s);
 int init_kernel_attributes();

@@ -1213,6 +1213,102 @@ int rgbid_ctx_transfer_bytes(rgbid_ctx* ctx, long long* h2d, long long* d2h) {
   return RGBID_OK;
 }
 
+int rgbid_remap_bilinear(rgbid_ctx* ctx, const double* src, int w, int h, const double* map_x,
+                         const double* map_y, int out_w, int out_h, double* out) {
+  if (!ctx || !src || !map_x || !map_y || !out || w <= 0 || h <= 0) return RGBID_E_ARG;
+  LaunchScope ls(ctx);
+  const size_t N = (size_t)w * h, M = (size_t)out_w * out_h;
+  double* d;
+  int rc = scratch_buf(ctx, "remap", N + 3 * M, &d);
+  if (rc) return rc;
+  H2D(d, src, sizeof(double) * N);
+  H2D(d + N, map_x, sizeof(double) * M);
+  H2D(d + N + M, map_y, sizeof(double) * M);
+  launch_remap_bilinear(d, w, h, d + N, d + N + M, (int)M, d + N + 2 * M, ctx->stream);
+  rc = check_launch(ctx);
+  if (rc) return rc;
+  D2H(out, d + N + 2 * M, sizeof(double) * M);
+  CK(cudaStreamSynchronize(ctx->stream));
+  return RGBID_OK;
+}
+
+long long rgbid_residuals_and_jacobians(rgbid_ctx* ctx, const double* I_A, const double* W_A,
+                                        const double* I_Bw, const double* W_Bw, int w, int h,
+                                        const rgbid_intrinsics* K, double lambda_n_min,
+                                        double* jets, unsigned char* has_depth, long long cap) {
+  if (!ctx || !I_A || !W_A || !I_Bw || !W_Bw || !K) return -RGBID_E_ARG;
+  LaunchScope ls(ctx);
+  const size_t N = (size_t)w * h;
+  double* d;
+  uint8_t* fl;
+  if (scratch_buf(ctx, "jets_in", 4 * N + 17 * N, &d)) return -RGBID_E_OOM;
+  if (scratch_buf(ctx, "jets_flag", N, &fl)) return -RGBID_E_OOM;
+  cudaStream_t st = ctx->stream;
+  cudaMemcpyAsync(d, I_A, sizeof(double) * N, cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(d + N, W_A, sizeof(double) * N, cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(d + 2 * N, I_Bw, sizeof(double) * N, cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(d + 3 * N, W_Bw, sizeof(double) * N, cudaMemcpyHostToDevice, st);
+  ctx->h2d_bytes += 32 * (long long)N;
+  rgbid_intrinsics k = *K;
+  k.width = w;
+  k.height = h;
+  LevelInfo li = make_level(k, w, h, 0);
+  launch_jets(d, d + N, d + 2 * N, d + 3 * N, li, lambda_n_min, d + 4 * N, fl, st);
+  if (check_launch(ctx)) return -RGBID_E_CUDA;
+  std::vector<double> rec(17 * N);
+  std::vector<uint8_t> flags(N);
+  cudaMemcpyAsync(rec.data(), d + 4 * N, sizeof(double) * 17 * N, cudaMemcpyDeviceToHost, st);
+  cudaMemcpyAsync(flags.data(), fl, N, cudaMemcpyDeviceToHost, st);
+  ctx->d2h_bytes += 137 * (long long)N;
+  if (cudaStreamSynchronize(st) != cudaSuccess) return -RGBID_E_CUDA;
+  long long n = 0;  // row-major compaction (the reference's push_back order)
+  for (size_t i = 0; i < N; ++i) {
+    if (!flags[i]) continue;
+    if (n < cap) {
+      if (jets) std::memcpy(jets + 17 * n, rec.data() + 17 * i, 17 * sizeof(double));
+      if (has_depth) has_depth[n] = flags[i] == 2;
+    }
+    ++n;
+  }
+  return n;
+}
+
+int rgbid_estimate_location_scale(rgbid_ctx* ctx, const double* r, long long n, double nu,
+                                  rgbid_tdist* out) {
+  if (!ctx || (!r && n > 0) || !out) return RGBID_E_ARG;
+  LaunchScope ls(ctx);
+  double* d;
+  int rc = scratch_buf(ctx, "tdist_vec", (size_t)n + 4, &d);
+  if (rc) return rc;
+  if (n > 0) H2D(d + 4, r, sizeof(double) * n);
+  launch_tdist_vec(d + 4, n, 0, nu, 0.0, d, ctx->stream);
+  rc = check_launch(ctx);
+  if (rc) return rc;
+  double o[3];
+  D2H(o, d, sizeof(o));
+  CK(cudaStreamSynchronize(ctx->stream));
+  out->mu = o[0];
+  out->sigma = o[1];
+  out->nu = o[2];
+  return RGBID_OK;
+}
+
+int rgbid_estimate_nu(rgbid_ctx* ctx, const double* r, long long n, double mu, double sigma,
+                      double* nu) {
+  if (!ctx || (!r && n > 0) || !nu) return RGBID_E_ARG;
+  LaunchScope ls(ctx);
+  double* d;
+  int rc = scratch_buf(ctx, "tdist_vec", (size_t)n + 4, &d);
+  if (rc) return rc;
+  if (n > 0) H2D(d + 4, r, sizeof(double) * n);
+  launch_tdist_vec(d + 4, n, 1, mu, sigma, d, ctx->stream);
+  rc = check_launch(ctx);
+  if (rc) return rc;
+  D2H(nu, d, sizeof(double));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return RGBID_OK;
+}
+
 int rgbid_selftest_division(rgbid_ctx* ctx, unsigned long long n, unsigned long long seed,
                             unsigned long long* mismatches) {
   if (!ctx || !mismatches) return RGBID_E_ARG;
