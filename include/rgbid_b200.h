@@ -234,6 +234,45 @@ int rgbid_forward_register(rgbid_ctx* ctx, const double* W_A, int width, int hei
                            const rgbid_pose* T_BA, const rgbid_intrinsics* K_A,
                            const rgbid_intrinsics* K_B, double* out);
 
+/* ---- front-end odometry driver (config 3) -------------------------------- */
+/* Restates Pipeline::process_frame / track / fuse_and_maybe_switch
+ * (src/pipeline.cpp:120-247) without the back-end; frames, reference and
+ * keyframe state resident in HBM. */
+typedef struct {
+  rgbid_align_config align;       /* PipelineConfig::alignment */
+  double keyframe_covisibility;   /* 0.7 (inc/pipeline.hpp:80) */
+  double reference_covisibility;  /* 0.9 (inc/pipeline.hpp:81) */
+  int buffer_capacity;            /* 30 (inc/pipeline.hpp:84) */
+} rgbid_frontend_config;
+
+/* FrameEstimate (inc/pipeline.hpp:25-31) */
+typedef struct {
+  double timestamp;
+  rgbid_pose T_W_k;
+  double cov[36]; /* step covariance, left-referenced in the previous frame */
+  int lost;
+  int keyframe_id; /* >= 0 when this frame started a keyframe */
+} rgbid_frame_estimate;
+
+typedef struct rgbid_frontend rgbid_frontend;
+int rgbid_frontend_default_config(rgbid_frontend_config* cfg);
+int rgbid_frontend_create(rgbid_ctx* ctx, const rgbid_intrinsics* K,
+                          const rgbid_frontend_config* cfg, rgbid_frontend** out);
+int rgbid_frontend_destroy(rgbid_frontend* fe);
+/* Pipeline::process_frame(frame, timestamp); *est = the frame's estimate */
+int rgbid_frontend_process(rgbid_frontend* fe, const double* I, const double* W, double timestamp,
+                           rgbid_frame_estimate* est);
+/* flush: absorb the open keyframe's buffered frames (Pipeline::finish front half) */
+int rgbid_frontend_finish(rgbid_frontend* fe);
+int rgbid_frontend_trajectory(rgbid_frontend* fe, rgbid_frame_estimate* out, int max, int* n);
+int rgbid_frontend_keyframes(rgbid_frontend* fe, int* frame_index, int max, int* n);
+int rgbid_frontend_current_keyframe(rgbid_frontend* fe, double* W, double* C, rgbid_pose* T_W_kf,
+                                    int* id);
+
+/* device helpers */
+int rgbid_frame_copy(rgbid_ctx* ctx, rgbid_frame* dst, const rgbid_frame* src);
+int rgbid_fill(rgbid_ctx* ctx, double* dev, long long n, double value);
+
 /* ---- remaining drop-in entry points (not on the align hot path) --------- */
 /* inverse_warp's sampling (src/warping.cpp:8-18): out(i) = bilinear(src, map_x(i), map_y(i))
  * for a coordinate map the caller evaluated from its f_w. */

@@ -62,6 +62,16 @@ class DepthIntrinsics_t(C.Structure):
                 ("q1", C.c_double * 9), ("p0", C.c_double * 2)]
 
 
+class FrontendConfig_t(C.Structure):
+    _fields_ = [("align", AlignConfig_t), ("keyframe_covisibility", C.c_double),
+                ("reference_covisibility", C.c_double), ("buffer_capacity", C.c_int)]
+
+
+class FrameEstimate_t(C.Structure):
+    _fields_ = [("timestamp", C.c_double), ("T_W_k", Pose_t), ("cov", C.c_double * 36),
+                ("lost", C.c_int), ("keyframe_id", C.c_int)]
+
+
 DP = C.POINTER(C.c_double)
 VP = C.c_void_p
 
@@ -136,6 +146,19 @@ EXPORTS = [
                                               C.POINTER(Intrinsics_t), C.c_int, DP]),
     ("rgbid_forward_register", C.c_int, [VP, DP, C.c_int, C.c_int, C.POINTER(Pose_t),
                                          C.POINTER(Intrinsics_t), C.POINTER(Intrinsics_t), DP]),
+    ("rgbid_frontend_default_config", C.c_int, [C.POINTER(FrontendConfig_t)]),
+    ("rgbid_frontend_create", C.c_int, [VP, C.POINTER(Intrinsics_t), C.POINTER(FrontendConfig_t),
+                                        C.POINTER(VP)]),
+    ("rgbid_frontend_destroy", C.c_int, [VP]),
+    ("rgbid_frontend_process", C.c_int, [VP, DP, DP, C.c_double, C.POINTER(FrameEstimate_t)]),
+    ("rgbid_frontend_finish", C.c_int, [VP]),
+    ("rgbid_frontend_trajectory", C.c_int, [VP, C.POINTER(FrameEstimate_t), C.c_int,
+                                            C.POINTER(C.c_int)]),
+    ("rgbid_frontend_keyframes", C.c_int, [VP, C.POINTER(C.c_int), C.c_int, C.POINTER(C.c_int)]),
+    ("rgbid_frontend_current_keyframe", C.c_int, [VP, DP, DP, C.POINTER(Pose_t),
+                                                  C.POINTER(C.c_int)]),
+    ("rgbid_frame_copy", C.c_int, [VP, VP, VP]),
+    ("rgbid_fill", C.c_int, [VP, DP, C.c_longlong, C.c_double]),
     ("rgbid_remap_bilinear", C.c_int, [VP, DP, C.c_int, C.c_int, DP, DP, C.c_int, C.c_int, DP]),
     ("rgbid_residuals_and_jacobians", C.c_longlong, [VP, DP, DP, DP, DP, C.c_int, C.c_int,
                                                      C.POINTER(Intrinsics_t), C.c_double, DP,

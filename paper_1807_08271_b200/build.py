@@ -19,7 +19,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CU_FLAGS = ["-O3", "-lineinfo", "--fmad=false", "-std=c++17", "-Xcompiler", "-fPIC",
             "-Xcompiler", "-ffp-contract=off", "-Xptxas", "-v"]
-CU_SRCS = ["align_kernels.cu", "fusion_kernels.cu", "runtime.cu"]
+CU_SRCS = ["align_kernels.cu", "fusion_kernels.cu", "runtime.cu", "frontend.cu"]
 CPP_SRCS = ["synth.cpp"]
 
 

@@ -18,6 +18,7 @@
 #include <math_constants.h>
 
 #include <cmath>
+#include <algorithm>
 #include <cstdio>
 
 #include "align_kernels.cuh"
@@ -1093,6 +1094,17 @@ void launch_warp_maps(const double* IB, const double* WB, int wb, int hb, const 
                       cudaStream_t s) {
   KScope ks_("warp_maps", s);
   k_warp_maps<<<(w * h + 255) / 256, 256, 0, s>>>(IB, WB, wb, hb, WA, w, h, m, oI, oW, omx, omy);
+}
+
+__global__ void k_fill(double* p, long long n, double v) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    p[i] = v;
+}
+void launch_fill(double* p, long long n, double v, cudaStream_t s) {
+  if (n <= 0) return;
+  KScope ks_("fill", s);
+  k_fill<<<(int)std::min<long long>((n + 255) / 256, 148 * 16), 256, 0, s>>>(p, n, v);
 }
 
 // ---------------------------------------------------------------------------

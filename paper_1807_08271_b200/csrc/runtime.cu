@@ -1316,6 +1316,22 @@ int rgbid_selftest_division(rgbid_ctx* ctx, unsigned long long n, unsigned long 
   return selftest_division(n, seed, mismatches, ctx->stream) ? RGBID_E_CUDA : RGBID_OK;
 }
 
+int rgbid_frame_copy(rgbid_ctx* ctx, rgbid_frame* dst, const rgbid_frame* src) {
+  if (!ctx || !dst || !src || dst->w != src->w || dst->h != src->h) return RGBID_E_ARG;
+  CK(cudaMemcpyAsync(dst->I, src->I, sizeof(double) * 2 * (size_t)src->w * src->h,
+                     cudaMemcpyDeviceToDevice, ctx->stream));
+  dst->pyr_levels = 0;
+  dst->pyr_lane = -1;
+  return RGBID_OK;
+}
+
+int rgbid_fill(rgbid_ctx* ctx, double* dev, long long n, double value) {
+  if (!ctx || (!dev && n > 0)) return RGBID_E_ARG;
+  LaunchScope ls(ctx);
+  launch_fill(dev, n, value, ctx->stream);
+  return check_launch(ctx);
+}
+
 int rgbid_frame_invalidate(rgbid_frame* f) {
   if (!f) return RGBID_E_ARG;
   f->pyr_levels = 0;

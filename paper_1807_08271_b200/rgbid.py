@@ -693,3 +693,99 @@ def synth_pair_device(a: DeviceFrame, b: DeviceFrame, K: Intrinsics, pair_seed: 
     a.ctx.check(a.ctx.lib.rgbid_synth_pair_device(a.ctx.h, a.h, b.h, C.byref(K.to_c()), pair_seed,
                                                   variant, C.byref(T)), "synth_pair_device")
     return Pose.from_c(T)
+
+
+# --------------------------------------------------------------------------- front-end (config 3)
+
+
+@dataclass
+class FrameEstimate:
+    """inc/pipeline.hpp:25-31"""
+    timestamp: float
+    T_W_k: Pose
+    cov: np.ndarray
+    lost: bool
+    keyframe_id: int
+
+    @staticmethod
+    def from_c(e) -> "FrameEstimate":
+        return FrameEstimate(e.timestamp, Pose.from_c(e.T_W_k), np.array(e.cov[:]).reshape(6, 6),
+                             bool(e.lost), e.keyframe_id)
+
+
+@dataclass
+class FrontendConfig:
+    """PipelineConfig's front-end fields (inc/pipeline.hpp:72-88)."""
+    alignment: AlignmentConfig = field(default_factory=AlignmentConfig)
+    keyframe_covisibility: float = 0.7
+    reference_covisibility: float = 0.9
+    buffer_capacity: int = 30
+
+    def to_c(self) -> abi.FrontendConfig_t:
+        c = abi.FrontendConfig_t()
+        c.align = self.alignment.to_c()
+        c.keyframe_covisibility = self.keyframe_covisibility
+        c.reference_covisibility = self.reference_covisibility
+        c.buffer_capacity = self.buffer_capacity
+        return c
+
+
+class Frontend:
+    """Pipeline front-end (src/pipeline.cpp:120-247) on the B200: process_frame,
+    trajectory, keyframes.  The back-end (loop closure, pose graph) is out of scope."""
+
+    def __init__(self, K: Intrinsics, config: Optional[FrontendConfig] = None,
+                 ctx: Optional[Context] = None):
+        self.ctx = ctx or default_context()
+        self.K = K
+        self.h = C.c_void_p()
+        self.ctx.check(self.ctx.lib.rgbid_frontend_create(
+            self.ctx.h, C.byref(K.to_c()), C.byref((config or FrontendConfig()).to_c()),
+            C.byref(self.h)), "frontend_create")
+
+    def process_frame(self, frame: FrameData, timestamp: float) -> FrameEstimate:
+        e = abi.FrameEstimate_t()
+        self.ctx.check(self.ctx.lib.rgbid_frontend_process(
+            self.h, dptr(frame.intensity), dptr(frame.inverse_depth), timestamp, C.byref(e)),
+            "frontend_process")
+        return FrameEstimate.from_c(e)
+
+    def finish(self):
+        self.ctx.check(self.ctx.lib.rgbid_frontend_finish(self.h), "frontend_finish")
+
+    def trajectory(self) -> List[FrameEstimate]:
+        n = C.c_int(0)
+        self.ctx.lib.rgbid_frontend_trajectory(self.h, None, 0, C.byref(n))
+        arr = (abi.FrameEstimate_t * max(1, n.value))()
+        self.ctx.lib.rgbid_frontend_trajectory(self.h, arr, n.value, C.byref(n))
+        return [FrameEstimate.from_c(e) for e in arr[: n.value]]
+
+    def keyframe_frame_index(self) -> List[int]:
+        n = C.c_int(0)
+        self.ctx.lib.rgbid_frontend_keyframes(self.h, None, 0, C.byref(n))
+        arr = (C.c_int * max(1, n.value))()
+        self.ctx.lib.rgbid_frontend_keyframes(self.h, arr, n.value, C.byref(n))
+        return list(arr[: n.value])
+
+    def keyframe_count(self) -> int:
+        return len(self.keyframe_frame_index())
+
+    def current_keyframe(self):
+        W = np.empty((self.K.height, self.K.width))
+        Cm = np.empty_like(W)
+        T = abi.Pose_t()
+        kid = C.c_int(0)
+        self.ctx.check(self.ctx.lib.rgbid_frontend_current_keyframe(
+            self.h, dptr(W), dptr(Cm), C.byref(T), C.byref(kid)), "current_keyframe")
+        return W, Cm, Pose.from_c(T), kid.value
+
+    def close(self):
+        if self.h:
+            self.ctx.lib.rgbid_frontend_destroy(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
