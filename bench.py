@@ -66,6 +66,36 @@ def parse():
     return p.parse_args()
 
 
+def partition(pairs, world, rank):
+    """Contiguous block of pair indices for this rank (strong scaling, no input scatter)."""
+    n_local = pairs // world
+    return rank * n_local, n_local
+
+
+def result_records(results, n_local):
+    """Fixed-size per-pair records (pose 12, status, iterations, cov_degenerate) for the gather."""
+    import numpy as np
+    rec = np.zeros((n_local, 16))
+    for i, r in enumerate(results):
+        rec[i, :9] = r.T_AB.R[:]
+        rec[i, 9:12] = r.T_AB.t[:]
+        rec[i, 12] = r.status
+        rec[i, 13] = r.total_iterations
+        rec[i, 14] = r.cov_degenerate
+    return rec
+
+
+def gather_records(rec, world, out, dist=None):
+    """The only collective of the benchmark: all_gather of the result records."""
+    import torch
+    t = torch.from_numpy(rec).to(out.device)
+    if world > 1:
+        dist.all_gather_into_tensor(out, t)
+    else:
+        out.copy_(t)
+    return out
+
+
 def dist_env():
     return (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
             int(os.environ.get("LOCAL_RANK", "0")))
@@ -226,8 +256,7 @@ def main():
     ctx = rg.Context(local)
     K = rg.simple_intrinsics(W0, H0, F0)
     cfg = rg.AlignmentConfig(levels=LEVELS, iterations=ITERS)
-    n_local = args.pairs // world
-    base = rank * n_local
+    base, n_local = partition(args.pairs, world, rank)
 
     # inputs resident in HBM: device-rendered pairs (pair seed = global index)
     A = [rg.DeviceFrame(W0, H0, ctx) for _ in range(n_local)]
@@ -239,18 +268,7 @@ def main():
     gathered = torch.empty((world * n_local, 16), dtype=torch.float64, device="cuda")
 
     def gather(results):
-        rec = np.zeros((n_local, 16))
-        for i, r in enumerate(results):
-            rec[i, :9] = r.T_AB.R[:]
-            rec[i, 9:12] = r.T_AB.t[:]
-            rec[i, 12] = r.status
-            rec[i, 13] = r.total_iterations
-            rec[i, 14] = r.cov_degenerate
-        t = torch.from_numpy(rec).to("cuda", non_blocking=False)
-        if world > 1:
-            dist.all_gather_into_tensor(gathered, t)
-        else:
-            gathered.copy_(t)
+        gather_records(result_records(results, n_local), world, gathered, dist)
         return results
 
     def step():
