@@ -14,6 +14,7 @@
 //                        (src/alignment.cpp:387-401) — no host round trip.
 // Compiled with --fmad=false: mask-deciding arithmetic rounds exactly like the
 // reference; reductions use a fixed tree (bit-reproducible run to run).
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <math_constants.h>
 
@@ -436,6 +437,10 @@ struct TD {
   double mu, sigma, nu;
 };
 
+struct Sample;
+template <int NV, int NT>
+__device__ __forceinline__ void sample_allsum(double (&v)[NV], Sample& S);
+
 __device__ __forceinline__ double t_weight(double x, double nu) { return (nu + 1.0) / (nu + x * x); }
 
 // 1/q for q >= 1 (t_weight denominators): MUFU seed + cubic Newton step (full precision).
@@ -454,16 +459,51 @@ __device__ __forceinline__ double rcp_q(double q) {
 }
 
 struct Sample {
-  const double* v;  // shared memory; thread t owns v[t], v[t + NT], ...
+  const double* v;  // shared memory; thread t owns v[t], v[t + NT], ... (this CTA's share)
   double* scratch;  // 2 x (NT/32 x 2) doubles for block_allsum
   int parity;
-  int m;
-  int kfull;        // rounds where every thread owns a sample (m / NT)
+  int m;            // sample size (all CTAs of the cluster)
+  int m_local;      // samples held by this CTA
+  int kfull;        // rounds where every thread owns a sample (m_local / NT)
+  int cs;           // cluster size sharing the sample (1 = single CTA)
+  double* cbuf;     // this CTA's [2][2] cluster exchange slots (shared memory)
   // memo of the last estimate_location_scale(nu) call: same sample + same nu
   // -> same result (e.g. the final refit repeating estimate_nu's, src/alignment.cpp:117,316)
   double memo_nu;
   TD memo;
 };
+
+// Sum over the whole sample: fixed-order block reduction, then (cluster mode)
+// a fixed-rank-order reduction of the CTA partials over DSMEM.  Every thread of
+// every CTA ends with the bit-identical total.  The cluster slots are double
+// buffered on the same parity as the block scratch, so one cluster barrier per
+// reduction suffices.
+template <int NV, int NT>
+__device__ __forceinline__ void sample_allsum(double (&v)[NV], Sample& S) {
+  const int p = S.parity;
+  block_allsum<NV, NT>(v, S.scratch, S.parity);
+  if (S.cs > 1) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cl = cg::this_cluster();
+    if (threadIdx.x == 0)
+#pragma unroll
+      for (int i = 0; i < NV; ++i) S.cbuf[p * 2 + i] = v[i];
+    cl.sync();
+    double part[kTdistCluster][NV];
+#pragma unroll
+    for (int r = 0; r < kTdistCluster; ++r) {  // all remote loads in flight at once
+      const double* rem = cl.map_shared_rank(S.cbuf, r);
+#pragma unroll
+      for (int i = 0; i < NV; ++i) part[r][i] = rem[p * 2 + i];
+    }
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      v[i] = 0.0;
+#pragma unroll
+      for (int r = 0; r < kTdistCluster; ++r) v[i] += part[r][i];
+    }
+  }
+}
 
 // sum over the thread's samples of f(v) into NACC accumulators (breaks the
 // add dependency chain); fixed assignment -> deterministic
@@ -479,8 +519,8 @@ __device__ __forceinline__ void sample_sum(const Sample& S, double (&acc)[NV], F
     f(v[k * NT], a0);
     f(v[(k + 1) * NT], a1);
   }
-  for (; k < kSPT; ++k)
-    if (k * NT + (int)threadIdx.x < S.m) f(v[k * NT], a0);
+  for (; k * NT < S.m_local; ++k)
+    if (k * NT + (int)threadIdx.x < S.m_local) f(v[k * NT], a0);
 #pragma unroll
   for (int i = 0; i < NV; ++i) acc[i] = a0[i] + a1[i];
 }
@@ -495,13 +535,13 @@ __device__ __forceinline__ TD loc_scale(Sample& S, double nu, double* scratch) {
   const double inv_m = 1.0 / (double)m;
   double a1[1];
   sample_sum<NT>(S, a1, [](double v, double (&a)[1]) { a[0] += v; });
-  block_allsum<1, NT>(a1, S.scratch, S.parity);
+  sample_allsum<1, NT>(a1, S);
   const double mu0 = a1[0] / (double)m;
   sample_sum<NT>(S, a1, [mu0](double v, double (&a)[1]) {
     const double d = v - mu0;
     a[0] = fma(d, d, a[0]);
   });
-  block_allsum<1, NT>(a1, S.scratch, S.parity);
+  sample_allsum<1, NT>(a1, S);
   double mu = mu0;
   double sigma = sqrt(a1[0] / (double)m);
   TD out;
@@ -519,14 +559,14 @@ __device__ __forceinline__ TD loc_scale(Sample& S, double nu, double* scratch) {
         a[0] += w;
         a[1] = fma(w, v, a[1]);
       });
-      block_allsum<2, NT>(a2, S.scratch, S.parity);
+      sample_allsum<2, NT>(a2, S);
       const double mu_new = a2[1] / a2[0];
       sample_sum<NT>(S, a1, [mu_new, c1, c2](double v, double (&a)[1]) {
         const double d = v - mu_new;
         const double w = c2 * rcp_q(fma(d, d, c1));
         a[0] = fma(w * d, d, a[0]);
       });
-      block_allsum<1, NT>(a1, S.scratch, S.parity);
+      sample_allsum<1, NT>(a1, S);
       const double sigma_new = dmax_std(1e-8, sqrt(a1[0] * inv_m));
       const double rel = fabs(sigma_new - sigma) / sigma;
       mu = mu_new;
@@ -567,7 +607,7 @@ __device__ __forceinline__ double stationarity(Sample& S, double mu, double sigm
     const double w = c2 * rcp_fast(fma(d, d, c1));
     acc[0] += (C + log(w)) - w;
   });
-  block_allsum<1, NT>(a, S.scratch, S.parity);
+  sample_allsum<1, NT>(a, S);
   return a[0] / (double)S.m;
 }
 
@@ -662,7 +702,10 @@ __global__ void __launch_bounds__(kTdistThreads, 2)
   Sample smp;
   smp.v = smp_sh;
   smp.m = n == 0 ? 0 : (int)((n - 1) / stride + 1);
+  smp.m_local = smp.m;
   smp.kfull = smp.m / NT;
+  smp.cs = 1;
+  smp.cbuf = nullptr;
   smp.memo_nu = -1.0;
   smp.scratch = scratch;
   smp.parity = 0;
@@ -716,14 +759,142 @@ __global__ void __launch_bounds__(kTdistThreads, 2)
   }
 }
 
+// Latency-mode K2: the sample of one (slot, residual type) is spread over a
+// cluster of kTdistCluster CTAs (sample s lives on rank s % CS); every pass
+// reduces in-CTA, then across the cluster through DSMEM.
+__global__ void __launch_bounds__(kTdistClusterThreads, 1)
+    k_tdist_cluster(const SlotIO* __restrict__ io, SlotState* __restrict__ st, LevelInfo li,
+                    int phase) {
+  constexpr int NT = kTdistClusterThreads, CS = kTdistCluster;
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  const int rank = (int)cl.block_rank();
+  const int type = blockIdx.x / CS, slot = blockIdx.y;
+  SlotState& S = st[slot];
+  if (!slot_active(S, li.level, phase)) return;  // uniform over the cluster
+  const SlotIO& o = io[slot];
+  const int* cnt = type ? o.cntW : o.cntI;
+  const unsigned* bits = type ? o.bitsW : o.bitsI;
+  const double* bv = type ? o.wb : o.ib;
+  const double* av = type ? (phase ? o.fWA : o.WA[li.level]) : (phase ? o.fIA : o.IA[li.level]);
+  extern __shared__ double dsm[];  // sample share [ceil(kMaxSample/CS)] + offs[ntiles + 1]
+  constexpr int kShare = (kMaxSample + CS - 1) / CS;
+  double* smp_sh = dsm;
+  int* offs = reinterpret_cast<int*>(dsm + kShare);
+  __shared__ int wsum[NT / 32];
+  __shared__ double scratch[NT / 32 * 2 * 2];
+  __shared__ double cbuf[4];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int nt = li.ntiles;
+  const int per = (nt + NT - 1) / NT;
+  const int b0 = min(nt, tid * per), b1 = min(nt, b0 + per);
+  int local = 0;
+  for (int i = b0; i < b1; ++i) local += cnt[i];
+  int incl = local;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, off);
+    if (lane >= off) incl += v;
+  }
+  if (lane == 31) wsum[wid] = incl;
+  __syncthreads();
+  int woff = 0, total = 0;
+  for (int k = 0; k < NT / 32; ++k) {
+    if (k < wid) woff += wsum[k];
+    total += wsum[k];
+  }
+  int run = woff + incl - local;
+  for (int i = b0; i < b1; ++i) {
+    offs[i] = run;
+    run += cnt[i];
+  }
+  if (tid == 0) offs[nt] = total;
+  __syncthreads();
+  const long long n = total;
+  const long long stride = n <= kMaxSample ? 1 : (n + kMaxSample - 1) / kMaxSample;
+  Sample smp;
+  smp.v = smp_sh;
+  smp.m = n == 0 ? 0 : (int)((n - 1) / stride + 1);
+  smp.m_local = smp.m > rank ? (smp.m - rank + CS - 1) / CS : 0;
+  for (int k = tid; k < smp.m_local; k += NT) {
+    const long long g = (long long)(rank + CS * k) * stride;
+    int lo = 0, hi = nt - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (offs[mid] <= g)
+        lo = mid;
+      else
+        hi = mid - 1;
+    }
+    int j = (int)(g - offs[lo]), word = 0;
+    unsigned msk = bits[lo * kWordsPerTile];
+    while (j >= __popc(msk)) {
+      j -= __popc(msk);
+      msk = bits[lo * kWordsPerTile + (++word)];
+    }
+    for (int q = 0; q < j; ++q) msk &= msk - 1u;
+    const int yl = lo / li.nseg, seg = lo - yl * li.nseg;
+    const int idx = yl * li.w + seg * li.tx + word * 32 + (__ffs(msk) - 1);
+    smp_sh[k] = bv[idx] - av[idx];
+  }
+  smp.kfull = smp.m_local / NT;
+  smp.cs = CS;
+  smp.cbuf = cbuf;
+  smp.memo_nu = -1.0;
+  smp.scratch = scratch;
+  smp.parity = 0;
+  cl.sync();  // every CTA's share (and cbuf) ready before the first cluster reduction
+  TD t = loc_scale<NT>(smp, 5.0, scratch);
+  t.sigma = dmax_std(t.sigma, 1e-8);
+  t.nu = estimate_nu<NT>(smp, t.mu, t.sigma, scratch);
+  if (t.nu < 4.99) {
+    const TD r = loc_scale<NT>(smp, t.nu, scratch);
+    if (r.sigma > 0.0) {
+      t.mu = r.mu;
+      t.sigma = dmax_std(r.sigma, 1e-8);
+    }
+  }
+  if (rank == 0 && tid == 0) {
+    rgbid_tdist out{t.mu, t.sigma, t.nu};
+    if (type == 0) {
+      S.tI = out;
+      S.nI = n;
+    } else {
+      S.tW = out;
+      S.nW = n;
+    }
+  }
+  cl.sync();  // no CTA exits while others may still read its cluster slots
+}
+
 int init_kernel_attributes() {
   const cudaError_t e =
       cudaFuncSetAttribute(k_tdist, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  const cudaError_t e2 =
+      cudaFuncSetAttribute(k_tdist_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
   cudaGetLastError();
-  return e == cudaSuccess ? 0 : 1;
+  return (e == cudaSuccess && e2 == cudaSuccess) ? 0 : 1;
 }
 
 void launch_tdist(const AlignLaunch& a, const LevelInfo& li, int phase, cudaStream_t s) {
+  if (a.nslots <= kTdistClusterMaxSlots) {  // latency mode: cluster per chain
+    KScope ks_("tdist_cluster", s);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * kTdistCluster, a.nslots);
+    cfg.blockDim = dim3(kTdistClusterThreads);
+    cfg.dynamicSmemBytes =
+        ((kMaxSample + kTdistCluster - 1) / kTdistCluster) * 8 + (li.ntiles + 1) * 4;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = kTdistCluster;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, k_tdist_cluster, a.io, a.st, li, phase);
+    return;
+  }
   KScope ks_("tdist", s);
   k_tdist<<<dim3(2, a.nslots), kTdistThreads, tdist_smem_bytes(li.ntiles), s>>>(a.io, a.st, li,
                                                                                  phase);
@@ -1196,7 +1367,10 @@ __global__ void __launch_bounds__(kTdistThreads, 2)
   Sample smp;
   smp.v = dsm;
   smp.m = n == 0 ? 0 : (int)((n - 1) / stride + 1);
+  smp.m_local = smp.m;
   smp.kfull = smp.m / NT;
+  smp.cs = 1;
+  smp.cbuf = nullptr;
   smp.memo_nu = -1.0;
   smp.scratch = scratch;
   smp.parity = 0;

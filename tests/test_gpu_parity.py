@@ -285,3 +285,48 @@ def test_kernels_launched(ctx):
     n0 = ctx.kernel_launches
     rg.align(f, f, K, ctx=ctx)
     assert ctx.kernel_launches > n0
+
+
+def _config4_inputs(K, i=0):
+    """W_m synthesised in a depth camera at T_DC =
+    random_pose(7, 0.025, 0.01), K_ir = K_rgb, beta0 = -0.005, beta1 = 1.02."""
+    T_DC = rg.random_pose(7, 0.025, 0.01)
+    T_WB = rg.random_pose(1000 + i, 0.003, 0.02)
+    fa = rg.render_plane(K, rg.Pose(), N_SLANT, -2.0, K.width / 80.0)
+    fb = rg.render_plane(K, T_WB, N_SLANT, -2.0, K.width / 80.0)
+    d = rg.DepthIntrinsics(beta0=-0.005, beta1=1.02, p0=(0.0, 0.0))
+    # what the depth sensor reports: the inverse depth seen from the depth camera,
+    # passed through the inverse of the linear correction
+    depth_views = []
+    for T_WC in (rg.Pose(), T_WB):
+        T_WD = T_WC * T_DC.inverse()
+        Wd = rg.render_plane(K, T_WD, N_SLANT, -2.0).inverse_depth
+        depth_views.append((Wd - d.beta0) / d.beta1)
+    return fa, fb, T_DC, d, depth_views
+
+
+def test_config4_unregistered_depth_path(ctx, orc):
+    """correct_inverse_depth -> forward_register (T_CD = T_DC^-1) -> 4-level align,
+    GPU vs oracle at every stage (bit-exact maps, pose within 1e-5)."""
+    K = rg.simple_intrinsics(320, 240, 240.0)
+    fa, fb, T_DC, d, (Wm_a, Wm_b) = _config4_inputs(K)
+    frames = []
+    for f, Wm in ((fa, Wm_a), (fb, Wm_b)):
+        g = rg.correct_inverse_depth(Wm, d, K, False, ctx)
+        o = orc.correct_inverse_depth(Wm, d.to_c(), K.to_c(), False)
+        assert bitwise_equal(g, o)
+        T_CD = T_DC.inverse()
+        gr = rg.forward_register(g, T_CD, K, K, ctx)
+        orr = orc.forward_register(o, T_CD.to_c(), K.to_c(), K.to_c())
+        assert bitwise_equal(gr, orr)
+        assert np.isfinite(gr).mean() > 0.8
+        frames.append(rg.FrameData(f.intensity, gr))
+    cfg = rg.AlignmentConfig(levels=4)
+    o = orc.align(frames[0].intensity, frames[0].inverse_depth, frames[1].intensity,
+                  frames[1].inverse_depth, K.to_c(), None, cfg.to_c())
+    if o.status != 0:
+        with pytest.raises(rg.DegenerateAlignmentError):
+            rg.align(frames[0], frames[1], K, config=cfg, ctx=ctx)
+        return
+    res = rg.align(frames[0], frames[1], K, config=cfg, ctx=ctx)
+    _check_align(res, o)
