@@ -107,33 +107,45 @@ __device__ __forceinline__ void bilinear2(const double* __restrict__ I, const do
   ow = bilin_fix(gy * (gx * b00 + fx * b10) + fy * (gx * b01 + fx * b11), b00, b10, b01, b11);
 }
 
-// one A pixel of inverse_geometric_warp — src/warping.cpp:96-111 (bit-identical)
+// one A pixel of inverse_geometric_warp — src/warping.cpp:96-111 (bit-identical).
+// Written branch-free (predicates + clamped, always-issued tap loads) so that
+// several pixels unrolled in one thread overlap their gathers.
 __device__ __forceinline__ void warp_px(const WarpMats& m, const double* __restrict__ IB,
                                         const double* __restrict__ WB, int wb, int hb, int x,
                                         int y, double w_a, double& oI, double& oW, double& mx,
                                         double& my) {
-  oI = CUDART_NAN;
-  oW = CUDART_NAN;
-  mx = CUDART_NAN;
-  my = CUDART_NAN;
-  if (!valid(w_a) || w_a <= 0.0) return;
-  const double qz = __drcp_rn(w_a);  // == 1.0 / w_a
-  const double qx = div_rcp((double)x, w_a, qz), qy = div_rcp((double)y, w_a, qz);
+  const bool v0 = valid(w_a) && w_a > 0.0;
+  const double wa = v0 ? w_a : 1.0;
+  const double qz = __drcp_rn(wa);  // == 1.0 / w_a
+  const double qx = div_rcp((double)x, wa, qz), qy = div_rcp((double)y, wa, qz);
   const double xb0 = red3(m.Rt_BA[0] * qx, m.Rt_BA[1] * qy, m.Rt_BA[2] * qz) + m.tt_BA[0];
   const double xb1 = red3(m.Rt_BA[3] * qx, m.Rt_BA[4] * qy, m.Rt_BA[5] * qz) + m.tt_BA[1];
   const double xb2 = red3(m.Rt_BA[6] * qx, m.Rt_BA[7] * qy, m.Rt_BA[8] * qz) + m.tt_BA[2];
-  if (xb2 <= 1e-12) return;
-  const double rz2 = __drcp_rn(xb2);
-  const double px = div_rcp(xb0, xb2, rz2), py = div_rcp(xb1, xb2, rz2);
-  mx = px;
-  my = py;
-  double w_meas;
-  bilinear2(IB, WB, wb, hb, px, py, oI, w_meas);
-  if (!valid(w_meas) || w_meas <= 0.0) return;
+  const bool v1 = v0 && xb2 > 1e-12;
+  const double z = v1 ? xb2 : 1.0;
+  const double rz2 = __drcp_rn(z);
+  const double px = div_rcp(xb0, z, rz2), py = div_rcp(xb1, z, rz2);
+  mx = v1 ? px : CUDART_NAN;
+  my = v1 ? py : CUDART_NAN;
+  const bool inb = v1 && (px >= 0.0 && px <= wb - 1.0 && py >= 0.0 && py <= hb - 1.0);
+  const double sx = inb ? px : 0.0, sy = inb ? py : 0.0;
+  const int x0 = (int)floor(sx), y0 = (int)floor(sy);
+  const int dx = x0 + 1 < wb ? 1 : 0;  // x1 = min(x0 + 1, w - 1)
+  const int dy = y0 + 1 < hb ? wb : 0; // y1 = min(y0 + 1, h - 1)
+  const double fx = sx - x0, fy = sy - y0, gx = 1 - fx, gy = 1 - fy;
+  const int i00 = y0 * wb + x0;
+  const double a00 = __ldg(IB + i00), a10 = __ldg(IB + i00 + dx), a01 = __ldg(IB + i00 + dy),
+               a11 = __ldg(IB + i00 + dy + dx);
+  const double b00 = __ldg(WB + i00), b10 = __ldg(WB + i00 + dx), b01 = __ldg(WB + i00 + dy),
+               b11 = __ldg(WB + i00 + dy + dx);
+  const double ri = bilin_fix(gy * (gx * a00 + fx * a10) + fy * (gx * a01 + fx * a11), a00, a10, a01, a11);
+  const double w_meas = bilin_fix(gy * (gx * b00 + fx * b10) + fy * (gx * b01 + fx * b11), b00, b10, b01, b11);
+  oI = inb ? ri : CUDART_NAN;
+  const bool v2 = inb && valid(w_meas) && w_meas > 0.0;
   const double rz = red3(m.Rt_AB[6] * px, m.Rt_AB[7] * py, m.Rt_AB[8] * 1.0);
-  const double za = rz / w_meas + m.tt_AB[2];
-  if (za <= 1e-12) return;
-  oW = __drcp_rn(za);  // == 1.0 / za
+  const double za = rz / (v2 ? w_meas : 1.0) + m.tt_AB[2];
+  const bool v3 = v2 && za > 1e-12;
+  oW = v3 ? __drcp_rn(za) : CUDART_NAN;  // == 1.0 / za
 }
 
 __device__ __forceinline__ double px_or_nan(const double* img, int w, int h, int x, int y) {
@@ -207,7 +219,7 @@ __device__ __forceinline__ void load_wm(const WarpMats& g, WarpMats& m) {
 // adds the warped-B conditions and ballots the row-major validity bits per
 // tile (compacted rank = prefix popcount, consumed by the sample gather of K2).
 template <int L>
-__global__ void __launch_bounds__(kTPB) k_warp_residuals(const SlotIO* __restrict__ io,
+__global__ void __launch_bounds__(kTPB, 6) k_warp_residuals(const SlotIO* __restrict__ io,
                                                          const SlotState* __restrict__ st,
                                                          LevelInfo li, int w0, int h0, int phase) {
   const int slot = blockIdx.y;
@@ -550,23 +562,25 @@ __device__ __forceinline__ TD loc_scale(Sample& S, double nu, double* scratch) {
   } else {
     const double nu1 = nu + 1.0;
     for (int it = 0; it < 50; ++it) {
-      // t_weight((v-mu)/sigma, nu) = (nu+1) s2 / (nu s2 + (v-mu)^2), s2 = sigma^2
+      // t_weight((v-mu)/sigma, nu) = c2 / (c1 + (v-mu)^2), c1 = nu s2, c2 = (nu+1) s2;
+      // the constant c2 is applied after the reduction (sums of 1/(c1 + d^2))
       const double s2 = sigma * sigma, c1 = nu * s2, c2 = nu1 * s2;
       double a2[2];
-      sample_sum<NT>(S, a2, [mu, c1, c2](double v, double (&a)[2]) {
+      sample_sum<NT>(S, a2, [mu, c1](double v, double (&a)[2]) {
         const double d = v - mu;
-        const double w = c2 * rcp_q(fma(d, d, c1));
-        a[0] += w;
-        a[1] = fma(w, v, a[1]);
+        const double r = rcp_q(fma(d, d, c1));
+        a[0] += r;
+        a[1] = fma(r, v, a[1]);
       });
       sample_allsum<2, NT>(a2, S);
-      const double mu_new = a2[1] / a2[0];
-      sample_sum<NT>(S, a1, [mu_new, c1, c2](double v, double (&a)[1]) {
+      const double mu_new = a2[1] / a2[0];  // (c2 sum r v) / (c2 sum r)
+      sample_sum<NT>(S, a1, [mu_new, c1](double v, double (&a)[1]) {
         const double d = v - mu_new;
-        const double w = c2 * rcp_q(fma(d, d, c1));
-        a[0] = fma(w * d, d, a[0]);
+        const double r = rcp_q(fma(d, d, c1));
+        a[0] = fma(r * d, d, a[0]);
       });
       sample_allsum<1, NT>(a1, S);
+      a1[0] *= c2;
       const double sigma_new = dmax_std(1e-8, sqrt(a1[0] * inv_m));
       const double rel = fabs(sigma_new - sigma) / sigma;
       mu = mu_new;
@@ -896,8 +910,24 @@ void launch_tdist(const AlignLaunch& a, const LevelInfo& li, int phase, cudaStre
     return;
   }
   KScope ks_("tdist", s);
-  k_tdist<<<dim3(2, a.nslots), kTdistThreads, tdist_smem_bytes(li.ntiles), s>>>(a.io, a.st, li,
-                                                                                 phase);
+  // highest launch priority: the FP64-bound chains claim SMs first, the other
+  // lane's memory-bound kernels fill around them
+  static int prio = [] {
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    return hi;
+  }();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2, a.nslots);
+  cfg.blockDim = dim3(kTdistThreads);
+  cfg.dynamicSmemBytes = tdist_smem_bytes(li.ntiles);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributePriority;
+  attr[0].val.priority = prio;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k_tdist, a.io, (SlotState*)a.st, li, phase);
 }
 
 // ---------------------------------------------------------------------------
