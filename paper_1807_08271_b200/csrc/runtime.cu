@@ -13,6 +13,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <functional>
 #include <map>
 #include <mutex>
 #include <string>
@@ -52,6 +53,7 @@ struct CachedGraph {
 struct Lane {
   cudaStream_t stream = nullptr;
   cudaEvent_t done = nullptr;
+  cudaEvent_t ready = nullptr;  // slot records uploaded (pair launches wait on it)
   int cap_slots = 0, cap_w = 0, cap_h = 0;
   double* ws_f64 = nullptr;
   int* ws_i32 = nullptr;
@@ -79,6 +81,7 @@ struct rgbid_ctx {
   rgbid_iter_trace* d_trace = nullptr;
   std::vector<rgbid_iter_trace> last_trace;
   bool use_graphs = true;
+  std::vector<cudaEvent_t> pair_events;  // stage events of co-scheduled chunk pairs
   // scratch device buffers for the one-shot host APIs
   std::map<std::string, std::pair<void*, size_t>> scratch;
   rgbid_frame* tmpA = nullptr;
@@ -381,30 +384,77 @@ int validate_cfg(const rgbid_align_config& c, int w, int h) {
   return RGBID_OK;
 }
 
-// Enqueue the whole align (all levels + covariance pass) for ctx->cap slots.
-void enqueue_align(cudaStream_t stream, const AlignLaunch& a, const rgbid_intrinsics& K,
-                   const rgbid_align_config& cfg) {
+// The whole align (all levels + covariance pass) as a list of stages; a stage
+// is one or more dependent kernel launches on one stream.  Stages cycle
+// K1 | K2 | K3+K4 per IRLS iteration so that two chunks offset by one stage
+// pair the FP64-bound Student-t kernel with a memory-bound kernel.
+using Stage = std::function<void(cudaStream_t)>;
+
+std::vector<Stage> align_stages(const AlignLaunch& a, const rgbid_intrinsics& K,
+                                const rgbid_align_config& cfg) {
+  std::vector<Stage> st;
   const LevelInfo li0 = make_level(K, a.w0, a.h0, 0);
-  launch_pyramid_slots(a, cfg.levels, stream);  // build_pyramid (src/alignment.cpp:369)
-  launch_amask(a, cfg.levels, 0, stream);        // A-side jet validity, once per align
+  const int levels = cfg.levels;
+  st.push_back([a, levels](cudaStream_t s) {
+    launch_pyramid_slots(a, levels, s);  // build_pyramid (src/alignment.cpp:369)
+    launch_amask(a, levels, 0, s);       // A-side validity + gradients, once per align
+  });
   for (int level = cfg.levels - 1; level >= 0; --level) {
     const LevelInfo li = make_level(K, a.w0, a.h0, level);
     const int iters = level_iters(cfg, level);
     for (int it = 0; it < iters; ++it) {
-      launch_warp_residuals(a, li, 0, stream);
-      launch_tdist(a, li, 0, stream);
-      launch_normal_equations(a, li, 0, stream);
-      launch_solve(a, li, li0, stream);
+      st.push_back([a, li](cudaStream_t s) { launch_warp_residuals(a, li, 0, s); });
+      st.push_back([a, li](cudaStream_t s) { launch_tdist(a, li, 0, s); });
+      st.push_back([a, li, li0](cudaStream_t s) {
+        launch_normal_equations(a, li, 0, s);
+        launch_solve(a, li, li0, s);
+      });
     }
   }
   // filtered_hessian_covariance — src/alignment.cpp:406-407, 411-436
-  launch_bilateral_pair(a, cfg.bilateral_sigma_space, cfg.bilateral_sigma_intensity,
-                        cfg.bilateral_sigma_depth, stream);
-  launch_amask(a, 1, 1, stream);
-  launch_warp_residuals(a, li0, 1, stream);
-  launch_tdist(a, li0, 1, stream);
-  launch_normal_equations(a, li0, 1, stream);
-  launch_covariance(a, li0, stream);
+  const double ss = cfg.bilateral_sigma_space, si = cfg.bilateral_sigma_intensity,
+               sd = cfg.bilateral_sigma_depth;
+  st.push_back([a, li0, ss, si, sd](cudaStream_t s) {
+    launch_bilateral_pair(a, ss, si, sd, s);
+    launch_amask(a, 1, 1, s);
+    launch_warp_residuals(a, li0, 1, s);
+  });
+  st.push_back([a, li0](cudaStream_t s) { launch_tdist(a, li0, 1, s); });
+  st.push_back([a, li0](cudaStream_t s) {
+    launch_normal_equations(a, li0, 1, s);
+    launch_covariance(a, li0, s);
+  });
+  return st;
+}
+
+void enqueue_align(cudaStream_t stream, const AlignLaunch& a, const rgbid_intrinsics& K,
+                   const rgbid_align_config& cfg) {
+  for (auto& f : align_stages(a, K, cfg)) f(stream);
+}
+
+// Two chunks in one launch sequence: stage s of B after stage s of A, stage
+// s+2 of A after stage s of B -> the pairs {A_{s+1}, B_s} run concurrently.
+void enqueue_align_pair(cudaStream_t sA, cudaStream_t sB, const AlignLaunch& a,
+                        const AlignLaunch& b, const rgbid_intrinsics& K,
+                        const rgbid_align_config& cfg, std::vector<cudaEvent_t>& ev) {
+  const std::vector<Stage> A = align_stages(a, K, cfg), B = align_stages(b, K, cfg);
+  const size_t n = A.size();
+  while (ev.size() < 2 * n + 1) {
+    cudaEvent_t e;
+    cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    ev.push_back(e);
+  }
+  cudaEventRecord(ev[2 * n], sA);  // fork B off A's stream (capture origin)
+  cudaStreamWaitEvent(sB, ev[2 * n], 0);
+  for (size_t i = 0; i < n; ++i) {
+    if (i >= 2) cudaStreamWaitEvent(sA, ev[n + i - 2], 0);
+    A[i](sA);
+    cudaEventRecord(ev[i], sA);
+    cudaStreamWaitEvent(sB, ev[i], 0);
+    B[i](sB);
+    cudaEventRecord(ev[n + i], sB);
+  }
+  cudaStreamWaitEvent(sA, ev[2 * n - 1], 0);  // join
 }
 
 // Unpacks the SlotState records of a lane's finished chunk into results.
@@ -448,10 +498,10 @@ int finish_chunk(rgbid_ctx* ctx, Lane& L) {
 
 // Enqueues n alignments (one chunk) on lane L: slot setup, H2D of the slot
 // records, the (cached) CUDA graph of the whole align, D2H of the results.
-int enqueue_chunk(rgbid_ctx* ctx, Lane& L, int n, const rgbid_frame* const* fa,
+int prepare_chunk(rgbid_ctx* ctx, Lane& L, int n, const rgbid_frame* const* fa,
                   const rgbid_frame* const* fb, const rgbid_intrinsics& K,
-                  const rgbid_pose* inits, const rgbid_align_config& cfg,
-                  rgbid_align_result* results, bool want_trace) {
+                  const rgbid_pose* inits, const rgbid_align_config& cfg, bool want_trace,
+                  AlignLaunch* out_a) {
   int rc = finish_chunk(ctx, L);  // the lane's previous chunk owns h_st_pinned
   if (rc) return rc;
   const int w = fa[0]->w, h = fa[0]->h;
@@ -537,46 +587,8 @@ int enqueue_chunk(rgbid_ctx* ctx, Lane& L, int n, const rgbid_frame* const* fa,
   a.eps = cfg.convergence_eps;
   a.lambda_n_min = cfg.lambda_n_min;
 
-  // every value baked into the launch sequence is part of the graph key
-  struct {
-    int nslots, trace, levels, w, h;
-    int iters[kMaxLevels];
-    double p[9];
-  } kb;
-  std::memset(&kb, 0, sizeof(kb));
-  kb.nslots = nslots;
-  kb.trace = want_trace;
-  kb.levels = cfg.levels;
-  kb.w = w;
-  kb.h = h;
-  for (int l = 0; l < cfg.levels; ++l) kb.iters[l] = level_iters(cfg, l);
-  const double p[9] = {cfg.convergence_eps, cfg.lambda_n_min, cfg.bilateral_sigma_space,
-                       cfg.bilateral_sigma_intensity, cfg.bilateral_sigma_depth, K.fx, K.fy, K.cx,
-                       K.cy};
-  std::memcpy(kb.p, p, sizeof(p));
-  const std::string key(reinterpret_cast<const char*>(&kb), sizeof(kb));
-  if (ctx->use_graphs && !ctx->prof.enabled) {
-    auto it = L.graphs.find(key);
-    if (it == L.graphs.end()) {
-      cudaGraph_t g;
-      CK(cudaStreamBeginCapture(L.stream, cudaStreamCaptureModeThreadLocal));
-      const long long before = ctx->launches;
-      enqueue_align(L.stream, a, K, cfg);
-      CachedGraph cg;
-      cg.launches = ctx->launches - before;
-      ctx->launches = before;
-      CK(cudaStreamEndCapture(L.stream, &g));
-      CK(cudaGraphInstantiate(&cg.exec, g, 0));
-      cudaGraphDestroy(g);
-      it = L.graphs.emplace(key, cg).first;
-    }
-    CK(cudaGraphLaunch(it->second.exec, L.stream));
-    ctx->launches += it->second.launches;
-  } else {
-    enqueue_align(L.stream, a, K, cfg);
-  }
-  rc = check_launch(ctx);
-  if (rc) return rc;
+  *out_a = a;
+  // remember what finish_chunk / the pyramid bookkeeping need
   for (int i = 0; i < nslots; ++i) {
     rgbid_frame* f = const_cast<rgbid_frame*>(fa[i]);
     if (L.h_io[i].build_pyr) {
@@ -585,13 +597,96 @@ int enqueue_chunk(rgbid_ctx* ctx, Lane& L, int n, const rgbid_frame* const* fa,
     }
     f->pyr_levels = std::max(f->pyr_levels, cfg.levels);
   }
-  D2HS(L.stream, L.h_st_pinned, L.d_st, sizeof(SlotState) * nslots);
+  return RGBID_OK;
+}
+
+std::string graph_key(int nA, int nB, bool trace, int w, int h, const rgbid_intrinsics& K,
+                      const rgbid_align_config& cfg) {
+  struct {
+    int nA, nB, trace, levels, w, h;
+    int iters[kMaxLevels];
+    double p[9];
+  } kb;
+  std::memset(&kb, 0, sizeof(kb));
+  kb.nA = nA;
+  kb.nB = nB;
+  kb.trace = trace;
+  kb.levels = cfg.levels;
+  kb.w = w;
+  kb.h = h;
+  for (int l = 0; l < cfg.levels; ++l) kb.iters[l] = level_iters(cfg, l);
+  const double p[9] = {cfg.convergence_eps, cfg.lambda_n_min, cfg.bilateral_sigma_space,
+                       cfg.bilateral_sigma_intensity, cfg.bilateral_sigma_depth, K.fx, K.fy, K.cx,
+                       K.cy};
+  std::memcpy(kb.p, p, sizeof(p));
+  return std::string(reinterpret_cast<const char*>(&kb), sizeof(kb));
+}
+
+// Launch (graph replay) + result D2H + completion event for one prepared chunk,
+// or for two prepared chunks co-scheduled (LB != nullptr).
+int launch_prepared(rgbid_ctx* ctx, Lane& L, const AlignLaunch& a, Lane* LB,
+                    const AlignLaunch* b, const rgbid_intrinsics& K,
+                    const rgbid_align_config& cfg, rgbid_align_result* resA,
+                    rgbid_align_result* resB, bool want_trace) {
+  const std::string key =
+      graph_key(a.nslots, LB ? b->nslots : 0, want_trace, a.w0, a.h0, K, cfg);
+  if (LB) {  // B's slot records were uploaded on its own stream
+    CK(cudaEventRecord(LB->ready, LB->stream));
+    CK(cudaStreamWaitEvent(L.stream, LB->ready, 0));
+  }
+  if (ctx->use_graphs && !ctx->prof.enabled) {
+    auto it = L.graphs.find(key);
+    if (it == L.graphs.end()) {
+      cudaGraph_t g;
+      CK(cudaStreamBeginCapture(L.stream, cudaStreamCaptureModeThreadLocal));
+      const long long before = ctx->launches;
+      if (LB)
+        enqueue_align_pair(L.stream, LB->stream, a, *b, K, cfg, ctx->pair_events);
+      else
+        enqueue_align(L.stream, a, K, cfg);
+      CachedGraph cg;
+      cg.launches = ctx->launches - before;
+      ctx->launches = before;
+      CK(cudaStreamEndCapture(L.stream, &g));
+      CK(cudaGraphInstantiateWithFlags(&cg.exec, g, cudaGraphInstantiateFlagUseNodePriority));
+      cudaGraphDestroy(g);
+      it = L.graphs.emplace(key, cg).first;
+    }
+    CK(cudaGraphLaunch(it->second.exec, L.stream));
+    ctx->launches += it->second.launches;
+  } else if (LB) {
+    enqueue_align_pair(L.stream, LB->stream, a, *b, K, cfg, ctx->pair_events);
+  } else {
+    enqueue_align(L.stream, a, K, cfg);
+  }
+  int rc = check_launch(ctx);
+  if (rc) return rc;
+  D2HS(L.stream, L.h_st_pinned, L.d_st, sizeof(SlotState) * a.nslots);
+  if (LB) D2HS(L.stream, LB->h_st_pinned, LB->d_st, sizeof(SlotState) * b->nslots);
   CK(cudaEventRecord(L.done, L.stream));
-  L.pend_n = nslots;
-  L.pend_results = results;
+  L.pend_n = a.nslots;
+  L.pend_results = resA;
   L.pend_levels = cfg.levels;
   L.pend_trace = want_trace;
+  if (LB) {
+    CK(cudaStreamWaitEvent(LB->stream, L.done, 0));
+    CK(cudaEventRecord(LB->done, LB->stream));
+    LB->pend_n = b->nslots;
+    LB->pend_results = resB;
+    LB->pend_levels = cfg.levels;
+    LB->pend_trace = false;
+  }
   return RGBID_OK;
+}
+
+int enqueue_chunk(rgbid_ctx* ctx, Lane& L, int n, const rgbid_frame* const* fa,
+                  const rgbid_frame* const* fb, const rgbid_intrinsics& K,
+                  const rgbid_pose* inits, const rgbid_align_config& cfg,
+                  rgbid_align_result* results, bool want_trace) {
+  AlignLaunch a;
+  int rc = prepare_chunk(ctx, L, n, fa, fb, K, inits, cfg, want_trace, &a);
+  if (rc) return rc;
+  return launch_prepared(ctx, L, a, nullptr, nullptr, K, cfg, results, nullptr, want_trace);
 }
 
 // n alignments on one lane, synchronous (single align / small batches)
@@ -650,7 +745,8 @@ int rgbid_ctx_create(int device, rgbid_ctx** out) {
   ctx->device = device;
   for (int k = 0; k < kLanes; ++k) {
     if (cudaStreamCreateWithFlags(&ctx->lanes[k].stream, cudaStreamNonBlocking) != cudaSuccess ||
-        cudaEventCreateWithFlags(&ctx->lanes[k].done, cudaEventDisableTiming) != cudaSuccess) {
+        cudaEventCreateWithFlags(&ctx->lanes[k].done, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ctx->lanes[k].ready, cudaEventDisableTiming) != cudaSuccess) {
       delete ctx;
       return RGBID_E_CUDA;
     }
@@ -683,7 +779,9 @@ int rgbid_ctx_destroy(rgbid_ctx* ctx) {
   if (ctx->tmpA) rgbid_frame_destroy(ctx, ctx->tmpA);
   if (ctx->tmpB) rgbid_frame_destroy(ctx, ctx->tmpB);
   cudaFree(ctx->d_trace);
+  for (auto& e : ctx->pair_events) cudaEventDestroy(e);
   for (auto& L : ctx->lanes) {
+    cudaEventDestroy(L.ready);
     cudaEventDestroy(L.done);
     cudaStreamDestroy(L.stream);
   }
@@ -870,13 +968,30 @@ int rgbid_align_batch(rgbid_ctx* ctx, int n, const rgbid_frame* const* a,
   // enqueued while chunk c runs)
   const int nch = (n + chunk - 1) / chunk;
   chunk = (n + nch - 1) / nch;
-  const int lanes = ctx->prof.enabled ? 1 : kLanes;  // profiling: serialised kernel times
-  int lane = 0;
-  for (int i0 = 0; i0 < n; i0 += chunk, lane = (lane + 1) % lanes) {
+  // chunks go out in co-scheduled pairs (one graph, stage-offset), except when
+  // profiling (serialised kernel times) or for a trailing single chunk
+  const bool pairs = !ctx->prof.enabled && std::getenv("RGBID_NO_PAIRS") == nullptr;
+  for (int i0 = 0; i0 < n;) {
     const int m = std::min(chunk, n - i0);
-    const int rc = enqueue_chunk(ctx, ctx->lanes[lane], m, a + i0, b + i0, *K,
-                                 inits ? inits + i0 : nullptr, c, results + i0, i0 == 0);
-    if (rc) return rc;
+    const int m2 = pairs ? std::min(chunk, n - i0 - m) : 0;
+    if (m2 > 0 && m2 == m) {
+      AlignLaunch pa, pb;
+      int rc = prepare_chunk(ctx, ctx->lanes[0], m, a + i0, b + i0, *K,
+                             inits ? inits + i0 : nullptr, c, i0 == 0, &pa);
+      if (rc) return rc;
+      rc = prepare_chunk(ctx, ctx->lanes[1], m2, a + i0 + m, b + i0 + m, *K,
+                         inits ? inits + i0 + m : nullptr, c, false, &pb);
+      if (rc) return rc;
+      rc = launch_prepared(ctx, ctx->lanes[0], pa, &ctx->lanes[1], &pb, *K, c, results + i0,
+                           results + i0 + m, i0 == 0);
+      if (rc) return rc;
+      i0 += m + m2;
+    } else {
+      const int rc = enqueue_chunk(ctx, ctx->lanes[0], m, a + i0, b + i0, *K,
+                                   inits ? inits + i0 : nullptr, c, results + i0, i0 == 0);
+      if (rc) return rc;
+      i0 += m;
+    }
   }
   for (auto& L : ctx->lanes) {
     const int rc = finish_chunk(ctx, L);
