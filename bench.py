@@ -342,6 +342,13 @@ def main():
         json.dump({"kernels": kstats, "bytes": {"total": tot_bytes, "warp": warp_bytes}},
                   open(args.profile_json, "w"), indent=1)
 
+    # measured FP64 FMA peak: denominator of the FP64-issue-bound Student-t kernel
+    fp64 = C.c_double(0.0)
+    ctx.check(ctx.lib.rgbid_measure_fp64_peak(ctx.h, C.byref(fp64)), "fp64_peak")
+    tdist_ms = sum(v[1] for k, v in kstats.items() if k.startswith("tdist"))
+    roofline["fp64_peak_tflops_measured"] = fp64.value
+    roofline["tdist_share_of_step"] = tdist_ms / prof_total if prof_total else None
+
     # latency: one pair, device-resident, 4 levels; + one keyframe fusion
     lat = {}
     if rank == 0:

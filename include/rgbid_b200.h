@@ -143,6 +143,12 @@ int rgbid_ctx_transfer_bytes(rgbid_ctx* ctx, long long* h2d, long long* d2h);
 int rgbid_frame_create(rgbid_ctx* ctx, int width, int height, rgbid_frame** out);
 int rgbid_frame_upload(rgbid_ctx* ctx, rgbid_frame* f, const double* I, const double* W);
 int rgbid_frame_download(rgbid_ctx* ctx, const rgbid_frame* f, double* I, double* W);
+/* Frame ingest from the sensor wire format — load_frame's decode (src/dataset.cpp:97-116):
+ * bgr (w*h*3 u8, may be NULL) -> gray (0.299R + 0.587G + 0.114B)/255; depth (w*h u16)
+ * -> scale/raw with raw 0 -> hole, scale = depth_scale / depth_factor (5000 for TUM).
+ * Uploads 5 B/px instead of 16 B/px of fp64 maps. */
+int rgbid_frame_decode(rgbid_ctx* ctx, rgbid_frame* f, const uint8_t* bgr, const uint16_t* depth,
+                       double scale);
 /* device pointers of the frame's level-0 maps (for zero-copy producers) */
 int rgbid_frame_device_ptrs(rgbid_frame* f, double** I_dev, double** W_dev);
 int rgbid_frame_destroy(rgbid_ctx* ctx, rgbid_frame* f);
@@ -299,6 +305,10 @@ int rgbid_estimate_nu(rgbid_ctx* ctx, const double* r, long long n, double mu, d
  * against IEEE division on n random operand pairs; *mismatches must be 0. */
 int rgbid_selftest_division(rgbid_ctx* ctx, unsigned long long n, unsigned long long seed,
                             unsigned long long* mismatches);
+
+/* measured FP64 FMA throughput of this device (TFLOP/s, FMA = 2 flops): the
+ * roofline denominator of the FP64-issue-bound Student-t kernel */
+int rgbid_measure_fp64_peak(rgbid_ctx* ctx, double* tflops);
 
 /* ---- synthetic inputs (restates /root/reference/proj/tests/synthetic.hpp) ---- */
 /* render_plane(K, T_WC, n, d) with plane_texture evaluated at tex_scale * (X, Y) */

@@ -79,6 +79,8 @@ def _sig(L, prefix):
                                                 P(Intrinsics_t), C.c_double, DP, P(C.c_int),
                                                 P(C.c_longlong)])
         sigs["downsample2"] = (None, [DP, C.c_int, C.c_int, DP])
+        sigs["decode_frame"] = (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_double,
+                                          DP, DP])
     else:
         sigs["align"] = (C.c_int, [DP, DP, DP, DP, C.c_int, C.c_int, P(Intrinsics_t), P(Pose_t),
                                    P(AlignConfig_t), P(AlignResult_t)])
@@ -271,6 +273,15 @@ class Oracle:
         out = np.empty(9)
         self._f("mat3_inverse")(dptr(m), dptr(out))
         return out.reshape(3, 3)
+
+    def decode_frame(self, bgr, depth, scale=5000.0):
+        h, w = depth.shape
+        I = np.empty((h, w))
+        W = np.empty((h, w))
+        depth = np.ascontiguousarray(depth, dtype=np.uint16)
+        bgr = np.ascontiguousarray(bgr, dtype=np.uint8)
+        self._f("decode_frame")(bgr.ctypes.data, depth.ctypes.data, w, h, scale, dptr(I), dptr(W))
+        return I, W
 
     # reference-only fixtures (tests/synthetic.hpp)
     def render_plane(self, K, T_WC, n=(0.0, 0.0, 1.0), d=-2.0):

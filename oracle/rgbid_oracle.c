@@ -1177,3 +1177,13 @@ int or_forward_register(const double* WA, int w, int h, const rgbid_pose* T_BA,
   free(inter);
   return 0;
 }
+
+/* load_frame's pixel decode — src/dataset.cpp:97-116 */
+int or_decode_frame(const unsigned char* bgr, const unsigned short* depth, int w, int h,
+                    double scale, double* I, double* W) {
+  for (int i = 0; i < w * h; ++i) {
+    if (bgr) I[i] = (0.299 * bgr[3 * i + 2] + 0.587 * bgr[3 * i + 1] + 0.114 * bgr[3 * i]) / 255.0;
+    W[i] = depth[i] == 0 ? NAN : scale / (double)depth[i];
+  }
+  return 0;
+}

@@ -57,6 +57,8 @@ int or_pose_update(const double xi[6], const rgbid_pose* T, rgbid_pose* out);
 int or_pose_inverse(const rgbid_pose* a, rgbid_pose* out);
 int or_pose_compose(const rgbid_pose* a, const rgbid_pose* b, rgbid_pose* out);
 int or_mat3_inverse(const double m[9], double out[9]);
+int or_decode_frame(const unsigned char* bgr, const unsigned short* depth, int w, int h,
+                    double scale, double* I, double* W);
 
 #ifdef __cplusplus
 }

@@ -108,6 +108,7 @@ EXPORTS = [
     ("rgbid_frame_download", C.c_int, [VP, VP, DP, DP]),
     ("rgbid_frame_device_ptrs", C.c_int, [VP, C.POINTER(DP), C.POINTER(DP)]),
     ("rgbid_frame_destroy", C.c_int, [VP, VP]),
+    ("rgbid_frame_decode", C.c_int, [VP, VP, C.c_void_p, C.c_void_p, C.c_double]),
     ("rgbid_frame_invalidate", C.c_int, [VP]),
     ("rgbid_build_pyramid", C.c_int, [VP, DP, DP, C.c_int, C.c_int, C.POINTER(Intrinsics_t),
                                       C.c_int, C.POINTER(DP), C.POINTER(DP),
@@ -169,6 +170,7 @@ EXPORTS = [
                                     C.POINTER(C.c_double)]),
     ("rgbid_selftest_division", C.c_int, [VP, C.c_ulonglong, C.c_ulonglong,
                                           C.POINTER(C.c_ulonglong)]),
+    ("rgbid_measure_fp64_peak", C.c_int, [VP, C.POINTER(C.c_double)]),
     ("rgbid_synth_render_plane", C.c_int, [C.POINTER(Intrinsics_t), C.POINTER(Pose_t), DP,
                                            C.c_double, C.c_double, DP, DP]),
     ("rgbid_synth_random_pose", C.c_int, [C.c_uint32, C.c_int, C.c_double, C.c_double,

@@ -1450,6 +1450,45 @@ __global__ void k_selftest_div(unsigned long long n, unsigned long long seed,
   if (bad) atomicAdd(mismatches, bad);
 }
 
+// FP64 FMA throughput probe: 8 independent DFMA chains per thread, all SMs.
+__global__ void k_fp64_peak(int iters, double seed, double* out) {
+  double a[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) a[i] = seed + threadIdx.x * 1e-9 + i;
+  const double b = 0.999999999, c = 1e-12;
+  for (int it = 0; it < iters; ++it)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) a[i] = fma(a[i], b, c);
+  double s = 0.0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += a[i];
+  if (s == 42.0) out[0] = s;  // keep the chains alive
+}
+
+double measure_fp64_tflops(cudaStream_t s) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  double* out;
+  cudaMalloc(&out, sizeof(double));
+  const int blocks = sms * 8, threads = 256, iters = 4096;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  k_fp64_peak<<<blocks, threads, 0, s>>>(64, 1.0, out);  // warm-up
+  cudaEventRecord(e0, s);
+  k_fp64_peak<<<blocks, threads, 0, s>>>(iters, 1.0, out);
+  cudaEventRecord(e1, s);
+  cudaEventSynchronize(e1);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(out);
+  const double flops = 2.0 * 8.0 * iters * (double)blocks * threads;
+  return flops / (ms * 1e-3) / 1e12;
+}
+
 int selftest_division(unsigned long long n, unsigned long long seed, unsigned long long* out,
                       cudaStream_t s) {
   unsigned long long* d;

@@ -115,6 +115,7 @@ void launch_warp_maps(const double* IB, const double* WB, int wb, int hb, const 
                       int h, const WarpMats& m, double* oI, double* oW, double* omx, double* omy,
                       cudaStream_t s);
 int tdist_smem_bytes(int ntiles);
+double measure_fp64_tflops(cudaStream_t s);
 void launch_fill(double* p, long long n, double v, cudaStream_t s);
 void launch_remap_bilinear(const double* src, int w, int h, const double* mx, const double* my,
                            int n, double* out, cudaStream_t s);

@@ -298,4 +298,26 @@ void launch_render(const SynthView& v, double* I, double* W, cudaStream_t s) {
   k_render<<<(v.w * v.h + 255) / 256, 256, 0, s>>>(v, I, W);
 }
 
+// ---------------------------------------------------------------------------
+// Frame ingest — load_frame's pixel decode (src/dataset.cpp:97-116): BGR8 ->
+// gray = (0.299 R + 0.587 G + 0.114 B) / 255, depth16 -> scale / raw (0 = hole).
+__global__ void k_decode_frame(const uint8_t* __restrict__ bgr, const uint16_t* __restrict__ depth,
+                               int n, double scale, double* __restrict__ I,
+                               double* __restrict__ W) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  if (bgr) {
+    const double b = bgr[3 * i], g = bgr[3 * i + 1], r = bgr[3 * i + 2];
+    I[i] = (0.299 * r + 0.587 * g + 0.114 * b) / 255.0;
+  }
+  const uint16_t raw = depth[i];
+  W[i] = raw == 0 ? CUDART_NAN : scale / (double)raw;
+}
+
+void launch_decode_frame(const uint8_t* bgr, const uint16_t* depth, int n, double scale, double* I,
+                         double* W, cudaStream_t s) {
+  KScope ks_("decode_frame", s);
+  k_decode_frame<<<(n + 255) / 256, 256, 0, s>>>(bgr, depth, n, scale, I, W);
+}
+
 }  // namespace rgbid_b200

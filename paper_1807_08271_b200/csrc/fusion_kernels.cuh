@@ -2,6 +2,8 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <cstdint>
+
 #include "hd_math.cuh"
 
 namespace rgbid_b200 {
@@ -42,5 +44,7 @@ void launch_forward_register(const double* WA, int w, int h, const RegisterMats&
                              unsigned long long* inter, int iw, int ih, int wb, int hb,
                              double* out, cudaStream_t s);
 void launch_render(const SynthView& v, double* I, double* W, cudaStream_t s);
+void launch_decode_frame(const uint8_t* bgr, const uint16_t* depth, int n, double scale, double* I,
+                         double* W, cudaStream_t s);
 
 }  // namespace rgbid_b200

@@ -1447,6 +1447,33 @@ int rgbid_fill(rgbid_ctx* ctx, double* dev, long long n, double value) {
   return check_launch(ctx);
 }
 
+int rgbid_frame_decode(rgbid_ctx* ctx, rgbid_frame* f, const uint8_t* bgr, const uint16_t* depth,
+                       double scale) {
+  if (!ctx || !f || !depth) return RGBID_E_ARG;
+  LaunchScope ls(ctx);
+  const size_t N = (size_t)f->w * f->h;
+  uint8_t* d;
+  int rc = scratch_buf(ctx, "decode", 5 * N, &d);
+  if (rc) return rc;
+  uint16_t* dd = reinterpret_cast<uint16_t*>(d + 3 * N);
+  if (bgr) H2D(d, bgr, 3 * N);
+  H2D(dd, depth, 2 * N);
+  if (!bgr) CK(cudaMemsetAsync(f->I, 0xff, sizeof(double) * N, ctx->stream));
+  launch_decode_frame(bgr ? d : nullptr, dd, (int)N, scale, f->I, f->W, ctx->stream);
+  f->pyr_levels = 0;
+  f->pyr_lane = -1;
+  rc = check_launch(ctx);
+  if (rc) return rc;
+  CK(cudaStreamSynchronize(ctx->stream));
+  return RGBID_OK;
+}
+
+int rgbid_measure_fp64_peak(rgbid_ctx* ctx, double* tflops) {
+  if (!ctx || !tflops) return RGBID_E_ARG;
+  *tflops = measure_fp64_tflops(ctx->stream);
+  return check_launch(ctx);
+}
+
 int rgbid_frame_invalidate(rgbid_frame* f) {
   if (!f) return RGBID_E_ARG;
   f->pyr_levels = 0;

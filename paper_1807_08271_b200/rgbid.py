@@ -340,6 +340,15 @@ class DeviceFrame:
         self.ctx.check(self.ctx.lib.rgbid_frame_upload(self.ctx.h, self.h, dptr(f.intensity),
                                                        dptr(f.inverse_depth)), "frame_upload")
 
+    def decode(self, bgr: Optional[np.ndarray], depth: np.ndarray, scale: float = 5000.0):
+        """load_frame's pixel decode (src/dataset.cpp:97-116) on the GPU: BGR8 (h, w, 3)
+        and 16-bit depth (h, w) -> intensity / inverse depth."""
+        depth = np.ascontiguousarray(depth, dtype=np.uint16)
+        b = None if bgr is None else np.ascontiguousarray(bgr, dtype=np.uint8)
+        self.ctx.check(self.ctx.lib.rgbid_frame_decode(
+            self.ctx.h, self.h, None if b is None else b.ctypes.data, depth.ctypes.data, scale),
+            "frame_decode")
+
     def download(self) -> FrameData:
         I = np.empty((self.height, self.width))
         W = np.empty((self.height, self.width))

@@ -330,3 +330,16 @@ def test_config4_unregistered_depth_path(ctx, orc):
         return
     res = rg.align(frames[0], frames[1], K, config=cfg, ctx=ctx)
     _check_align(res, o)
+
+
+def test_frame_decode_bitwise(ctx, orc):
+    """Frame ingest (src/dataset.cpp:97-116) on the GPU equals the restatement bit for bit."""
+    rng = np.random.default_rng(3)
+    bgr = rng.integers(0, 256, size=(480, 640, 3), dtype=np.uint8)
+    depth = rng.integers(0, 65535, size=(480, 640), dtype=np.uint16)
+    depth[rng.random((480, 640)) < 0.05] = 0
+    f = rg.DeviceFrame(640, 480, ctx)
+    f.decode(bgr, depth, 5000.0)
+    g = f.download()
+    I, W = orc.decode_frame(bgr, depth, 5000.0)
+    assert bitwise_equal(g.intensity, I) and bitwise_equal(g.inverse_depth, W)
