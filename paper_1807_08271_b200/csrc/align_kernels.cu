@@ -998,12 +998,13 @@ __global__ void __launch_bounds__(kTPB, 2) k_normal_eq(const SlotIO* __restrict_
   for (int p = 0; p < kPixK3; ++p) {
     const int k = (blockIdx.x * kPixK3 + p) * kTPB + threadIdx.x;
     if (k >= N) break;
-    const unsigned a = am[k];
-    if (!(a & 1u)) continue;
-    const double i_b = ibp[k];
-    if (!valid(i_b)) continue;
+    // every load of the pixel issued at once (one memory round trip; the
+    // validity tests below only select)
+    const unsigned a = __ldg(am + k);
+    const double i_b = __ldcs(ibp + k), w_b = __ldcs(wbp + k);
     const double w_a = __ldg(WA + k), i_a = __ldg(IA + k);
-    const double2 gI = __ldg(ag + 2 * k);
+    const double2 gI = __ldg(ag + 2 * k), gW = __ldg(ag + 2 * k + 1);
+    if (!(a & 1u) || !valid(i_b)) continue;
     const int y = k / w, x = k - y * w;
     const double px = x, py = y;
     const double ax = li.cx - px, ay = li.cy - py;  // A(0,2), A(1,2)
@@ -1027,9 +1028,7 @@ __global__ void __launch_bounds__(kTPB, 2) k_normal_eq(const SlotIO* __restrict_
       const double wi = nuI1 * rcp_fast(fma(xi_, xi_, nuI)) * is2i;
       accum(acc, J, wi, rI);
     }
-    const double w_b = wbp[k];
     if (!((a & 2u) && valid(w_b) && w_b > 0.0)) continue;
-    const double2 gW = __ldg(ag + 2 * k + 1);
     // geometric row: s = w_a (g_W A + w_b e_z) ; J_W = (s, X x s)
     const double g0 = gW.x * li.fx, g1 = gW.y * li.fy, g2 = gW.x * ax + gW.y * ay;
     {
