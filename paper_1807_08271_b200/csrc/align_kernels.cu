@@ -331,6 +331,71 @@ __global__ void __launch_bounds__(kTPB, 6) k_warp_residuals(const SlotIO* __rest
   }
 }
 
+// Level-0 K1: 128 threads per 256-pixel tile, two independent pixels per thread
+// (x and x + 128) so their dependent load chains (W_A -> gathers) overlap.
+__global__ void __launch_bounds__(128, 12) k_warp_residuals_l0(const SlotIO* __restrict__ io,
+                                                                const SlotState* __restrict__ st,
+                                                                LevelInfo li, int w0, int h0,
+                                                                int phase) {
+  const int slot = blockIdx.y;
+  const SlotState& S = st[slot];
+  if (!slot_active(S, 0, phase)) return;
+  __shared__ WarpMats wm;
+  if (threadIdx.x < 24)
+    reinterpret_cast<double*>(&wm)[threadIdx.x] = reinterpret_cast<const double*>(&S.wm)[threadIdx.x];
+  const SlotIO& o = io[slot];
+  const double* __restrict__ WAw = phase ? o.fWA : o.WA[0];
+  const uint8_t* __restrict__ am = o.amask[0];
+  const double* __restrict__ IB = o.IB;
+  const double* __restrict__ WB = o.WB;
+  __syncthreads();
+  const int tid = threadIdx.x;
+  const int tile = blockIdx.x;
+  const int yl = tile / li.nseg, seg = tile - yl * li.nseg;
+  const int xl0 = seg * li.tx;
+  const int nx = min(li.tx, li.w - xl0);
+  bool jet[2], dep[2];
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int lx = tid + 128 * q;
+    jet[q] = dep[q] = false;
+    if (lx < nx) {
+      const int idx = yl * w0 + xl0 + lx;
+      const unsigned a = __ldg(am + idx);
+      double ib, wb, d0, d1;
+      warp_px(wm, IB, WB, w0, h0, xl0 + lx, yl, __ldg(WAw + idx), ib, wb, d0, d1);
+      o.ib[idx] = ib;
+      o.wb[idx] = wb;
+      jet[q] = (a & 1u) && valid(ib);
+      dep[q] = jet[q] && (a & 2u) && valid(wb) && wb > 0.0;
+    }
+  }
+  __shared__ int wcnt[2][8];
+  const int lane = tid & 31, wid = tid >> 5;
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const unsigned bj = __ballot_sync(0xffffffffu, jet[q]), bd = __ballot_sync(0xffffffffu, dep[q]);
+    if (lane == 0) {
+      const int word = wid + 4 * q;  // pixels [32 word, 32 word + 32) of the tile
+      wcnt[0][word] = __popc(bj);
+      wcnt[1][word] = __popc(bd);
+      o.bitsI[tile * kWordsPerTile + word] = bj;
+      o.bitsW[tile * kWordsPerTile + word] = bd;
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int tI = 0, tW = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      tI += wcnt[0][k];
+      tW += wcnt[1][k];
+    }
+    o.cntI[tile] = tI;
+    o.cntW[tile] = tW;
+  }
+}
+
 // A-side part of residuals_and_jacobians, constant over the IRLS iterations:
 // validity (src/alignment.cpp:209-211,227) and gradient_at of I_A and W_A
 // (src/alignment.cpp:165-191) per level pixel.  phase 1 = from the filtered A
@@ -398,7 +463,7 @@ void launch_warp_residuals(const AlignLaunch& a, const LevelInfo& li, int phase,
   KScope ks_(kLevelNames[phase ? 1 : 0][li.level], s);
   dim3 grid(li.ntiles, a.nslots);
   switch (li.level) {
-    case 0: k_warp_residuals<0><<<grid, kTPB, 0, s>>>(a.io, a.st, li, a.w0, a.h0, phase); break;
+    case 0: k_warp_residuals_l0<<<grid, 128, 0, s>>>(a.io, a.st, li, a.w0, a.h0, phase); break;
     case 1: k_warp_residuals<1><<<grid, kTPB, 0, s>>>(a.io, a.st, li, a.w0, a.h0, phase); break;
     case 2: k_warp_residuals<2><<<grid, kTPB, 0, s>>>(a.io, a.st, li, a.w0, a.h0, phase); break;
     case 3: k_warp_residuals<3><<<grid, kTPB, 0, s>>>(a.io, a.st, li, a.w0, a.h0, phase); break;
