@@ -65,6 +65,8 @@ def build(verbose: bool = False, force: bool = False) -> str:
     if force or procs or _stale(LIB, objs):
         cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart"]
         subprocess.run(cmd, check=True)
+    import ctypes
+    ctypes.CDLL(LIB)  # fail the build on unresolved symbols
     return LIB
 
 

@@ -219,9 +219,13 @@ __device__ __forceinline__ void load_wm(const WarpMats& g, WarpMats& m) {
 // adds the warped-B conditions and ballots the row-major validity bits per
 // tile (compacted rank = prefix popcount, consumed by the sample gather of K2).
 template <int L>
-__global__ void __launch_bounds__(kTPB, 6) k_warp_residuals(const SlotIO* __restrict__ io,
-                                                         const SlotState* __restrict__ st,
-                                                         LevelInfo li, int w0, int h0, int phase) {
+__host__ __device__ constexpr int k1_threads() { return L >= 2 ? 256 : 128; }  // two row groups from level 2 on
+
+template <int L>
+__global__ void __launch_bounds__(k1_threads<L>(), 2048 / k1_threads<L>() / 2) k_warp_residuals(const SlotIO* __restrict__ io,
+                                                           const SlotState* __restrict__ st,
+                                                           LevelInfo li, int w0, int h0, int phase) {
+  static_assert(L >= 1, "level 0 uses k_warp_residuals_l0");
   const int slot = blockIdx.y;
   const SlotState& S = st[slot];
   if (!slot_active(S, L, phase)) return;
@@ -230,7 +234,7 @@ __global__ void __launch_bounds__(kTPB, 6) k_warp_residuals(const SlotIO* __rest
     reinterpret_cast<double*>(&wm)[threadIdx.x] = reinterpret_cast<const double*>(&S.wm)[threadIdx.x];
   const SlotIO& o = io[slot];
   const double* __restrict__ WAw = phase ? o.fWA : o.WA[0];
-  const uint8_t* __restrict__ am = o.amask[L];  // level-0 entries rebuilt for phase 1
+  const uint8_t* __restrict__ am = o.amask[L];
   const double* __restrict__ IB = o.IB;
   const double* __restrict__ WB = o.WB;
   __syncthreads();
@@ -240,94 +244,84 @@ __global__ void __launch_bounds__(kTPB, 6) k_warp_residuals(const SlotIO* __rest
   const int yl = tile / li.nseg, seg = tile - yl * li.nseg;
   const int xl0 = seg * li.tx;
   const int nx = min(li.tx, li.w - xl0);
-  double ib = CUDART_NAN, wb = CUDART_NAN, d0, d1;
-
-  if constexpr (L == 0) {
-    if (tid < nx) {
-      const int x = xl0 + tid;
-      warp_px(wm, IB, WB, w0, h0, x, yl, __ldg(WAw + yl * w0 + x), ib, wb, d0, d1);
-    }
-  } else {
-    __shared__ double sI[2048], sW[2048];
-    int cw = nx << L, ch = 1 << L;
-    // full-res block: cw = nx * 2^L <= 256 columns (one per thread) x 2^L rows
-    if (tid < cw) {
-      const int x = (xl0 << L) + tid;
+  // Level-1 block of the tile: cw = nx * 2^(L-1) columns (<= 128, one per thread) x
+  // 2^(L-1) rows.  Each level-1 pixel = downsample2 of its 2x2 full-res warps,
+  // computed in registers (4 independent gather chains), taps in the reference
+  // order (0,0),(1,0),(0,1),(1,1) (inc/image.hpp:77-85).
+  __shared__ double sI[512], sW[512];
+  constexpr int NT = k1_threads<L>(), NG = NT / 128;  // row groups
+  int cw = nx << (L - 1), ch = 1 << (L - 1);
+  const int col = tid & 127, grp = tid >> 7;
+  if (col < cw) {
+    const int x = (xl0 << L) + 2 * col;
 #pragma unroll
-      for (int r = 0; r < (1 << L); ++r) {
-        const int y = (yl << L) + r;
-        double vi, vw;
-        warp_px(wm, IB, WB, w0, h0, x, y, __ldg(WAw + y * w0 + x), vi, vw, d0, d1);
-        sI[r * cw + tid] = vi;
-        sW[r * cw + tid] = vw;
+    for (int rr = 0; rr < (1 << (L - 1)) / NG; ++rr) {
+      const int r = rr * NG + grp;
+      const int y = (yl << L) + 2 * r;
+      double vi[4], vw[4], d0, d1;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int xx = x + (q & 1), yy = y + (q >> 1);
+        warp_px(wm, IB, WB, w0, h0, xx, yy, __ldg(WAw + yy * w0 + xx), vi[q], vw[q], d0, d1);
       }
+      sI[r * cw + col] = ds4(vi[0], vi[1], vi[2], vi[3]);
+      sW[r * cw + col] = ds4(vw[0], vw[1], vw[2], vw[3]);
+    }
+  }
+  __syncthreads();
+  // remaining downsample stages in shared memory (level 1 -> L)
+#pragma unroll
+  for (int s = 1; s < L; ++s) {
+    const int ow = cw >> 1;
+    constexpr int kMaxOh = (L >= 2) ? (1 << (L - 2)) : 1;
+    const int oh = ch >> 1;
+    double oi[kMaxOh], owv[kMaxOh];
+    if (tid < ow) {
+#pragma unroll
+      for (int r = 0; r < kMaxOh; ++r)
+        if (r < oh) {
+          const int i0 = (2 * r) * cw + 2 * tid, i1 = i0 + cw;
+          oi[r] = ds4(sI[i0], sI[i0 + 1], sI[i1], sI[i1 + 1]);
+          owv[r] = ds4(sW[i0], sW[i0 + 1], sW[i1], sW[i1 + 1]);
+        }
     }
     __syncthreads();
+    if (tid < ow) {
 #pragma unroll
-    for (int s = 0; s < L; ++s) {
-      // stage s: (cw x ch) -> (cw/2 x ch/2); thread tid owns output column tid
-      const int ow = cw >> 1;
-      constexpr int kMaxOh = 1 << (L - 1);
-      const int oh = ch >> 1;
-      double oi[kMaxOh], owv[kMaxOh];
-      if (tid < ow) {
-#pragma unroll
-        for (int r = 0; r < kMaxOh; ++r)
-          if (r < oh) {
-            const int i0 = (2 * r) * cw + 2 * tid, i1 = i0 + cw;
-            oi[r] = ds4(sI[i0], sI[i0 + 1], sI[i1], sI[i1 + 1]);
-            owv[r] = ds4(sW[i0], sW[i0 + 1], sW[i1], sW[i1 + 1]);
-          }
-      }
-      __syncthreads();
-      if (tid < ow) {
-#pragma unroll
-        for (int r = 0; r < kMaxOh; ++r)
-          if (r < oh) {
-            sI[r * ow + tid] = oi[r];
-            sW[r * ow + tid] = owv[r];
-          }
-      }
-      __syncthreads();
-      cw = ow;
-      ch = oh;
+      for (int r = 0; r < kMaxOh; ++r)
+        if (r < oh) {
+          sI[r * ow + tid] = oi[r];
+          sW[r * ow + tid] = owv[r];
+        }
     }
-    if (tid < nx) {
-      ib = sI[tid];
-      wb = sW[tid];
-    }
+    __syncthreads();
+    cw = ow;
+    ch = oh;
   }
 
   bool jet = false, dep = false;
   if (tid < nx) {
     const int idx = yl * li.w + xl0 + tid;
+    const double ib = sI[tid], wb = sW[tid];
     o.ib[idx] = ib;
     o.wb[idx] = wb;
-    const unsigned a = am[idx];
+    const unsigned a = __ldg(am + idx);
     jet = (a & 1u) && valid(ib);
     dep = jet && (a & 2u) && valid(wb) && wb > 0.0;
   }
   const unsigned bj = __ballot_sync(0xffffffffu, jet), bd = __ballot_sync(0xffffffffu, dep);
-  __shared__ int wcnt[2][kTPB / 32];
+  __shared__ int wcnt[2][4];
   const int lane = tid & 31, wid = tid >> 5;
-  if (lane == 0) {
+  if (lane == 0 && wid < 4) {  // level pixels live in the first 128 threads
     wcnt[0][wid] = __popc(bj);
     wcnt[1][wid] = __popc(bd);
-    if (wid < kWordsPerTile) {
-      o.bitsI[tile * kWordsPerTile + wid] = bj;
-      o.bitsW[tile * kWordsPerTile + wid] = bd;
-    }
+    o.bitsI[tile * kWordsPerTile + wid] = bj;
+    o.bitsW[tile * kWordsPerTile + wid] = bd;
   }
   __syncthreads();
   if (tid == 0) {
-    int tI = 0, tW = 0;
-#pragma unroll
-    for (int k = 0; k < kTPB / 32; ++k) {
-      tI += wcnt[0][k];
-      tW += wcnt[1][k];
-    }
-    o.cntI[tile] = tI;
-    o.cntW[tile] = tW;
+    o.cntI[tile] = wcnt[0][0] + wcnt[0][1] + wcnt[0][2] + wcnt[0][3];
+    o.cntW[tile] = wcnt[1][0] + wcnt[1][1] + wcnt[1][2] + wcnt[1][3];
   }
 }
 
@@ -464,11 +458,11 @@ void launch_warp_residuals(const AlignLaunch& a, const LevelInfo& li, int phase,
   dim3 grid(li.ntiles, a.nslots);
   switch (li.level) {
     case 0: k_warp_residuals_l0<<<grid, 128, 0, s>>>(a.io, a.st, li, a.w0, a.h0, phase); break;
-    case 1: k_warp_residuals<1><<<grid, kTPB, 0, s>>>(a.io, a.st, li, a.w0, a.h0, phase); break;
-    case 2: k_warp_residuals<2><<<grid, kTPB, 0, s>>>(a.io, a.st, li, a.w0, a.h0, phase); break;
-    case 3: k_warp_residuals<3><<<grid, kTPB, 0, s>>>(a.io, a.st, li, a.w0, a.h0, phase); break;
-    case 4: k_warp_residuals<4><<<grid, kTPB, 0, s>>>(a.io, a.st, li, a.w0, a.h0, phase); break;
-    case 5: k_warp_residuals<5><<<grid, kTPB, 0, s>>>(a.io, a.st, li, a.w0, a.h0, phase); break;
+    case 1: k_warp_residuals<1><<<grid, k1_threads<1>(), 0, s>>>(a.io, a.st, li, a.w0, a.h0, phase); break;
+    case 2: k_warp_residuals<2><<<grid, k1_threads<2>(), 0, s>>>(a.io, a.st, li, a.w0, a.h0, phase); break;
+    case 3: k_warp_residuals<3><<<grid, k1_threads<3>(), 0, s>>>(a.io, a.st, li, a.w0, a.h0, phase); break;
+    case 4: k_warp_residuals<4><<<grid, k1_threads<4>(), 0, s>>>(a.io, a.st, li, a.w0, a.h0, phase); break;
+    case 5: k_warp_residuals<5><<<grid, k1_threads<5>(), 0, s>>>(a.io, a.st, li, a.w0, a.h0, phase); break;
     default: return;
   }
 }
