@@ -15,7 +15,8 @@ MAX_LEVELS = 8
 OK, E_DEGENERATE, E_CUDA, E_ARG, E_OOM = 0, 1, 2, 3, 4
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "librgbid_b200.so")
+# RGBID_LIB: an alternative in-tree build (kernel variants under build/, tools/ only)
+LIB_PATH = os.environ.get("RGBID_LIB") or os.path.join(_HERE, "_lib", "librgbid_b200.so")
 
 
 class Intrinsics_t(C.Structure):

@@ -13,12 +13,15 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-OUT = os.path.join(HERE, "_lib")
+# RGBID_BUILD_DIR: build an instrumented / variant library elsewhere (tools/)
+OUT = os.environ.get("RGBID_BUILD_DIR") or os.path.join(HERE, "_lib")
 LIB = os.path.join(OUT, "librgbid_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CU_FLAGS = ["-O3", "-lineinfo", "--fmad=false", "-std=c++17", "-Xcompiler", "-fPIC",
             "-Xcompiler", "-ffp-contract=off", "-Xptxas", "-v"]
+# extra nvcc flags for instrumented builds (e.g. -DRGBID_TDIST_TRACE, tools/tdist_phases.py)
+CU_FLAGS += os.environ.get("RGBID_NVFLAGS", "").split()
 CU_SRCS = ["align_kernels.cu", "fusion_kernels.cu", "runtime.cu", "frontend.cu"]
 CPP_SRCS = ["synth.cpp"]
 

@@ -508,6 +508,21 @@ struct TD {
   double mu, sigma, nu;
 };
 
+// Phase counters for the Student-t chain (thread 0 of each CTA; instrumented
+// builds only: RGBID_NVFLAGS=-DRGBID_TDIST_TRACE, read by tools/tdist_phases.py)
+#ifdef RGBID_TDIST_TRACE
+__device__ unsigned long long g_tph[16];
+#define TPH_T(v) const unsigned long long v = clock64()
+#define TPH_ADD(i, t0) \
+  if (threadIdx.x == 0) atomicAdd(&g_tph[i], (unsigned long long)(clock64() - (t0)))
+#define TPH_CNT(i, n) \
+  if (threadIdx.x == 0) atomicAdd(&g_tph[i], (unsigned long long)(n))
+#else
+#define TPH_T(v)
+#define TPH_ADD(i, t0)
+#define TPH_CNT(i, n)
+#endif
+
 struct Sample;
 template <int NV, int NT>
 __device__ __forceinline__ void sample_allsum(double (&v)[NV], Sample& S);
@@ -551,6 +566,7 @@ struct Sample {
 // reduction suffices.
 template <int NV, int NT>
 __device__ __forceinline__ void sample_allsum(double (&v)[NV], Sample& S) {
+  TPH_T(tr0);
   const int p = S.parity;
   block_allsum<NV, NT>(v, S.scratch, S.parity);
   if (S.cs > 1) {
@@ -574,26 +590,153 @@ __device__ __forceinline__ void sample_allsum(double (&v)[NV], Sample& S) {
       for (int r = 0; r < kTdistCluster; ++r) v[i] += part[r][i];
     }
   }
+  TPH_ADD(8, tr0);
+  TPH_CNT(9, 1);
 }
 
-// sum over the thread's samples of f(v) into NACC accumulators (breaks the
-// add dependency chain); fixed assignment -> deterministic
+// sum over the thread's samples of f(v): bodies of 8 independent samples into
+// 4 accumulators (the per-sample chains are latency-bound with one CTA per SM);
+// fixed assignment -> deterministic
 template <int NT, int NV, typename F>
 __device__ __forceinline__ void sample_sum(const Sample& S, double (&acc)[NV], F f) {
-  double a0[NV], a1[NV];
+  double a[4][NV];
 #pragma unroll
-  for (int i = 0; i < NV; ++i) a0[i] = a1[i] = 0.0;
+  for (int j = 0; j < 4; ++j)
+#pragma unroll
+    for (int i = 0; i < NV; ++i) a[j][i] = 0.0;
   const double* v = S.v + threadIdx.x;
   int k = 0;
-#pragma unroll 2
-  for (; k + 1 < S.kfull; k += 2) {
-    f(v[k * NT], a0);
-    f(v[(k + 1) * NT], a1);
+  for (; k + 7 < S.kfull; k += 8) {
+    double x[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) x[u] = v[(k + u) * NT];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) f(x[u], a[u & 3]);
   }
   for (; k * NT < S.m_local; ++k)
-    if (k * NT + (int)threadIdx.x < S.m_local) f(v[k * NT], a0);
+    if (k * NT + (int)threadIdx.x < S.m_local) f(v[k * NT], a[0]);
 #pragma unroll
-  for (int i = 0; i < NV; ++i) acc[i] = a0[i] + a1[i];
+  for (int i = 0; i < NV; ++i) acc[i] = (a[0][i] + a[1][i]) + (a[2][i] + a[3][i]);
+}
+
+// Running product of positive normal doubles kept as mantissa in [1,2) and an
+// integer binary exponent: sum(log q) = log(mantissa) + E ln2 with one log per
+// thread.  Rounding: one ulp per multiply (k ulps over k factors), the same order
+// as summing k correctly-rounded logs.  `bad` latches a non-normal intermediate.
+struct LogProd {
+  double p = 1.0;
+  int e = 0;
+  bool bad = false;
+  __device__ __forceinline__ void renorm() {
+    const long long b = __double_as_longlong(p);
+    const int ex = (int)((unsigned long long)b >> 52);  // p > 0: sign bit clear
+    bad |= (ex == 0) | (ex == 0x7ff);
+    e += ex - 1023;
+    p = __longlong_as_double((b & 0x000FFFFFFFFFFFFFll) | 0x3FF0000000000000ll);
+  }
+};
+
+// Sums over the thread's samples of r = 1/q, q = (v-mu)^2 + c1 (> 0), and
+// optionally of r v (WV) and log q (WL).  Eight samples form one fraction
+// N/D (pairwise tree, D = prod q): one reciprocal per 8 samples instead of 8
+// (the FP64 MUFU reciprocal issues at a quarter of the DFMA rate), all terms
+// positive except r v's numerators.  D also feeds the running log-product, so
+// sum(log q) costs one log per thread.  A thread with any D outside
+// [1e-250, 1e250] (only for |v - mu| > 1e30 or c1 < 1e-31) redoes its share
+// with exact per-sample division and logs.
+#ifndef RGBID_QBODY
+#define RGBID_QBODY 4
+#endif
+constexpr int kQBody = RGBID_QBODY;  // samples per fraction
+
+// sum_i 1/q_i = N/D (and sum_i x_i/q_i = NV/D) over BW samples, pairwise tree
+template <int BW, bool WV>
+__device__ __forceinline__ void frac_tree(const double (&q)[BW], const double (&x)[BW], double& D,
+                                          double& NR, double& NV) {
+  double d[BW / 2], n[BW / 2], mv[BW / 2];
+#pragma unroll
+  for (int i = 0; i < BW / 2; ++i) {
+    d[i] = q[2 * i] * q[2 * i + 1];
+    n[i] = q[2 * i] + q[2 * i + 1];
+    if (WV) mv[i] = fma(x[2 * i], q[2 * i + 1], x[2 * i + 1] * q[2 * i]);
+  }
+#pragma unroll
+  for (int w = BW / 2; w > 1; w >>= 1)
+#pragma unroll
+    for (int i = 0; i < w / 2; ++i) {
+      n[i] = fma(n[2 * i], d[2 * i + 1], n[2 * i + 1] * d[2 * i]);
+      if (WV) mv[i] = fma(mv[2 * i], d[2 * i + 1], mv[2 * i + 1] * d[2 * i]);
+      d[i] = d[2 * i] * d[2 * i + 1];
+    }
+  D = d[0];
+  NR = n[0];
+  if (WV) NV = mv[0];
+}
+
+// one body of q_sums: BW samples k..k+BW-1 of this thread; MASKED pads the
+// samples past m_local with q = 1, x = 0 (1/q = 1 each, subtracted by the caller;
+// log 1 = 0; x/q = 0)
+template <int NT, int BW, bool WV, bool WL, bool MASKED>
+__device__ __forceinline__ void q_body(const Sample& S, const double* v, int k, double mu, double c1,
+                                       double& sr, double& sv, LogProd& P, bool& bad) {
+  double x[BW], q[BW];
+#pragma unroll
+  for (int u = 0; u < BW; ++u) {
+    const bool ok = !MASKED || (k + u) * NT + (int)threadIdx.x < S.m_local;
+    x[u] = ok ? v[(k + u) * NT] : 0.0;
+    const double d = x[u] - mu;
+    q[u] = ok ? fma(d, d, c1) : 1.0;
+  }
+  double D, NR, NV;
+  frac_tree<BW, WV>(q, x, D, NR, NV);
+  bad |= !(D > 1e-250 && D < 1e250);
+  const double inv = rcp_fast(D);
+  sr = fma(NR, inv, sr);
+  if (WV) sv = fma(NV, inv, sv);
+  if (WL) {
+    P.p *= D;
+    P.renorm();
+  }
+}
+
+template <int NT, bool WV, bool WL>
+__device__ __forceinline__ void q_sums(const Sample& S, double mu, double c1, double (&out)[3]) {
+  constexpr int BW = kQBody;
+  const double* v = S.v + threadIdx.x;
+  double sr = 0.0, sv = 0.0, slog = 0.0;
+  LogProd P;
+  bool bad = false;
+  int k = 0;
+  for (; k + BW - 1 < S.kfull; k += BW)  // branch-free bodies
+    q_body<NT, BW, WV, WL, false>(S, v, k, mu, c1, sr, sv, P, bad);
+  const int kend = (S.m_local + NT - 1) / NT;
+  for (; k < kend; k += BW) {  // the rest, padded
+    q_body<NT, BW, WV, WL, true>(S, v, k, mu, c1, sr, sv, P, bad);
+    int npad = 0;
+#pragma unroll
+    for (int u = 0; u < BW; ++u) npad += (k + u) * NT + (int)threadIdx.x < S.m_local ? 0 : 1;
+    sr -= (double)npad;
+  }
+  if (bad) {  // exact per-sample division for this thread's share
+    sr = sv = 0.0;
+    for (int kk = 0; kk * NT < S.m_local; ++kk)
+      if (kk * NT + (int)threadIdx.x < S.m_local) {
+        const double x = v[kk * NT], d = x - mu, q = fma(d, d, c1), r = 1.0 / q;
+        sr += r;
+        if (WV) sv = fma(r, x, sv);
+        if (WL) slog += log(q);
+      }
+  }
+  out[0] = sr;
+  out[1] = sv;
+  if (WL) {
+    if (bad) {
+      out[2] = slog;
+    } else {
+      const double E = (double)P.e;  // E * ln2_hi exact (ln2_hi has 21 trailing zero bits)
+      out[2] = log(P.p) + (E * 6.93147180369123816490e-01 + E * 1.90821492927058770002e-10);
+    }
+  }
 }
 
 // estimate_location_scale on the shared-memory sample — src/alignment.cpp:61-101
@@ -603,6 +746,8 @@ __device__ __forceinline__ TD loc_scale(Sample& S, double nu, double* scratch) {
   const int m = S.m;
   if (m == 0) return p;
   if (S.memo_nu == nu) return S.memo;
+  TPH_T(tl0);
+  TPH_CNT(2, 1);
   const double inv_m = 1.0 / (double)m;
   double a1[1];
   sample_sum<NT>(S, a1, [](double v, double (&a)[1]) { a[0] += v; });
@@ -622,32 +767,28 @@ __device__ __forceinline__ TD loc_scale(Sample& S, double nu, double* scratch) {
     const double nu1 = nu + 1.0;
     for (int it = 0; it < 50; ++it) {
       // t_weight((v-mu)/sigma, nu) = c2 / (c1 + (v-mu)^2), c1 = nu s2, c2 = (nu+1) s2;
-      // the constant c2 is applied after the reduction (sums of 1/(c1 + d^2))
+      // the constant c2 is applied after the reduction (sums of r = 1/(c1 + d^2))
       const double s2 = sigma * sigma, c1 = nu * s2, c2 = nu1 * s2;
-      double a2[2];
-      sample_sum<NT>(S, a2, [mu, c1](double v, double (&a)[2]) {
-        const double d = v - mu;
-        const double r = rcp_q(fma(d, d, c1));
-        a[0] += r;
-        a[1] = fma(r, v, a[1]);
-      });
+      double a3[3];
+      q_sums<NT, true, false>(S, mu, c1, a3);
+      double a2[2] = {a3[0], a3[1]};
       sample_allsum<2, NT>(a2, S);
       const double mu_new = a2[1] / a2[0];  // (c2 sum r v) / (c2 sum r)
-      sample_sum<NT>(S, a1, [mu_new, c1](double v, double (&a)[1]) {
-        const double d = v - mu_new;
-        const double r = rcp_q(fma(d, d, c1));
-        a[0] = fma(r * d, d, a[0]);
-      });
+      // sum w d^2 = c2 sum d^2 / (d^2 + c1) = c2 (m - c1 sum r)
+      q_sums<NT, false, false>(S, mu_new, c1, a3);
+      a1[0] = a3[0];
       sample_allsum<1, NT>(a1, S);
-      a1[0] *= c2;
+      a1[0] = c2 * fma(-c1, a1[0], (double)m);
       const double sigma_new = dmax_std(1e-8, sqrt(a1[0] * inv_m));
       const double rel = fabs(sigma_new - sigma) / sigma;
       mu = mu_new;
       sigma = sigma_new;
+      TPH_CNT(3, 1);
       if (rel < 1e-4) break;
     }
     out = TD{mu, dmax_std(sigma, 1e-8), nu};
   }
+  TPH_ADD(1, tl0);
   S.memo_nu = nu;
   S.memo = out;
   return out;
@@ -666,22 +807,27 @@ __device__ __forceinline__ double digamma_d(double x) {
   return result;
 }
 
-// stationarity of solve_nu — src/alignment.cpp:132-141 (the nu-only part C hoisted;
-// per-sample term (C + log w) - w as in the reference).
+// stationarity of solve_nu — src/alignment.cpp:132-141.  With x = (v-mu)/sigma,
+// w = c2/q where q = d^2 + c1, c1 = nu s^2, c2 = (nu+1) s^2, d = v - mu, so
+//   mean(C + log w - w) = C + log c2 - mean(log q) - c2 mean(1/q),
+// C the nu-only part of the reference's per-sample term; sum(1/q) and sum(log q)
+// come from one q_sums pass.
 template <int NT>
 __device__ __forceinline__ double stationarity(Sample& S, double mu, double sigma, double nu,
                                                double* scratch) {
+  TPH_T(ts0);
   const double C = (((-digamma_d(nu / 2.0) + log(nu / 2.0)) + digamma_d((nu + 1.0) / 2.0)) -
                     log((nu + 1.0) / 2.0)) + 1.0;
   const double s2 = sigma * sigma, c1 = nu * s2, c2 = (nu + 1.0) * s2;
-  double a[1];
-  sample_sum<NT>(S, a, [mu, c1, c2, C](double v, double (&acc)[1]) {
-    const double d = v - mu;
-    const double w = c2 * rcp_fast(fma(d, d, c1));
-    acc[0] += (C + log(w)) - w;
-  });
-  sample_allsum<1, NT>(a, S);
-  return a[0] / (double)S.m;
+  double a3[3];
+  q_sums<NT, false, true>(S, mu, c1, a3);
+  double a[2] = {a3[2], a3[0]};
+  TPH_ADD(6, ts0);
+  sample_allsum<2, NT>(a, S);
+  const double inv_m = 1.0 / (double)S.m;
+  TPH_ADD(4, ts0);
+  TPH_CNT(5, 1);
+  return ((C + log(c2)) - a[0] * inv_m) - c2 * (a[1] * inv_m);
 }
 
 // solve_nu — src/alignment.cpp:131-157
@@ -722,24 +868,50 @@ __device__ __forceinline__ double estimate_nu(Sample& S, double mu, double sigma
   return nu;
 }
 
-int tdist_smem_bytes(int ntiles) { return kMaxSample * 8 + (ntiles + 1) * 4; }
+// validity words used per K1 tile (tx / 32, >= 1) and their log2
+__host__ __device__ inline int tile_words_log2(int tx) {
+  return tx >= 256 ? 3 : tx >= 128 ? 2 : tx >= 64 ? 1 : 0;
+}
 
-__global__ void __launch_bounds__(kTdistThreads, 2)
-    k_tdist(const SlotIO* __restrict__ io, SlotState* __restrict__ st, LevelInfo li, int phase) {
-  constexpr int NT = kTdistThreads;
-  const int type = blockIdx.x, slot = blockIdx.y;
-  SlotState& S = st[slot];
-  if (!slot_active(S, li.level, phase)) return;
+// position of the j-th (0-based) set bit of m (j < popc(m))
+__device__ __forceinline__ int select_bit(unsigned m, int j) {
+  int pos = 0;
+#pragma unroll
+  for (int w = 16; w > 0; w >>= 1) {
+    const int c = __popc(m & ((1u << w) - 1u));
+    if (j >= c) {
+      j -= c;
+      m >>= w;
+      pos += w;
+    }
+  }
+  return pos;
+}
+
+// K2a: systematic sample of the valid residuals of one (slot, residual type) —
+// src/alignment.cpp:50-57 over the residual order of src/alignment.cpp:216-231.
+// Gathering the sampled residuals is a DRAM-latency-bound scatter read; as its
+// own kernel (small shared memory, many CTAs per SM) it runs at full occupancy
+// and overlaps the other lane's FP64-bound K2b, which then streams the compact
+// sample.  grid (kGatherCTAs, 2, slots); CTA c owns samples [c, c+1) * chunk.
+// Every CTA scans the per-tile counts itself (1440 ints at 640x480, L2-resident).
+constexpr int kGatherThreads = 256, kGatherCTAs = 8;
+constexpr int kGatherChunk = (kMaxSample + kGatherCTAs - 1) / kGatherCTAs;
+
+__global__ void __launch_bounds__(kGatherThreads)
+    k_gather(const SlotIO* __restrict__ io, const SlotState* __restrict__ st, LevelInfo li,
+             int phase) {
+  constexpr int NT = kGatherThreads;
+  const int type = blockIdx.y, slot = blockIdx.z;
+  if (!slot_active(st[slot], li.level, phase)) return;
   const SlotIO& o = io[slot];
   const int* cnt = type ? o.cntW : o.cntI;
   const unsigned* bits = type ? o.bitsW : o.bitsI;
   const double* bv = type ? o.wb : o.ib;  // warped B at this level
   const double* av = type ? (phase ? o.fWA : o.WA[li.level]) : (phase ? o.fIA : o.IA[li.level]);
-  extern __shared__ double dsm[];  // sample[kMaxSample] + offs[ntiles + 1]
-  double* smp_sh = dsm;
-  int* offs = reinterpret_cast<int*>(dsm + kMaxSample);
+  extern __shared__ int offs[];  // [ntiles + 1]
+  __shared__ long long sidx[kGatherChunk];
   __shared__ int wsum[NT / 32];
-  __shared__ double scratch[NT / 32 * 2 * 2];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int nt = li.ntiles;
 
@@ -747,7 +919,7 @@ __global__ void __launch_bounds__(kTdistThreads, 2)
   const int per = (nt + NT - 1) / NT;
   const int b0 = min(nt, tid * per), b1 = min(nt, b0 + per);
   int local = 0;
-  for (int i = b0; i < b1; ++i) local += cnt[i];
+  for (int i = b0; i < b1; ++i) local += __ldg(cnt + i);
   int incl = local;
 #pragma unroll
   for (int off = 1; off < 32; off <<= 1) {
@@ -764,13 +936,96 @@ __global__ void __launch_bounds__(kTdistThreads, 2)
   int run = woff + incl - local;
   for (int i = b0; i < b1; ++i) {
     offs[i] = run;
-    run += cnt[i];
+    run += __ldg(cnt + i);
   }
   if (tid == 0) offs[nt] = total;
+  if (blockIdx.x == 0 && tid == 0) o.nsmp[type] = total;
   __syncthreads();
 
-  // systematic sample straight into registers: sample s = k*NT + tid
   const long long n = total;
+  const long long stride = n <= kMaxSample ? 1 : (n + kMaxSample - 1) / kMaxSample;
+  const int m = n == 0 ? 0 : (int)((n - 1) / stride + 1);
+  const int c0 = blockIdx.x * kGatherChunk, c1 = min(m, c0 + kGatherChunk);
+  if (c0 >= c1) return;  // uniform over the CTA
+
+  // pass 1: sample s -> its level pixel.  Thread tid takes contiguous samples:
+  // one binary search over the tile offsets, then a forward walk over the
+  // validity words (row-major pixel order within each tile row).
+  {
+    const int lw = tile_words_log2(li.tx), wpt = 1 << lw;
+    const int spt = (c1 - c0 + NT - 1) / NT;
+    const int s0 = min(c1, c0 + tid * spt), s1 = min(c1, s0 + spt);
+    if (s0 < s1) {
+      long long g = (long long)s0 * stride;
+      int lo = 0, hi = nt - 1;
+      while (lo < hi) {  // last tile with offs[t] <= g
+        const int mid = (lo + hi + 1) >> 1;
+        if (offs[mid] <= g)
+          lo = mid;
+        else
+          hi = mid - 1;
+      }
+      int tile = lo, w = 0, yl = lo / li.nseg, seg = lo - yl * li.nseg;
+      long long base = offs[lo];  // rank of the first valid pixel of word w
+      unsigned msk = __ldg(bits + tile * kWordsPerTile);
+      int c = __popc(msk);
+      for (int s = s0; s < s1; ++s, g += stride) {
+        int j = (int)(g - base);
+        while (j >= c) {
+          j -= c;
+          base += c;
+          if (++w == wpt) {
+            w = 0;
+            ++tile;
+            if (++seg == li.nseg) {
+              seg = 0;
+              ++yl;
+            }
+          }
+          msk = __ldg(bits + tile * kWordsPerTile + w);
+          c = __popc(msk);
+        }
+        sidx[s - c0] = yl * li.w + seg * li.tx + w * 32 + select_bit(msk, j);
+      }
+    }
+  }
+  __syncthreads();
+  // pass 2: the residual values, four samples' loads in flight per thread;
+  // coalesced stores of the compact sample
+  double* out = o.smp + (size_t)type * kMaxSample;
+  for (int s = c0 + tid; s < c1; s += 4 * NT) {
+    long long ix[4];
+    double b[4], a[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) ix[u] = s + u * NT < c1 ? sidx[s + u * NT - c0] : -1;
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (ix[u] >= 0) {
+        b[u] = __ldg(bv + ix[u]);
+        a[u] = __ldg(av + ix[u]);
+      }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (ix[u] >= 0) out[s + u * NT] = b[u] - a[u];  // r_I = i_b - i_a / r_W = w_b - w_a (src/alignment.cpp:222,229)
+  }
+}
+
+// K2b: Student-t fit of one (slot, residual type) on its compact sample.  One
+// CTA per SM (the sample fills shared memory): all 128 registers per thread.
+__global__ void __launch_bounds__(kTdistThreads, 1)
+    k_tdist(const SlotIO* __restrict__ io, SlotState* __restrict__ st, LevelInfo li, int phase) {
+  constexpr int NT = kTdistThreads;
+  const int type = blockIdx.x, slot = blockIdx.y;
+  SlotState& S = st[slot];
+  if (!slot_active(S, li.level, phase)) return;
+  TPH_T(tk0);
+  const SlotIO& o = io[slot];
+  extern __shared__ double dsm[];  // sample[kMaxSample]
+  double* smp_sh = dsm;
+  __shared__ double scratch[NT / 32 * 2 * 2];
+  const int tid = threadIdx.x;
+
+  const long long n = o.nsmp[type];
   const long long stride = n <= kMaxSample ? 1 : (n + kMaxSample - 1) / kMaxSample;
   Sample smp;
   smp.v = smp_sh;
@@ -782,30 +1037,15 @@ __global__ void __launch_bounds__(kTdistThreads, 2)
   smp.memo_nu = -1.0;
   smp.scratch = scratch;
   smp.parity = 0;
-  for (int k = 0; k < kSPT; ++k) {
-    const int s = k * NT + tid;
-    if (s < smp.m) {
-      const long long g = (long long)s * stride;
-      int lo = 0, hi = nt - 1;
-      while (lo < hi) {  // last tile with offs[t] <= g
-        const int mid = (lo + hi + 1) >> 1;
-        if (offs[mid] <= g)
-          lo = mid;
-        else
-          hi = mid - 1;
-      }
-      // j-th set bit of tile lo's row-major validity mask -> level pixel
-      int j = (int)(g - offs[lo]), word = 0;
-      unsigned msk = bits[lo * kWordsPerTile];
-      while (j >= __popc(msk)) {
-        j -= __popc(msk);
-        msk = bits[lo * kWordsPerTile + (++word)];
-      }
-      for (int q = 0; q < j; ++q) msk &= msk - 1u;
-      const int yl = lo / li.nseg, seg = lo - yl * li.nseg;
-      const int idx = yl * li.w + seg * li.tx + word * 32 + (__ffs(msk) - 1);
-      smp_sh[s] = bv[idx] - av[idx];  // r_I = i_b - i_a / r_W = w_b - w_a (src/alignment.cpp:222,229)
-    }
+  const double* gs = o.smp + (size_t)type * kMaxSample;
+  for (int s = tid; s < smp.m; s += 4 * NT) {
+    double x[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (s + u * NT < smp.m) x[u] = __ldcs(gs + s + u * NT);
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (s + u * NT < smp.m) smp_sh[s + u * NT] = x[u];
   }
   __syncthreads();
 
@@ -830,6 +1070,7 @@ __global__ void __launch_bounds__(kTdistThreads, 2)
       S.nW = n;
     }
   }
+  TPH_ADD(7, tk0);
 }
 
 // Latency-mode K2: the sample of one (slot, residual type) is spread over a
@@ -940,9 +1181,22 @@ __global__ void __launch_bounds__(kTdistClusterThreads, 1)
   cl.sync();  // no CTA exits while others may still read its cluster slots
 }
 
+#ifdef RGBID_TDIST_TRACE
+extern "C" int rgbid_debug_tdist_phases(unsigned long long* out, int reset) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out, g_tph, sizeof(g_tph));
+  if (reset) {
+    static const unsigned long long z[16] = {};
+    cudaMemcpyToSymbol(g_tph, z, sizeof(z));
+  }
+  return 0;
+}
+#endif
+
 int init_kernel_attributes() {
   const cudaError_t e =
-      cudaFuncSetAttribute(k_tdist, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      cudaFuncSetAttribute(k_tdist, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSample * 8);
+  cudaFuncSetAttribute(k_gather, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
   const cudaError_t e2 =
       cudaFuncSetAttribute(k_tdist_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
   cudaGetLastError();
@@ -968,6 +1222,11 @@ void launch_tdist(const AlignLaunch& a, const LevelInfo& li, int phase, cudaStre
     cudaLaunchKernelEx(&cfg, k_tdist_cluster, a.io, a.st, li, phase);
     return;
   }
+  {
+    KScope ks_("gather", s);
+    k_gather<<<dim3(kGatherCTAs, 2, a.nslots), kGatherThreads, (li.ntiles + 1) * sizeof(int), s>>>(
+        a.io, a.st, li, phase);
+  }
   KScope ks_("tdist", s);
   // highest launch priority: the FP64-bound chains claim SMs first, the other
   // lane's memory-bound kernels fill around them
@@ -979,7 +1238,7 @@ void launch_tdist(const AlignLaunch& a, const LevelInfo& li, int phase, cudaStre
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(2, a.nslots);
   cfg.blockDim = dim3(kTdistThreads);
-  cfg.dynamicSmemBytes = tdist_smem_bytes(li.ntiles);
+  cfg.dynamicSmemBytes = kMaxSample * sizeof(double);
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributePriority;
@@ -1445,7 +1704,7 @@ void launch_jets(const double* IA, const double* WA, const double* IBw, const do
 // estimate_location_scale (mode 0) / estimate_nu (mode 1) on a residual vector
 // (src/alignment.cpp:61-127): systematic sample into smem, then the same
 // device chain as k_tdist.
-__global__ void __launch_bounds__(kTdistThreads, 2)
+__global__ void __launch_bounds__(kTdistThreads, 1)  // one CTA per SM (sample in smem)
     k_tdist_vec(const double* __restrict__ r, long long n, int mode, double a, double b,
                 double* __restrict__ out) {
   constexpr int NT = kTdistThreads;

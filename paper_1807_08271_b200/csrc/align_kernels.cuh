@@ -16,7 +16,10 @@ namespace rgbid_b200 {
 constexpr int kMaxLevels = 6;       // GPU supports levels <= 6 (80x60 at level 3 for VGA)
 constexpr int kMaxSample = 19200;   // src/alignment.cpp:47
 constexpr int kTPB = 256;           // warp/residual/normal-equation kernels
-constexpr int kTdistThreads = 512;  // Student-t kernel (sample in shared memory)
+#ifndef RGBID_TDIST_THREADS
+#define RGBID_TDIST_THREADS 512
+#endif
+constexpr int kTdistThreads = RGBID_TDIST_THREADS;  // Student-t kernel (sample in shared memory)
 constexpr int kNPart = 28;          // 21 (lower H) + 6 (b) + 1 (cost)
 constexpr int kTraceMax = 64;
 constexpr int kTdistCluster = 8;         // CTAs per Student-t chain in latency mode
@@ -62,6 +65,8 @@ struct SlotIO {
   unsigned* bitsI;               // per K1 tile validity bitmask [ntiles][kWordsPerTile]
   unsigned* bitsW;
   double* part;                  // K3 partial sums [ntiles3][kNPart]
+  double* smp;                   // K2 systematic samples [2][kMaxSample] (r_I, r_W; k_gather)
+  int* nsmp;                     // K2 valid residual counts [2] (k_gather)
   int build_pyr;                 // 1: this slot builds frame A's pyramid levels >= 1
 };
 

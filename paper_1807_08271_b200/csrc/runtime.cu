@@ -263,10 +263,10 @@ size_t pyr_pixels(int w, int h) {
 size_t slot_f64(int w, int h) {
   const size_t N = (size_t)w * h;
   const size_t part = (size_t)((N + kTPB * kPixK3 - 1) / (kTPB * kPixK3)) * kNPart;
-  return 4 * N + 4 * pyr_pixels(w, h) + part;
+  return 4 * N + 4 * pyr_pixels(w, h) + part + 2 * (size_t)kMaxSample;
 }
 size_t slot_u8(int w, int h) { return (pyr_pixels(w, h) + 255) & ~(size_t)255; }
-size_t slot_i32(int w, int h) { return 2 * max_tiles(w, h) * (1 + kWordsPerTile); }
+size_t slot_i32(int w, int h) { return 2 * max_tiles(w, h) * (1 + kWordsPerTile) + 2; }
 
 void free_lane_ws(Lane& L) {
   if (L.ws_f64) cudaFree(L.ws_f64);
@@ -538,11 +538,13 @@ int prepare_chunk(rgbid_ctx* ctx, Lane& L, int n, const rgbid_frame* const* fa,
       g += 4 * (size_t)(w >> l) * (h >> l);
     }
     o.part = g;
+    o.smp = base + (sf - 2 * (size_t)kMaxSample);
     int* ib32 = L.ws_i32 + si * i;
     o.cntI = ib32;
     o.cntW = ib32 + mt;
     o.bitsI = reinterpret_cast<unsigned*>(ib32 + 2 * mt);
     o.bitsW = o.bitsI + mt * kWordsPerTile;
+    o.nsmp = ib32 + 2 * mt * (1 + kWordsPerTile);
     uint8_t* u8 = L.ws_u8 + su * i;
     for (int l = 0; l < kMaxLevels; ++l) {
       o.amask[l] = u8;
