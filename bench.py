@@ -34,6 +34,7 @@ UNIT = "alignments/s"
 W0, H0, F0 = 640, 480, 480.0
 LEVELS, ITERS = 4, [10, 5, 4]  # level 3 defaults to 5 (src/alignment.cpp:373-374)
 M_BYTES = W0 * H0 * 8  # one fp64 map
+N0 = W0 * H0
 
 
 def workload_config(args, world):
@@ -237,6 +238,29 @@ def algorithmic_bytes(results):
     return tot, warp
 
 
+# ncu-measured per full-res pixel constants of the warp_residuals family
+# (profiles/r01_k1_ncu_v14.txt): fp64 flop = dadd + dmul + 2 dfma per pixel warped
+# (level 0 / covariance pass: 112; levels >= 1 add the in-tile downsample: ~122-124),
+# and DRAM bytes per slot-iteration at level 0 (read + write / 512 slots).
+K1_FLOP_PER_PX = {0: 112.0, 1: 121.4, 2: 123.8, 3: 124.5}
+K1_TRAFFIC_L0 = (3.919025e9 + 2.545017e9) / 512
+
+
+def warp_flops(results):
+    """fp64 flops executed by the warp_residuals family: every iteration at every
+    level warps all N0 full-res pixels (src/alignment.cpp:378-379), plus the
+    covariance pass (level 0 kernel)."""
+    tot = 0.0
+    for r in results:
+        if r.status != 0:
+            continue
+        for k in range(r.n_levels):
+            lv = r.level_log[k]
+            tot += lv.iterations * N0 * K1_FLOP_PER_PX.get(lv.level, K1_FLOP_PER_PX[3])
+        tot += N0 * K1_FLOP_PER_PX[0]
+    return tot
+
+
 def main():
     args = parse()
     rank, world, local = dist_env()
@@ -328,7 +352,11 @@ def main():
     roofline = {
         "bound": "hbm", "kernel": "warp_residuals",
         "achieved": (warp_bytes / (warp_ms / 1e3)) / 1e9 if warp_ms else None,
-        "peak": peak, "unit": "GB/s", "traffic": None, "peak_source": peak_src,
+        "peak": peak, "unit": "GB/s", "peak_source": peak_src,
+        # ncu dram read+write per slot-iteration of the level-0 launch vs SURVEY 8(d)'s
+        # algorithmic B_it(0) = 5M: no wasted re-reads
+        "traffic": K1_TRAFFIC_L0, "traffic_algorithmic": 5 * M_BYTES,
+        "traffic_unit": "bytes per slot-iteration at level 0 (profiles/r01_k1_ncu_v14.txt)",
         "frac": ((warp_bytes / (warp_ms / 1e3)) / 1e9) / peak if warp_ms else None,
         "kernel_share_of_step": warp_ms / prof_total if prof_total else None,
         "dominant_kernel": dom[0], "dominant_share": dom[1][1] / prof_total if prof_total else None,
@@ -347,6 +375,17 @@ def main():
     ctx.check(ctx.lib.rgbid_measure_fp64_peak(ctx.h, C.byref(fp64)), "fp64_peak")
     tdist_ms = sum(v[1] for k, v in kstats.items() if k.startswith("tdist"))
     roofline["fp64_peak_tflops_measured"] = fp64.value
+    # the warp kernels are fp64-issue- and load-latency-bound rather than HBM-bound
+    # (~2.8 TB/s and ~31% fp64 instruction issue per ncu): report both ceilings
+    wfl = warp_flops(presults)
+    if warp_ms and fp64.value > 0:
+        ach = wfl / (warp_ms / 1e3) / 1e12
+        roofline["fp64"] = {"kernel": "warp_residuals", "achieved": ach, "peak": fp64.value,
+                            "unit": "TFLOP/s", "frac": ach / fp64.value,
+                            "flop_per_px": K1_FLOP_PER_PX,
+                            "note": "ncu-measured flop per full-res pixel x pixels warped in "
+                                    "the profiled step / its CUDA-event time; peak = "
+                                    "rgbid_measure_fp64_peak (dependent-free DFMA stream)"}
     roofline["tdist_share_of_step"] = tdist_ms / prof_total if prof_total else None
 
     # latency: one pair, device-resident, 4 levels; + one keyframe fusion

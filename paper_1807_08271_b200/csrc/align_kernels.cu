@@ -218,11 +218,23 @@ __device__ __forceinline__ void load_wm(const WarpMats& g, WarpMats& m) {
 // iterations: they are precomputed once per alignment into amask (k_amask); K1
 // adds the warped-B conditions and ballots the row-major validity bits per
 // tile (compacted rank = prefix popcount, consumed by the sample gather of K2).
+// thread layout of K1 at level L: k1_cw columns x k1_ng row groups (<= 256
+// threads) over the tile's level-1 block (tx * 2^(L-1) columns x 2^(L-1) rows,
+// <= 512 values); each thread computes 2^(L-1) / k1_ng level-1 values of four
+// full-res warps each (512-thread CTAs at level 3 measured slower)
 template <int L>
-__host__ __device__ constexpr int k1_threads() { return L >= 2 ? 256 : 128; }  // two row groups from level 2 on
+__host__ __device__ constexpr int k1_cw() {
+  return (k1_tx(L) << (L - 1)) < 128 ? (k1_tx(L) << (L - 1)) : 128;
+}
+template <int L>
+__host__ __device__ constexpr int k1_ng() {
+  return (1 << (L - 1)) < 256 / k1_cw<L>() ? (1 << (L - 1)) : 256 / k1_cw<L>();
+}
+template <int L>
+__host__ __device__ constexpr int k1_threads() { return k1_cw<L>() * k1_ng<L>(); }
 
 template <int L>
-__global__ void __launch_bounds__(k1_threads<L>(), 2048 / k1_threads<L>() / 2) k_warp_residuals(const SlotIO* __restrict__ io,
+__global__ void __launch_bounds__(k1_threads<L>(), 1024 / k1_threads<L>()) k_warp_residuals(const SlotIO* __restrict__ io,
                                                            const SlotState* __restrict__ st,
                                                            LevelInfo li, int w0, int h0, int phase) {
   static_assert(L >= 1, "level 0 uses k_warp_residuals_l0");
@@ -249,9 +261,9 @@ __global__ void __launch_bounds__(k1_threads<L>(), 2048 / k1_threads<L>() / 2) k
   // computed in registers (4 independent gather chains), taps in the reference
   // order (0,0),(1,0),(0,1),(1,1) (inc/image.hpp:77-85).
   __shared__ double sI[512], sW[512];
-  constexpr int NT = k1_threads<L>(), NG = NT / 128;  // row groups
+  constexpr int CW = k1_cw<L>(), NG = k1_ng<L>();  // thread columns x row groups
   int cw = nx << (L - 1), ch = 1 << (L - 1);
-  const int col = tid & 127, grp = tid >> 7;
+  const int col = tid % CW, grp = tid / CW;
   if (col < cw) {
     const int x = (xl0 << L) + 2 * col;
 #pragma unroll
@@ -1010,11 +1022,13 @@ __global__ void __launch_bounds__(kGatherThreads)
   }
 }
 
-// K2b: Student-t fit of one (slot, residual type) on its compact sample.  One
-// CTA per SM (the sample fills shared memory): all 128 registers per thread.
-__global__ void __launch_bounds__(kTdistThreads, 1)
+// K2b: Student-t fit of one (slot, residual type) on its compact sample.  NT
+// threads hold the sample in shared memory, ~38 samples per thread: NT = 512 for
+// the 19200-sample cap (one CTA per SM, all 128 registers per thread), smaller
+// CTAs -- several per SM -- for coarse levels whose pixel count caps the sample.
+template <int NT>
+__global__ void __launch_bounds__(NT, kTdistThreads / NT)
     k_tdist(const SlotIO* __restrict__ io, SlotState* __restrict__ st, LevelInfo li, int phase) {
-  constexpr int NT = kTdistThreads;
   const int type = blockIdx.x, slot = blockIdx.y;
   SlotState& S = st[slot];
   if (!slot_active(S, li.level, phase)) return;
@@ -1195,7 +1209,8 @@ extern "C" int rgbid_debug_tdist_phases(unsigned long long* out, int reset) {
 
 int init_kernel_attributes() {
   const cudaError_t e =
-      cudaFuncSetAttribute(k_tdist, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSample * 8);
+      cudaFuncSetAttribute(k_tdist<kTdistThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           kMaxSample * 8);
   cudaFuncSetAttribute(k_gather, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
   const cudaError_t e2 =
       cudaFuncSetAttribute(k_tdist_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
@@ -1235,17 +1250,24 @@ void launch_tdist(const AlignLaunch& a, const LevelInfo& li, int phase, cudaStre
     cudaDeviceGetStreamPriorityRange(&lo, &hi);
     return hi;
   }();
+  const int mcap = std::min(kMaxSample, li.w * li.h);  // sample size bound at this level
+  const int nt = mcap > kMaxSample / 2 ? kTdistThreads : mcap > kMaxSample / 4 ? 256 : 128;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(2, a.nslots);
-  cfg.blockDim = dim3(kTdistThreads);
-  cfg.dynamicSmemBytes = kMaxSample * sizeof(double);
+  cfg.blockDim = dim3(nt);
+  cfg.dynamicSmemBytes = mcap * sizeof(double);
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributePriority;
   attr[0].val.priority = prio;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, k_tdist, a.io, (SlotState*)a.st, li, phase);
+  if (nt == kTdistThreads)
+    cudaLaunchKernelEx(&cfg, k_tdist<kTdistThreads>, a.io, (SlotState*)a.st, li, phase);
+  else if (nt == 256)
+    cudaLaunchKernelEx(&cfg, k_tdist<256>, a.io, (SlotState*)a.st, li, phase);
+  else
+    cudaLaunchKernelEx(&cfg, k_tdist<128>, a.io, (SlotState*)a.st, li, phase);
 }
 
 // ---------------------------------------------------------------------------
@@ -1535,61 +1557,155 @@ void launch_downsample2(const double* I, const double* W, int w, int h, double* 
   k_downsample2<<<(n + 255) / 256, 256, 0, s>>>(I, W, w, h, oI, oW);
 }
 
-// bilateral_filter — src/alignment.cpp:252-277
-__device__ __forceinline__ double bilateral_px(const double* img, int w, int h, int x, int y,
-                                               double inv2ss, double inv2sr) {
-  const double c = img[(size_t)y * w + x];
-  if (!valid(c)) return CUDART_NAN;
+// exp(x) for x <= 0: 2^(j/64) table (shared memory) x degree-6 polynomial on
+// |r| <= ln2/128, within ~1 ulp of the correctly rounded value (the parity
+// tests bound the filtered maps at 1e-14 relative).  x < -708 (subnormal or
+// zero results) and NaN go through the library exp.
+__constant__ double c_exp2_64[64] = {
+    1.0, 1.0108892860517005, 1.0218971486541166, 1.0330248790212284,
+    1.0442737824274138, 1.0556451783605572, 1.0671404006768237, 1.0787607977571199,
+    1.0905077326652577, 1.102382583307841, 1.1143867425958924, 1.1265216186082418,
+    1.1387886347566916, 1.1511892299529827, 1.1637248587775775, 1.1763969916502812,
+    1.189207115002721, 1.202156731452703, 1.215247359980469, 1.22848053610687,
+    1.241857812073484, 1.255380757024691, 1.2690509571917332, 1.2828700160787783,
+    1.2968395546510096, 1.3109612115247644, 1.3252366431597413, 1.339667524053303,
+    1.3542555469368927, 1.3690024229745905, 1.383909881963832, 1.3989796725383112,
+    1.4142135623730951, 1.42961333839197, 1.4451808069770467, 1.460917794180647,
+    1.4768261459394993, 1.4929077282912648, 1.5091644275934228, 1.5255981507445384,
+    1.5422108254079407, 1.559004400237837, 1.5759808451078865, 1.593142151342267,
+    1.6104903319492543, 1.6280274218573478, 1.645755478153965, 1.6636765803267364,
+    1.681792830507429, 1.7001063537185235, 1.718619298122478, 1.7373338352737062,
+    1.7562521603732995, 1.7753764925265212, 1.7947090750031072, 1.8142521755003989,
+    1.8340080864093424, 1.8539791250833855, 1.8741676341103, 1.8945759815869656,
+    1.9152065613971474, 1.9360617934922943, 1.9571441241754002, 1.978456026387951};
+
+__device__ __forceinline__ double exp_le0(double x, const double* __restrict__ tab) {
+  if (!(x >= -708.0)) return exp(x);
+  const double kMagic = 6755399441055744.0;            // 1.5 * 2^52: round to integer
+  const double kd = fma(x, 92.33248261689366, kMagic);  // x * 64 / ln2
+  const int n = __double2loint(kd);
+  const double k = kd - kMagic;
+  double r = fma(-k, 0.01083042469326756, x);  // ln2/64, hi part (k * hi exact)
+  r = fma(-k, 2.9815858269852933e-12, r);      // lo part
+  double pl = fma(r, 1.0 / 720.0, 1.0 / 120.0);
+  pl = fma(r, pl, 1.0 / 24.0);
+  pl = fma(r, pl, 1.0 / 6.0);
+  pl = fma(r, pl, 0.5);
+  pl = fma(r, pl, 1.0);
+  const double em1 = r * pl;  // e^r - 1
+  const double t = tab[n & 63];
+  const double scale = __longlong_as_double((long long)((n >> 6) + 1023) << 52);
+  return fma(t, em1, t) * scale;
+}
+
+// bilateral_filter — src/alignment.cpp:252-277, tiled.  The tap weight
+// exp(-(dx^2+dy^2)/(2 ss^2) - (v-c)^2/(2 sr^2)) is the same double for the
+// ordered pairs (p, q) and (q, p) ((v-c)^2 == (c-v)^2 bit for bit), so each
+// unordered pair's exp is evaluated once, by the raster-earlier pixel ("forward"
+// offsets dy > 0, or dy == 0 and dx > 0), into shared memory; every output pixel
+// then accumulates its 5x5 window in the reference order.
+constexpr int kBTW = 32, kBTH = 8;                 // output tile, one pixel per thread
+constexpr int kBRW = kBTW + 8, kBRH = kBTH + 4;    // input region from (x0-4, y0-2)
+constexpr int kBAW = kBTW + 4, kBAH = kBTH + 2;    // forward-weight owners from (x0-2, y0-2)
+constexpr int kBNA = kBAW * kBAH;
+
+__device__ __forceinline__ void bilateral_tile(const double* __restrict__ img, int w, int h,
+                                               double inv2ss, double inv2sr,
+                                               double* __restrict__ out, int x0, int y0,
+                                               const double* tab, double* reg, double* fw) {
+  constexpr int FDX[12] = {1, 2, -2, -1, 0, 1, 2, -2, -1, 0, 1, 2};
+  constexpr int FDY[12] = {0, 0, 1, 1, 1, 1, 1, 2, 2, 2, 2, 2};
+  const int tid = threadIdx.x;
+  for (int i = tid; i < kBRW * kBRH; i += kBTW * kBTH) {
+    const int ry = i / kBRW, rx = i - ry * kBRW;
+    const int gx = x0 - 4 + rx, gy = y0 - 2 + ry;
+    reg[i] = (gx >= 0 && gx < w && gy >= 0 && gy < h) ? __ldg(img + (size_t)gy * w + gx)
+                                                      : CUDART_NAN;  // out of bounds = skipped
+  }
+  __syncthreads();
+  for (int a = tid; a < kBNA; a += kBTW * kBTH) {
+    const int ay = a / kBAW, ax = a - ay * kBAW;
+    const double c = reg[ay * kBRW + ax + 2];
+#pragma unroll
+    for (int o = 0; o < 12; ++o) {
+      const double v = reg[(ay + FDY[o]) * kBRW + ax + 2 + FDX[o]];
+      const double arg =
+          (double)(-(FDX[o] * FDX[o] + FDY[o] * FDY[o])) * inv2ss - (v - c) * (v - c) * inv2sr;
+      fw[o * kBNA + a] = exp_le0(arg, tab);
+    }
+  }
+  __syncthreads();
+  const int tx = tid % kBTW, ty = tid / kBTW;
+  const int x = x0 + tx, y = y0 + ty;
+  if (x >= w || y >= h) return;
+  const double c = reg[(ty + 2) * kBRW + tx + 4];
+  if (!valid(c)) {
+    out[(size_t)y * w + x] = CUDART_NAN;
+    return;
+  }
   double wsum = 0.0, vsum = 0.0;
+#pragma unroll
   for (int dy = -2; dy <= 2; ++dy)
+#pragma unroll
     for (int dx = -2; dx <= 2; ++dx) {
-      const int sx = x + dx, sy = y + dy;
-      if (!(sx >= 0 && sx < w && sy >= 0 && sy < h)) continue;
-      const double v = img[(size_t)sy * w + sx];
+      const double v = reg[(ty + 2 + dy) * kBRW + tx + 4 + dx];
       if (!valid(v)) continue;
-      const double wt = exp(-(dx * dx + dy * dy) * inv2ss - (v - c) * (v - c) * inv2sr);
+      double wt;
+      if (dy == 0 && dx == 0) {
+        wt = 1.0;  // exp(+0.0)
+      } else {
+        const bool fwd = dy > 0 || (dy == 0 && dx > 0);
+        const int fdx = fwd ? dx : -dx, fdy = fwd ? dy : -dy;
+        const int o = fdy == 0 ? fdx - 1 : (fdy == 1 ? 4 + fdx : 9 + fdx);
+        const int a = fwd ? (ty + 2) * kBAW + tx + 2 : (ty + 2 + dy) * kBAW + tx + 2 + dx;
+        wt = fw[o * kBNA + a];
+      }
       wsum += wt;
       vsum += wt * v;
     }
-  return vsum / wsum;
+  out[(size_t)y * w + x] = vsum / wsum;
 }
 
-__global__ void k_bilateral(const double* __restrict__ img, int w, int h, double inv2ss,
-                            double inv2sr, double* __restrict__ out) {
-  const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= w * h) return;
-  const int y = k / w, x = k - y * w;
-  out[k] = bilateral_px(img, w, h, x, y, inv2ss, inv2sr);
+__device__ __forceinline__ void load_exp_table(double* tab) {
+  if (threadIdx.x < 64) tab[threadIdx.x] = c_exp2_64[threadIdx.x];
+}
+
+__global__ void __launch_bounds__(kBTW * kBTH) k_bilateral(const double* __restrict__ img, int w,
+                                                           int h, double inv2ss, double inv2sr,
+                                                           double* __restrict__ out) {
+  __shared__ double tab[64], reg[kBRW * kBRH], fw[12 * kBNA];
+  load_exp_table(tab);
+  bilateral_tile(img, w, h, inv2ss, inv2sr, out, blockIdx.x * kBTW, blockIdx.y * kBTH, tab, reg, fw);
 }
 
 void launch_bilateral(const double* img, int w, int h, double ss, double sr, double* out,
                       cudaStream_t s) {
   const double inv2ss = 1.0 / (2.0 * ss * ss), inv2sr = 1.0 / (2.0 * sr * sr);
   KScope ks_("bilateral", s);
-  k_bilateral<<<(w * h + 255) / 256, 256, 0, s>>>(img, w, h, inv2ss, inv2sr, out);
+  k_bilateral<<<dim3((w + kBTW - 1) / kBTW, (h + kBTH - 1) / kBTH), kBTW * kBTH, 0, s>>>(
+      img, w, h, inv2ss, inv2sr, out);
 }
 
-// both filtered maps of every active slot (covariance pass input)
-__global__ void k_bilateral_slots(const SlotIO* __restrict__ io, const SlotState* __restrict__ st,
-                                  int w, int h, double inv2ss, double inv2sr_i, double inv2sr_w) {
-  const int slot = blockIdx.y;
+// both filtered maps of every active slot (covariance pass input); grid.z = map
+__global__ void __launch_bounds__(kBTW * kBTH)
+    k_bilateral_slots(const SlotIO* __restrict__ io, const SlotState* __restrict__ st, int w,
+                      int h, double inv2ss, double inv2sr_i, double inv2sr_w) {
+  const int slot = blockIdx.z >> 1, map = blockIdx.z & 1;
   if (st[slot].status != RGBID_OK) return;
   const SlotIO& o = io[slot];
-  const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= w * h) return;
-  const int y = k / w, x = k - y * w;
-  o.fIA[k] = bilateral_px(o.IA[0], w, h, x, y, inv2ss, inv2sr_i);
-  o.fWA[k] = bilateral_px(o.WA[0], w, h, x, y, inv2ss, inv2sr_w);
+  __shared__ double tab[64], reg[kBRW * kBRH], fw[12 * kBNA];
+  load_exp_table(tab);
+  bilateral_tile(map ? o.WA[0] : o.IA[0], w, h, inv2ss, map ? inv2sr_w : inv2sr_i,
+                 map ? o.fWA : o.fIA, blockIdx.x * kBTW, blockIdx.y * kBTH, tab, reg, fw);
 }
 
 void launch_bilateral_pair(const AlignLaunch& a, double ss, double sr_i, double sr_w,
                            cudaStream_t s) {
   const double inv2ss = 1.0 / (2.0 * ss * ss);
   const double ii = 1.0 / (2.0 * sr_i * sr_i), iw = 1.0 / (2.0 * sr_w * sr_w);
-  const int n = a.w0 * a.h0;
   KScope ks_("bilateral_slots", s);
-  k_bilateral_slots<<<dim3((n + 255) / 256, a.nslots), 256, 0, s>>>(a.io, a.st, a.w0, a.h0,
-                                                                     inv2ss, ii, iw);
+  k_bilateral_slots<<<dim3((a.w0 + kBTW - 1) / kBTW, (a.h0 + kBTH - 1) / kBTH, 2 * a.nslots),
+                      kBTW * kBTH, 0, s>>>(a.io, a.st, a.w0, a.h0, inv2ss, ii, iw);
 }
 
 // inverse_geometric_warp producing all four WarpedFrame maps (drop-in + tests)

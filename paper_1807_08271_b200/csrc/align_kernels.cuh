@@ -29,7 +29,7 @@ constexpr int kPixK3 = 8;           // pixels per thread in the normal-equation 
 
 // K1 tiling of level l: tile = (level row, segment of tx level pixels).
 // Full-res pixels per tile = tx * 4^l <= 2048 (smem staging of the warp).
-__host__ __device__ inline int k1_tx(int l) {
+__host__ __device__ constexpr int k1_tx(int l) {
   const int a = 256 >> l, b = 2048 >> (2 * l);
   const int m = a < b ? a : b;
   return m < 1 ? 1 : m;
