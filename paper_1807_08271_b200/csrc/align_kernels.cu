@@ -1560,7 +1560,7 @@ void launch_downsample2(const double* I, const double* W, int w, int h, double* 
 // exp(x) for x <= 0: 2^(j/64) table (shared memory) x degree-6 polynomial on
 // |r| <= ln2/128, within ~1 ulp of the correctly rounded value (the parity
 // tests bound the filtered maps at 1e-14 relative).  x < -708 (subnormal or
-// zero results) and NaN go through the library exp.
+// zero results) goes through the library exp; NaN yields NaN.
 __constant__ double c_exp2_64[64] = {
     1.0, 1.0108892860517005, 1.0218971486541166, 1.0330248790212284,
     1.0442737824274138, 1.0556451783605572, 1.0671404006768237, 1.0787607977571199,
@@ -1580,7 +1580,7 @@ __constant__ double c_exp2_64[64] = {
     1.9152065613971474, 1.9360617934922943, 1.9571441241754002, 1.978456026387951};
 
 __device__ __forceinline__ double exp_le0(double x, const double* __restrict__ tab) {
-  if (!(x >= -708.0)) return exp(x);
+  if (x < -708.0) return exp(x);
   const double kMagic = 6755399441055744.0;            // 1.5 * 2^52: round to integer
   const double kd = fma(x, 92.33248261689366, kMagic);  // x * 64 / ln2
   const int n = __double2loint(kd);
@@ -1649,7 +1649,6 @@ __device__ __forceinline__ void bilateral_tile(const double* __restrict__ img, i
 #pragma unroll
     for (int dx = -2; dx <= 2; ++dx) {
       const double v = reg[(ty + 2 + dy) * kBRW + tx + 4 + dx];
-      if (!valid(v)) continue;
       double wt;
       if (dy == 0 && dx == 0) {
         wt = 1.0;  // exp(+0.0)
@@ -1660,8 +1659,10 @@ __device__ __forceinline__ void bilateral_tile(const double* __restrict__ img, i
         const int a = fwd ? (ty + 2) * kBAW + tx + 2 : (ty + 2 + dy) * kBAW + tx + 2 + dx;
         wt = fw[o * kBNA + a];
       }
-      wsum += wt;
-      vsum += wt * v;
+      // invalid taps are skipped: adding +0.0 leaves both sums bit-identical
+      const bool ok = valid(v);
+      wsum += ok ? wt : 0.0;
+      vsum += ok ? wt * v : 0.0;
     }
   out[(size_t)y * w + x] = vsum / wsum;
 }
