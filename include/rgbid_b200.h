@@ -310,6 +310,46 @@ int rgbid_selftest_division(rgbid_ctx* ctx, unsigned long long n, unsigned long 
  * roofline denominator of the FP64-issue-bound Student-t kernel */
 int rgbid_measure_fp64_peak(rgbid_ctx* ctx, double* tflops);
 
+/* ---- loop-closure dense refinement ------------------- */
+/* reference LoopConstraint (include/rgbid/loop.hpp:19-26) */
+typedef struct {
+  int i, j;          /* keyframe ids (i = query, j = match) */
+  rgbid_pose T_ij;   /* pose of j in i's frame */
+  double info[36];   /* row-major 6x6, symmetrised cov^-1 */
+  int inliers;
+  double hull_fraction;
+  double score;
+} rgbid_loop_constraint;
+
+/* std::optional<LoopConstraint> make_loop_constraint(kf_i, kf_j, T_init, K, geom, config,
+ * align_config) — src/loop.cpp:174-203, the back-end's second caller of align.  The
+ * place-recognition inputs (geom.inliers, geom.hull_fraction) pass through.  A
+ * degenerate alignment or a refined covisibility below min_covisibility (0.3 by default,
+ * include/rgbid/loop.hpp:46) gives *accepted = 0 (std::nullopt) and RGBID_OK.  Runs on
+ * ctx's stream: a second context on another host thread refines loops concurrently
+ * with the front-end. */
+int rgbid_make_loop_constraint(rgbid_ctx* ctx, const rgbid_frame* kf_i, const rgbid_frame* kf_j,
+                               int id_i, int id_j, const rgbid_intrinsics* K,
+                               const rgbid_pose* T_init, const rgbid_align_config* cfg,
+                               double min_covisibility, int inliers, double hull_fraction,
+                               rgbid_loop_constraint* out, int* accepted);
+
+/* ---- normals and map export --------------------------- */
+/* NormalMap normal_map(W, K) — src/segmentation.cpp:10-57.  Host buffers, w x h each;
+ * holes propagate (NaN), degenerate pixels get -e_z. */
+int rgbid_normal_map(rgbid_ctx* ctx, const double* W, int width, int height,
+                     const rgbid_intrinsics* K, double* nx, double* ny, double* nz);
+
+/* PointCloud export_map(keyframes, K, voxel) — src/pipeline.cpp:463-527.
+ * Keyframe k: intensity I[k], inverse depth W[k] (host, width x height), pose T_W_kf[k].
+ * points: capacity x 3 doubles (x, y, z), colors: capacity x 3 bytes (r, g, b).
+ * *n = points in the cloud; if it exceeds capacity nothing is written and
+ * RGBID_E_ARG is returned (n_kf * width * height always suffices). */
+int rgbid_export_map(rgbid_ctx* ctx, int n_kf, const double* const* I, const double* const* W,
+                     int width, int height, const rgbid_pose* T_W_kf, const rgbid_intrinsics* K,
+                     double voxel, double* points, unsigned char* colors, long long capacity,
+                     long long* n);
+
 /* ---- synthetic inputs (restates /root/reference/proj/tests/synthetic.hpp) ---- */
 /* render_plane(K, T_WC, n, d) with plane_texture evaluated at tex_scale * (X, Y) */
 int rgbid_synth_render_plane(const rgbid_intrinsics* K, const rgbid_pose* T_WC, const double n[3],

@@ -214,6 +214,14 @@ class Oracle:
         self._f("bilateral_filter")(dptr(img), w, h, ss, sr, dptr(out))
         return out
 
+    def normal_map(self, W, K):
+        """src/segmentation.cpp:10-57 (reference build only)"""
+        assert self.kind == "REF", "normal_map is checked against the reference build"
+        h, w = W.shape
+        nx, ny, nz = (np.empty_like(W) for _ in range(3))
+        self._f("normal_map")(dptr(W), w, h, C.byref(K), dptr(nx), dptr(ny), dptr(nz))
+        return nx, ny, nz
+
     def integrate_frame(self, kf_I, kf_W, kf_C, fI, fW, T, K, sigma_w):
         """In place on kf_W, kf_C (and kf_I untouched)."""
         h, w = kf_W.shape

@@ -14,6 +14,7 @@
 #include "rgbid/alignment.hpp"
 #include "rgbid/camera.hpp"
 #include "rgbid/fusion.hpp"
+#include "rgbid/segmentation.hpp"
 #include "rgbid/warping.hpp"
 #include "synthetic.hpp"  // /root/reference/proj/tests/synthetic.hpp
 #include "../include/rgbid_b200.h"
@@ -232,6 +233,16 @@ int ref_filtered_hessian_covariance(const double* IA, const double* WA, const do
 // src/alignment.cpp:252-277
 int ref_bilateral_filter(const double* img, int w, int h, double ss, double sr, double* out) {
   from_img(bilateral_filter(to_img(img, w, h), ss, sr), out);
+  return 0;
+}
+
+// src/segmentation.cpp:10-57
+int ref_normal_map(const double* W, int w, int h, const rgbid_intrinsics* K, double* nx,
+                   double* ny, double* nz) {
+  const NormalMap n = normal_map(to_img(W, w, h), to_K(K));
+  from_img(n.nx, nx);
+  from_img(n.ny, ny);
+  from_img(n.nz, nz);
   return 0;
 }
 

@@ -73,6 +73,11 @@ class FrameEstimate_t(C.Structure):
                 ("lost", C.c_int), ("keyframe_id", C.c_int)]
 
 
+class LoopConstraint_t(C.Structure):
+    _fields_ = [("i", C.c_int), ("j", C.c_int), ("T_ij", Pose_t), ("info", C.c_double * 36),
+                ("inliers", C.c_int), ("hull_fraction", C.c_double), ("score", C.c_double)]
+
+
 DP = C.POINTER(C.c_double)
 VP = C.c_void_p
 
@@ -172,6 +177,17 @@ EXPORTS = [
     ("rgbid_selftest_division", C.c_int, [VP, C.c_ulonglong, C.c_ulonglong,
                                           C.POINTER(C.c_ulonglong)]),
     ("rgbid_measure_fp64_peak", C.c_int, [VP, C.POINTER(C.c_double)]),
+    ("rgbid_make_loop_constraint", C.c_int, [VP, VP, VP, C.c_int, C.c_int,
+                                             C.POINTER(Intrinsics_t), C.POINTER(Pose_t),
+                                             C.POINTER(AlignConfig_t), C.c_double, C.c_int,
+                                             C.c_double, C.POINTER(LoopConstraint_t),
+                                             C.POINTER(C.c_int)]),
+    ("rgbid_normal_map", C.c_int, [VP, DP, C.c_int, C.c_int, C.POINTER(Intrinsics_t), DP, DP,
+                                   DP]),
+    ("rgbid_export_map", C.c_int, [VP, C.c_int, C.POINTER(DP), C.POINTER(DP), C.c_int, C.c_int,
+                                   C.POINTER(Pose_t), C.POINTER(Intrinsics_t), C.c_double, DP,
+                                   C.POINTER(C.c_ubyte), C.c_longlong,
+                                   C.POINTER(C.c_longlong)]),
     ("rgbid_synth_render_plane", C.c_int, [C.POINTER(Intrinsics_t), C.POINTER(Pose_t), DP,
                                            C.c_double, C.c_double, DP, DP]),
     ("rgbid_synth_random_pose", C.c_int, [C.c_uint32, C.c_int, C.c_double, C.c_double,

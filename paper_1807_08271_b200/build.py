@@ -22,7 +22,7 @@ CU_FLAGS = ["-O3", "-lineinfo", "--fmad=false", "-std=c++17", "-Xcompiler", "-fP
             "-Xcompiler", "-ffp-contract=off", "-Xptxas", "-v"]
 # extra nvcc flags for instrumented builds (e.g. -DRGBID_TDIST_TRACE, tools/tdist_phases.py)
 CU_FLAGS += os.environ.get("RGBID_NVFLAGS", "").split()
-CU_SRCS = ["align_kernels.cu", "fusion_kernels.cu", "runtime.cu", "frontend.cu"]
+CU_SRCS = ["align_kernels.cu", "fusion_kernels.cu", "map_kernels.cu", "runtime.cu", "frontend.cu"]
 CPP_SRCS = ["synth.cpp"]
 
 

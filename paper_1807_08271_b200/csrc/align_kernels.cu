@@ -1310,7 +1310,10 @@ __device__ __forceinline__ void accum(double (&acc)[kNPart], const double (&J)[6
   acc[27] = fma(w * r, r, acc[27]);
 }
 
-__global__ void __launch_bounds__(kTPB, 2) k_normal_eq(const SlotIO* __restrict__ io,
+#ifndef RGBID_K3_MINBLOCKS
+#define RGBID_K3_MINBLOCKS 2
+#endif
+__global__ void __launch_bounds__(kTPB, RGBID_K3_MINBLOCKS) k_normal_eq(const SlotIO* __restrict__ io,
                                                     const SlotState* __restrict__ st, LevelInfo li,
                                                     int phase, double lambda_n_min) {
   const int slot = blockIdx.y;

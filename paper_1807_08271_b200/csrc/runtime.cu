@@ -22,6 +22,7 @@
 #include "../../include/rgbid_b200.h"
 #include "align_kernels.cuh"
 #include "fusion_kernels.cuh"
+#include "map_kernels.cuh"
 
 using namespace rgbid_b200;
 
@@ -1196,6 +1197,119 @@ int rgbid_covisibility_ratio(rgbid_ctx* ctx, const rgbid_frame* a, const rgbid_f
   }
   if (empty) *empty = e;
   return RGBID_OK;
+}
+
+// make_loop_constraint — src/loop.cpp:174-203
+int rgbid_make_loop_constraint(rgbid_ctx* ctx, const rgbid_frame* kf_i, const rgbid_frame* kf_j,
+                               int id_i, int id_j, const rgbid_intrinsics* K,
+                               const rgbid_pose* T_init, const rgbid_align_config* cfg,
+                               double min_covisibility, int inliers, double hull_fraction,
+                               rgbid_loop_constraint* out, int* accepted) {
+  if (!ctx || !kf_i || !kf_j || !K || !out || !accepted) return RGBID_E_ARG;
+  *accepted = 0;
+  rgbid_align_result res;
+  int rc = rgbid_align(ctx, kf_i, kf_j, K, T_init, cfg, &res);
+  if (rc == RGBID_E_DEGENERATE) return RGBID_OK;  // catch (DegenerateAlignmentError) -> nullopt
+  if (rc) return rc;
+  // refined-overlap gate on covisibility_ratio(kf_i, kf_j, T_AB^-1, K, sigma_w = tdist_depth.sigma)
+  const PoseD T_BA = pose_inverse(pose_of(&res.T_AB));
+  rgbid_pose tba;
+  pose_to(T_BA, tba.R, tba.t);
+  double ratio = 0.0;
+  int empty = 0;
+  rc = rgbid_covisibility_ratio(ctx, kf_i, kf_j, &tba, K, res.tdist_depth.sigma, &ratio, &empty,
+                                nullptr);
+  if (rc) return rc;
+  if (empty || ratio < min_covisibility) return RGBID_OK;
+  std::memset(out, 0, sizeof(*out));
+  out->i = id_i;
+  out->j = id_j;
+  out->T_ij = res.T_AB;
+  double inv[36];
+  lu_inverse6(res.cov, inv);  // Mat6::inverse (partial-pivot LU)
+  for (int r = 0; r < 6; ++r)
+    for (int c = 0; c < 6; ++c) out->info[r * 6 + c] = 0.5 * (inv[r * 6 + c] + inv[c * 6 + r]);
+  out->inliers = inliers;
+  out->hull_fraction = hull_fraction;
+  *accepted = 1;
+  return RGBID_OK;
+}
+
+// normal_map — src/segmentation.cpp:10-57
+int rgbid_normal_map(rgbid_ctx* ctx, const double* W, int w, int h, const rgbid_intrinsics* K,
+                     double* nx, double* ny, double* nz) {
+  if (!ctx || !W || !K || !nx || !ny || !nz || w <= 0 || h <= 0) return RGBID_E_ARG;
+  LaunchScope ls(ctx);
+  const size_t N = (size_t)w * h;
+  double* d;
+  int rc = scratch_buf(ctx, "normal_map", 4 * N, &d);
+  if (rc) return rc;
+  H2D(d, W, sizeof(double) * N);
+  launch_normal_map(d, w, h, K_mat(K->fx, K->fy, K->cx, K->cy), d + N, d + 2 * N, d + 3 * N,
+                    ctx->stream);
+  rc = check_launch(ctx);
+  if (rc) return rc;
+  D2H(nx, d + N, sizeof(double) * N);
+  D2H(ny, d + 2 * N, sizeof(double) * N);
+  D2H(nz, d + 3 * N, sizeof(double) * N);
+  CK(cudaStreamSynchronize(ctx->stream));
+  return RGBID_OK;
+}
+
+// export_map — src/pipeline.cpp:463-527
+int rgbid_export_map(rgbid_ctx* ctx, int n_kf, const double* const* I, const double* const* W,
+                     int w, int h, const rgbid_pose* T_W_kf, const rgbid_intrinsics* K,
+                     double voxel, double* points, unsigned char* colors, long long capacity,
+                     long long* n) {
+  if (!ctx || n_kf < 0 || (n_kf > 0 && (!I || !W || !T_W_kf)) || !K || !n || w <= 0 || h <= 0)
+    return RGBID_E_ARG;
+  *n = 0;
+  if (n_kf == 0) return RGBID_OK;
+  LaunchScope ls(ctx);
+  const size_t N = (size_t)w * h;
+  double* d;
+  int rc = scratch_buf(ctx, "export_map", 2 * N * n_kf, &d);
+  if (rc) return rc;
+  const M3 Km = K_mat(K->fx, K->fy, K->cx, K->cy), Kinv = m3_inv(Km);
+  std::vector<ExportKF> kfs(n_kf);
+  for (int k = 0; k < n_kf; ++k) {
+    if (!I[k] || !W[k]) return RGBID_E_ARG;
+    double* dI = d + 2 * N * k;
+    double* dW = dI + N;
+    H2D(dI, I[k], sizeof(double) * N);
+    H2D(dW, W[k], sizeof(double) * N);
+    ExportKF& e = kfs[k];
+    e.I = dI;
+    e.W = dW;
+    e.T_W_kf = pose_of(&T_W_kf[k]);
+    e.W_prev = nullptr;
+    if (k > 0) {  // T_prev_kf = T_W_prev^-1 T_W_kf; Rt = K R K^-1; tt = K t
+      e.W_prev = d + 2 * N * (k - 1) + N;
+      const PoseD Tp = pose_compose(pose_inverse(pose_of(&T_W_kf[k - 1])), e.T_W_kf);
+      e.Rt = m3_mul(m3_mul(Km, Tp.R), Kinv);
+      e.tt = m3_mulv(Km, Tp.t);
+    }
+  }
+  double* dp = nullptr;
+  uint8_t* dc = nullptr;
+  long long cnt = 0;
+  const int e = export_map_device(kfs.data(), n_kf, w, h, Kinv, voxel, ctx->stream, &dp, &dc, &cnt);
+  if (e) {
+    ctx->err = std::string("export_map: ") + cudaGetErrorString((cudaError_t)e);
+    return RGBID_E_CUDA;
+  }
+  *n = cnt;
+  rc = RGBID_OK;
+  if (cnt > capacity || (cnt > 0 && (!points || !colors))) {
+    rc = RGBID_E_ARG;
+  } else if (cnt > 0) {
+    D2H(points, dp, sizeof(double) * 3 * cnt);
+    D2H(colors, dc, 3 * cnt);
+  }
+  cudaFreeAsync(dp, ctx->stream);
+  cudaFreeAsync(dc, ctx->stream);
+  CK(cudaStreamSynchronize(ctx->stream));
+  return rc;
 }
 
 int rgbid_correct_inverse_depth(rgbid_ctx* ctx, const double* Wm, int w, int h,

@@ -798,3 +798,100 @@ class Frontend:
             self.close()
         except Exception:
             pass
+
+
+# --------------------------------------------------------------------------- back-end callers
+
+
+@dataclass
+class LoopConfig:
+    """include/rgbid/loop.hpp:38-48 (the dense-refinement gate; retrieval fields are
+    the out-of-scope place-recognition front end's)."""
+    min_covisibility: float = 0.3
+
+
+@dataclass
+class LoopConstraint:
+    """include/rgbid/loop.hpp:19-26"""
+    i: int = 0
+    j: int = 0
+    T_ij: Pose = field(default_factory=Pose)
+    info: np.ndarray = field(default_factory=lambda: np.eye(6))
+    inliers: int = 0
+    hull_fraction: float = 0.0
+    score: float = 0.0
+
+
+def make_loop_constraint(kf_i, kf_j, id_i: int, id_j: int, T_init: Pose, K: Intrinsics,
+                         inliers: int = 0, hull_fraction: float = 0.0,
+                         config: Optional[LoopConfig] = None,
+                         align_config: Optional[AlignmentConfig] = None,
+                         ctx: Optional[Context] = None) -> Optional[LoopConstraint]:
+    """src/loop.cpp:174-203: dense refinement of a loop candidate -> LoopConstraint,
+    or None (std::nullopt) when the alignment is degenerate or the refined
+    covisibility falls below config.min_covisibility.  kf_i/kf_j: FrameData or
+    DeviceFrame.  Use a separate Context per host thread to refine loops
+    concurrently with tracking (each context owns a stream)."""
+    ctx = ctx or default_context()
+    fi = kf_i if isinstance(kf_i, DeviceFrame) else DeviceFrame.from_frame(kf_i, ctx)
+    fj = kf_j if isinstance(kf_j, DeviceFrame) else DeviceFrame.from_frame(kf_j, ctx)
+    cfg = (align_config or AlignmentConfig()).to_c()
+    out = abi.LoopConstraint_t()
+    acc = C.c_int(0)
+    ctx.check(ctx.lib.rgbid_make_loop_constraint(
+        ctx.h, fi.h, fj.h, id_i, id_j, C.byref(K.to_c()), C.byref(T_init.to_c()), C.byref(cfg),
+        (config or LoopConfig()).min_covisibility, inliers, hull_fraction, C.byref(out),
+        C.byref(acc)), "make_loop_constraint")
+    if not acc.value:
+        return None
+    return LoopConstraint(out.i, out.j, Pose.from_c(out.T_ij),
+                          np.array(out.info[:]).reshape(6, 6), out.inliers, out.hull_fraction,
+                          out.score)
+
+
+@dataclass
+class NormalMap:
+    """include/rgbid/segmentation.hpp:12-24"""
+    nx: np.ndarray
+    ny: np.ndarray
+    nz: np.ndarray
+
+
+def normal_map(W: np.ndarray, K: Intrinsics, ctx: Optional[Context] = None) -> NormalMap:
+    """src/segmentation.cpp:10-57"""
+    ctx = ctx or default_context()
+    W = np.ascontiguousarray(W, dtype=np.float64)
+    h, w = W.shape
+    nx, ny, nz = (np.empty_like(W) for _ in range(3))
+    ctx.check(ctx.lib.rgbid_normal_map(ctx.h, dptr(W), w, h, C.byref(K.to_c()), dptr(nx),
+                                       dptr(ny), dptr(nz)), "normal_map")
+    return NormalMap(nx, ny, nz)
+
+
+@dataclass
+class PointCloud:
+    """include/rgbid/pipeline.hpp:90-93 (points N x 3 float64, colors N x 3 uint8)"""
+    points: np.ndarray
+    colors: np.ndarray
+
+
+def export_map(keyframes: Sequence[Keyframe], K: Intrinsics, voxel: float,
+               ctx: Optional[Context] = None) -> PointCloud:
+    """src/pipeline.cpp:463-527"""
+    ctx = ctx or default_context()
+    n = len(keyframes)
+    if n == 0:
+        return PointCloud(np.zeros((0, 3)), np.zeros((0, 3), np.uint8))
+    h, w = keyframes[0].inverse_depth.shape
+    Is = [np.ascontiguousarray(k.intensity, dtype=np.float64) for k in keyframes]
+    Ws = [np.ascontiguousarray(k.inverse_depth, dtype=np.float64) for k in keyframes]
+    poses = (abi.Pose_t * n)(*[k.T_W_kf.to_c() for k in keyframes])
+    cap = n * w * h
+    pts = np.empty((cap, 3), np.float64)
+    cols = np.empty((cap, 3), np.uint8)
+    cnt = C.c_longlong(0)
+    ctx.check(ctx.lib.rgbid_export_map(ctx.h, n, abi.dptr_array(Is), abi.dptr_array(Ws), w, h,
+                                       poses, C.byref(K.to_c()), voxel, dptr(pts),
+                                       cols.ctypes.data_as(C.POINTER(C.c_ubyte)), cap,
+                                       C.byref(cnt)), "export_map")
+    return PointCloud(pts[: cnt.value].copy(), cols[: cnt.value].copy())

@@ -222,3 +222,25 @@ def test_synth_matches_reference_fixtures(R_):
     f = rg.render_plane(K, T, N_SLANT, -2.0, 1.0)
     I, W = R_.render_plane(K.to_c(), T.to_c(), N_SLANT, -2.0)
     assert bitwise_equal(f.intensity, I) and bitwise_equal(f.inverse_depth, W)
+
+
+@needs_ref
+def test_backend_oracles_sane(R_):
+    """SURVEY 8(f) rank 4 checkers: the reference normal_map (built unchanged from
+    src/segmentation.cpp) gives unit normals facing the camera; the export_map
+    restatement keeps only novel pixels and the voxel grid only merges."""
+    from oracle import map_oracle
+    K = rg.simple_intrinsics(80, 60, 60.0)
+    fa, _, _ = pair(K, 2, "noisy", holes=True)
+    nx, ny, nz = R_.normal_map(fa.inverse_depth, K.to_c())
+    m = np.isfinite(fa.inverse_depth) & (fa.inverse_depth > 0)
+    assert np.array_equal(np.isfinite(nz), m)
+    n = np.sqrt(nx[m] ** 2 + ny[m] ** 2 + nz[m] ** 2)
+    assert np.allclose(n, 1.0) and (nz[m] <= 0).all()
+    kfs = [(fa.intensity, fa.inverse_depth, rg.Pose().to_c()),
+           (fa.intensity, fa.inverse_depth, rg.Pose().to_c())]
+    p0, c0 = map_oracle.export_map(kfs, K.to_c(), 0.0)
+    # the second, identical keyframe adds only pixels whose bilinear taps touch a hole
+    assert m.sum() <= len(p0) < 1.2 * m.sum()
+    pv, cv = map_oracle.export_map(kfs, K.to_c(), 0.1)
+    assert 0 < len(pv) < len(p0) and cv.dtype == np.uint8
