@@ -564,43 +564,91 @@ struct Sample {
   int m_local;      // samples held by this CTA
   int kfull;        // rounds where every thread owns a sample (m_local / NT)
   int cs;           // cluster size sharing the sample (1 = single CTA)
-  double* cbuf;     // this CTA's [2][2] cluster exchange slots (shared memory)
+  double* cbuf;     // this CTA's [2][kTdistCluster * NW * 2] warp-partial slots (cluster mode)
+  uint64_t* cmbar;  // this CTA's two mbarriers guarding cbuf's halves (cluster mode)
+  int cred;         // cluster reductions done
+  int rank;         // this CTA's rank in the cluster
   // memo of the last estimate_location_scale(nu) call: same sample + same nu
   // -> same result (e.g. the final refit repeating estimate_nu's, src/alignment.cpp:117,316)
   double memo_nu;
   TD memo;
 };
 
-// Sum over the whole sample: fixed-order block reduction, then (cluster mode)
-// a fixed-rank-order reduction of the CTA partials over DSMEM.  Every thread of
-// every CTA ends with the bit-identical total.  The cluster slots are double
-// buffered on the same parity as the block scratch, so one cluster barrier per
-// reduction suffices.
+// Cluster-wide sum (latency mode): every warp's lane d pushes the warp's partials
+// into CTA d's slot array with st.async, completing transaction bytes on CTA d's
+// mbarrier; each CTA waits on its own mbarrier, then reduces the CS x NW slots in
+// a fixed tree -- identical bits in every thread of every CTA, with no block or
+// cluster barrier.  The slots and mbarriers are double buffered: a CTA cannot run
+// two reductions ahead of a peer (its reduction r+1 needs the peer's r+1
+// partials, sent only after the peer consumed r).
+template <int NV, int NT>
+__device__ __forceinline__ void cluster_allsum(double (&v)[NV], Sample& S) {
+  constexpr int NW = NT / 32, CS = kTdistCluster, NP = CS * NW;
+  static_assert(NP == 64, "two slots per lane in the final tree");
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int p = S.cred & 1;
+  const unsigned ph = (unsigned)(S.cred >> 1) & 1u;
+  ++S.cred;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1)
+#pragma unroll
+    for (int i = 0; i < NV; ++i) v[i] += __shfl_xor_sync(0xffffffffu, v[i], off);
+  double* buf = S.cbuf + p * (NP * 2);
+  uint64_t* mb = S.cmbar + p;
+  if (threadIdx.x == 0) {
+    const unsigned a = (unsigned)__cvta_generic_to_shared(mb);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a),
+                 "r"((unsigned)(NP * NV * 8))
+                 : "memory");
+  }
+  if (lane < CS) {
+    unsigned rem_buf, rem_mb;
+    const unsigned lb = (unsigned)__cvta_generic_to_shared(buf + (S.rank * NW + wid) * NV);
+    const unsigned lm = (unsigned)__cvta_generic_to_shared(mb);
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rem_buf) : "r"(lb), "r"(lane));
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rem_mb) : "r"(lm), "r"(lane));
+#pragma unroll
+    for (int i = 0; i < NV; ++i)
+      asm volatile(
+          "st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(
+              rem_buf + 8 * i),
+          "l"(__double_as_longlong(v[i])), "r"(rem_mb)
+          : "memory");
+  }
+  {
+    const unsigned a = (unsigned)__cvta_generic_to_shared(mb);
+    unsigned done = 0;
+    do {
+      asm volatile(
+          "{ .reg .pred P; mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P, [%1], %2;"
+          " selp.u32 %0, 1, 0, P; }"
+          : "=r"(done)
+          : "r"(a), "r"(ph)
+          : "memory");
+    } while (!done);
+  }
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    double t = buf[lane * NV + i] + buf[(lane + 32) * NV + i];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
+    v[i] = t;
+  }
+}
+
+// Sum over the whole sample: fixed-order block reduction (single CTA), or the
+// cluster-wide push reduction (latency mode).  Every thread of every CTA ends
+// with the bit-identical total.
 template <int NV, int NT>
 __device__ __forceinline__ void sample_allsum(double (&v)[NV], Sample& S) {
   TPH_T(tr0);
-  const int p = S.parity;
-  block_allsum<NV, NT>(v, S.scratch, S.parity);
-  if (S.cs > 1) {
-    namespace cg = cooperative_groups;
-    cg::cluster_group cl = cg::this_cluster();
-    if (threadIdx.x == 0)
-#pragma unroll
-      for (int i = 0; i < NV; ++i) S.cbuf[p * 2 + i] = v[i];
-    cl.sync();
-    double part[kTdistCluster][NV];
-#pragma unroll
-    for (int r = 0; r < kTdistCluster; ++r) {  // all remote loads in flight at once
-      const double* rem = cl.map_shared_rank(S.cbuf, r);
-#pragma unroll
-      for (int i = 0; i < NV; ++i) part[r][i] = rem[p * 2 + i];
-    }
-#pragma unroll
-    for (int i = 0; i < NV; ++i) {
-      v[i] = 0.0;
-#pragma unroll
-      for (int r = 0; r < kTdistCluster; ++r) v[i] += part[r][i];
-    }
+  if constexpr (NT == kTdistClusterThreads) {
+    if (S.cs > 1)
+      cluster_allsum<NV, NT>(v, S);
+    else
+      block_allsum<NV, NT>(v, S.scratch, S.parity);
+  } else {
+    block_allsum<NV, NT>(v, S.scratch, S.parity);
   }
   TPH_ADD(8, tr0);
   TPH_CNT(9, 1);
@@ -1048,6 +1096,9 @@ __global__ void __launch_bounds__(NT, kTdistThreads / NT)
   smp.kfull = smp.m / NT;
   smp.cs = 1;
   smp.cbuf = nullptr;
+  smp.cmbar = nullptr;
+  smp.cred = 0;
+  smp.rank = 0;
   smp.memo_nu = -1.0;
   smp.scratch = scratch;
   smp.parity = 0;
@@ -1111,8 +1162,17 @@ __global__ void __launch_bounds__(kTdistClusterThreads, 1)
   int* offs = reinterpret_cast<int*>(dsm + kShare);
   __shared__ int wsum[NT / 32];
   __shared__ double scratch[NT / 32 * 2 * 2];
-  __shared__ double cbuf[4];
+  __shared__ double cbuf[2 * CS * (NT / 32) * 2];
+  __shared__ __align__(8) uint64_t cmbar[2];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  if (tid == 0) {
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(
+                       (unsigned)__cvta_generic_to_shared(&cmbar[i]))
+                   : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
   const int nt = li.ntiles;
   const int per = (nt + NT - 1) / NT;
   const int b0 = min(nt, tid * per), b1 = min(nt, b0 + per);
@@ -1168,6 +1228,9 @@ __global__ void __launch_bounds__(kTdistClusterThreads, 1)
   smp.kfull = smp.m_local / NT;
   smp.cs = CS;
   smp.cbuf = cbuf;
+  smp.cmbar = cmbar;
+  smp.cred = 0;
+  smp.rank = rank;
   smp.memo_nu = -1.0;
   smp.scratch = scratch;
   smp.parity = 0;
@@ -1838,6 +1901,9 @@ __global__ void __launch_bounds__(kTdistThreads, 1)  // one CTA per SM (sample i
   smp.kfull = smp.m / NT;
   smp.cs = 1;
   smp.cbuf = nullptr;
+  smp.cmbar = nullptr;
+  smp.cred = 0;
+  smp.rank = 0;
   smp.memo_nu = -1.0;
   smp.scratch = scratch;
   smp.parity = 0;
