@@ -584,7 +584,7 @@ struct Sample {
 template <int NV, int NT>
 __device__ __forceinline__ void cluster_allsum(double (&v)[NV], Sample& S) {
   constexpr int NW = NT / 32, CS = kTdistCluster, NP = CS * NW;
-  static_assert(NP == 64, "two slots per lane in the final tree");
+  static_assert(NP % 32 == 0 && CS <= 32, "whole slots per lane in the final tree");
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int p = S.cred & 1;
   const unsigned ph = (unsigned)(S.cred >> 1) & 1u;
@@ -629,7 +629,9 @@ __device__ __forceinline__ void cluster_allsum(double (&v)[NV], Sample& S) {
   }
 #pragma unroll
   for (int i = 0; i < NV; ++i) {
-    double t = buf[lane * NV + i] + buf[(lane + 32) * NV + i];
+    double t = buf[lane * NV + i];
+#pragma unroll
+    for (int j = 1; j < NP / 32; ++j) t += buf[(lane + 32 * j) * NV + i];
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
     v[i] = t;
@@ -1081,6 +1083,7 @@ __global__ void __launch_bounds__(NT, kTdistThreads / NT)
   SlotState& S = st[slot];
   if (!slot_active(S, li.level, phase)) return;
   TPH_T(tk0);
+  TPH_CNT(10, 1);
   const SlotIO& o = io[slot];
   extern __shared__ double dsm[];  // sample[kMaxSample]
   double* smp_sh = dsm;
@@ -1151,6 +1154,8 @@ __global__ void __launch_bounds__(kTdistClusterThreads, 1)
   const int type = blockIdx.x / CS, slot = blockIdx.y;
   SlotState& S = st[slot];
   if (!slot_active(S, li.level, phase)) return;  // uniform over the cluster
+  TPH_T(tk0);
+  TPH_CNT(10, 1);
   const SlotIO& o = io[slot];
   const int* cnt = type ? o.cntW : o.cntI;
   const unsigned* bits = type ? o.bitsW : o.bitsI;
@@ -1203,27 +1208,66 @@ __global__ void __launch_bounds__(kTdistClusterThreads, 1)
   Sample smp;
   smp.v = smp_sh;
   smp.m = n == 0 ? 0 : (int)((n - 1) / stride + 1);
-  smp.m_local = smp.m > rank ? (smp.m - rank + CS - 1) / CS : 0;
-  for (int k = tid; k < smp.m_local; k += NT) {
-    const long long g = (long long)(rank + CS * k) * stride;
-    int lo = 0, hi = nt - 1;
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (offs[mid] <= g)
-        lo = mid;
-      else
-        hi = mid - 1;
+  // CTA `rank` holds the contiguous samples [c0, c1); thread tid a contiguous run of
+  // them: one binary search over the tile offsets, then a forward walk over the
+  // validity words (as k_gather), the pixel indices parked in the sample slots
+  const int share = (smp.m + CS - 1) / CS;
+  const int c0 = min(smp.m, rank * share), c1 = min(smp.m, c0 + share);
+  smp.m_local = c1 - c0;
+  long long* sidx = reinterpret_cast<long long*>(smp_sh);
+  {
+    const int lw = tile_words_log2(li.tx), wpt = 1 << lw;
+    const int spt = (smp.m_local + NT - 1) / NT;
+    const int s0 = min(c1, c0 + tid * spt), s1 = min(c1, s0 + spt);
+    if (s0 < s1) {
+      long long g = (long long)s0 * stride;
+      int lo = 0, hi = nt - 1;
+      while (lo < hi) {  // last tile with offs[t] <= g
+        const int mid = (lo + hi + 1) >> 1;
+        if (offs[mid] <= g)
+          lo = mid;
+        else
+          hi = mid - 1;
+      }
+      int tile = lo, w = 0, yl = lo / li.nseg, seg = lo - yl * li.nseg;
+      long long base = offs[lo];
+      unsigned msk = __ldg(bits + tile * kWordsPerTile);
+      int c = __popc(msk);
+      for (int s = s0; s < s1; ++s, g += stride) {
+        int j = (int)(g - base);
+        while (j >= c) {
+          j -= c;
+          base += c;
+          if (++w == wpt) {
+            w = 0;
+            ++tile;
+            if (++seg == li.nseg) {
+              seg = 0;
+              ++yl;
+            }
+          }
+          msk = __ldg(bits + tile * kWordsPerTile + w);
+          c = __popc(msk);
+        }
+        sidx[s - c0] = yl * li.w + seg * li.tx + w * 32 + select_bit(msk, j);
+      }
     }
-    int j = (int)(g - offs[lo]), word = 0;
-    unsigned msk = bits[lo * kWordsPerTile];
-    while (j >= __popc(msk)) {
-      j -= __popc(msk);
-      msk = bits[lo * kWordsPerTile + (++word)];
-    }
-    for (int q = 0; q < j; ++q) msk &= msk - 1u;
-    const int yl = lo / li.nseg, seg = lo - yl * li.nseg;
-    const int idx = yl * li.w + seg * li.tx + word * 32 + (__ffs(msk) - 1);
-    smp_sh[k] = bv[idx] - av[idx];
+  }
+  __syncthreads();
+  for (int k = tid; k < smp.m_local; k += 4 * NT) {  // values, four loads in flight
+    long long ix[4];
+    double bb[4], aa[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) ix[u] = k + u * NT < smp.m_local ? sidx[k + u * NT] : -1;
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (ix[u] >= 0) {
+        bb[u] = __ldg(bv + ix[u]);
+        aa[u] = __ldg(av + ix[u]);
+      }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (ix[u] >= 0) smp_sh[k + u * NT] = bb[u] - aa[u];  // r_I = i_b - i_a / r_W = w_b - w_a
   }
   smp.kfull = smp.m_local / NT;
   smp.cs = CS;
@@ -1234,6 +1278,7 @@ __global__ void __launch_bounds__(kTdistClusterThreads, 1)
   smp.memo_nu = -1.0;
   smp.scratch = scratch;
   smp.parity = 0;
+  TPH_ADD(0, tk0);
   cl.sync();  // every CTA's share (and cbuf) ready before the first cluster reduction
   TD t = loc_scale<NT>(smp, 5.0, scratch);
   t.sigma = dmax_std(t.sigma, 1e-8);
@@ -1255,6 +1300,7 @@ __global__ void __launch_bounds__(kTdistClusterThreads, 1)
       S.nW = n;
     }
   }
+  TPH_ADD(7, tk0);
   cl.sync();  // no CTA exits while others may still read its cluster slots
 }
 
@@ -1277,6 +1323,8 @@ int init_kernel_attributes() {
   cudaFuncSetAttribute(k_gather, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
   const cudaError_t e2 =
       cudaFuncSetAttribute(k_tdist_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+  if (kTdistCluster > 8)
+    cudaFuncSetAttribute(k_tdist_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   cudaGetLastError();
   return (e == cudaSuccess && e2 == cudaSuccess) ? 0 : 1;
 }

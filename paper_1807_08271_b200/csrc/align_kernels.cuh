@@ -22,9 +22,15 @@ constexpr int kTPB = 256;           // warp/residual/normal-equation kernels
 constexpr int kTdistThreads = RGBID_TDIST_THREADS;  // Student-t kernel (sample in shared memory)
 constexpr int kNPart = 28;          // 21 (lower H) + 6 (b) + 1 (cost)
 constexpr int kTraceMax = 64;
-constexpr int kTdistCluster = 8;         // CTAs per Student-t chain in latency mode
+#ifndef RGBID_TDIST_CLUSTER
+#define RGBID_TDIST_CLUSTER 8
+#endif
+constexpr int kTdistCluster = RGBID_TDIST_CLUSTER;  // CTAs per Student-t chain in latency mode
 constexpr int kTdistClusterMaxSlots = 8; // batches up to this size use the cluster kernel
-constexpr int kTdistClusterThreads = 256;
+#ifndef RGBID_TDIST_CLUSTER_THREADS
+#define RGBID_TDIST_CLUSTER_THREADS 256
+#endif
+constexpr int kTdistClusterThreads = RGBID_TDIST_CLUSTER_THREADS;
 constexpr int kPixK3 = 8;           // pixels per thread in the normal-equation kernel
 
 // K1 tiling of level l: tile = (level row, segment of tx level pixels).

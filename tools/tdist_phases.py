@@ -12,13 +12,14 @@ ctx = rg.Context(0)
 L = ctx.lib
 L.rgbid_debug_tdist_phases.argtypes = [C.POINTER(C.c_ulonglong), C.c_int]
 K = rg.simple_intrinsics(640, 480, 480.0)
-n = int(sys.argv[1]) if len(sys.argv) > 1 else 512
+n = int(sys.argv[1]) if len(sys.argv) > 1 else 512  # n <= 8: latency mode (cluster kernel)
 A = [rg.DeviceFrame(640, 480, ctx) for _ in range(n)]
 B = [rg.DeviceFrame(640, 480, ctx) for _ in range(n)]
 for i in range(n):
     rg.synth_pair_device(A[i], B[i], K, i, 1)
 buf = (C.c_ulonglong * 16)()
-names = {0: "gather", 1: "loc_scale", 4: "stationarity", 6: "stat_pass", 8: "allsum", 7: "kernel"}
+names = {0: "gather", 1: "loc_scale", 4: "stationarity", 6: "stat_pass", 8: "allsum", 7: "kernel",
+         3: "ls_iters(count)", 9: "allsums(count)", 2: "ls_calls(count)", 5: "stat_calls(count)"}
 for lv in range(-1, 4):
     # one iteration at level `lv` only (levels = lv + 1, zero iterations on the finer
     # levels); lv = -1: no iterations at all -> the final covariance's refit only
