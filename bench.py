@@ -37,18 +37,25 @@ M_BYTES = W0 * H0 * 8  # one fp64 map
 N0 = W0 * H0
 
 
+def pairs_total(args, world):
+    """weak scaling: --pairs per GPU; strong: --pairs split over the GPUs"""
+    return args.pairs * world if args.scaling == "weak" else args.pairs
+
+
 def workload_config(args, world):
     return {
         "workload": "config5: batched independent 640x480 frame-pair alignments, "
                     "4-level pyramid, iterations {10,5,4,5} + filtered-Hessian covariance",
-        "pairs_total": args.pairs,
-        "pairs_per_gpu": args.pairs // world,
+        "pairs_total": pairs_total(args, world),
+        "pairs_per_gpu": pairs_total(args, world) // world,
         "levels": LEVELS,
         "iterations": [10, 5, 4, 5],
         "variant": "noisy+occluder" if args.variant == 1 else "clean",
         "image": f"{W0}x{H0} fp64 (intensity + inverse depth), f={F0}",
-        "parallelism": f"pairs partitioned over {world} GPU(s); NCCL all_gather of results only",
-        "l2": "inputs (9.8 MB/pair, 40 GB total) exceed the 126 MB L2; no flush needed",
+        "parallelism": (f"{args.scaling} scaling over {world} GPU(s): each rank renders and aligns "
+                        f"its own contiguous block of pair indices; NCCL all_gather of result "
+                        f"records only"),
+        "l2": "inputs (9.8 MB/pair, 40 GB per GPU) exceed the 126 MB L2; no flush needed",
     }
 
 
@@ -57,7 +64,11 @@ def parse():
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=3)
     p.add_argument("--warmup", type=int, default=3)
-    p.add_argument("--pairs", type=int, default=4096)
+    p.add_argument("--pairs", type=int, default=4096,
+                   help="pairs per GPU (weak scaling) or in total (--scaling strong)")
+    p.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                   help="weak: every GPU aligns its own --pairs independent pairs (the path "
+                        "partitions into independent units, SURVEY 8e); strong: --pairs split")
     p.add_argument("--variant", type=int, default=1, help="0 clean, 1 noisy+occluder")
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--no-e2e", action="store_true")
@@ -67,9 +78,10 @@ def parse():
     return p.parse_args()
 
 
-def partition(pairs, world, rank):
-    """Contiguous block of pair indices for this rank (strong scaling, no input scatter)."""
-    n_local = pairs // world
+def partition(pairs, world, rank, scaling="strong"):
+    """Contiguous block of pair indices for this rank (no input scatter: each rank
+    renders its own).  strong: `pairs` in total; weak: `pairs` per rank."""
+    n_local = pairs if scaling == "weak" else pairs // world
     return rank * n_local, n_local
 
 
@@ -209,7 +221,8 @@ def run_reference(args, rank, world):
               f"{cores} threads, one pair per thread at a time")
     line = {
         "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": args.scaling,
         "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
         "config": workload_config(args, world),
         "cpu_baseline": {"value": rate, "unit": UNIT, "cores": cores, "kind": kind,
@@ -280,7 +293,7 @@ def main():
     ctx = rg.Context(local)
     K = rg.simple_intrinsics(W0, H0, F0)
     cfg = rg.AlignmentConfig(levels=LEVELS, iterations=ITERS)
-    base, n_local = partition(args.pairs, world, rank)
+    base, n_local = partition(args.pairs, world, rank, args.scaling)
 
     # inputs resident in HBM: device-rendered pairs (pair seed = global index)
     A = [rg.DeviceFrame(W0, H0, ctx) for _ in range(n_local)]
@@ -324,7 +337,7 @@ def main():
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
-    value = args.pairs * args.steps / (ms_max / 1000.0)
+    value = pairs_total(args, world) * args.steps / (ms_max / 1000.0)
     statuses = {int(r.status) for r in results}
     n_ok = sum(1 for r in results if r.status == 0)
     mean_iters = float(np.mean([r.total_iterations for r in results if r.status == 0] or [0]))
@@ -456,7 +469,7 @@ def main():
         t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
         if world > 1:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e = {"value": args.pairs * e2e_steps / (float(t.item()) / 1e3), "unit": UNIT,
+        e2e = {"value": pairs_total(args, world) * e2e_steps / (float(t.item()) / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": h2d // e2e_steps, "d2h_bytes_per_step": d2h // e2e_steps,
                "path": "rgbid_align_batch_host (C-ABI) from pinned host buffers, 2 lanes x chunks of 512; "
                        f"host pool of {P} distinct pairs cycled"}
@@ -478,7 +491,7 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (device-rendered textured slanted plane, SURVEY 8d)",
             "config": workload_config(args, world),
             "clocks": clk, "gpu_launches": launches, "e2e": e2e, "roofline": roofline,

@@ -67,6 +67,15 @@ def test_partition_covers_all_pairs(world):
     assert seen == list(range(4096))
 
 
+@pytest.mark.parametrize("world", [2, 8])
+def test_weak_partition_gives_each_rank_its_own_pairs(world):
+    import bench
+    blocks = [bench.partition(4096, world, r, "weak") for r in range(world)]
+    assert all(n == 4096 for _, n in blocks)
+    seen = [i for base, n in blocks for i in range(base, base + n)]
+    assert seen == list(range(4096 * world))
+
+
 def test_reference_arm_nonzero_rank_exits_clean():
     env = dict(os.environ, RANK="1", WORLD_SIZE="2", LOCAL_RANK="1")
     p = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference"],
