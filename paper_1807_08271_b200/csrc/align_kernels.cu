@@ -1517,9 +1517,161 @@ __global__ void __launch_bounds__(kTPB, RGBID_K3_MINBLOCKS) k_normal_eq(const Sl
 static const char* kNeNames[kMaxLevels] = {"normal_eq_L0", "normal_eq_L1", "normal_eq_L2",
                                             "normal_eq_L3", "normal_eq_L4", "normal_eq_L5"};
 
+#ifndef RGBID_K3_MMA
+#define RGBID_K3_MMA 1
+#endif
+
+// D = A B + C, one m8n8k4 fp64 tensor-core MMA (A row-major 8x4, B col-major 4x8;
+// lane l holds A[l/4][l%4], B[l%4][l/4], C[l/4][2(l%4) + {0,1}])
+__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+// K3 on the FP64 tensor cores.  Same jets and weights as k_normal_eq; each warp
+// stages its 32 pixel rows x = (J, r, 0) and w in shared memory and accumulates
+// C += sum_k w_k x_k x_k^T with 8 MMAs per row type, so the 8x8 system (H, the
+// J^T W r column, the cost) lives in two fp64 registers per lane instead of 28 --
+// the register file no longer caps occupancy.  Invalid rows are zeroed (w and x).
+#ifndef RGBID_K3_MMA_MINB
+#define RGBID_K3_MMA_MINB 3
+#endif
+__global__ void __launch_bounds__(kTPB, RGBID_K3_MMA_MINB) k_normal_eq_mma(const SlotIO* __restrict__ io,
+                                                        const SlotState* __restrict__ st,
+                                                        LevelInfo li, int phase,
+                                                        double lambda_n_min) {
+  const int slot = blockIdx.y;
+  const SlotState& S = st[slot];
+  if (!slot_active(S, li.level, phase)) return;  // uniform over the CTA
+  const SlotIO& o = io[slot];
+  const double* __restrict__ IA = phase ? o.fIA : o.IA[li.level];
+  const double* __restrict__ WA = phase ? o.fWA : o.WA[li.level];
+  const uint8_t* __restrict__ am = o.amask[li.level];
+  const double2* __restrict__ ag = reinterpret_cast<const double2*>(o.agrad[li.level]);
+  const double* __restrict__ ibp = o.ib;
+  const double* __restrict__ wbp = o.wb;
+  constexpr int XS = 9;  // 8 components + w per staged row
+  __shared__ double xs[kTPB / 32][32 * XS];
+  __shared__ double cst[kTPB / 32][64];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double* xw = xs[wid];
+  const double muI = S.tI.mu, isgI = 1.0 / S.tI.sigma, nuI = dmax_std(S.tI.nu, S.tW.nu);
+  const double muW = S.tW.mu, isgW = 1.0 / S.tW.sigma, nuW = S.tW.nu;
+  const double nuI1 = nuI + 1.0, nuW1 = nuW + 1.0;
+  const double is2i = isgI * isgI, is2w = isgW * isgW;
+  const int w = li.w;
+  const double* Ki = li.Kinv;
+  const int N = li.w * li.h;
+  double c0 = 0.0, c1 = 0.0;
+  auto mma_rows = [&]() {
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int row = 4 * j + (lane & 3);
+      const double xv = xw[row * XS + (lane >> 2)], wv = xw[row * XS + 8];
+      dmma884(c0, c1, wv * xv, xv);
+    }
+    __syncwarp();
+  };
+#pragma unroll 1
+  for (int p = 0; p < kPixK3; ++p) {
+    const int k0i = (blockIdx.x * kPixK3 + p) * kTPB + threadIdx.x;
+    const bool inr = k0i < N;
+    const int k = inr ? k0i : 0;
+    const unsigned a = __ldg(am + k);
+    const double i_b = __ldcs(ibp + k), w_b = __ldcs(wbp + k);
+    const double w_a = __ldg(WA + k), i_a = __ldg(IA + k);
+    const double2 gI = __ldg(ag + 2 * k), gW = __ldg(ag + 2 * k + 1);
+    const bool jet = inr && (a & 1u) && valid(i_b);
+    const bool dep = jet && (a & 2u) && valid(w_b) && w_b > 0.0;
+    const int y = k / w, x = k - y * w;
+    const double px = x, py = y;
+    const double ax = li.cx - px, ay = li.cy - py;
+    const double iwa = 1.0 / w_a;
+    const double k0 = red3(Ki[0] * px, Ki[1] * py, Ki[2]), k1 = red3(Ki[3] * px, Ki[4] * py, Ki[5]),
+                 k2 = red3(Ki[6] * px, Ki[7] * py, Ki[8]);
+    const double X0 = k0 * iwa, X1 = k1 * iwa, X2 = k2 * iwa;
+    {  // photometric row
+      const double s0 = w_a * gI.x, s1 = w_a * gI.y;
+      const double u0 = s0 * li.fx, u1 = s1 * li.fy, u2 = s0 * ax + s1 * ay;
+      const double rI = i_b - i_a;
+      const double xi_ = (rI - muI) * isgI;
+      const double wi = nuI1 * rcp_fast(fma(xi_, xi_, nuI)) * is2i;
+      double* r = xw + lane * XS;
+      r[0] = jet ? u0 : 0.0;
+      r[1] = jet ? u1 : 0.0;
+      r[2] = jet ? u2 : 0.0;
+      r[3] = jet ? X1 * u2 - X2 * u1 : 0.0;
+      r[4] = jet ? X2 * u0 - X0 * u2 : 0.0;
+      r[5] = jet ? X0 * u1 - X1 * u0 : 0.0;
+      r[6] = jet ? rI : 0.0;
+      r[7] = 0.0;
+      r[8] = jet ? wi : 0.0;
+    }
+    mma_rows();
+    {  // geometric row
+      const double g0 = gW.x * li.fx, g1 = gW.y * li.fy, g2 = gW.x * ax + gW.y * ay;
+      const double s0 = w_a * g0, s1 = w_a * g1, s2 = w_a * (g2 + w_b);
+      double lambda = 1.0;
+      {
+        const double n0 = g0 * iwa, n1 = g1 * iwa, n2 = g2 * iwa + 1.0;
+        const double nn2 = n0 * n0 + n1 * n1 + n2 * n2;
+        if (!(sqrt(nn2) < 1e-12)) {
+          const double rr2 = k0 * k0 + k1 * k1 + k2 * k2;
+          double c = (n0 * k0 + n1 * k1 + n2 * k2) * rsqrt(nn2) * rsqrt(rr2);
+          if (n2 < 0) c = -c;
+          lambda = dmax_std(lambda_n_min, c);
+        }
+      }
+      const double rW = w_b - w_a;
+      const double xw_ = (rW - muW) * isgW;
+      const double ww = lambda * nuW1 * rcp_fast(fma(xw_, xw_, nuW)) * is2w;
+      double* r = xw + lane * XS;
+      r[0] = dep ? s0 : 0.0;
+      r[1] = dep ? s1 : 0.0;
+      r[2] = dep ? s2 : 0.0;
+      r[3] = dep ? X1 * s2 - X2 * s1 : 0.0;
+      r[4] = dep ? X2 * s0 - X0 * s2 : 0.0;
+      r[5] = dep ? X0 * s1 - X1 * s0 : 0.0;
+      r[6] = dep ? rW : 0.0;
+      r[7] = 0.0;
+      r[8] = dep ? ww : 0.0;
+    }
+    mma_rows();
+  }
+  cst[wid][(lane >> 2) * 8 + 2 * (lane & 3)] = c0;
+  cst[wid][(lane >> 2) * 8 + 2 * (lane & 3) + 1] = c1;
+  __syncthreads();
+  if (threadIdx.x < kNPart) {  // partial q in k_normal_eq's order
+    const int q = threadIdx.x;
+    int r, c;
+    if (q < 21) {
+      r = 0;
+      while ((r + 1) * (r + 2) / 2 <= q) ++r;
+      c = q - r * (r + 1) / 2;
+    } else if (q < 27) {
+      r = q - 21;
+      c = 6;
+    } else {
+      r = 6;
+      c = 6;
+    }
+    double t = 0.0;
+#pragma unroll
+    for (int wv = 0; wv < kTPB / 32; ++wv) t += cst[wv][r * 8 + c];
+    o.part[(size_t)blockIdx.x * kNPart + q] = t;
+  }
+}
+
 void launch_normal_equations(const AlignLaunch& a, const LevelInfo& li, int phase, cudaStream_t s) {
   KScope ks_(phase ? "normal_eq_cov" : kNeNames[li.level], s);
-  k_normal_eq<<<dim3(li.ntiles3, a.nslots), kTPB, 0, s>>>(a.io, a.st, li, phase, a.lambda_n_min);
+  if (RGBID_K3_MMA)
+    k_normal_eq_mma<<<dim3(li.ntiles3, a.nslots), kTPB, 0, s>>>(a.io, a.st, li, phase,
+                                                                a.lambda_n_min);
+  else
+    k_normal_eq<<<dim3(li.ntiles3, a.nslots), kTPB, 0, s>>>(a.io, a.st, li, phase,
+                                                            a.lambda_n_min);
 }
 
 // fixed-order reduction of the per-tile partials into H (full, mirrored), b, cost
