@@ -246,6 +246,7 @@ __global__ void __launch_bounds__(k1_threads<L>(), 1024 / k1_threads<L>()) k_war
     reinterpret_cast<double*>(&wm)[threadIdx.x] = reinterpret_cast<const double*>(&S.wm)[threadIdx.x];
   const SlotIO& o = io[slot];
   const double* __restrict__ WAw = phase ? o.fWA : o.WA[0];
+  const double* __restrict__ IAl = phase ? o.fIA : o.IA[L];
   const uint8_t* __restrict__ am = o.amask[L];
   const double* __restrict__ IB = o.IB;
   const double* __restrict__ WB = o.WB;
@@ -315,7 +316,7 @@ __global__ void __launch_bounds__(k1_threads<L>(), 1024 / k1_threads<L>()) k_war
   if (tid < nx) {
     const int idx = yl * li.w + xl0 + tid;
     const double ib = sI[tid], wb = sW[tid];
-    o.ib[idx] = ib;
+    o.ib[idx] = ib - __ldg(IAl + idx);  // r_I (src/alignment.cpp:222), consumed by K2 and K3
     o.wb[idx] = wb;
     const unsigned a = __ldg(am + idx);
     jet = (a & 1u) && valid(ib);
@@ -351,6 +352,7 @@ __global__ void __launch_bounds__(128, 12) k_warp_residuals_l0(const SlotIO* __r
     reinterpret_cast<double*>(&wm)[threadIdx.x] = reinterpret_cast<const double*>(&S.wm)[threadIdx.x];
   const SlotIO& o = io[slot];
   const double* __restrict__ WAw = phase ? o.fWA : o.WA[0];
+  const double* __restrict__ IA0 = phase ? o.fIA : o.IA[0];
   const uint8_t* __restrict__ am = o.amask[0];
   const double* __restrict__ IB = o.IB;
   const double* __restrict__ WB = o.WB;
@@ -368,9 +370,10 @@ __global__ void __launch_bounds__(128, 12) k_warp_residuals_l0(const SlotIO* __r
     if (lx < nx) {
       const int idx = yl * w0 + xl0 + lx;
       const unsigned a = __ldg(am + idx);
+      const double ia = __ldg(IA0 + idx);
       double ib, wb, d0, d1;
       warp_px(wm, IB, WB, w0, h0, xl0 + lx, yl, __ldg(WAw + idx), ib, wb, d0, d1);
-      o.ib[idx] = ib;
+      o.ib[idx] = ib - ia;  // r_I (src/alignment.cpp:222), consumed by K2 and K3
       o.wb[idx] = wb;
       jet[q] = (a & 1u) && valid(ib);
       dep[q] = jet[q] && (a & 2u) && valid(wb) && wb > 0.0;
@@ -488,7 +491,6 @@ void launch_warp_residuals(const AlignLaunch& a, const LevelInfo& li, int phase,
 // MUFU-seeded Newton reciprocal for t_weight (<= 1-2 ulp per term; the
 // reference's sums are sequential, ours a fixed tree — both only change
 // rounding, well inside the 1e-4 normal-equation tolerance).
-constexpr int kSPT = (kMaxSample + kTdistThreads - 1) / kTdistThreads;
 
 // Block-wide sum; every thread receives the bit-identical total.  The scratch
 // has two halves used alternately (the caller's parity flips per call), so one
@@ -969,8 +971,8 @@ __global__ void __launch_bounds__(kGatherThreads)
   const SlotIO& o = io[slot];
   const int* cnt = type ? o.cntW : o.cntI;
   const unsigned* bits = type ? o.bitsW : o.bitsI;
-  const double* bv = type ? o.wb : o.ib;  // warped B at this level
-  const double* av = type ? (phase ? o.fWA : o.WA[li.level]) : (phase ? o.fIA : o.IA[li.level]);
+  const double* bv = type ? o.wb : o.ib;  // warped W_B / r_I (K1) at this level
+  const double* av = phase ? o.fWA : o.WA[li.level];
   extern __shared__ int offs[];  // [ntiles + 1]
   __shared__ long long sidx[kGatherChunk];
   __shared__ int wsum[NT / 32];
@@ -1064,11 +1066,11 @@ __global__ void __launch_bounds__(kGatherThreads)
     for (int u = 0; u < 4; ++u)
       if (ix[u] >= 0) {
         b[u] = __ldg(bv + ix[u]);
-        a[u] = __ldg(av + ix[u]);
+        a[u] = type ? __ldg(av + ix[u]) : 0.0;
       }
 #pragma unroll
     for (int u = 0; u < 4; ++u)
-      if (ix[u] >= 0) out[s + u * NT] = b[u] - a[u];  // r_I = i_b - i_a / r_W = w_b - w_a (src/alignment.cpp:222,229)
+      if (ix[u] >= 0) out[s + u * NT] = type ? b[u] - a[u] : b[u];  // r_W = w_b - w_a / r_I stored by K1
   }
 }
 
@@ -1160,7 +1162,7 @@ __global__ void __launch_bounds__(kTdistClusterThreads, 1)
   const int* cnt = type ? o.cntW : o.cntI;
   const unsigned* bits = type ? o.bitsW : o.bitsI;
   const double* bv = type ? o.wb : o.ib;
-  const double* av = type ? (phase ? o.fWA : o.WA[li.level]) : (phase ? o.fIA : o.IA[li.level]);
+  const double* av = phase ? o.fWA : o.WA[li.level];  // (r_I is stored by K1)
   extern __shared__ double dsm[];  // sample share [ceil(kMaxSample/CS)] + offs[ntiles + 1]
   constexpr int kShare = (kMaxSample + CS - 1) / CS;
   double* smp_sh = dsm;
@@ -1263,11 +1265,11 @@ __global__ void __launch_bounds__(kTdistClusterThreads, 1)
     for (int u = 0; u < 4; ++u)
       if (ix[u] >= 0) {
         bb[u] = __ldg(bv + ix[u]);
-        aa[u] = __ldg(av + ix[u]);
+        aa[u] = type ? __ldg(av + ix[u]) : 0.0;
       }
 #pragma unroll
     for (int u = 0; u < 4; ++u)
-      if (ix[u] >= 0) smp_sh[k + u * NT] = bb[u] - aa[u];  // r_I = i_b - i_a / r_W = w_b - w_a
+      if (ix[u] >= 0) smp_sh[k + u * NT] = type ? bb[u] - aa[u] : bb[u];  // r_W / r_I (K1)
   }
   smp.kfull = smp.m_local / NT;
   smp.cs = CS;
@@ -1431,7 +1433,6 @@ __global__ void __launch_bounds__(kTPB, RGBID_K3_MINBLOCKS) k_normal_eq(const Sl
   const SlotState& S = st[slot];
   if (!slot_active(S, li.level, phase)) return;
   const SlotIO& o = io[slot];
-  const double* __restrict__ IA = phase ? o.fIA : o.IA[li.level];
   const double* __restrict__ WA = phase ? o.fWA : o.WA[li.level];
   const uint8_t* __restrict__ am = o.amask[li.level];
   const double2* __restrict__ ag = reinterpret_cast<const double2*>(o.agrad[li.level]);
@@ -1455,10 +1456,10 @@ __global__ void __launch_bounds__(kTPB, RGBID_K3_MINBLOCKS) k_normal_eq(const Sl
     // every load of the pixel issued at once (one memory round trip; the
     // validity tests below only select)
     const unsigned a = __ldg(am + k);
-    const double i_b = __ldcs(ibp + k), w_b = __ldcs(wbp + k);
-    const double w_a = __ldg(WA + k), i_a = __ldg(IA + k);
+    const double r_I = __ldcs(ibp + k), w_b = __ldcs(wbp + k);  // r_I = i_b - i_a (K1)
+    const double w_a = __ldg(WA + k);
     const double2 gI = __ldg(ag + 2 * k), gW = __ldg(ag + 2 * k + 1);
-    if (!(a & 1u) || !valid(i_b)) continue;
+    if (!(a & 1u) || !valid(r_I)) continue;  // bit0 implies valid(i_a): valid(r_I) == valid(i_b)
     const int y = k / w, x = k - y * w;
     const double px = x, py = y;
     const double ax = li.cx - px, ay = li.cy - py;  // A(0,2), A(1,2)
@@ -1477,7 +1478,7 @@ __global__ void __launch_bounds__(kTPB, RGBID_K3_MINBLOCKS) k_normal_eq(const Sl
       J[3] = X1 * u2 - X2 * u1;
       J[4] = X2 * u0 - X0 * u2;
       J[5] = X0 * u1 - X1 * u0;
-      const double rI = i_b - i_a;
+      const double rI = r_I;
       const double xi_ = (rI - muI) * isgI;
       const double wi = nuI1 * rcp_fast(fma(xi_, xi_, nuI)) * is2i;
       accum(acc, J, wi, rI);
@@ -1545,7 +1546,6 @@ __global__ void __launch_bounds__(kTPB, RGBID_K3_MMA_MINB) k_normal_eq_mma(const
   const SlotState& S = st[slot];
   if (!slot_active(S, li.level, phase)) return;  // uniform over the CTA
   const SlotIO& o = io[slot];
-  const double* __restrict__ IA = phase ? o.fIA : o.IA[li.level];
   const double* __restrict__ WA = phase ? o.fWA : o.WA[li.level];
   const uint8_t* __restrict__ am = o.amask[li.level];
   const double2* __restrict__ ag = reinterpret_cast<const double2*>(o.agrad[li.level]);
@@ -1580,10 +1580,10 @@ __global__ void __launch_bounds__(kTPB, RGBID_K3_MMA_MINB) k_normal_eq_mma(const
     const bool inr = k0i < N;
     const int k = inr ? k0i : 0;
     const unsigned a = __ldg(am + k);
-    const double i_b = __ldcs(ibp + k), w_b = __ldcs(wbp + k);
-    const double w_a = __ldg(WA + k), i_a = __ldg(IA + k);
+    const double r_I = __ldcs(ibp + k), w_b = __ldcs(wbp + k);  // r_I = i_b - i_a (K1)
+    const double w_a = __ldg(WA + k);
     const double2 gI = __ldg(ag + 2 * k), gW = __ldg(ag + 2 * k + 1);
-    const bool jet = inr && (a & 1u) && valid(i_b);
+    const bool jet = inr && (a & 1u) && valid(r_I);  // bit0 implies valid(i_a)
     const bool dep = jet && (a & 2u) && valid(w_b) && w_b > 0.0;
     const int y = k / w, x = k - y * w;
     const double px = x, py = y;
@@ -1595,7 +1595,7 @@ __global__ void __launch_bounds__(kTPB, RGBID_K3_MMA_MINB) k_normal_eq_mma(const
     {  // photometric row
       const double s0 = w_a * gI.x, s1 = w_a * gI.y;
       const double u0 = s0 * li.fx, u1 = s1 * li.fy, u2 = s0 * ax + s1 * ay;
-      const double rI = i_b - i_a;
+      const double rI = r_I;
       const double xi_ = (rI - muI) * isgI;
       const double wi = nuI1 * rcp_fast(fma(xi_, xi_, nuI)) * is2i;
       double* r = xw + lane * XS;

@@ -60,8 +60,8 @@ struct SlotIO {
   const double* WB;
   double* fIA;                   // bilateral-filtered A (covariance pass)
   double* fWA;
-  double* ib;                    // warped B at the current level (level-size maps)
-  double* wb;
+  double* ib;                    // r_I = warped I_B - I_A at the current level (K1)
+  double* wb;                    // warped W_B at the current level
   uint8_t* amask[kMaxLevels];    // A-side jet validity per level pixel (bit0 photometric, bit1 depth)
   double* agrad[kMaxLevels];     // A-side gradients per level pixel {gI_x, gI_y, gW_x, gW_y}
                                  // (level-0 entries are rebuilt from the filtered A for the
