@@ -343,3 +343,51 @@ def test_frame_decode_bitwise(ctx, orc):
     g = f.download()
     I, W = orc.decode_frame(bgr, depth, 5000.0)
     assert bitwise_equal(g.intensity, I) and bitwise_equal(g.inverse_depth, W)
+
+
+@pytest.mark.parametrize("size,levels", [((97, 71, 70.0), 3), ((320, 240, 240.0), 4)])
+def test_batch_throughput_path_matches_oracle(ctx, orc, size, levels):
+    """> 8 pairs take the throughput path (k_gather + k_tdist<NT> instead of the
+    cluster kernel): each result against the oracle, ragged sizes included."""
+    K = rg.simple_intrinsics(*size)
+    cfg = rg.AlignmentConfig(levels=levels)
+    pairs = [pair(K, 20 + i, "noisy", holes=bool(i % 2)) for i in range(12)]
+    A = [rg.DeviceFrame.from_frame(p[0], ctx) for p in pairs]
+    B = [rg.DeviceFrame.from_frame(p[1], ctx) for p in pairs]
+    out = rg.align_batch(A, B, K, config=cfg, ctx=ctx)
+    checked = 0
+    for (fa, fb, _), r in zip(pairs, out):
+        o = orc.align(fa.intensity, fa.inverse_depth, fb.intensity, fb.inverse_depth, K.to_c(),
+                      None, cfg.to_c())
+        assert (r.status == 1) == (o.status == 1)
+        if o.status == 0:
+            _check_align(rg.rgbid._result_or_raise(r), o)
+            checked += 1
+    assert checked >= 8
+
+
+@pytest.mark.parametrize("size", [(97, 71, 70.0), (333, 251, 250.0)])
+def test_align_ragged_sizes(ctx, orc, size):
+    """Widths/heights that are not multiples of the K1 tiles or of 2^levels."""
+    K = rg.simple_intrinsics(*size)
+    fa, fb, _ = pair(K, 2, "noisy", holes=True)
+    for levels in (3, 4):
+        cfg = rg.AlignmentConfig(levels=levels)
+        o = orc.align(fa.intensity, fa.inverse_depth, fb.intensity, fb.inverse_depth, K.to_c(),
+                      None, cfg.to_c())
+        if o.status == 1:
+            with pytest.raises(rg.DegenerateAlignmentError):
+                rg.align(fa, fb, K, config=cfg, ctx=ctx)
+            continue
+        _check_align(rg.align(fa, fb, K, config=cfg, ctx=ctx), o)
+
+
+def test_align_1280x960(ctx, orc):
+    """A frame 4x VGA: 4800 level-0 K1 tiles, larger scans and shared-memory tables."""
+    K = rg.simple_intrinsics(1280, 960, 960.0)
+    fa, fb, _ = pair(K, 4, "noisy", holes=True)
+    cfg = rg.AlignmentConfig(levels=4)
+    o = orc.align(fa.intensity, fa.inverse_depth, fb.intensity, fb.inverse_depth, K.to_c(), None,
+                  cfg.to_c())
+    assert o.status == 0
+    _check_align(rg.align(fa, fb, K, config=cfg, ctx=ctx), o)
