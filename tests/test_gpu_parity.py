@@ -391,3 +391,33 @@ def test_align_1280x960(ctx, orc):
                   cfg.to_c())
     assert o.status == 0
     _check_align(rg.align(fa, fb, K, config=cfg, ctx=ctx), o)
+
+
+def test_all_hole_inputs(ctx, orc):
+    """Empty inputs (every pixel a hole): align throws like the reference (fewer than
+    6 jets, zero spectrum) on both the single-pair and the batch path; fusion leaves
+    the keyframe untouched; covisibility reports an empty frame."""
+    K = rg.simple_intrinsics(80, 60, 60.0)
+    nan = np.full((60, 80), np.nan)
+    empty = rg.FrameData(nan.copy(), nan.copy())
+    good, fb, _ = pair(K, 3, "noisy")
+    o = orc.align(empty.intensity, empty.inverse_depth, fb.intensity, fb.inverse_depth,
+                  K.to_c(), None, rg.AlignmentConfig().to_c())
+    assert o.status == 1
+    with pytest.raises(rg.DegenerateAlignmentError) as e:
+        rg.align(empty, fb, K, ctx=ctx)
+    assert np.all(np.array(e.value.spectrum) == 0.0)
+    # batch (throughput path): empty pairs fail alone
+    A = [rg.DeviceFrame.from_frame(empty if i % 3 == 0 else good, ctx) for i in range(10)]
+    B = [rg.DeviceFrame.from_frame(fb, ctx) for _ in range(10)]
+    out = rg.align_batch(A, B, K, ctx=ctx)
+    assert [r.status for r in out] == [1 if i % 3 == 0 else 0 for i in range(10)]
+    # fusion with an empty frame: keyframe unchanged (W and C)
+    kf = rg.make_keyframe(good, rg.Pose(), 0, 0.0)
+    W0, C0 = kf.inverse_depth.copy(), kf.weight.copy()
+    rg.integrate_frame(kf, empty, rg.Pose(), K, 0.01, ctx)
+    assert bitwise_equal(kf.inverse_depth, W0) and bitwise_equal(kf.weight, C0)
+    cv = rg.covisibility_ratio(empty, good, rg.Pose(), K, 0.01, ctx)
+    ro, eo, _ = orc.covisibility_ratio(empty.intensity, empty.inverse_depth, good.intensity,
+                                       good.inverse_depth, rg.Pose().to_c(), K.to_c(), 0.01)
+    assert cv.empty_frame and eo and cv.ratio == ro == 0.0
