@@ -78,7 +78,7 @@ __device__ __forceinline__ double bilinear(const double* __restrict__ img, int w
   return (1 - fy) * ((1 - fx) * v00 + fx * v10) + fy * ((1 - fx) * v01 + fx * v11);
 }
 
-// bilinear of I_B and W_B at the same point, sharing the tap setup.
+// bilinear fix-up for the warp's shared-tap evaluation of I_B and W_B.
 // Fast path: the interpolation formula is evaluated directly; it is finite only
 // if all four taps are finite (NaN/inf taps propagate through the products and
 // sums, including 0 * inf), so the explicit tap checks of inc/image.hpp:59 are
@@ -87,24 +87,6 @@ __device__ __forceinline__ double bilinear(const double* __restrict__ img, int w
 __device__ __forceinline__ double bilin_fix(double r, double a, double b, double c, double d) {
   if (isfinite(r)) return r;
   return (valid(a) && valid(b) && valid(c) && valid(d)) ? r : CUDART_NAN;
-}
-__device__ __forceinline__ void bilinear2(const double* __restrict__ I, const double* __restrict__ W,
-                                          int w, int h, double x, double y, double& oi,
-                                          double& ow) {
-  oi = CUDART_NAN;
-  ow = CUDART_NAN;
-  if (!(x >= 0.0 && x <= w - 1.0 && y >= 0.0 && y <= h - 1.0)) return;
-  const int x0 = (int)floor(x), y0 = (int)floor(y);
-  const int dx = x0 + 1 < w ? 1 : 0;        // x1 = min(x0 + 1, w - 1)
-  const int dy = y0 + 1 < h ? w : 0;        // y1 = min(y0 + 1, h - 1)
-  const double fx = x - x0, fy = y - y0, gx = 1 - fx, gy = 1 - fy;
-  const int i00 = y0 * w + x0;
-  const double a00 = __ldg(I + i00), a10 = __ldg(I + i00 + dx), a01 = __ldg(I + i00 + dy),
-               a11 = __ldg(I + i00 + dy + dx);
-  const double b00 = __ldg(W + i00), b10 = __ldg(W + i00 + dx), b01 = __ldg(W + i00 + dy),
-               b11 = __ldg(W + i00 + dy + dx);
-  oi = bilin_fix(gy * (gx * a00 + fx * a10) + fy * (gx * a01 + fx * a11), a00, a10, a01, a11);
-  ow = bilin_fix(gy * (gx * b00 + fx * b10) + fy * (gx * b01 + fx * b11), b00, b10, b01, b11);
 }
 
 // one A pixel of inverse_geometric_warp — src/warping.cpp:96-111 (bit-identical).
@@ -178,15 +160,6 @@ __device__ __forceinline__ bool gradient_at(const double* img, int w, int h, int
   return true;
 }
 
-__device__ __forceinline__ bool gradient_ok(const double* img, int w, int h, int x, int y) {
-  if (!valid(px_or_nan(img, w, h, x, y))) return false;
-  if (!valid(px_or_nan(img, w, h, x - 1, y)) && !valid(px_or_nan(img, w, h, x + 1, y)))
-    return false;
-  if (!valid(px_or_nan(img, w, h, x, y - 1)) && !valid(px_or_nan(img, w, h, x, y + 1)))
-    return false;
-  return true;
-}
-
 // 2x2 NaN-aware mean — inc/image.hpp:73-91 (tap order (0,0),(1,0),(0,1),(1,1))
 __device__ __forceinline__ double ds4(double a, double b, double c, double d) {
   double sum = 0.0;
@@ -196,19 +169,6 @@ __device__ __forceinline__ double ds4(double a, double b, double c, double d) {
   if (valid(c)) sum += c, ++n;
   if (valid(d)) sum += d, ++n;
   return n > 0 ? sum / n : CUDART_NAN;
-}
-
-__device__ __forceinline__ void load_wm(const WarpMats& g, WarpMats& m) {
-#pragma unroll
-  for (int i = 0; i < 9; ++i) {
-    m.Rt_BA[i] = g.Rt_BA[i];
-    m.Rt_AB[i] = g.Rt_AB[i];
-  }
-#pragma unroll
-  for (int i = 0; i < 3; ++i) {
-    m.tt_BA[i] = g.tt_BA[i];
-    m.tt_AB[i] = g.tt_AB[i];
-  }
 }
 
 // ---------------------------------------------------------------------------
