@@ -2,16 +2,22 @@
 // src/alignment.cpp:367-436, src/warping.cpp:76-114, inc/image.hpp:51-91).
 //
 // Per IRLS iteration (one launch each, all slots of a batch at once):
-//   K1 k_warp_residuals  warp full-res B by T (src/warping.cpp:94-112), stage it
-//                        in smem, downsample to the level (src/alignment.cpp:355-363),
-//                        residual validity (src/alignment.cpp:206-227) and row-major
-//                        compaction of r_I / r_W per tile (systematic-sample ranks).
-//   K2 k_tdist           gather the systematic sample (src/alignment.cpp:50-57) and
-//                        run the Student-t chain (src/alignment.cpp:61-157,288-320).
-//   K3 k_normal_eq       recompute jets (src/alignment.cpp:212-244), robust weights
-//                        and the 21+6+1 fp64 sums (src/alignment.cpp:321-335).
-//   K4 k_solve           fixed-order reduce, rank test, LDLT, SE(3) update, convergence
+//   K1  k_warp_residuals(_l0)  warp full-res B by T (src/warping.cpp:94-112),
+//                        downsample to the level (src/alignment.cpp:355-363),
+//                        store r_I = i_b - i_a and w_b, residual validity
+//                        (src/alignment.cpp:206-227) as row-major per-tile ballots.
+//   K2a k_gather         the systematic sample (src/alignment.cpp:50-57) from the
+//                        ballots, compacted in global memory (batches).
+//   K2b k_tdist<NT>      the Student-t chain (src/alignment.cpp:61-157,288-320) on
+//                        the compact sample in shared memory; k_tdist_cluster does
+//                        K2a+K2b for <= 8 pairs over an 8-CTA cluster (latency mode).
+//   K3  k_normal_eq_mma  jets (src/alignment.cpp:212-244), robust weights and the
+//                        21+6+1 fp64 sums (src/alignment.cpp:321-335) on the FP64
+//                        tensor cores (k_normal_eq: the FMA version).
+//   K4  k_solve          fixed-order reduce, rank test, LDLT, SE(3) update, convergence
 //                        (src/alignment.cpp:387-401) — no host round trip.
+// Once per align: k_pyramid_slots, k_prep_A (A-side validity + gradients); the
+// covariance pass adds k_bilateral_slots and k_covariance.
 // Compiled with --fmad=false: mask-deciding arithmetic rounds exactly like the
 // reference; reductions use a fixed tree (bit-reproducible run to run).
 #include <cooperative_groups.h>
