@@ -471,7 +471,7 @@ def main():
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e = {"value": pairs_total(args, world) * e2e_steps / (float(t.item()) / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": h2d // e2e_steps, "d2h_bytes_per_step": d2h // e2e_steps,
-               "path": "rgbid_align_batch_host (C-ABI) from pinned host buffers, 2 lanes x chunks of 1024; "
+               "path": "rgbid_align_batch_host (C-ABI) from pinned host buffers, 2 lanes x chunks of 512; "
                        f"host pool of {P} distinct pairs cycled"}
 
     cpu = None
