@@ -175,16 +175,19 @@ class ClockSampler:
 
 
 def host_pairs(n, variant, seed0=0):
-    """Host-rendered pairs of the same scene model (tests/scenes.py, noisy variant
-    = I+N(0,.005), W+N(0,.002), 20% near occluder)."""
+    """The benchmark's pairs seed0..seed0+n-1 rendered on the host
+    (rgbid_synth_pair_host: the same scene model and generator as the device
+    rendering of the timed arm, host libm)."""
+    from concurrent.futures import ThreadPoolExecutor
     import paper_1807_08271_b200 as rg
-    from tests.scenes import pair
     K = rg.simple_intrinsics(W0, H0, F0)
-    out = []
-    for i in range(n):
-        fa, fb, _ = pair(K, seed0 + i, "noisy" if variant else "clean")
-        out.append((fa.intensity, fa.inverse_depth, fb.intensity, fb.inverse_depth))
-    return K, out
+
+    def one(i):
+        fa, fb, _ = rg.synth_pair_host(K, seed0 + i, variant)
+        return (fa.intensity, fa.inverse_depth, fb.intensity, fb.inverse_depth)
+
+    with ThreadPoolExecutor(max_workers=os.cpu_count() or 1) as ex:
+        return K, list(ex.map(one, range(n)))
 
 
 def cpu_reference_rate(pairs, K, cores):
@@ -216,9 +219,10 @@ def run_reference(args, rank, world):
             vals.append((rate, dt))
     rate = statistics.median(v[0] for v in vals)
     ms = statistics.median(v[1] for v in vals) * 1000.0
-    sample = (f"{n} host-rendered 640x480 pairs (same scene model, "
-              f"{'noisy+occluder' if args.variant else 'clean'}) per step, 4-level align on "
-              f"{cores} threads, one pair per thread at a time")
+    sample = (f"the benchmark's first {n} 640x480 pairs "
+              f"({'noisy+occluder' if args.variant else 'clean'}), rendered on the host by the "
+              f"same generator, per step; 4-level align + covariance on {cores} threads, one "
+              f"pair per thread at a time")
     line = {
         "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
@@ -476,18 +480,24 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
+        # the reference arm's measurement, in a clean process (this one holds a CUDA
+        # context, torch threads and pinned pools that slow a host-thread sweep ~1.5x):
+        # the benchmark's first n pairs from the same generator, rendered on the host
         cores = os.cpu_count() or 1
         n = args.cpu_sample or max(8, cores)
-        hp = []
-        for i in range(n):  # identical inputs: the first n device-rendered pairs
-            fa, fb = A[i].download(), B[i].download()
-            hp.append((fa.intensity, fa.inverse_depth, fb.intensity, fb.inverse_depth))
-        cpu_reference_rate(hp, K, cores)  # untimed warm-up (first-touch allocations)
-        rate, dt, kind, ok = cpu_reference_rate(hp, K, cores)
-        cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": kind,
-               "sample": f"first {n} of the benchmark's pairs (identical inputs), 4-level align "
-                         f"+ covariance on {cores} host threads, {dt:.1f} s wall after one "
-                         f"untimed warm-up run"}
+        env = {k: v for k, v in os.environ.items()
+               if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK", "LOCAL_WORLD_SIZE")}
+        pr = subprocess.run([sys.executable, os.path.abspath(__file__), "--impl", "reference",
+                             "--steps", "1", "--warmup", "1", "--cpu-sample", str(n),
+                             "--variant", str(args.variant)],
+                            env=env, capture_output=True, text=True, timeout=900)
+        try:
+            ref = json.loads(pr.stdout.strip().splitlines()[-1])
+            cpu = dict(ref["cpu_baseline"])
+            cpu["sample"] += " (bench.py --impl reference in a subprocess)"
+        except (IndexError, KeyError, ValueError):
+            cpu = {"value": None, "unit": UNIT, "cores": cores, "kind": "reference",
+                   "sample": "reference subprocess failed: " + pr.stderr.strip()[-200:]}
 
     if rank == 0:
         line = {

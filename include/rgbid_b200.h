@@ -366,6 +366,10 @@ int rgbid_synth_add_noise(double* I, double* W, int width, int height, uint32_t 
 int rgbid_synth_pair_device(rgbid_ctx* ctx, rgbid_frame* a, rgbid_frame* b,
                             const rgbid_intrinsics* K, uint32_t pair_seed, int variant,
                             rgbid_pose* T_AB_truth);
+/* The same pair on the host (host libm: equal to the device rendering up to the
+ * last bits of sin/cos/log): the reference arm's inputs, generated without the GPU. */
+int rgbid_synth_pair_host(const rgbid_intrinsics* K, uint32_t pair_seed, int variant, double* I_A,
+                          double* W_A, double* I_B, double* W_B, rgbid_pose* T_AB_truth);
 
 #ifdef __cplusplus
 }

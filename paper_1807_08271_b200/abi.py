@@ -196,6 +196,8 @@ EXPORTS = [
                                         C.c_double]),
     ("rgbid_synth_pair_device", C.c_int, [VP, VP, VP, C.POINTER(Intrinsics_t), C.c_uint32,
                                           C.c_int, C.POINTER(Pose_t)]),
+    ("rgbid_synth_pair_host", C.c_int, [C.POINTER(Intrinsics_t), C.c_uint32, C.c_int, DP, DP,
+                                        DP, DP, C.POINTER(Pose_t)]),
 ]
 
 _lib = None

@@ -1361,12 +1361,79 @@ int rgbid_forward_register(rgbid_ctx* ctx, const double* WA, int w, int h, const
   return RGBID_OK;
 }
 
+namespace {
+void synth_pair_views(const rgbid_intrinsics* K, uint32_t pair_seed, int variant, SynthView* va,
+                      SynthView* vb, rgbid_pose* T_AB_truth);
+}  // namespace
+
 int rgbid_synth_pair_device(rgbid_ctx* ctx, rgbid_frame* a, rgbid_frame* b,
                             const rgbid_intrinsics* K, uint32_t pair_seed, int variant,
                             rgbid_pose* T_AB_truth) {
-  if (!ctx || !a || !b || !K) return RGBID_E_ARG;
+  if (!ctx || !a || !b || !K || a->w != K->width || a->h != K->height || b->w != a->w ||
+      b->h != a->h)
+    return RGBID_E_ARG;
   LaunchScope ls(ctx);
   // Pair geometry: A at a small random pose, B = A * random_pose(seed, 3 mm, 0.02 rad)
+  SynthView va, vb;
+  synth_pair_views(K, pair_seed, variant, &va, &vb, T_AB_truth);
+  launch_render(va, a->I, a->W, ctx->stream);
+  launch_render(vb, b->I, b->W, ctx->stream);
+  a->pyr_levels = 0;
+  b->pyr_levels = 0;
+  int rc = check_launch(ctx);
+  if (rc) return rc;
+  CK(cudaStreamSynchronize(ctx->stream));
+  return RGBID_OK;
+}
+
+namespace {
+// host restatement of fusion_kernels.cu's k_render (plane_texture_d, splitmix/Box-Muller)
+double plane_texture_h(double x, double y) {
+  return 0.5 + 0.2 * std::sin(7.3 * x) * std::cos(5.9 * y) + 0.15 * std::sin(3.1 * x + 2.7 * y) +
+         0.1 * std::cos(11.0 * x - 4.0 * y);
+}
+unsigned long long splitmix_h(unsigned long long z) {
+  z += 0x9e3779b97f4a7c15ull;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+double gauss_h(unsigned long long key) {
+  const unsigned long long a = splitmix_h(key), b = splitmix_h(key ^ 0xda3e39cb94b95bdbull);
+  const double u1 = ((a >> 11) + 0.5) * (1.0 / 9007199254740992.0);
+  const double u2 = ((b >> 11) + 0.5) * (1.0 / 9007199254740992.0);
+  return std::sqrt(-2.0 * std::log(u1)) * std::cos(6.283185307179586 * u2);
+}
+void render_h(const SynthView& v, double* I, double* W) {
+  for (int i = 0; i < v.w * v.h; ++i) {
+    const int y = i / v.w, x = i - y * v.w;
+    const V3 p = {{(double)x, (double)y, 1.0}};
+    const V3 kp = m3_mulv(v.Kinv, p);
+    const V3 r = m3_mulv(v.R, kp);
+    const double denom = red3(v.n[0] * r.v[0], v.n[1] * r.v[1], v.n[2] * r.v[2]);
+    double iv = std::nan(""), wv = std::nan("");
+    if (std::fabs(denom) >= 1e-12) {
+      const double lambda = -(red3(v.n[0] * v.t[0], v.n[1] * v.t[1], v.n[2] * v.t[2]) + v.d) / denom;
+      if (lambda > 0.05) {
+        const double X = v.t[0] + lambda * r.v[0], Y = v.t[1] + lambda * r.v[1];
+        iv = plane_texture_h(v.tex_scale * X, v.tex_scale * Y);
+        wv = 1.0 / lambda;
+      }
+    }
+    if (v.noise_i > 0.0 && std::isfinite(iv)) iv += v.noise_i * gauss_h(v.seed * 0x100000000ull + 2ull * i);
+    if (v.noise_w > 0.0 && std::isfinite(wv))
+      wv += v.noise_w * gauss_h(v.seed * 0x100000000ull + 2ull * i + 1);
+    if (v.occluder && x < v.w / 5) {
+      iv = plane_texture_h(7.0 + 0.1 * x * 80.0 / v.w, 3.0 + 0.1 * y * 80.0 / v.w);
+      wv = 1.0;
+    }
+    I[i] = iv;
+    W[i] = wv;
+  }
+}
+// the pair geometry and views of rgbid_synth_pair_device
+void synth_pair_views(const rgbid_intrinsics* K, uint32_t pair_seed, int variant, SynthView* va,
+                      SynthView* vb, rgbid_pose* T_AB_truth) {
   rgbid_pose pa, pab;
   rgbid_synth_random_pose(5000u + pair_seed, 0, 0.01, 0.01, &pa);
   rgbid_synth_random_pose(1000u + pair_seed, 0, 0.003, 0.02, &pab);
@@ -1376,10 +1443,10 @@ int rgbid_synth_pair_device(rgbid_ctx* ctx, rgbid_frame* a, rgbid_frame* b,
   double n[3] = {0.2, -0.15, 1.0};
   const double nn = std::sqrt(red3(n[0] * n[0], n[1] * n[1], n[2] * n[2]));
   for (double& v : n) v /= nn;
-  auto view = [&](const PoseD& T, int noisy, unsigned long long seed) {
+  auto view = [&](const PoseD& T, unsigned long long seed) {
     SynthView v;
-    v.w = a->w;
-    v.h = a->h;
+    v.w = K->width;
+    v.h = K->height;
     v.Kinv = m3_inv(K_mat(K->fx, K->fy, K->cx, K->cy));
     v.R = T.R;
     for (int i = 0; i < 3; ++i) {
@@ -1387,22 +1454,26 @@ int rgbid_synth_pair_device(rgbid_ctx* ctx, rgbid_frame* a, rgbid_frame* b,
       v.n[i] = n[i];
     }
     v.d = -2.0;
-    v.tex_scale = a->w / 80.0;
-    v.noise_i = noisy ? 0.005 : 0.0;
-    v.noise_w = noisy ? 0.002 : 0.0;
+    v.tex_scale = K->width / 80.0;
+    v.noise_i = variant ? 0.005 : 0.0;
+    v.noise_w = variant ? 0.002 : 0.0;
     v.seed = seed;
     v.occluder = 0;
     return v;
   };
-  SynthView va = view(TA, variant, 2u * pair_seed + 1), vb = view(TB, variant, 2u * pair_seed + 2);
-  vb.occluder = variant ? 1 : 0;
-  launch_render(va, a->I, a->W, ctx->stream);
-  launch_render(vb, b->I, b->W, ctx->stream);
-  a->pyr_levels = 0;
-  b->pyr_levels = 0;
-  int rc = check_launch(ctx);
-  if (rc) return rc;
-  CK(cudaStreamSynchronize(ctx->stream));
+  *va = view(TA, 2u * pair_seed + 1);
+  *vb = view(TB, 2u * pair_seed + 2);
+  vb->occluder = variant ? 1 : 0;
+}
+}  // namespace
+
+int rgbid_synth_pair_host(const rgbid_intrinsics* K, uint32_t pair_seed, int variant, double* IA,
+                          double* WA, double* IB, double* WB, rgbid_pose* T_AB_truth) {
+  if (!K || !IA || !WA || !IB || !WB || K->width <= 0 || K->height <= 0) return RGBID_E_ARG;
+  SynthView va, vb;
+  synth_pair_views(K, pair_seed, variant, &va, &vb, T_AB_truth);
+  render_h(va, IA, WA);
+  render_h(vb, IB, WB);
   return RGBID_OK;
 }
 

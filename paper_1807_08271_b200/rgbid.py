@@ -687,6 +687,19 @@ def random_pose(seed: int, t_scale: float = 1.0, angle_scale: float = 1.0, skip:
     return Pose.from_c(out)
 
 
+def synth_pair_host(K: Intrinsics, pair_seed: int, variant: int = 1):
+    """Pair `pair_seed` of the bench's synthetic workload (rgbid_synth_pair_device's
+    scene model) rendered on the host: (frame_a, frame_b, T_AB_truth)."""
+    h, w = K.height, K.width
+    IA, WA, IB, WB = (np.empty((h, w)) for _ in range(4))
+    T = abi.Pose_t()
+    rc = abi.lib().rgbid_synth_pair_host(C.byref(K.to_c()), pair_seed, variant, dptr(IA), dptr(WA),
+                                         dptr(IB), dptr(WB), C.byref(T))
+    if rc != abi.OK:
+        raise ValueError("synth_pair_host: invalid argument")
+    return FrameData(IA, WA), FrameData(IB, WB), Pose.from_c(T)
+
+
 def add_noise(frame: FrameData, seed: int, sigma_i: float, sigma_w: float) -> FrameData:
     f = frame.copy()
     h, w = f.inverse_depth.shape

@@ -421,3 +421,18 @@ def test_all_hole_inputs(ctx, orc):
     ro, eo, _ = orc.covisibility_ratio(empty.intensity, empty.inverse_depth, good.intensity,
                                        good.inverse_depth, rg.Pose().to_c(), K.to_c(), 0.01)
     assert cv.empty_frame and eo and cv.ratio == ro == 0.0
+
+
+def test_synth_pair_host_equals_device(ctx):
+    """The reference arm renders the benchmark's pairs on the host; they equal the
+    device rendering of the timed arm up to host-vs-device libm rounding."""
+    K = rg.simple_intrinsics(640, 480, 480.0)
+    for seed in (0, 7):
+        A, B = rg.DeviceFrame(640, 480, ctx), rg.DeviceFrame(640, 480, ctx)
+        rg.synth_pair_device(A, B, K, seed, 1)
+        ha, hb, _ = rg.synth_pair_host(K, seed, 1)
+        for d, h in ((A.download(), ha), (B.download(), hb)):
+            for x, y in ((d.intensity, h.intensity), (d.inverse_depth, h.inverse_depth)):
+                assert np.array_equal(np.isnan(x), np.isnan(y))
+                m = ~np.isnan(x)
+                assert np.abs(x[m] - y[m]).max() <= 1e-12

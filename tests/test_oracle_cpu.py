@@ -244,3 +244,15 @@ def test_backend_oracles_sane(R_):
     assert m.sum() <= len(p0) < 1.2 * m.sum()
     pv, cv = map_oracle.export_map(kfs, K.to_c(), 0.1)
     assert 0 < len(pv) < len(p0) and cv.dtype == np.uint8
+
+
+def test_synth_pair_host_deterministic():
+    """The reference arm's input generator (host, no GPU): same seed -> same pair,
+    different seeds -> different noise; holes only where the plane is not visible."""
+    K = rg.simple_intrinsics(80, 60, 60.0)
+    a1, b1, T1 = rg.synth_pair_host(K, 3, 1)
+    a2, b2, T2 = rg.synth_pair_host(K, 3, 1)
+    a3, _, _ = rg.synth_pair_host(K, 4, 1)
+    assert bitwise_equal(a1.intensity, a2.intensity) and bitwise_equal(b1.inverse_depth, b2.inverse_depth)
+    assert not np.array_equal(a1.intensity, a3.intensity)
+    assert np.isfinite(a1.inverse_depth).all() and (b1.inverse_depth[:, : 80 // 5] == 1.0).all()
