@@ -206,10 +206,27 @@ __global__ void k_voxel_average(const unsigned long long* __restrict__ skey,
 
 inline unsigned blocks(long long n, int t) { return (unsigned)((n + t - 1) / t); }
 
-template <typename T>
-cudaError_t alloc(T** p, size_t count, cudaStream_t s) {
-  return cudaMallocAsync(reinterpret_cast<void**>(p), sizeof(T) * (count ? count : 1), s);
-}
+// stream-ordered temporaries of one export_map call, freed on every exit path
+struct AsyncPool {
+  cudaStream_t s;
+  void* p[16] = {};
+  int n = 0;
+  explicit AsyncPool(cudaStream_t st) : s(st) {}
+  ~AsyncPool() {
+    for (int i = 0; i < n; ++i)
+      if (p[i]) cudaFreeAsync(p[i], s);
+  }
+  template <typename T>
+  cudaError_t alloc(T** out, size_t count) {
+    const cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(out), sizeof(T) * (count ? count : 1), s);
+    if (e == cudaSuccess) p[n++] = *out;
+    return e;
+  }
+  void release(const void* q) {  // keep q (handed to the caller)
+    for (int i = 0; i < n; ++i)
+      if (p[i] == q) p[i] = nullptr;
+  }
+};
 
 cudaError_t exclusive_sum(const int* in, int* out, long long n, cudaStream_t s) {
   size_t tmp = 0;
@@ -234,6 +251,7 @@ void launch_normal_map(const double* W, int w, int h, const M3& Km, double* nx, 
 int export_map_device(const ExportKF* kfs, int n_kf, int w, int h, const M3& Kinv, double voxel,
                       cudaStream_t s, double** d_points, uint8_t** d_colors, long long* count) {
   const long long N = (long long)w * h, T = N * n_kf;
+  AsyncPool pool(s);
   int *flag = nullptr, *pos = nullptr;
   double* pts = nullptr;
   uint8_t* col = nullptr;
@@ -243,10 +261,10 @@ int export_map_device(const ExportKF* kfs, int n_kf, int w, int h, const M3& Kin
     e = (x);            \
     if (e) return (int)e; \
   } while (0)
-  EX_CK(alloc(&flag, T, s));
-  EX_CK(alloc(&pos, T, s));
-  EX_CK(alloc(&pts, 3 * T, s));
-  EX_CK(alloc(&col, 3 * T, s));
+  EX_CK(pool.alloc(&flag, T));
+  EX_CK(pool.alloc(&pos, T));
+  EX_CK(pool.alloc(&pts, 3 * T));
+  EX_CK(pool.alloc(&col, 3 * T));
   for (int k = 0; k < n_kf; ++k) {
     KScope ks_("export_points", s);
     k_export_points<<<blocks(N, 256), 256, 0, s>>>(kfs[k], w, h, Kinv, flag + k * N,
@@ -261,18 +279,16 @@ int export_map_device(const ExportKF* kfs, int n_kf, int w, int h, const M3& Kin
   const long long n = (long long)last_pos + last_flag;
   double* cpts = nullptr;
   uint8_t* ccol = nullptr;
-  EX_CK(alloc(&cpts, 3 * n, s));
-  EX_CK(alloc(&ccol, 3 * n, s));
+  EX_CK(pool.alloc(&cpts, 3 * n));
+  EX_CK(pool.alloc(&ccol, 3 * n));
   {
     KScope ks_("export_compact", s);
     k_compact<<<blocks(T, 256), 256, 0, s>>>(flag, pos, T, pts, col, cpts, ccol);
   }
   EX_CK(cudaGetLastError());
-  cudaFreeAsync(flag, s);
-  cudaFreeAsync(pos, s);
-  cudaFreeAsync(pts, s);
-  cudaFreeAsync(col, s);
   if (voxel <= 0.0 || n == 0) {
+    pool.release(cpts);
+    pool.release(ccol);
     *d_points = cpts;
     *d_colors = ccol;
     *count = n;
@@ -281,13 +297,13 @@ int export_map_device(const ExportKF* kfs, int n_kf, int w, int h, const M3& Kin
   // voxel filter — src/pipeline.cpp:502-527
   unsigned long long *key = nullptr, *skey = nullptr;
   int *idx = nullptr, *sidx = nullptr, *head = nullptr, *first = nullptr, *opos = nullptr;
-  EX_CK(alloc(&key, n, s));
-  EX_CK(alloc(&skey, n, s));
-  EX_CK(alloc(&idx, n, s));
-  EX_CK(alloc(&sidx, n, s));
-  EX_CK(alloc(&head, n, s));
-  EX_CK(alloc(&first, n, s));
-  EX_CK(alloc(&opos, n, s));
+  EX_CK(pool.alloc(&key, n));
+  EX_CK(pool.alloc(&skey, n));
+  EX_CK(pool.alloc(&idx, n));
+  EX_CK(pool.alloc(&sidx, n));
+  EX_CK(pool.alloc(&head, n));
+  EX_CK(pool.alloc(&first, n));
+  EX_CK(pool.alloc(&opos, n));
   EX_CK(cudaMemsetAsync(first, 0, sizeof(int) * n, s));
   {
     KScope ks_("voxel_keys", s);
@@ -296,9 +312,8 @@ int export_map_device(const ExportKF* kfs, int n_kf, int w, int h, const M3& Kin
   size_t tmp = 0;
   EX_CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, key, skey, idx, sidx, (int)n, 0, 64, s));
   void* t = nullptr;
-  EX_CK(cudaMallocAsync(&t, tmp ? tmp : 1, s));
+  EX_CK(pool.alloc(reinterpret_cast<char**>(&t), tmp));
   EX_CK(cub::DeviceRadixSort::SortPairs(t, tmp, key, skey, idx, sidx, (int)n, 0, 64, s));  // stable
-  cudaFreeAsync(t, s);
   {
     KScope ks_("voxel_heads", s);
     k_voxel_heads<<<blocks(n, 256), 256, 0, s>>>(skey, sidx, n, head, first);
@@ -312,17 +327,16 @@ int export_map_device(const ExportKF* kfs, int n_kf, int w, int h, const M3& Kin
   const long long nv = (long long)lp + lf;
   double* vpts = nullptr;
   uint8_t* vcol = nullptr;
-  EX_CK(alloc(&vpts, 3 * nv, s));
-  EX_CK(alloc(&vcol, 3 * nv, s));
+  EX_CK(pool.alloc(&vpts, 3 * nv));
+  EX_CK(pool.alloc(&vcol, 3 * nv));
   {
     KScope ks_("voxel_average", s);
     k_voxel_average<<<blocks(n, 256), 256, 0, s>>>(skey, sidx, head, opos, n, cpts, ccol, vpts,
                                                    vcol);
   }
   EX_CK(cudaGetLastError());
-  for (void* p : {(void*)key, (void*)skey, (void*)idx, (void*)sidx, (void*)head, (void*)first,
-                  (void*)opos, (void*)cpts, (void*)ccol})
-    cudaFreeAsync(p, s);
+  pool.release(vpts);
+  pool.release(vcol);
 #undef EX_CK
   *d_points = vpts;
   *d_colors = vcol;
