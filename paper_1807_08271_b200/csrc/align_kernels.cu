@@ -1289,10 +1289,12 @@ int init_kernel_attributes() {
       cudaFuncSetAttribute(k_tdist<kTdistThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            kMaxSample * 8);
   // the smaller CTAs serve sample caps up to kMaxSample / 2 (256) and / 4 (128)
-  cudaFuncSetAttribute(k_tdist<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       kMaxSample / 2 * 8);
-  cudaFuncSetAttribute(k_tdist<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       kMaxSample / 4 * 8);
+  if (kTdistThreads != 256)
+    cudaFuncSetAttribute(k_tdist<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kMaxSample / 2 * 8);
+  if (kTdistThreads != 128)
+    cudaFuncSetAttribute(k_tdist<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kMaxSample / 4 * 8);
   cudaFuncSetAttribute(k_gather, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
   const cudaError_t e2 =
       cudaFuncSetAttribute(k_tdist_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
