@@ -449,33 +449,40 @@ def main():
                 fb.inverse_depth
         ptrs = [[pn[i % P, k].ctypes.data_as(abi.DP) for i in range(n_local)] for k in range(4)]
         arrs = [(abi.DP * n_local)(*p) for p in ptrs]
-        res = (abi.AlignResult_t * n_local)()
+        res = [(abi.AlignResult_t * n_local)() for _ in range(2)]
         cfg_c, K_c = cfg.to_c(), K.to_c()
 
-        def e2e_step():
-            ctx.check(ctx.lib.rgbid_align_batch_host(ctx.h, n_local, *arrs, W0, H0, C.byref(K_c),
-                                                     None, C.byref(cfg_c), 512, res),
-                      "align_batch_host")
+        def e2e_step(k):
+            # streaming form: step k's first uploads overlap step k-1's last chunks;
+            # results alternate between two arrays (step k-1's finish during step k)
+            ctx.check(ctx.lib.rgbid_align_batch_host_async(ctx.h, n_local, *arrs, W0, H0,
+                                                           C.byref(K_c), None, C.byref(cfg_c),
+                                                           512, res[k % 2]),
+                      "align_batch_host_async")
 
-        e2e_step()
+        e2e_step(0)
+        ctx.check(ctx.lib.rgbid_align_batch_host_wait(ctx.h), "align_batch_host_wait")
         ctx.reset_stats()
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        e2e_steps = max(1, min(args.steps, 2))
-        for _ in range(e2e_steps):
-            e2e_step()
+        e2e_steps = max(1, min(args.steps, 3))
+        for k in range(e2e_steps):
+            e2e_step(k)
+        ctx.check(ctx.lib.rgbid_align_batch_host_wait(ctx.h), "align_batch_host_wait")
         e1.record(stream)
         torch.cuda.synchronize()
+        assert all(r.status in (0, 1) for r in res[(e2e_steps - 1) % 2])
         h2d, d2h = ctx.transfer_bytes()
         t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
         if world > 1:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e = {"value": pairs_total(args, world) * e2e_steps / (float(t.item()) / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": h2d // e2e_steps, "d2h_bytes_per_step": d2h // e2e_steps,
-               "path": "rgbid_align_batch_host (C-ABI) from pinned host buffers, 2 lanes x chunks of 512; "
+               "path": "rgbid_align_batch_host_async/_wait (C-ABI) from pinned host buffers, 2 lanes "
+                       "x chunks of 512, consecutive steps streamed; "
                        f"host pool of {P} distinct pairs cycled"}
 
     cpu = None

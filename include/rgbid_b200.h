@@ -200,6 +200,20 @@ int rgbid_align_batch_host(rgbid_ctx* ctx, int n, const double* const* I_A,
                            const rgbid_intrinsics* K, const rgbid_pose* inits,
                            const rgbid_align_config* cfg, int chunk,
                            rgbid_align_result* results);
+/* Streaming form of rgbid_align_batch_host: returns once every chunk is enqueued;
+ * the last chunks (one per stream) may still be running, and their entries of
+ * `results` (and the host buffers they read) must stay valid until the next
+ * rgbid_align_batch_host_async / rgbid_align_batch_host call on ctx, or until
+ * rgbid_align_batch_host_wait.  Consecutive calls overlap one batch's first
+ * uploads with the previous batch's last chunks. */
+int rgbid_align_batch_host_async(rgbid_ctx* ctx, int n, const double* const* I_A,
+                                 const double* const* W_A, const double* const* I_B,
+                                 const double* const* W_B, int width, int height,
+                                 const rgbid_intrinsics* K, const rgbid_pose* inits,
+                                 const rgbid_align_config* cfg, int chunk,
+                                 rgbid_align_result* results);
+/* Completes every chunk a previous async call left in flight (results written). */
+int rgbid_align_batch_host_wait(rgbid_ctx* ctx);
 
 /* Mat6 filtered_hessian_covariance(a, b, K, T_AB, config, &degenerate) — src/alignment.cpp:411-436 */
 int rgbid_filtered_hessian_covariance(rgbid_ctx* ctx, const rgbid_frame* a, const rgbid_frame* b,

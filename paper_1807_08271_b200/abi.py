@@ -137,6 +137,12 @@ EXPORTS = [
                                          C.POINTER(Intrinsics_t), C.POINTER(Pose_t),
                                          C.POINTER(AlignConfig_t), C.c_int,
                                          C.POINTER(AlignResult_t)]),
+    ("rgbid_align_batch_host_async", C.c_int, [VP, C.c_int, C.POINTER(DP), C.POINTER(DP),
+                                               C.POINTER(DP), C.POINTER(DP), C.c_int, C.c_int,
+                                               C.POINTER(Intrinsics_t), C.POINTER(Pose_t),
+                                               C.POINTER(AlignConfig_t), C.c_int,
+                                               C.POINTER(AlignResult_t)]),
+    ("rgbid_align_batch_host_wait", C.c_int, [VP]),
     ("rgbid_filtered_hessian_covariance", C.c_int, [VP, VP, VP, C.POINTER(Intrinsics_t),
                                                     C.POINTER(Pose_t), C.POINTER(AlignConfig_t),
                                                     DP, C.POINTER(C.c_int)]),

@@ -1005,11 +1005,15 @@ int rgbid_align_batch(rgbid_ctx* ctx, int n, const rgbid_frame* const* a,
   return RGBID_OK;
 }
 
-int rgbid_align_batch_host(rgbid_ctx* ctx, int n, const double* const* IA,
-                           const double* const* WA, const double* const* IB,
-                           const double* const* WB, int w, int h, const rgbid_intrinsics* K,
-                           const rgbid_pose* inits, const rgbid_align_config* cfg, int chunk,
-                           rgbid_align_result* results) {
+// Enqueues the uploads and alignments of one host batch; the lanes' last chunks
+// may still be in flight on return (their results are written by finish_chunk:
+// when the lane is next reused, or by rgbid_align_batch_host_wait).
+static int align_batch_host_enqueue(rgbid_ctx* ctx, int n, const double* const* IA,
+                                    const double* const* WA, const double* const* IB,
+                                    const double* const* WB, int w, int h,
+                                    const rgbid_intrinsics* K, const rgbid_pose* inits,
+                                    const rgbid_align_config* cfg, int chunk,
+                                    rgbid_align_result* results) {
   if (!ctx || n < 0 || !K || (n > 0 && (!IA || !WA || !IB || !WB || !results)))
     return RGBID_E_ARG;
   if (n == 0) return RGBID_OK;
@@ -1062,11 +1066,37 @@ int rgbid_align_batch_host(rgbid_ctx* ctx, int n, const double* const* IA,
                        inits ? inits + i0 : nullptr, c, results + i0, i0 == 0);
     if (rc) return cleanup(), rc;
   }
+  return RGBID_OK;
+}
+
+int rgbid_align_batch_host_wait(rgbid_ctx* ctx) {
+  if (!ctx) return RGBID_E_ARG;
+  LaunchScope ls(ctx);
   for (auto& L : ctx->lanes) {
     const int rc = finish_chunk(ctx, L);
-    if (rc) return cleanup(), rc;
+    if (rc) return rc;
   }
   return RGBID_OK;
+}
+
+int rgbid_align_batch_host_async(rgbid_ctx* ctx, int n, const double* const* IA,
+                                 const double* const* WA, const double* const* IB,
+                                 const double* const* WB, int w, int h,
+                                 const rgbid_intrinsics* K, const rgbid_pose* inits,
+                                 const rgbid_align_config* cfg, int chunk,
+                                 rgbid_align_result* results) {
+  return align_batch_host_enqueue(ctx, n, IA, WA, IB, WB, w, h, K, inits, cfg, chunk, results);
+}
+
+int rgbid_align_batch_host(rgbid_ctx* ctx, int n, const double* const* IA,
+                           const double* const* WA, const double* const* IB,
+                           const double* const* WB, int w, int h, const rgbid_intrinsics* K,
+                           const rgbid_pose* inits, const rgbid_align_config* cfg, int chunk,
+                           rgbid_align_result* results) {
+  const int rc = align_batch_host_enqueue(ctx, n, IA, WA, IB, WB, w, h, K, inits, cfg, chunk,
+                                          results);
+  const int rw = rgbid_align_batch_host_wait(ctx);
+  return rc ? rc : rw;
 }
 
 int rgbid_filtered_hessian_covariance(rgbid_ctx* ctx, const rgbid_frame* a, const rgbid_frame* b,

@@ -436,3 +436,28 @@ def test_synth_pair_host_equals_device(ctx):
                 assert np.array_equal(np.isnan(x), np.isnan(y))
                 m = ~np.isnan(x)
                 assert np.abs(x[m] - y[m]).max() <= 1e-12
+
+
+def test_align_batch_host_async_equals_sync(ctx):
+    """Streaming host batches (rgbid_align_batch_host_async + _wait, consecutive calls
+    overlapping) give the same results as the synchronous call, bit for bit."""
+    import ctypes as C
+    from paper_1807_08271_b200 import abi
+    K = rg.simple_intrinsics(160, 120, 120.0)
+    pairs = [pair(K, 30 + i, "noisy") for i in range(20)]
+    maps = [np.ascontiguousarray(m) for p in pairs for m in (p[0].intensity, p[0].inverse_depth,
+                                                             p[1].intensity, p[1].inverse_depth)]
+    arrs = [(abi.DP * 20)(*[abi.dptr(maps[4 * i + k]) for i in range(20)]) for k in range(4)]
+    cfg = rg.AlignmentConfig(levels=3).to_c()
+    Kc = K.to_c()
+    sync = (abi.AlignResult_t * 20)()
+    ctx.check(ctx.lib.rgbid_align_batch_host(ctx.h, 20, *arrs, 160, 120, C.byref(Kc), None,
+                                             C.byref(cfg), 6, sync), "sync")
+    outs = [(abi.AlignResult_t * 20)() for _ in range(3)]
+    for o in outs:  # three streamed calls, chunks of 6 over two lanes
+        ctx.check(ctx.lib.rgbid_align_batch_host_async(ctx.h, 20, *arrs, 160, 120, C.byref(Kc),
+                                                       None, C.byref(cfg), 6, o), "async")
+    ctx.check(ctx.lib.rgbid_align_batch_host_wait(ctx.h), "wait")
+    for o in outs:
+        for a, b in zip(o, sync):
+            assert bytes(a) == bytes(b)
