@@ -477,6 +477,65 @@ def align_batch(frames_a: Sequence[DeviceFrame], frames_b: Sequence[DeviceFrame]
     return list(res)
 
 
+@dataclass
+class PixelJet:
+    """inc/alignment.hpp:48-56"""
+    x: int
+    y: int
+    r_I: float
+    r_W: float
+    J_I: np.ndarray
+    J_W: np.ndarray
+    lambda_n: float
+    has_depth: bool
+
+
+def residuals_and_jacobians(frame_a: FrameData, warped: WarpedFrame, K: Intrinsics,
+                            lambda_n_min: float = 0.1, ctx: Optional[Context] = None,
+                            as_array: bool = False):
+    """src/alignment.cpp:195-250.  Returns the jets in row-major order (PixelJet
+    list, or with as_array=True an (n, 17) array {x, y, r_I, r_W, J_I[6], J_W[6],
+    lambda_n} plus the has_depth flags)."""
+    ctx = ctx or default_context()
+    h, w = frame_a.inverse_depth.shape
+    cap = w * h
+    jets = np.empty((cap, 17))
+    flags = np.empty(cap, dtype=np.uint8)
+    n = ctx.lib.rgbid_residuals_and_jacobians(
+        ctx.h, dptr(np.ascontiguousarray(frame_a.intensity)),
+        dptr(np.ascontiguousarray(frame_a.inverse_depth)),
+        dptr(np.ascontiguousarray(warped.intensity)),
+        dptr(np.ascontiguousarray(warped.inverse_depth)), w, h, C.byref(K.to_c()), lambda_n_min,
+        dptr(jets), flags.ctypes.data_as(C.POINTER(C.c_ubyte)), cap)
+    if n < 0:
+        ctx.check(int(n), "residuals_and_jacobians")
+    jets, flags = jets[:n].copy(), flags[:n].astype(bool)
+    if as_array:
+        return jets, flags
+    return [PixelJet(int(j[0]), int(j[1]), j[2], j[3], j[4:10].copy(), j[10:16].copy(), j[16], f)
+            for j, f in zip(jets, flags)]
+
+
+def estimate_location_scale(residuals, nu: float, ctx: Optional[Context] = None) -> TDistParams:
+    """src/alignment.cpp:61-101 (systematic sample of <= 19200, IRLS on the device)"""
+    ctx = ctx or default_context()
+    r = np.ascontiguousarray(residuals, dtype=np.float64)
+    t = abi.TDist_t()
+    ctx.check(ctx.lib.rgbid_estimate_location_scale(ctx.h, dptr(r), len(r), nu, C.byref(t)),
+              "estimate_location_scale")
+    return TDistParams(t.mu, t.sigma, t.nu)
+
+
+def estimate_nu(residuals, mu: float, sigma: float, ctx: Optional[Context] = None) -> float:
+    """src/alignment.cpp:109-127"""
+    ctx = ctx or default_context()
+    r = np.ascontiguousarray(residuals, dtype=np.float64)
+    out = C.c_double(0.0)
+    ctx.check(ctx.lib.rgbid_estimate_nu(ctx.h, dptr(r), len(r), mu, sigma, C.byref(out)),
+              "estimate_nu")
+    return out.value
+
+
 def filtered_hessian_covariance(frame_a, frame_b, K: Intrinsics, T_AB: Pose,
                                 config: Optional[AlignmentConfig] = None,
                                 ctx: Optional[Context] = None):

@@ -461,3 +461,60 @@ def test_align_batch_host_async_equals_sync(ctx):
     for o in outs:
         for a, b in zip(o, sync):
             assert bytes(a) == bytes(b)
+
+
+def test_drain_buffer_semantics(ctx):
+    """tests/test_fusion.cpp:185-210 on the device: draining an empty buffer is a
+    no-op; three buffered frames are all integrated (C = 1 + 3)."""
+    K = rg.simple_intrinsics(20, 16, 20.0)
+    f = rg.render_plane(K, rg.Pose())
+    kf = rg.make_keyframe(f, rg.Pose(), 0, 0.0)
+    before = kf.inverse_depth.copy()
+    rg.drain_buffer_step(kf, rg.FrameBuffer(30), K, 0.01, ctx)
+    assert bitwise_equal(kf.inverse_depth, before)
+    base = rg.FrameData(np.full((16, 20), 0.5), np.full((16, 20), 0.5))
+    kf = rg.make_keyframe(base, rg.Pose(), 0, 0.0)
+    buf = rg.FrameBuffer(30)
+    for t in (0.1, 0.2, 0.3):
+        buf.push(rg.BufferedFrame(base, rg.Pose(), t))
+    for _ in range(3):
+        rg.drain_buffer_step(kf, buf, K, 0.05, ctx)
+    assert buf.empty() and kf.weight[8, 10] == pytest.approx(4.0)
+
+
+@pytest.mark.parametrize("size", [(80, 60, 60.0), (640, 480, 480.0)])
+def test_residuals_and_jacobians_bitwise(ctx, orc, size):
+    """src/alignment.cpp:195-250 through the C-ABI: the jet set, order, residuals,
+    Jacobians and has_depth flags equal the oracle's bit for bit; lambda_n within a
+    few ulp (the device normalises n and the ray with rsqrt, src/alignment.cpp:233-244
+    divides by sqrt)."""
+    K = rg.simple_intrinsics(*size)
+    fa, fb, T = pair(K, 8, "noisy", holes=True)
+    wp = rg.inverse_geometric_warp(fb.intensity, fb.inverse_depth, fa.inverse_depth, T, K, ctx)
+    jets, flags = rg.residuals_and_jacobians(fa, wp, K, ctx=ctx, as_array=True)
+    jo, fo = orc.residuals_and_jacobians(fa.intensity, fa.inverse_depth, wp.intensity,
+                                         wp.inverse_depth, K.to_c())
+    assert jets.shape == jo.shape and len(jets) > 100
+    assert bitwise_equal(jets[:, :16], jo[:, :16]) and np.array_equal(flags, fo)
+    rel = np.abs(jets[:, 16] - jo[:, 16]) / np.abs(jo[:, 16])
+    assert rel.max() <= 1e-14, f"lambda_n max relative difference {rel.max():.2e}"
+    first = rg.residuals_and_jacobians(fa, wp, K, ctx=ctx)[0]
+    assert (first.x, first.y) == (int(jo[0, 0]), int(jo[0, 1]))
+
+
+def test_student_t_entry_points_match_oracle(ctx, orc):
+    """estimate_location_scale / estimate_nu (src/alignment.cpp:61-127) through the
+    C-ABI on t-distributed and Gaussian residuals, above and below the 19200 cap."""
+    rng = np.random.default_rng(5)
+    for n, nu_true in ((5000, 3.0), (50000, 6.0)):
+        r = 0.1 + 0.8 * rng.standard_t(nu_true, size=n)
+        for nu in (5.0, nu_true):
+            g = rg.estimate_location_scale(r, nu, ctx)
+            o = orc.estimate_location_scale(r, nu)
+            assert g.mu == pytest.approx(o[0], rel=1e-9, abs=1e-12)
+            assert g.sigma == pytest.approx(o[1], rel=1e-9)
+        mu, s, _ = orc.estimate_location_scale(r, 5.0)
+        assert rg.estimate_nu(r, mu, s, ctx) == pytest.approx(orc.estimate_nu(r, mu, s), rel=1e-9)
+    gauss = rng.normal(size=30000)
+    mu, s, _ = orc.estimate_location_scale(gauss, 10.0)
+    assert rg.estimate_nu(gauss, mu, s, ctx) == pytest.approx(orc.estimate_nu(gauss, mu, s))
