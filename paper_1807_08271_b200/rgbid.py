@@ -239,6 +239,19 @@ class CudaError(RuntimeError):
     pass
 
 
+def digamma(x: float) -> float:
+    """src/alignment.cpp:32-43 (host scalar helper, as in the reference)."""
+    import math
+    result = 0.0
+    while x < 6.0:
+        result -= 1.0 / x
+        x += 1.0
+    inv = 1.0 / x
+    inv2 = inv * inv
+    return result + (math.log(x) - 0.5 * inv
+                     - inv2 * (1.0 / 12.0 - inv2 * (1.0 / 120.0 - inv2 / 252.0)))
+
+
 def t_weight(x: float, nu: float) -> float:
     """inc/alignment.hpp:35"""
     return (nu + 1.0) / (nu + x * x)
@@ -403,6 +416,30 @@ class WarpedFrame:
     inverse_depth: np.ndarray
     map_x: np.ndarray
     map_y: np.ndarray
+
+
+def inverse_warp(src: np.ndarray, f_w, out_width: int, out_height: int,
+                 ctx: Optional[Context] = None) -> np.ndarray:
+    """src/warping.cpp:8-18: out(x, y) = bilinear(src, f_w((x, y))).  f_w is
+    evaluated on the host (vectorised over the output grid when it accepts
+    arrays); the sampling runs on the device (rgbid_remap_bilinear)."""
+    ctx = ctx or default_context()
+    src = np.ascontiguousarray(src, dtype=np.float64)
+    h, w = src.shape
+    ys, xs = np.mgrid[0:out_height, 0:out_width].astype(np.float64)
+    try:
+        mx, my = f_w(np.stack([xs, ys]))
+        mx = np.broadcast_to(np.asarray(mx, dtype=np.float64), xs.shape)
+        my = np.broadcast_to(np.asarray(my, dtype=np.float64), xs.shape)
+    except Exception:  # scalar f_w: per pixel
+        q = [f_w(np.array([x, y])) for y in range(out_height) for x in range(out_width)]
+        mx = np.array([v[0] for v in q]).reshape(xs.shape)
+        my = np.array([v[1] for v in q]).reshape(xs.shape)
+    mx, my = np.ascontiguousarray(mx), np.ascontiguousarray(my)
+    out = np.empty((out_height, out_width))
+    ctx.check(ctx.lib.rgbid_remap_bilinear(ctx.h, dptr(src), w, h, dptr(mx), dptr(my), out_width,
+                                           out_height, dptr(out)), "inverse_warp")
+    return out
 
 
 def inverse_geometric_warp(I_B, W_B, W_A, T_AB: Pose, K: Intrinsics,

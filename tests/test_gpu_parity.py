@@ -518,3 +518,30 @@ def test_student_t_entry_points_match_oracle(ctx, orc):
     gauss = rng.normal(size=30000)
     mu, s, _ = orc.estimate_location_scale(gauss, 10.0)
     assert rg.estimate_nu(gauss, mu, s, ctx) == pytest.approx(orc.estimate_nu(gauss, mu, s))
+
+
+def test_inverse_warp_bitwise(ctx):
+    """src/warping.cpp:8-18 with include/rgbid/image.hpp:51-62 bilinear, restated in
+    plain Python floats; f_w as a vectorised and as a scalar callable."""
+    rng = np.random.default_rng(3)
+    src = rng.random((16, 20))
+    src[5, 7] = np.nan
+
+    def bil(img, x, y):
+        h, w = img.shape
+        if not (0 <= x <= w - 1 and 0 <= y <= h - 1):
+            return np.nan
+        x0, y0 = int(np.floor(x)), int(np.floor(y))
+        x1, y1 = min(x0 + 1, w - 1), min(y0 + 1, h - 1)
+        fx, fy = x - x0, y - y0
+        v = [img[y0, x0], img[y0, x1], img[y1, x0], img[y1, x1]]
+        if not all(np.isfinite(v)):
+            return np.nan
+        return (1 - fy) * ((1 - fx) * v[0] + fx * v[1]) + fy * ((1 - fx) * v[2] + fx * v[3])
+
+    f_vec = lambda p: (0.9 * p[0] + 0.37, 1.05 * p[1] - 0.2)  # noqa: E731
+    f_sca = lambda p: np.array([0.9 * p[0] + 0.37, 1.05 * p[1] - 0.2])  # noqa: E731
+    ref = np.array([[bil(src, 0.9 * x + 0.37, 1.05 * y - 0.2) for x in range(22)]
+                    for y in range(15)])
+    assert bitwise_equal(rg.inverse_warp(src, f_vec, 22, 15, ctx), ref)
+    assert bitwise_equal(rg.inverse_warp(src, f_sca, 22, 15, ctx), ref)
