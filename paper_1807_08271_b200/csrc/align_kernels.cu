@@ -30,6 +30,11 @@
 
 #include "align_kernels.cuh"
 
+#ifndef RGBID_K1_IWB
+#define RGBID_K1_IWB 1  // level-0 K1 samples frame B from an interleaved {I, W} copy
+                        // (-11% per launch; levels >= 1 measured slower: register pairs spill)
+#endif
+
 namespace rgbid_b200 {
 
 thread_local long long* g_launch_counter = nullptr;
@@ -126,6 +131,48 @@ __device__ __forceinline__ void warp_px(const WarpMats& m, const double* __restr
                a11 = __ldg(IB + i00 + dy + dx);
   const double b00 = __ldg(WB + i00), b10 = __ldg(WB + i00 + dx), b01 = __ldg(WB + i00 + dy),
                b11 = __ldg(WB + i00 + dy + dx);
+  const double ri = bilin_fix(gy * (gx * a00 + fx * a10) + fy * (gx * a01 + fx * a11), a00, a10, a01, a11);
+  const double w_meas = bilin_fix(gy * (gx * b00 + fx * b10) + fy * (gx * b01 + fx * b11), b00, b10, b01, b11);
+  oI = inb ? ri : CUDART_NAN;
+  const bool v2 = inb && valid(w_meas) && w_meas > 0.0;
+  const double rz = red3(m.Rt_AB[6] * px, m.Rt_AB[7] * py, m.Rt_AB[8] * 1.0);
+  const double za = rz / (v2 ? w_meas : 1.0) + m.tt_AB[2];
+  const bool v3 = v2 && za > 1e-12;
+  oW = v3 ? __drcp_rn(za) : CUDART_NAN;  // == 1.0 / za
+}
+
+// warp_px on frame B stored interleaved {I, W}: the four bilinear taps are four
+// 16-byte loads instead of eight 8-byte loads (same values, same arithmetic).
+// Written branch-free (predicates + clamped, always-issued tap loads) so that
+// several pixels unrolled in one thread overlap their gathers.
+__device__ __forceinline__ void warp_px_iw(const WarpMats& m, const double2* __restrict__ IWB,
+                                           int wb, int hb, int x,
+                                        int y, double w_a, double& oI, double& oW, double& mx,
+                                        double& my) {
+  const bool v0 = valid(w_a) && w_a > 0.0;
+  const double wa = v0 ? w_a : 1.0;
+  const double qz = __drcp_rn(wa);  // == 1.0 / w_a
+  const double qx = div_rcp((double)x, wa, qz), qy = div_rcp((double)y, wa, qz);
+  const double xb0 = red3(m.Rt_BA[0] * qx, m.Rt_BA[1] * qy, m.Rt_BA[2] * qz) + m.tt_BA[0];
+  const double xb1 = red3(m.Rt_BA[3] * qx, m.Rt_BA[4] * qy, m.Rt_BA[5] * qz) + m.tt_BA[1];
+  const double xb2 = red3(m.Rt_BA[6] * qx, m.Rt_BA[7] * qy, m.Rt_BA[8] * qz) + m.tt_BA[2];
+  const bool v1 = v0 && xb2 > 1e-12;
+  const double z = v1 ? xb2 : 1.0;
+  const double rz2 = __drcp_rn(z);
+  const double px = div_rcp(xb0, z, rz2), py = div_rcp(xb1, z, rz2);
+  mx = v1 ? px : CUDART_NAN;
+  my = v1 ? py : CUDART_NAN;
+  const bool inb = v1 && (px >= 0.0 && px <= wb - 1.0 && py >= 0.0 && py <= hb - 1.0);
+  const double sx = inb ? px : 0.0, sy = inb ? py : 0.0;
+  const int x0 = (int)floor(sx), y0 = (int)floor(sy);
+  const int dx = x0 + 1 < wb ? 1 : 0;  // x1 = min(x0 + 1, w - 1)
+  const int dy = y0 + 1 < hb ? wb : 0; // y1 = min(y0 + 1, h - 1)
+  const double fx = sx - x0, fy = sy - y0, gx = 1 - fx, gy = 1 - fy;
+  const int i00 = y0 * wb + x0;
+  const double2 t00 = __ldg(IWB + i00), t10 = __ldg(IWB + i00 + dx), t01 = __ldg(IWB + i00 + dy),
+                t11 = __ldg(IWB + i00 + dy + dx);
+  const double a00 = t00.x, a10 = t10.x, a01 = t01.x, a11 = t11.x;
+  const double b00 = t00.y, b10 = t10.y, b01 = t01.y, b11 = t11.y;
   const double ri = bilin_fix(gy * (gx * a00 + fx * a10) + fy * (gx * a01 + fx * a11), a00, a10, a01, a11);
   const double w_meas = bilin_fix(gy * (gx * b00 + fx * b10) + fy * (gx * b01 + fx * b11), b00, b10, b01, b11);
   oI = inb ? ri : CUDART_NAN;
@@ -344,7 +391,10 @@ __global__ void __launch_bounds__(128, RGBID_K1L0_MINB) k_warp_residuals_l0(cons
       const unsigned a = __ldg(am + idx);
       const double ia = __ldg(IA0 + idx);
       double ib, wb, d0, d1;
-      warp_px(wm, IB, WB, w0, h0, xl0 + lx, yl, __ldg(WAw + idx), ib, wb, d0, d1);
+      if (RGBID_K1_IWB)
+        warp_px_iw(wm, o.IWB, w0, h0, xl0 + lx, yl, __ldg(WAw + idx), ib, wb, d0, d1);
+      else
+        warp_px(wm, IB, WB, w0, h0, xl0 + lx, yl, __ldg(WAw + idx), ib, wb, d0, d1);
       o.ib[idx] = ib - ia;  // r_I (src/alignment.cpp:222), consumed by K2 and K3
       o.wb[idx] = wb;
       jet[q] = (a & 1u) && valid(ib);
@@ -400,6 +450,23 @@ __global__ void k_prep_A(const SlotIO* __restrict__ io, const SlotState* __restr
   double2* gp = reinterpret_cast<double2*>(o.agrad[level] + 4 * (size_t)k);
   gp[0] = make_double2(g[0], g[1]);
   gp[1] = make_double2(g[2], g[3]);
+}
+
+// frame B interleaved {I, W} for K1's taps, once per align
+__global__ void k_interleave_B(const SlotIO* __restrict__ io, const SlotState* __restrict__ st,
+                               int n) {
+  const int slot = blockIdx.y;
+  if (st[slot].status != RGBID_OK) return;
+  const SlotIO& o = io[slot];
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < n) o.IWB[k] = make_double2(__ldg(o.IB + k), __ldg(o.WB + k));
+}
+
+void launch_interleave_B(const AlignLaunch& a, cudaStream_t s) {
+  if (!RGBID_K1_IWB) return;
+  KScope ks_("interleave_B", s);
+  const int n = a.w0 * a.h0;
+  k_interleave_B<<<dim3((n + 255) / 256, a.nslots), 256, 0, s>>>(a.io, a.st, n);
 }
 
 void launch_amask(const AlignLaunch& a, int levels, int phase, cudaStream_t s) {

@@ -58,6 +58,7 @@ struct SlotIO {
   double* WA[kMaxLevels];
   const double* IB;              // frame B, level 0
   const double* WB;
+  double2* IWB;                  // frame B interleaved {I, W} (K1's bilinear taps)
   double* fIA;                   // bilateral-filtered A (covariance pass)
   double* fWA;
   double* ib;                    // r_I = warped I_B - I_A at the current level (K1)
@@ -118,6 +119,7 @@ void launch_downsample2(const double* I, const double* W, int w, int h, double* 
                         cudaStream_t s);
 void launch_pyramid_slots(const AlignLaunch& a, int levels, cudaStream_t s);
 void launch_amask(const AlignLaunch& a, int levels, int phase, cudaStream_t s);
+void launch_interleave_B(const AlignLaunch& a, cudaStream_t s);
 void launch_bilateral_pair(const AlignLaunch& a, double ss, double sr_i, double sr_w,
                            cudaStream_t s);
 void launch_bilateral(const double* img, int w, int h, double ss, double sr, double* out,

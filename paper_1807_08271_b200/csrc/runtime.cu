@@ -264,7 +264,9 @@ size_t pyr_pixels(int w, int h) {
 size_t slot_f64(int w, int h) {
   const size_t N = (size_t)w * h;
   const size_t part = (size_t)((N + kTPB * kPixK3 - 1) / (kTPB * kPixK3)) * kNPart;
-  return 4 * N + 4 * pyr_pixels(w, h) + part + 2 * (size_t)kMaxSample;
+  // ... + K2 samples + interleaved frame B (16-byte aligned: the total stays even)
+  const size_t f = 4 * N + 4 * pyr_pixels(w, h) + part + 2 * (size_t)kMaxSample;
+  return ((f + 1) & ~(size_t)1) + 2 * N;
 }
 size_t slot_u8(int w, int h) { return (pyr_pixels(w, h) + 255) & ~(size_t)255; }
 size_t slot_i32(int w, int h) { return 2 * max_tiles(w, h) * (1 + kWordsPerTile) + 2; }
@@ -399,6 +401,7 @@ std::vector<Stage> align_stages(const AlignLaunch& a, const rgbid_intrinsics& K,
   st.push_back([a, levels](cudaStream_t s) {
     launch_pyramid_slots(a, levels, s);  // build_pyramid (src/alignment.cpp:369)
     launch_amask(a, levels, 0, s);       // A-side validity + gradients, once per align
+    launch_interleave_B(a, s);           // B as {I, W} pairs for K1's bilinear taps
   });
   for (int level = cfg.levels - 1; level >= 0; --level) {
     const LevelInfo li = make_level(K, a.w0, a.h0, level);
@@ -539,7 +542,8 @@ int prepare_chunk(rgbid_ctx* ctx, Lane& L, int n, const rgbid_frame* const* fa,
       g += 4 * (size_t)(w >> l) * (h >> l);
     }
     o.part = g;
-    o.smp = base + (sf - 2 * (size_t)kMaxSample);
+    o.IWB = reinterpret_cast<double2*>(base + (sf - 2 * N));  // sf and N*2 even: 16-B aligned
+    o.smp = base + (sf - 2 * N - 2 * (size_t)kMaxSample);
     int* ib32 = L.ws_i32 + si * i;
     o.cntI = ib32;
     o.cntW = ib32 + mt;
