@@ -332,8 +332,7 @@ __global__ void __launch_bounds__(k1_threads<L>(), RGBID_K1_THREADS_PER_SM / k1_
   if (tid < nx) {
     const int idx = yl * li.w + xl0 + tid;
     const double ib = sI[tid], wb = sW[tid];
-    o.ib[idx] = ib - __ldg(IAl + idx);  // r_I (src/alignment.cpp:222), consumed by K2 and K3
-    o.wb[idx] = wb;
+    o.ibw[idx] = make_double2(ib - __ldg(IAl + idx), wb);  // r_I (src/alignment.cpp:222), w_b
     const unsigned a = __ldg(am + idx);
     jet = (a & 1u) && valid(ib);
     dep = jet && (a & 2u) && valid(wb) && wb > 0.0;
@@ -395,8 +394,7 @@ __global__ void __launch_bounds__(128, RGBID_K1L0_MINB) k_warp_residuals_l0(cons
         warp_px_iw(wm, o.IWB, w0, h0, xl0 + lx, yl, __ldg(WAw + idx), ib, wb, d0, d1);
       else
         warp_px(wm, IB, WB, w0, h0, xl0 + lx, yl, __ldg(WAw + idx), ib, wb, d0, d1);
-      o.ib[idx] = ib - ia;  // r_I (src/alignment.cpp:222), consumed by K2 and K3
-      o.wb[idx] = wb;
+      o.ibw[idx] = make_double2(ib - ia, wb);  // r_I (src/alignment.cpp:222), w_b: K2, K3
       jet[q] = (a & 1u) && valid(ib);
       dep[q] = jet[q] && (a & 2u) && valid(wb) && wb > 0.0;
     }
@@ -1010,7 +1008,8 @@ __global__ void __launch_bounds__(kGatherThreads)
   const SlotIO& o = io[slot];
   const int* cnt = type ? o.cntW : o.cntI;
   const unsigned* bits = type ? o.bitsW : o.bitsI;
-  const double* bv = type ? o.wb : o.ib;  // warped W_B / r_I (K1) at this level
+  // r_I (type 0) / warped W_B (type 1) at this level: component `type` of K1's pairs
+  const double* bv = reinterpret_cast<const double*>(o.ibw) + type;
   const double* av = phase ? o.fWA : o.WA[li.level];
   extern __shared__ int offs[];  // [ntiles + 1]
   __shared__ long long sidx[kGatherChunk];
@@ -1104,7 +1103,7 @@ __global__ void __launch_bounds__(kGatherThreads)
 #pragma unroll
     for (int u = 0; u < 4; ++u)
       if (ix[u] >= 0) {
-        b[u] = __ldg(bv + ix[u]);
+        b[u] = __ldg(bv + 2 * ix[u]);
         a[u] = type ? __ldg(av + ix[u]) : 0.0;
       }
 #pragma unroll
@@ -1200,7 +1199,7 @@ __global__ void __launch_bounds__(kTdistClusterThreads, 1)
   const SlotIO& o = io[slot];
   const int* cnt = type ? o.cntW : o.cntI;
   const unsigned* bits = type ? o.bitsW : o.bitsI;
-  const double* bv = type ? o.wb : o.ib;
+  const double* bv = reinterpret_cast<const double*>(o.ibw) + type;  // r_I / w_b pairs
   const double* av = phase ? o.fWA : o.WA[li.level];  // (r_I is stored by K1)
   extern __shared__ double dsm[];  // sample share [ceil(kMaxSample/CS)] + offs[ntiles + 1]
   constexpr int kShare = (kMaxSample + CS - 1) / CS;
@@ -1303,7 +1302,7 @@ __global__ void __launch_bounds__(kTdistClusterThreads, 1)
 #pragma unroll
     for (int u = 0; u < 4; ++u)
       if (ix[u] >= 0) {
-        bb[u] = __ldg(bv + ix[u]);
+        bb[u] = __ldg(bv + 2 * ix[u]);
         aa[u] = type ? __ldg(av + ix[u]) : 0.0;
       }
 #pragma unroll
@@ -1482,8 +1481,7 @@ __global__ void __launch_bounds__(kTPB, RGBID_K3_MINBLOCKS) k_normal_eq(const Sl
   const double* __restrict__ WA = phase ? o.fWA : o.WA[li.level];
   const uint8_t* __restrict__ am = o.amask[li.level];
   const double2* __restrict__ ag = reinterpret_cast<const double2*>(o.agrad[li.level]);
-  const double* __restrict__ ibp = o.ib;
-  const double* __restrict__ wbp = o.wb;
+  const double2* __restrict__ ibwp = o.ibw;
   __shared__ double scratch[(kTPB / 32) * kNPart];
   const double muI = S.tI.mu, isgI = 1.0 / S.tI.sigma, nuI = dmax_std(S.tI.nu, S.tW.nu);
   const double muW = S.tW.mu, isgW = 1.0 / S.tW.sigma, nuW = S.tW.nu;
@@ -1502,7 +1500,8 @@ __global__ void __launch_bounds__(kTPB, RGBID_K3_MINBLOCKS) k_normal_eq(const Sl
     // every load of the pixel issued at once (one memory round trip; the
     // validity tests below only select)
     const unsigned a = __ldg(am + k);
-    const double r_I = __ldcs(ibp + k), w_b = __ldcs(wbp + k);  // r_I = i_b - i_a (K1)
+    const double2 rw = __ldcs(ibwp + k);  // {r_I = i_b - i_a, w_b} (K1)
+    const double r_I = rw.x, w_b = rw.y;
     const double w_a = __ldg(WA + k);
     const double2 gI = __ldg(ag + 2 * k), gW = __ldg(ag + 2 * k + 1);
     if (!(a & 1u) || !valid(r_I)) continue;  // bit0 implies valid(i_a): valid(r_I) == valid(i_b)
@@ -1595,8 +1594,7 @@ __global__ void __launch_bounds__(kTPB, RGBID_K3_MMA_MINB) k_normal_eq_mma(const
   const double* __restrict__ WA = phase ? o.fWA : o.WA[li.level];
   const uint8_t* __restrict__ am = o.amask[li.level];
   const double2* __restrict__ ag = reinterpret_cast<const double2*>(o.agrad[li.level]);
-  const double* __restrict__ ibp = o.ib;
-  const double* __restrict__ wbp = o.wb;
+  const double2* __restrict__ ibwp = o.ibw;
   constexpr int XS = 9;  // 8 components + w per staged row
   __shared__ double xs[kTPB / 32][32 * XS];
   __shared__ double cst[kTPB / 32][64];
@@ -1626,7 +1624,8 @@ __global__ void __launch_bounds__(kTPB, RGBID_K3_MMA_MINB) k_normal_eq_mma(const
     const bool inr = k0i < N;
     const int k = inr ? k0i : 0;
     const unsigned a = __ldg(am + k);
-    const double r_I = __ldcs(ibp + k), w_b = __ldcs(wbp + k);  // r_I = i_b - i_a (K1)
+    const double2 rw = __ldcs(ibwp + k);  // {r_I = i_b - i_a, w_b} (K1)
+    const double r_I = rw.x, w_b = rw.y;
     const double w_a = __ldg(WA + k);
     const double2 gI = __ldg(ag + 2 * k), gW = __ldg(ag + 2 * k + 1);
     const bool jet = inr && (a & 1u) && valid(r_I);  // bit0 implies valid(i_a)

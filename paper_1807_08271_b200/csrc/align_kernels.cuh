@@ -61,8 +61,7 @@ struct SlotIO {
   double2* IWB;                  // frame B interleaved {I, W} (K1's bilinear taps)
   double* fIA;                   // bilateral-filtered A (covariance pass)
   double* fWA;
-  double* ib;                    // r_I = warped I_B - I_A at the current level (K1)
-  double* wb;                    // warped W_B at the current level
+  double2* ibw;                  // {r_I = warped I_B - I_A, warped W_B} per level pixel (K1)
   uint8_t* amask[kMaxLevels];    // A-side jet validity per level pixel (bit0 photometric, bit1 depth)
   double* agrad[kMaxLevels];     // A-side gradients per level pixel {gI_x, gI_y, gW_x, gW_y}
                                  // (level-0 entries are rebuilt from the filtered A for the

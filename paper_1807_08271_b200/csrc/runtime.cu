@@ -532,8 +532,7 @@ int prepare_chunk(rgbid_ctx* ctx, Lane& L, int n, const rgbid_frame* const* fa,
     o.IB = fb[i]->I;
     o.WB = fb[i]->W;
     double* base = L.ws_f64 + sf * i;
-    o.ib = base;
-    o.wb = base + N;
+    o.ibw = reinterpret_cast<double2*>(base);  // 2N doubles, 16-B aligned
     o.fIA = base + 2 * N;
     o.fWA = base + 3 * N;
     double* g = base + 4 * N;
