@@ -30,9 +30,12 @@
 
 #include "align_kernels.cuh"
 
+#ifndef RGBID_K1_IWB_LEVELS
+#define RGBID_K1_IWB_LEVELS 1  // levels >= 1 too (with the 1536-thread cap below; at 32
+                               // registers the register pairs spill and it measured slower)
+#endif
 #ifndef RGBID_K1_IWB
-#define RGBID_K1_IWB 1  // level-0 K1 samples frame B from an interleaved {I, W} copy
-                        // (-11% per launch; levels >= 1 measured slower: register pairs spill)
+#define RGBID_K1_IWB 1  // K1 samples frame B from an interleaved {I, W} copy (L0: -11%)
 #endif
 
 namespace rgbid_b200 {
@@ -248,7 +251,8 @@ __host__ __device__ constexpr int k1_threads() { return k1_cw<L>() * k1_ng<L>();
 
 template <int L>
 #ifndef RGBID_K1_THREADS_PER_SM
-#define RGBID_K1_THREADS_PER_SM 2048  // 32 registers: the L1-cached spills cost less than the occupancy gains (-16%)
+#define RGBID_K1_THREADS_PER_SM 1536  // 40 registers: occupancy over L1-cached spills (-16% vs 64
+                                      // registers; 1536 best with the interleaved {I, W} taps)
 #endif
 __global__ void __launch_bounds__(k1_threads<L>(), RGBID_K1_THREADS_PER_SM / k1_threads<L>()) k_warp_residuals(const SlotIO* __restrict__ io,
                                                            const SlotState* __restrict__ st,
@@ -291,7 +295,10 @@ __global__ void __launch_bounds__(k1_threads<L>(), RGBID_K1_THREADS_PER_SM / k1_
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const int xx = x + (q & 1), yy = y + (q >> 1);
-        warp_px(wm, IB, WB, w0, h0, xx, yy, __ldg(WAw + yy * w0 + xx), vi[q], vw[q], d0, d1);
+        if (RGBID_K1_IWB_LEVELS)
+          warp_px_iw(wm, o.IWB, w0, h0, xx, yy, __ldg(WAw + yy * w0 + xx), vi[q], vw[q], d0, d1);
+        else
+          warp_px(wm, IB, WB, w0, h0, xx, yy, __ldg(WAw + yy * w0 + xx), vi[q], vw[q], d0, d1);
       }
       sI[r * cw + col] = ds4(vi[0], vi[1], vi[2], vi[3]);
       sW[r * cw + col] = ds4(vw[0], vw[1], vw[2], vw[3]);
