@@ -797,7 +797,9 @@ __device__ __forceinline__ void q_body(const Sample& S, const double* v, int k, 
   }
   double D, NR, NV;
   frac_tree<BW, WV>(q, x, D, NR, NV);
-  bad |= !(D > 1e-250 && D < 1e250);
+  // D within ~[1.4e-250, 5.5e250] on the exponent bits (integer pipe, biased exponents
+  // 193..1853); NaN, inf, zero and negative D all fall outside
+  bad |= ((unsigned)__double2hiint(D) >> 20) - 193u > 1660u;
   const double inv = rcp_fast(D);
   sr = fma(NR, inv, sr);
   if (WV) sv = fma(NV, inv, sv);
