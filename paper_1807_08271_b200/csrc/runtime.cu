@@ -48,9 +48,9 @@ struct CachedGraph {
 }  // namespace
 
 // One execution lane of the alignment driver: a stream, a slot workspace and the
-// CUDA graphs captured on it.  Batches alternate chunks over the lanes so that
-// the FP64-bound Student-t kernels of one chunk overlap the memory/latency-bound
-// warp and normal-equation kernels of the other.
+// CUDA graphs captured on it.  Batches alternate chunks over the lanes (chunk
+// c+1's uploads / setup overlap chunk c's kernels; co-scheduled chunk pairs fill
+// each other's tails, ~1%).
 struct Lane {
   cudaStream_t stream = nullptr;
   cudaEvent_t done = nullptr;
@@ -245,8 +245,9 @@ PoseD pose_of(const rgbid_pose* p) {
   return pose_from(p->R, p->t);
 }
 
-// Per-slot workspace: ib, wb, fIA, fWA (N doubles each) + K3 partials;
-// A-side masks (all levels + covariance pass); per-tile counts + validity bitmasks.
+// Per-slot workspace: ibw ({r_I, w_b} pairs, 2N doubles), fIA, fWA (N each), the
+// A-side gradients (all levels), K3 partials, the K2 samples (2 x kMaxSample) and
+// frame B interleaved (2N); A-side masks; per-tile counts + validity bitmasks.
 size_t max_tiles(int w, int h) {
   size_t mx = 0;
   for (int l = 0; l < kMaxLevels; ++l) {
