@@ -1877,147 +1877,221 @@ void launch_downsample2(const double* I, const double* W, int w, int h, double* 
   k_downsample2<<<(n + 255) / 256, 256, 0, s>>>(I, W, w, h, oI, oW);
 }
 
-// exp(x) for x <= 0: 2^(j/64) table (shared memory) x degree-6 polynomial on
-// |r| <= ln2/128, within ~1 ulp of the correctly rounded value (the parity
-// tests bound the filtered maps at 1e-14 relative).  x < -708 (subnormal or
-// zero results) goes through the library exp; NaN yields NaN.
-__constant__ double c_exp2_64[64] = {
-    1.0, 1.0108892860517005, 1.0218971486541166, 1.0330248790212284,
-    1.0442737824274138, 1.0556451783605572, 1.0671404006768237, 1.0787607977571199,
-    1.0905077326652577, 1.102382583307841, 1.1143867425958924, 1.1265216186082418,
-    1.1387886347566916, 1.1511892299529827, 1.1637248587775775, 1.1763969916502812,
-    1.189207115002721, 1.202156731452703, 1.215247359980469, 1.22848053610687,
-    1.241857812073484, 1.255380757024691, 1.2690509571917332, 1.2828700160787783,
-    1.2968395546510096, 1.3109612115247644, 1.3252366431597413, 1.339667524053303,
-    1.3542555469368927, 1.3690024229745905, 1.383909881963832, 1.3989796725383112,
-    1.4142135623730951, 1.42961333839197, 1.4451808069770467, 1.460917794180647,
-    1.4768261459394993, 1.4929077282912648, 1.5091644275934228, 1.5255981507445384,
-    1.5422108254079407, 1.559004400237837, 1.5759808451078865, 1.593142151342267,
-    1.6104903319492543, 1.6280274218573478, 1.645755478153965, 1.6636765803267364,
-    1.681792830507429, 1.7001063537185235, 1.718619298122478, 1.7373338352737062,
-    1.7562521603732995, 1.7753764925265212, 1.7947090750031072, 1.8142521755003989,
-    1.8340080864093424, 1.8539791250833855, 1.8741676341103, 1.8945759815869656,
-    1.9152065613971474, 1.9360617934922943, 1.9571441241754002, 1.978456026387951};
+// exp(x) for x <= 0, branch-free: 2^(j/32) table held one entry per lane and
+// read with a warp shuffle (no shared-memory bank conflicts; every lane of the warp
+// must call it) x degree-6 polynomial on |r| <= ln2/64, within ~1 ulp of the
+// correctly rounded value (the parity tests bound the filtered maps at 1e-14
+// relative).  x is clamped at -746 (NaN and -inf too), so results below the normal
+// range come out as subnormals (one extra rounding) or zero, and NaN/-inf
+// arguments give 0.
+__constant__ double c_exp2_32[32] = {
+    1.0, 1.0218971486541166, 1.0442737824274138, 1.0671404006768237,
+    1.0905077326652577, 1.1143867425958924, 1.1387886347566916, 1.1637248587775775,
+    1.189207115002721, 1.215247359980469, 1.241857812073484, 1.2690509571917332,
+    1.2968395546510096, 1.3252366431597413, 1.3542555469368927, 1.383909881963832,
+    1.4142135623730951, 1.4451808069770467, 1.4768261459394993, 1.5091644275934228,
+    1.5422108254079407, 1.5759808451078865, 1.6104903319492543, 1.645755478153965,
+    1.681792830507429, 1.718619298122478, 1.7562521603732995, 1.7947090750031072,
+    1.8340080864093424, 1.8741676341103, 1.9152065613971474, 1.9571441241754002};
 
-__device__ __forceinline__ double exp_le0(double x, const double* __restrict__ tab) {
-  if (x < -708.0) return exp(x);
+__device__ __forceinline__ double exp2_32_lane() { return c_exp2_32[threadIdx.x & 31]; }
+
+__device__ __forceinline__ double exp_le0(double x, double tlane) {
+  x = fmax(x, -746.0);                                 // maxNum: NaN -> -746
   const double kMagic = 6755399441055744.0;            // 1.5 * 2^52: round to integer
-  const double kd = fma(x, 92.33248261689366, kMagic);  // x * 64 / ln2
+  const double kd = fma(x, 46.16624130844683, kMagic);  // x * 32 / ln2
   const int n = __double2loint(kd);
   const double k = kd - kMagic;
-  double r = fma(-k, 0.01083042469326756, x);  // ln2/64, hi part (k * hi exact)
-  r = fma(-k, 2.9815858269852933e-12, r);      // lo part
+  double r = fma(-k, 0.02166084938653512, x);  // ln2/32, hi part (32 bits: k * hi exact)
+  r = fma(-k, 5.9631716539705866e-12, r);      // lo part
   double pl = fma(r, 1.0 / 720.0, 1.0 / 120.0);
   pl = fma(r, pl, 1.0 / 24.0);
   pl = fma(r, pl, 1.0 / 6.0);
   pl = fma(r, pl, 0.5);
   pl = fma(r, pl, 1.0);
   const double em1 = r * pl;  // e^r - 1
-  const double t = tab[n & 63];
-  const double scale = __longlong_as_double((long long)((n >> 6) + 1023) << 52);
-  return fma(t, em1, t) * scale;
+  const double t = __shfl_sync(0xffffffffu, tlane, n & 31);
+  const int m = n >> 5, m1 = m >> 1, m2 = m - m1;  // 2^m = 2^m2 * 2^m1, both normal
+  const double s1 = __longlong_as_double((long long)(m1 + 1023) << 52);
+  const double s2 = __longlong_as_double((long long)(m2 + 1023) << 52);
+  return fma(t, em1, t) * s2 * s1;
 }
 
 // bilateral_filter — src/alignment.cpp:252-277, tiled.  The tap weight
 // exp(-(dx^2+dy^2)/(2 ss^2) - (v-c)^2/(2 sr^2)) is the same double for the
 // ordered pairs (p, q) and (q, p) ((v-c)^2 == (c-v)^2 bit for bit), so each
-// unordered pair's exp is evaluated once, by the raster-earlier pixel ("forward"
-// offsets dy > 0, or dy == 0 and dx > 0), into shared memory; every output pixel
-// then accumulates its 5x5 window in the reference order.
-constexpr int kBTW = 32, kBTH = 8;                 // output tile, one pixel per thread
-constexpr int kBRW = kBTW + 8, kBRH = kBTH + 4;    // input region from (x0-4, y0-2)
-constexpr int kBAW = kBTW + 4, kBAH = kBTH + 2;    // forward-weight owners from (x0-2, y0-2)
-constexpr int kBNA = kBAW * kBAH;
+// unordered pair's exp is evaluated once, for the raster-earlier pixel p and the
+// "forward" offset o = q - p (dy > 0, or dy == 0 and dx > 0).  Per offset, the
+// owners p with p or p + o in the 32 x 8 output tile lie in a 36 x (8 + dy) box
+// (x from -2, y from -dy).  A 36 x 8 thread grid evaluates the first 8 box rows of
+// all 12 offsets (straight-line, the same thread-relative addresses for every
+// offset) and then the 540 remaining entries (rows 8, 9) -- ~15.6 exps per output
+// pixel, no per-item index arithmetic on the main pass.  A pair with an invalid end
+// gets weight 0 (the valid end skips it in the reference and the invalid end
+// outputs NaN) and invalid taps read value 0, so every output accumulates its 5x5
+// window in the reference order with no per-tap tests: a skipped tap adds +0.0 to
+// both sums, which leaves them bit-identical (neither sum is ever -0.0).
+#ifndef RGBID_BIL_MINB
+#define RGBID_BIL_MINB 5  // 5 x 288 threads per SM (40 registers)
+#endif
+#ifndef RGBID_BIL_ROWS
+#define RGBID_BIL_ROWS 2  // output rows per thread in the accumulation
+#endif
+constexpr int kBTW = 32, kBTH = 8;               // output tile
+constexpr int kBRW = kBTW + 8, kBRH = kBTH + 4;  // input region from (x0-4, y0-2)
+constexpr int kBFP = kBTW + 4;                   // box pitch (x from -2)
+constexpr int kBNT = kBFP * kBTH;                // 288 threads: one per main-pass box entry
+// forward offsets o = 0..11: (1,0) (2,0) (-2..2,1) (-2..2,2)
+__host__ __device__ constexpr int bil_dx(int o) { return o < 2 ? o + 1 : (o < 7 ? o - 4 : o - 9); }
+__host__ __device__ constexpr int bil_dy(int o) { return o < 2 ? 0 : (o < 7 ? 1 : 2); }
+// box rows before offset o (sum of kBTH + dy over the earlier offsets)
+__host__ __device__ constexpr int bil_rows(int o) {
+  return kBTH * o + (o <= 2 ? 0 : (o <= 7 ? o - 2 : 5 + 2 * (o - 7)));
+}
+constexpr int kBFW = kBFP * bil_rows(12);  // forward weights, doubles
+constexpr int kBExtra = 5 * kBFP + 5 * 2 * kBFP;  // box rows >= kBTH: 540 entries
+
+__device__ __forceinline__ double bil_weight(const double* reg, int rc, int rv, double so,
+                                             double inv2sr, double tab) {
+  const double c = reg[rc], v = reg[rv];
+  // an invalid end (NaN, +-inf) gives a NaN or -inf argument -> weight 0
+  return exp_le0(so - (v - c) * (v - c) * inv2sr, tab);
+}
+
+template <int O>
+__device__ __forceinline__ void bil_main(int t, int rb, double inv2ss, double inv2sr,
+                                         double tab, const double* reg, double* fw) {
+  constexpr int dx = bil_dx(O), dy = bil_dy(O);
+  const double so = (double)(-(dx * dx + dy * dy)) * inv2ss;
+  // box entry (lx, ly) = owner (lx - 2, ly - dy); rb = region index of (lx - 2, ly)
+  fw[kBFP * bil_rows(O) + t] = bil_weight(reg, rb - dy * kBRW, rb + dx, so, inv2sr, tab);
+  if constexpr (O + 1 < 12) bil_main<O + 1>(t, rb, inv2ss, inv2sr, tab, reg, fw);
+}
 
 __device__ __forceinline__ void bilateral_tile(const double* __restrict__ img, int w, int h,
                                                double inv2ss, double inv2sr,
                                                double* __restrict__ out, int x0, int y0,
-                                               const double* tab, double* reg, double* fw) {
-  constexpr int FDX[12] = {1, 2, -2, -1, 0, 1, 2, -2, -1, 0, 1, 2};
-  constexpr int FDY[12] = {0, 0, 1, 1, 1, 1, 1, 2, 2, 2, 2, 2};
-  const int tid = threadIdx.x;
-  for (int i = tid; i < kBRW * kBRH; i += kBTW * kBTH) {
+                                               double* reg, double* reg0, double* fw) {
+  const int t = threadIdx.x;
+  const double tab = exp2_32_lane();
+  for (int i = t; i < kBRW * kBRH; i += kBNT) {
     const int ry = i / kBRW, rx = i - ry * kBRW;
     const int gx = x0 - 4 + rx, gy = y0 - 2 + ry;
-    reg[i] = (gx >= 0 && gx < w && gy >= 0 && gy < h) ? __ldg(img + (size_t)gy * w + gx)
-                                                      : CUDART_NAN;  // out of bounds = skipped
+    const double v = (gx >= 0 && gx < w && gy >= 0 && gy < h) ? __ldg(img + (size_t)gy * w + gx)
+                                                             : CUDART_NAN;  // out of bounds = skipped
+    reg[i] = v;
+    reg0[i] = valid(v) ? v : 0.0;
   }
   __syncthreads();
-  for (int a = tid; a < kBNA; a += kBTW * kBTH) {
-    const int ay = a / kBAW, ax = a - ay * kBAW;
-    const double c = reg[ay * kBRW + ax + 2];
+  {
+    const int ly = t / kBFP, lx = t - ly * kBFP;
+    bil_main<0>(t, (ly + 2) * kBRW + lx + 2, inv2ss, inv2sr, tab, reg, fw);
+  }
+  // rows >= kBTH of the dy = 1 boxes (o = 2..6, one row) and dy = 2 boxes (o = 7..11,
+  // two rows): two rounds run by every lane (the exp's shuffle), stores predicated
 #pragma unroll
-    for (int o = 0; o < 12; ++o) {
-      const double v = reg[(ay + FDY[o]) * kBRW + ax + 2 + FDX[o]];
-      const double arg =
-          (double)(-(FDX[o] * FDX[o] + FDY[o] * FDY[o])) * inv2ss - (v - c) * (v - c) * inv2sr;
-      fw[o * kBNA + a] = exp_le0(arg, tab);
+  for (int k = 0; k < (kBExtra + kBNT - 1) / kBNT; ++k) {
+    const int e0 = t + k * kBNT;
+    const bool live = e0 < kBExtra;
+    const int e = live ? e0 : 0;
+    int o, lx, ly, dy;
+    if (e < 5 * kBFP) {
+      o = 2 + e / kBFP;
+      lx = e - (o - 2) * kBFP;
+      ly = kBTH;
+      dy = 1;
+    } else {
+      const int f = e - 5 * kBFP;
+      const int q = f / (2 * kBFP), r = f - q * (2 * kBFP);
+      o = 7 + q;
+      ly = kBTH + r / kBFP;
+      lx = r - (ly - kBTH) * kBFP;
+      dy = 2;
     }
+    const int dx = dy == 1 ? o - 4 : o - 9;
+    const double so = (double)(-(dx * dx + dy * dy)) * inv2ss;
+    const int rb = (ly + 2) * kBRW + lx + 2;
+    const double wt = bil_weight(reg, rb - dy * kBRW, rb + dx, so, inv2sr, tab);
+    if (live) fw[kBFP * bil_rows(o) + ly * kBFP + lx] = wt;
   }
   __syncthreads();
-  const int tx = tid % kBTW, ty = tid / kBTW;
-  const int x = x0 + tx, y = y0 + ty;
-  if (x >= w || y >= h) return;
-  const double c = reg[(ty + 2) * kBRW + tx + 4];
-  if (!valid(c)) {
-    out[(size_t)y * w + x] = CUDART_NAN;
-    return;
-  }
-  double wsum = 0.0, vsum = 0.0;
+  // outputs: each of kBTW * kBTH / R threads accumulates R vertically adjacent
+  // pixels row by row over their (R + 4) x 5 joint window, each window row's values
+  // read once for all of them (5 (R + 4) value reads per R pixels instead of 25 R)
+  constexpr int R = RGBID_BIL_ROWS;
+  if (t >= kBTW * kBTH / R) return;
+  const int tx = t % kBTW, ty0 = R * (t / kBTW);
+  const int x = x0 + tx;
+  if (x >= w || y0 + ty0 >= h) return;
+  double ws[R], vs[R];
 #pragma unroll
-  for (int dy = -2; dy <= 2; ++dy)
+  for (int p = 0; p < R; ++p) ws[p] = vs[p] = 0.0;
 #pragma unroll
-    for (int dx = -2; dx <= 2; ++dx) {
-      const double v = reg[(ty + 2 + dy) * kBRW + tx + 4 + dx];
-      double wt;
-      if (dy == 0 && dx == 0) {
-        wt = 1.0;  // exp(+0.0)
-      } else {
-        const bool fwd = dy > 0 || (dy == 0 && dx > 0);
-        const int fdx = fwd ? dx : -dx, fdy = fwd ? dy : -dy;
-        const int o = fdy == 0 ? fdx - 1 : (fdy == 1 ? 4 + fdx : 9 + fdx);
-        const int a = fwd ? (ty + 2) * kBAW + tx + 2 : (ty + 2 + dy) * kBAW + tx + 2 + dx;
-        wt = fw[o * kBNA + a];
+  for (int j = -2; j <= R + 1; ++j) {  // window row, relative to the first pixel
+    double v[5];
+#pragma unroll
+    for (int dx = -2; dx <= 2; ++dx) v[dx + 2] = reg0[(ty0 + 2 + j) * kBRW + tx + 4 + dx];
+#pragma unroll
+    for (int pix = 0; pix < R; ++pix) {
+      const int dy = j - pix;  // tap row relative to this pixel
+      if (dy < -2 || dy > 2) continue;
+      const int ty = ty0 + pix;
+#pragma unroll
+      for (int dx = -2; dx <= 2; ++dx) {
+        double wt;
+        if (dy == 0 && dx == 0) {
+          wt = 1.0;  // exp(+0.0)
+        } else {
+          const bool fwd = dy > 0 || (dy == 0 && dx > 0);
+          const int fdx = fwd ? dx : -dx, fdy = fwd ? dy : -dy;
+          const int o = fdy == 0 ? fdx - 1 : (fdy == 1 ? 4 + fdx : 9 + fdx);
+          // owner p (forward) or p - o (backward); box row = owner y + fdy, col = owner x + 2
+          const int ox = fwd ? tx : tx + dx, oy = fwd ? ty : ty + dy;
+          wt = fw[kBFP * bil_rows(o) + (oy + fdy) * kBFP + ox + 2];
+        }
+        ws[pix] += wt;
+        vs[pix] += wt * v[dx + 2];
       }
-      // invalid taps are skipped: adding +0.0 leaves both sums bit-identical
-      const bool ok = valid(v);
-      wsum += ok ? wt : 0.0;
-      vsum += ok ? wt * v : 0.0;
     }
-  out[(size_t)y * w + x] = vsum / wsum;
+  }
+#pragma unroll
+  for (int p = 0; p < R; ++p)
+    if (y0 + ty0 + p < h)
+      out[(size_t)(y0 + ty0 + p) * w + x] =
+          valid(reg[(ty0 + p + 2) * kBRW + tx + 4]) ? vs[p] / ws[p] : CUDART_NAN;
 }
 
-__device__ __forceinline__ void load_exp_table(double* tab) {
-  if (threadIdx.x < 64) tab[threadIdx.x] = c_exp2_64[threadIdx.x];
-}
+struct BilateralSmem {
+  double reg[kBRW * kBRH], reg0[kBRW * kBRH], fw[kBFW];
+};
 
-__global__ void __launch_bounds__(kBTW * kBTH) k_bilateral(const double* __restrict__ img, int w,
+__global__ void __launch_bounds__(kBNT, RGBID_BIL_MINB) k_bilateral(const double* __restrict__ img, int w,
                                                            int h, double inv2ss, double inv2sr,
                                                            double* __restrict__ out) {
-  __shared__ double tab[64], reg[kBRW * kBRH], fw[12 * kBNA];
-  load_exp_table(tab);
-  bilateral_tile(img, w, h, inv2ss, inv2sr, out, blockIdx.x * kBTW, blockIdx.y * kBTH, tab, reg, fw);
+  __shared__ BilateralSmem sm;
+  bilateral_tile(img, w, h, inv2ss, inv2sr, out, blockIdx.x * kBTW, blockIdx.y * kBTH, sm.reg,
+                 sm.reg0, sm.fw);
 }
 
 void launch_bilateral(const double* img, int w, int h, double ss, double sr, double* out,
                       cudaStream_t s) {
   const double inv2ss = 1.0 / (2.0 * ss * ss), inv2sr = 1.0 / (2.0 * sr * sr);
   KScope ks_("bilateral", s);
-  k_bilateral<<<dim3((w + kBTW - 1) / kBTW, (h + kBTH - 1) / kBTH), kBTW * kBTH, 0, s>>>(
+  k_bilateral<<<dim3((w + kBTW - 1) / kBTW, (h + kBTH - 1) / kBTH), kBNT, 0, s>>>(
       img, w, h, inv2ss, inv2sr, out);
 }
 
 // both filtered maps of every active slot (covariance pass input); grid.z = map
-__global__ void __launch_bounds__(kBTW * kBTH)
+__global__ void __launch_bounds__(kBNT, RGBID_BIL_MINB)
     k_bilateral_slots(const SlotIO* __restrict__ io, const SlotState* __restrict__ st, int w,
                       int h, double inv2ss, double inv2sr_i, double inv2sr_w) {
   const int slot = blockIdx.z >> 1, map = blockIdx.z & 1;
   if (st[slot].status != RGBID_OK) return;
   const SlotIO& o = io[slot];
-  __shared__ double tab[64], reg[kBRW * kBRH], fw[12 * kBNA];
-  load_exp_table(tab);
+  __shared__ BilateralSmem sm;
   bilateral_tile(map ? o.WA[0] : o.IA[0], w, h, inv2ss, map ? inv2sr_w : inv2sr_i,
-                 map ? o.fWA : o.fIA, blockIdx.x * kBTW, blockIdx.y * kBTH, tab, reg, fw);
+                 map ? o.fWA : o.fIA, blockIdx.x * kBTW, blockIdx.y * kBTH, sm.reg, sm.reg0,
+                 sm.fw);
 }
 
 void launch_bilateral_pair(const AlignLaunch& a, double ss, double sr_i, double sr_w,
@@ -2026,7 +2100,7 @@ void launch_bilateral_pair(const AlignLaunch& a, double ss, double sr_i, double 
   const double ii = 1.0 / (2.0 * sr_i * sr_i), iw = 1.0 / (2.0 * sr_w * sr_w);
   KScope ks_("bilateral_slots", s);
   k_bilateral_slots<<<dim3((a.w0 + kBTW - 1) / kBTW, (a.h0 + kBTH - 1) / kBTH, 2 * a.nslots),
-                      kBTW * kBTH, 0, s>>>(a.io, a.st, a.w0, a.h0, inv2ss, ii, iw);
+                      kBNT, 0, s>>>(a.io, a.st, a.w0, a.h0, inv2ss, ii, iw);
 }
 
 // inverse_geometric_warp producing all four WarpedFrame maps (drop-in + tests)

@@ -162,6 +162,24 @@ def test_bilateral_matches_oracle(ctx, orc):
         assert np.abs(g[m] - o[m]).max() <= 1e-14 * np.abs(o[m]).max()
 
 
+@pytest.mark.parametrize("shape", [(23, 37), (9, 33), (480, 640)])
+def test_bilateral_ragged_and_nonfinite(ctx, orc, shape):
+    """tiles cut by the image border, +-inf and NaN taps (is_valid = isfinite),
+    far-apart values whose weights underflow to zero"""
+    rng = np.random.default_rng(shape[0])
+    img = rng.random(shape)
+    img[rng.random(shape) < 0.05] = np.nan
+    img[rng.random(shape) < 0.02] = np.inf
+    img[rng.random(shape) < 0.02] = -np.inf
+    img[rng.random(shape) < 0.05] *= 1e3
+    for sr in (0.05, 0.5):
+        g = rg.bilateral_filter(img, 2.0, sr, ctx)
+        o = orc.bilateral_filter(img, 2.0, sr)
+        assert bitwise_equal(np.isnan(g), np.isnan(o))
+        m = ~np.isnan(o)
+        assert np.abs(g[m] - o[m]).max() <= 1e-14 * np.abs(o[m]).max()
+
+
 def test_filtered_hessian_covariance(ctx, orc):
     K = vga()
     fa, fb, T = pair(K, 4, "noisy", True)
