@@ -204,6 +204,13 @@ def test_library_exports_every_declared_symbol():
     assert sorted(n for n, _, _ in abi.EXPORTS) == names
 
 
+def test_integration_doc_indexes_every_entry_point():
+    doc = open(os.path.join(ROOT, "INTEGRATION.md")).read()
+    index = doc[doc.index("## 4. Entry-point index"):]
+    missing = [n for n in _header_functions() if f"`{n}`" not in index]
+    assert not missing, missing
+
+
 def test_library_fails_loudly_without_gpu():
     if have_gpu():
         pytest.skip("GPU present")
