@@ -432,31 +432,6 @@ __global__ void __launch_bounds__(128, RGBID_K1L0_MINB) k_warp_residuals_l0(cons
   }
 }
 
-// A-side part of residuals_and_jacobians, constant over the IRLS iterations:
-// validity (src/alignment.cpp:209-211,227) and gradient_at of I_A and W_A
-// (src/alignment.cpp:165-191) per level pixel.  phase 1 = from the filtered A
-// into the level-0 slots (covariance pass, after the level loop).
-__global__ void k_prep_A(const SlotIO* __restrict__ io, const SlotState* __restrict__ st, int level,
-                         int w, int h, int phase) {
-  const int slot = blockIdx.y;
-  if (st[slot].status != RGBID_OK) return;
-  const SlotIO& o = io[slot];
-  const double* IA = phase ? o.fIA : o.IA[level];
-  const double* WA = phase ? o.fWA : o.WA[level];
-  const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= w * h) return;
-  const int y = k / w, x = k - y * w;
-  const double w_a = WA[k], i_a = IA[k];
-  double g[4] = {0.0, 0.0, 0.0, 0.0};
-  unsigned m = 0;
-  if (valid(w_a) && w_a > 0.0 && valid(i_a) && gradient_at(IA, w, h, x, y, g[0], g[1])) m |= 1u;
-  if (gradient_at(WA, w, h, x, y, g[2], g[3])) m |= 2u;
-  o.amask[level][k] = (uint8_t)m;
-  double2* gp = reinterpret_cast<double2*>(o.agrad[level] + 4 * (size_t)k);
-  gp[0] = make_double2(g[0], g[1]);
-  gp[1] = make_double2(g[2], g[3]);
-}
-
 // frame B interleaved {I, W} for K1's taps, once per align
 __global__ void k_interleave_B(const SlotIO* __restrict__ io, const SlotState* __restrict__ st,
                                int n) {
@@ -478,7 +453,8 @@ void launch_amask(const AlignLaunch& a, int levels, int phase, cudaStream_t s) {
   for (int l = 0; l < levels; ++l) {
     const int w = a.w0 >> l, h = a.h0 >> l;
     KScope ks_("prep_A", s);
-    k_prep_A<<<dim3((w * h + 255) / 256, a.nslots), 256, 0, s>>>(a.io, a.st, l, w, h, phase);
+    k_prep_A<<<dim3((w + kPTW - 1) / kPTW, (h + kPTH - 1) / kPTH, a.nslots), kPTW * kPTH, 0, s>>>(
+        a.io, a.st, l, w, h, phase);
   }
 }
 
