@@ -432,6 +432,74 @@ __global__ void __launch_bounds__(128, RGBID_K1L0_MINB) k_warp_residuals_l0(cons
   }
 }
 
+// A-side part of residuals_and_jacobians, constant over the IRLS iterations:
+// validity (src/alignment.cpp:209-211,227) and gradient_at of I_A and W_A
+// (src/alignment.cpp:165-191) per level pixel.  phase 1 = from the filtered A
+// into the level-0 slots (covariance pass, after the level loop).
+// Tiled: a 32 x 8 pixel tile per CTA with its 1-pixel halo of I_A and W_A staged
+// in shared memory (coalesced row loads, NaN outside the image = the reference's
+// out-of-bounds hole), so every 3 x 3 stencil read is a shared load.
+constexpr int kPTW = 32, kPTH = 8, kPRW = kPTW + 2, kPRH = kPTH + 2;
+
+// gradient_at on the staged tile (same tests and expressions)
+__device__ __forceinline__ bool grad_sm(const double* t, int i, double& gx, double& gy) {
+  const double c = t[i];
+  if (!valid(c)) return false;
+  const double l = t[i - 1], r = t[i + 1];
+  if (valid(l) && valid(r))
+    gx = (r - l) / 2.0;
+  else if (valid(r))
+    gx = r - c;
+  else if (valid(l))
+    gx = c - l;
+  else
+    return false;
+  const double u = t[i - kPRW], d = t[i + kPRW];
+  if (valid(u) && valid(d))
+    gy = (d - u) / 2.0;
+  else if (valid(d))
+    gy = d - c;
+  else if (valid(u))
+    gy = c - u;
+  else
+    return false;
+  return true;
+}
+
+__global__ void __launch_bounds__(kPTW * kPTH) k_prep_A(const SlotIO* __restrict__ io,
+                                                         const SlotState* __restrict__ st,
+                                                         int level, int w, int h, int phase) {
+  const int slot = blockIdx.z;
+  if (st[slot].status != RGBID_OK) return;
+  const SlotIO& o = io[slot];
+  const double* IA = phase ? o.fIA : o.IA[level];
+  const double* WA = phase ? o.fWA : o.WA[level];
+  __shared__ double tI[kPRW * kPRH], tW[kPRW * kPRH];
+  const int x0 = blockIdx.x * kPTW, y0 = blockIdx.y * kPTH, t = threadIdx.x;
+  for (int i = t; i < kPRW * kPRH; i += kPTW * kPTH) {
+    const int ry = i / kPRW, rx = i - ry * kPRW;
+    const int gx = x0 - 1 + rx, gy = y0 - 1 + ry;
+    const bool in = gx >= 0 && gx < w && gy >= 0 && gy < h;
+    const size_t k = (size_t)gy * w + gx;
+    tI[i] = in ? __ldg(IA + k) : CUDART_NAN;
+    tW[i] = in ? __ldg(WA + k) : CUDART_NAN;
+  }
+  __syncthreads();
+  const int tx = t % kPTW, ty = t / kPTW, x = x0 + tx, y = y0 + ty;
+  if (x >= w || y >= h) return;
+  const int i = (ty + 1) * kPRW + tx + 1;
+  const size_t k = (size_t)y * w + x;
+  const double w_a = tW[i], i_a = tI[i];
+  double g[4] = {0.0, 0.0, 0.0, 0.0};
+  unsigned m = 0;
+  if (valid(w_a) && w_a > 0.0 && valid(i_a) && grad_sm(tI, i, g[0], g[1])) m |= 1u;
+  if (grad_sm(tW, i, g[2], g[3])) m |= 2u;
+  o.amask[level][k] = (uint8_t)m;
+  double2* gp = reinterpret_cast<double2*>(o.agrad[level] + 4 * k);
+  gp[0] = make_double2(g[0], g[1]);
+  gp[1] = make_double2(g[2], g[3]);
+}
+
 // frame B interleaved {I, W} for K1's taps, once per align
 __global__ void k_interleave_B(const SlotIO* __restrict__ io, const SlotState* __restrict__ st,
                                int n) {
