@@ -452,12 +452,14 @@ def main():
         res = [(abi.AlignResult_t * n_local)() for _ in range(2)]
         cfg_c, K_c = cfg.to_c(), K.to_c()
 
+        E2E_CHUNK = int(os.environ.get("RGBID_E2E_CHUNK", "512"))
+
         def e2e_step(k):
             # streaming form: step k's first uploads overlap step k-1's last chunks;
             # results alternate between two arrays (step k-1's finish during step k)
             ctx.check(ctx.lib.rgbid_align_batch_host_async(ctx.h, n_local, *arrs, W0, H0,
                                                            C.byref(K_c), None, C.byref(cfg_c),
-                                                           512, res[k % 2]),
+                                                           E2E_CHUNK, res[k % 2]),
                       "align_batch_host_async")
 
         e2e_step(0)
@@ -482,7 +484,7 @@ def main():
         e2e = {"value": pairs_total(args, world) * e2e_steps / (float(t.item()) / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": h2d // e2e_steps, "d2h_bytes_per_step": d2h // e2e_steps,
                "path": "rgbid_align_batch_host_async/_wait (C-ABI) from pinned host buffers, 2 lanes "
-                       "x chunks of 512, consecutive steps streamed; "
+                       f"x chunks of {E2E_CHUNK}, consecutive steps streamed; "
                        f"host pool of {P} distinct pairs cycled"}
 
     cpu = None
