@@ -1561,7 +1561,7 @@ __global__ void __launch_bounds__(kTPB, RGBID_K3_MINBLOCKS) k_normal_eq(const Sl
     const int y = k / w, x = k - y * w;
     const double px = x, py = y;
     const double ax = li.cx - px, ay = li.cy - py;  // A(0,2), A(1,2)
-    const double iwa = 1.0 / w_a;
+    const double iwa = rcp_fast(w_a);  // H is tolerance-checked: MUFU + Newton, no IEEE divide
     const double k0 = red3(Ki[0] * px, Ki[1] * py, Ki[2]), k1 = red3(Ki[3] * px, Ki[4] * py, Ki[5]),
                  k2 = red3(Ki[6] * px, Ki[7] * py, Ki[8]);
     const double X0 = k0 * iwa, X1 = k1 * iwa, X2 = k2 * iwa;
@@ -1598,9 +1598,9 @@ __global__ void __launch_bounds__(kTPB, RGBID_K3_MINBLOCKS) k_normal_eq(const Sl
     {
       const double n0 = g0 * iwa, n1 = g1 * iwa, n2 = g2 * iwa + 1.0;
       const double nn2 = n0 * n0 + n1 * n1 + n2 * n2;
-      if (!(sqrt(nn2) < 1e-12)) {
+      if (!(nn2 < 1e-24)) {  // ||n|| < 1e-12 without the sqrt
         const double rr2 = k0 * k0 + k1 * k1 + k2 * k2;
-        double c = (n0 * k0 + n1 * k1 + n2 * k2) * rsqrt(nn2) * rsqrt(rr2);
+        double c = (n0 * k0 + n1 * k1 + n2 * k2) * rsqrt(nn2 * rr2);
         if (n2 < 0) c = -c;
         lambda = dmax_std(lambda_n_min, c);
       }
@@ -1686,7 +1686,7 @@ __global__ void __launch_bounds__(kTPB, RGBID_K3_MMA_MINB) k_normal_eq_mma(const
     const int y = k / w, x = k - y * w;
     const double px = x, py = y;
     const double ax = li.cx - px, ay = li.cy - py;
-    const double iwa = 1.0 / w_a;
+    const double iwa = rcp_fast(w_a);  // H is tolerance-checked: MUFU + Newton, no IEEE divide
     const double k0 = red3(Ki[0] * px, Ki[1] * py, Ki[2]), k1 = red3(Ki[3] * px, Ki[4] * py, Ki[5]),
                  k2 = red3(Ki[6] * px, Ki[7] * py, Ki[8]);
     const double X0 = k0 * iwa, X1 = k1 * iwa, X2 = k2 * iwa;
@@ -1715,9 +1715,9 @@ __global__ void __launch_bounds__(kTPB, RGBID_K3_MMA_MINB) k_normal_eq_mma(const
       {
         const double n0 = g0 * iwa, n1 = g1 * iwa, n2 = g2 * iwa + 1.0;
         const double nn2 = n0 * n0 + n1 * n1 + n2 * n2;
-        if (!(sqrt(nn2) < 1e-12)) {
+        if (!(nn2 < 1e-24)) {  // ||n|| < 1e-12 without the sqrt
           const double rr2 = k0 * k0 + k1 * k1 + k2 * k2;
-          double c = (n0 * k0 + n1 * k1 + n2 * k2) * rsqrt(nn2) * rsqrt(rr2);
+          double c = (n0 * k0 + n1 * k1 + n2 * k2) * rsqrt(nn2 * rr2);
           if (n2 < 0) c = -c;
           lambda = dmax_std(lambda_n_min, c);
         }
