@@ -1171,8 +1171,8 @@ __global__ void __launch_bounds__(kGatherThreads)
 // the 19200-sample cap (one CTA per SM, all 128 registers per thread), smaller
 // CTAs -- several per SM -- for coarse levels whose pixel count caps the sample.
 template <int NT>
-__global__ void __launch_bounds__(NT, kTdistThreads / NT)
-    k_tdist(const SlotIO* __restrict__ io, SlotState* __restrict__ st, LevelInfo li, int phase) {
+__device__ __forceinline__ void tdist_chain(const SlotIO* __restrict__ io, SlotState* __restrict__ st,
+                                            LevelInfo li, int phase) {
   const int type = blockIdx.x, slot = blockIdx.y;
   SlotState& S = st[slot];
   if (!slot_active(S, li.level, phase)) return;
@@ -1233,6 +1233,23 @@ __global__ void __launch_bounds__(NT, kTdistThreads / NT)
     }
   }
   TPH_ADD(7, tk0);
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT, kTdistThreads / NT)
+    k_tdist(const SlotIO* __restrict__ io, SlotState* __restrict__ st, LevelInfo li, int phase) {
+  tdist_chain<NT>(io, st, li, phase);
+}
+
+// The full-cap chain with a register cap instead of launch bounds: at <= 80 registers
+// (no spills) a 512-thread chain leaves a third of the register file to CTAs of the
+// other lane's kernels (K1 / K3) on the same SM.
+#ifndef RGBID_TDIST_MAXREG
+#define RGBID_TDIST_MAXREG 80
+#endif
+__global__ void __maxnreg__(RGBID_TDIST_MAXREG)
+    k_tdist_big(const SlotIO* __restrict__ io, SlotState* __restrict__ st, LevelInfo li, int phase) {
+  tdist_chain<kTdistThreads>(io, st, li, phase);
 }
 
 // Latency-mode K2: the sample of one (slot, residual type) is spread over a
@@ -1412,7 +1429,7 @@ extern "C" int rgbid_debug_tdist_phases(unsigned long long* out, int reset) {
 
 int init_kernel_attributes() {
   const cudaError_t e =
-      cudaFuncSetAttribute(k_tdist<kTdistThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      cudaFuncSetAttribute(k_tdist_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            kMaxSample * 8);
   // the smaller CTAs serve sample caps up to kMaxSample / 2 (256) and / 4 (128)
   if (kTdistThreads != 256)
@@ -1475,7 +1492,7 @@ void launch_tdist(const AlignLaunch& a, const LevelInfo& li, int phase, cudaStre
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   if (nt == kTdistThreads)
-    cudaLaunchKernelEx(&cfg, k_tdist<kTdistThreads>, a.io, (SlotState*)a.st, li, phase);
+    cudaLaunchKernelEx(&cfg, k_tdist_big, a.io, (SlotState*)a.st, li, phase);
   else if (nt == 256)
     cudaLaunchKernelEx(&cfg, k_tdist<256>, a.io, (SlotState*)a.st, li, phase);
   else
