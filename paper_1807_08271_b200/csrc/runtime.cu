@@ -968,8 +968,8 @@ int rgbid_align_batch(rgbid_ctx* ctx, int n, const rgbid_frame* const* a,
   if (validate_cfg(c, a[0]->w, a[0]->h)) return RGBID_E_ARG;
   LaunchScope ls(ctx);
   cudaSetDevice(ctx->device);
-  // chunk so the slot workspace stays bounded (~23 MB per VGA slot: 2 lanes x
-  // 1024 slots = 48 GB); 1024 measured 1.5% faster than 512 (fewer, fuller waves)
+  // chunk so the slot workspace stays bounded (~28.6 MB per VGA slot: 2 lanes x
+  // 1024 slots = 59 GB); 1024 measured 1.5% faster than 512 (fewer, fuller waves)
   const char* env = std::getenv("RGBID_BATCH_SLOTS");
   int chunk = env ? std::max(1, atoi(env)) : 1024;
   // balanced chunks alternating over the lanes (chunk c+1 is prepared and
