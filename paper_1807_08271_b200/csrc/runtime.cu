@@ -71,7 +71,10 @@ struct Lane {
   bool pend_trace = false;
   unsigned long long seq = 0;  // chunks enqueued on this lane
 };
-constexpr int kLanes = 2;
+#ifndef RGBID_LANES
+#define RGBID_LANES 2
+#endif
+constexpr int kLanes = RGBID_LANES;  // chunks co-scheduled per group (stage offsets 0..kLanes-1)
 
 struct rgbid_ctx {
   int device = 0;
@@ -88,7 +91,7 @@ struct rgbid_ctx {
   rgbid_frame* tmpA = nullptr;
   rgbid_frame* tmpB = nullptr;
   // device frames reused by rgbid_align_batch_host across calls ([lane][slot] A/B)
-  std::vector<rgbid_frame*> host_fa[2], host_fb[2];
+  std::vector<rgbid_frame*> host_fa[kLanes], host_fb[kLanes];
   // profiling (per-kernel CUDA-event times) and host<->device byte counters
   Profiler prof;
   std::map<std::string, std::pair<long long, double>> kstats;  // name -> (launches, ms)
@@ -437,6 +440,33 @@ void enqueue_align(cudaStream_t stream, const AlignLaunch& a, const rgbid_intrin
   for (auto& f : align_stages(a, K, cfg)) f(stream);
 }
 
+// G chunks in one launch sequence: stage s of chunk j after stage s of chunk j-1,
+// stage s+G of chunk 0 after stage s of chunk G-1 -> chunks run one stage apart
+// (G = 2: the pairs {A_{s+1}, B_s} run concurrently).
+void enqueue_align_group(const std::vector<cudaStream_t>& sj, const std::vector<AlignLaunch>& aj,
+                         const rgbid_intrinsics& K, const rgbid_align_config& cfg,
+                         std::vector<cudaEvent_t>& ev) {
+  const int G = (int)sj.size();
+  std::vector<std::vector<Stage>> S;
+  for (int j = 0; j < G; ++j) S.push_back(align_stages(aj[j], K, cfg));
+  const size_t n = S[0].size();
+  while (ev.size() < G * n + 1) {
+    cudaEvent_t e;
+    cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    ev.push_back(e);
+  }
+  cudaEventRecord(ev[G * n], sj[0]);  // fork off chunk 0's stream (capture origin)
+  for (int j = 1; j < G; ++j) cudaStreamWaitEvent(sj[j], ev[G * n], 0);
+  for (size_t i = 0; i < n; ++i)
+    for (int j = 0; j < G; ++j) {
+      if (j == 0 && i >= (size_t)G) cudaStreamWaitEvent(sj[0], ev[(G - 1) * n + i - G], 0);
+      if (j > 0) cudaStreamWaitEvent(sj[j], ev[(j - 1) * n + i], 0);
+      S[j][i](sj[j]);
+      cudaEventRecord(ev[j * n + i], sj[j]);
+    }
+  cudaStreamWaitEvent(sj[0], ev[(G - 1) * n + n - 1], 0);  // join
+}
+
 // Two chunks in one launch sequence: stage s of B after stage s of A, stage
 // s+2 of A after stage s of B -> the pairs {A_{s+1}, B_s} run concurrently.
 void enqueue_align_pair(cudaStream_t sA, cudaStream_t sB, const AlignLaunch& a,
@@ -686,6 +716,60 @@ int launch_prepared(rgbid_ctx* ctx, Lane& L, const AlignLaunch& a, Lane* LB,
   return RGBID_OK;
 }
 
+// Launch (graph replay) of G prepared chunks co-scheduled on lanes 0..G-1, result
+// D2H and completion events (launch_prepared generalised).
+int launch_group(rgbid_ctx* ctx, int G, const AlignLaunch* aj, const rgbid_intrinsics& K,
+                 const rgbid_align_config& cfg, rgbid_align_result* const* res, bool want_trace) {
+  Lane& L = ctx->lanes[0];
+  std::string key = graph_key(aj[0].nslots, aj[1].nslots, want_trace, aj[0].w0, aj[0].h0, K, cfg);
+  for (int j = 2; j < G; ++j) key += std::to_string(aj[j].nslots) + ",";
+  key += "G" + std::to_string(G);
+  std::vector<cudaStream_t> sj;
+  std::vector<AlignLaunch> av(aj, aj + G);
+  for (int j = 0; j < G; ++j) sj.push_back(ctx->lanes[j].stream);
+  for (int j = 1; j < G; ++j) {  // chunk j's slot records were uploaded on its own stream
+    CK(cudaEventRecord(ctx->lanes[j].ready, ctx->lanes[j].stream));
+    CK(cudaStreamWaitEvent(L.stream, ctx->lanes[j].ready, 0));
+  }
+  if (ctx->use_graphs && !ctx->prof.enabled) {
+    auto it = L.graphs.find(key);
+    if (it == L.graphs.end()) {
+      cudaGraph_t g;
+      CK(cudaStreamBeginCapture(L.stream, cudaStreamCaptureModeThreadLocal));
+      const long long before = ctx->launches;
+      enqueue_align_group(sj, av, K, cfg, ctx->pair_events);
+      CachedGraph cg;
+      cg.launches = ctx->launches - before;
+      ctx->launches = before;
+      CK(cudaStreamEndCapture(L.stream, &g));
+      CK(cudaGraphInstantiateWithFlags(&cg.exec, g, cudaGraphInstantiateFlagUseNodePriority));
+      cudaGraphDestroy(g);
+      it = L.graphs.emplace(key, cg).first;
+    }
+    CK(cudaGraphLaunch(it->second.exec, L.stream));
+    ctx->launches += it->second.launches;
+  } else {
+    enqueue_align_group(sj, av, K, cfg, ctx->pair_events);
+  }
+  int rc = check_launch(ctx);
+  if (rc) return rc;
+  for (int j = 0; j < G; ++j)
+    D2HS(L.stream, ctx->lanes[j].h_st_pinned, ctx->lanes[j].d_st, sizeof(SlotState) * aj[j].nslots);
+  CK(cudaEventRecord(L.done, L.stream));
+  for (int j = 0; j < G; ++j) {
+    Lane& Lj = ctx->lanes[j];
+    if (j > 0) {
+      CK(cudaStreamWaitEvent(Lj.stream, L.done, 0));
+      CK(cudaEventRecord(Lj.done, Lj.stream));
+    }
+    Lj.pend_n = aj[j].nslots;
+    Lj.pend_results = res[j];
+    Lj.pend_levels = cfg.levels;
+    Lj.pend_trace = j == 0 && want_trace;
+  }
+  return RGBID_OK;
+}
+
 int enqueue_chunk(rgbid_ctx* ctx, Lane& L, int n, const rgbid_frame* const* fa,
                   const rgbid_frame* const* fb, const rgbid_intrinsics& K,
                   const rgbid_pose* inits, const rgbid_align_config& cfg,
@@ -779,7 +863,7 @@ int rgbid_ctx_destroy(rgbid_ctx* ctx) {
   }
   for (auto& s : ctx->scratch)
     if (s.second.first) cudaFree(s.second.first);
-  for (int k = 0; k < 2; ++k) {
+  for (int k = 0; k < kLanes; ++k) {
     for (auto* f : ctx->host_fa[k]) rgbid_frame_destroy(ctx, f);
     for (auto* f : ctx->host_fb[k]) rgbid_frame_destroy(ctx, f);
   }
@@ -974,7 +1058,8 @@ int rgbid_align_batch(rgbid_ctx* ctx, int n, const rgbid_frame* const* a,
   int chunk = env ? std::max(1, atoi(env)) : 1024;
   // balanced chunks alternating over the lanes (chunk c+1 is prepared and
   // enqueued while chunk c runs)
-  const int nch = (n + chunk - 1) / chunk;
+  int nch = (n + chunk - 1) / chunk;
+  if (kLanes > 2 && nch > 1) nch = (nch + kLanes - 1) / kLanes * kLanes;  // whole groups
   chunk = (n + nch - 1) / nch;
   // chunks go out in co-scheduled pairs (one graph, stage-offset), except when
   // profiling (serialised kernel times) or for a trailing single chunk
@@ -982,7 +1067,20 @@ int rgbid_align_batch(rgbid_ctx* ctx, int n, const rgbid_frame* const* a,
   for (int i0 = 0; i0 < n;) {
     const int m = std::min(chunk, n - i0);
     const int m2 = pairs ? std::min(chunk, n - i0 - m) : 0;
-    if (m2 > 0 && m2 == m) {
+    if (kLanes > 2 && pairs && n - i0 >= kLanes * m && m > 0) {  // a full group of equal chunks
+      AlignLaunch aj[kLanes];
+      rgbid_align_result* rj[kLanes];
+      for (int j = 0; j < kLanes; ++j) {
+        const int o = i0 + j * m;
+        int rc = prepare_chunk(ctx, ctx->lanes[j], m, a + o, b + o, *K, inits ? inits + o : nullptr,
+                               c, j == 0 && i0 == 0, &aj[j]);
+        if (rc) return rc;
+        rj[j] = results + o;
+      }
+      int rc = launch_group(ctx, kLanes, aj, *K, c, rj, i0 == 0);
+      if (rc) return rc;
+      i0 += kLanes * m;
+    } else if (m2 > 0 && m2 == m) {
       AlignLaunch pa, pb;
       int rc = prepare_chunk(ctx, ctx->lanes[0], m, a + i0, b + i0, *K,
                              inits ? inits + i0 : nullptr, c, i0 == 0, &pa);
@@ -1005,7 +1103,7 @@ int rgbid_align_batch(rgbid_ctx* ctx, int n, const rgbid_frame* const* a,
     const int rc = finish_chunk(ctx, L);
     if (rc) return rc;
   }
-  CK(cudaStreamSynchronize(ctx->lanes[1].stream));
+  for (auto& L : ctx->lanes) CK(cudaStreamSynchronize(L.stream));
   return RGBID_OK;
 }
 
