@@ -260,7 +260,7 @@ def algorithmic_bytes(results):
 # (level 0 / covariance pass: 112; levels >= 1 add the in-tile downsample: ~122-124),
 # and DRAM bytes per slot-iteration at level 0 (read + write / 512 slots).
 K1_FLOP_PER_PX = {0: 112.0, 1: 121.4, 2: 123.8, 3: 124.5}
-K1_TRAFFIC_L0 = (3.919025e9 + 2.545017e9) / 512
+K1_TRAFFIC_L0 = (5.191611e9 + 2.551423e9) / 512
 
 
 def warp_flops(results):
@@ -373,7 +373,7 @@ def main():
         # ncu dram read+write per slot-iteration of the level-0 launch vs SURVEY 8(d)'s
         # algorithmic B_it(0) = 5M: no wasted re-reads
         "traffic": K1_TRAFFIC_L0, "traffic_algorithmic": 5 * M_BYTES,
-        "traffic_unit": "bytes per slot-iteration at level 0 (profiles/r01_k1_ncu_v14.txt)",
+        "traffic_unit": "bytes per slot-iteration at level 0 (profiles/r01_k1_ncu_v35.txt)",
         "frac": ((warp_bytes / (warp_ms / 1e3)) / 1e9) / peak if warp_ms else None,
         "kernel_share_of_step": warp_ms / prof_total if prof_total else None,
         "dominant_kernel": dom[0], "dominant_share": dom[1][1] / prof_total if prof_total else None,
