@@ -2,17 +2,21 @@
 """bench.py — frame-pair alignments/sec @640x480, 4-level (BASELINE.json config 5),
 plus ms/frame latency.
 
-Our arm (default):  `python bench.py --gpus N --steps K --warmup W` (torchrun for N>1,
-one rank per GPU over NCCL).  Each rank holds its share of the 4096 independent
-640x480 frame pairs resident in HBM (device-rendered, SURVEY §8d scene), and one
-step aligns all of them (rgbid_align_batch: 4 levels, iterations {10,5,4,5} +
-the filtered-Hessian covariance pass).  The only collective is the NCCL
-all_gather of the fixed-size result records.  Timed with CUDA events on the
-library stream, max over ranks.  Rank 0 prints one JSON line.
+Our arm (default):  `python bench.py --gpus N --steps K --warmup W`.  With N > 1 and
+no torchrun environment the script re-executes itself under
+`torch.distributed.run` (one rank per GPU over NCCL, 127.0.0.1 rendezvous).  Config
+5 read literally: 4096 independent 640x480 frame pairs IN TOTAL, partitioned into
+contiguous blocks of pair indices over the ranks; each rank renders
+its block resident in HBM and one step aligns it (rgbid_align_batch: 4 levels,
+iterations {10,5,4,5} + the filtered-Hessian covariance pass).  The only
+collective is the NCCL all_gather of the fixed-size result records.  Timed with
+CUDA events on the library stream, max over ranks.  Rank 0 prints one JSON line.
+At N > 1 a weak-scaling figure (4096 pairs per GPU) is added as a secondary field.
 
 Reference arm: `python bench.py --impl reference ...` times the reference's own
 CPU implementation (oracle/_ref: the unmodified reference sources compiled in
-place) on the host cores, on a bounded sample of the same workload.
+place) on the host cores, on a bounded sample of the same workload rendered by
+oracle/_build/librgbid_synth.so (the CUDA library is never loaded in that arm).
 """
 from __future__ import annotations
 
@@ -20,6 +24,7 @@ import argparse
 import ctypes as C
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -35,27 +40,36 @@ W0, H0, F0 = 640, 480, 480.0
 LEVELS, ITERS = 4, [10, 5, 4]  # level 3 defaults to 5 (src/alignment.cpp:373-374)
 M_BYTES = W0 * H0 * 8  # one fp64 map
 N0 = W0 * H0
+CPU_SAMPLE = 64  # pairs per reference-arm step (both scene variants)
+LAT_RUNS = 16    # single-thread latency runs (median)
 
 
-def pairs_total(args, world):
-    """weak scaling: --pairs per GPU; strong: --pairs split over the GPUs"""
-    return args.pairs * world if args.scaling == "weak" else args.pairs
+def pair_variant(i, variant):
+    """scene variant of pair i: 'mixed' alternates noisy+occluder (1) and
+    noisy+occluder+holes/border (2), SURVEY §8(d)"""
+    return 1 + (i & 1) if variant == "mixed" else int(variant)
+
+
+def variant_name(variant):
+    return {"mixed": "mixed: even pairs noisy+occluder, odd pairs noisy+occluder+5% W/2% I "
+                     "holes+20 px W border band",
+            "0": "clean", "1": "noisy+occluder", "2": "noisy+occluder+holes+border"}[str(variant)]
 
 
 def workload_config(args, world):
     return {
         "workload": "config5: batched independent 640x480 frame-pair alignments, "
                     "4-level pyramid, iterations {10,5,4,5} + filtered-Hessian covariance",
-        "pairs_total": pairs_total(args, world),
-        "pairs_per_gpu": pairs_total(args, world) // world,
+        "pairs_total": args.pairs,
+        "pairs_per_gpu": args.pairs // world,
         "levels": LEVELS,
         "iterations": [10, 5, 4, 5],
-        "variant": "noisy+occluder" if args.variant == 1 else "clean",
+        "variant": variant_name(args.variant),
         "image": f"{W0}x{H0} fp64 (intensity + inverse depth), f={F0}",
-        "parallelism": (f"{args.scaling} scaling over {world} GPU(s): each rank renders and aligns "
-                        f"its own contiguous block of pair indices; NCCL all_gather of result "
-                        f"records only"),
-        "l2": "inputs (9.8 MB/pair, 40 GB per GPU) exceed the 126 MB L2; no flush needed",
+        "parallelism": (f"strong scaling over {world} GPU(s): {args.pairs} pairs in total, rank r "
+                        f"renders and aligns the contiguous block of pair indices "
+                        f"[r*n/N, (r+1)*n/N); NCCL all_gather of result records only"),
+        "l2": "inputs (9.8 MB/pair, 40 GB per 4096 pairs) exceed the 126 MB L2; no flush needed",
     }
 
 
@@ -64,25 +78,28 @@ def parse():
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=3)
     p.add_argument("--warmup", type=int, default=3)
-    p.add_argument("--pairs", type=int, default=4096,
-                   help="pairs per GPU (weak scaling) or in total (--scaling strong)")
-    p.add_argument("--scaling", default="weak", choices=["weak", "strong"],
-                   help="weak: every GPU aligns its own --pairs independent pairs (the path "
-                        "partitions into independent units, SURVEY 8e); strong: --pairs split")
-    p.add_argument("--variant", type=int, default=1, help="0 clean, 1 noisy+occluder")
+    p.add_argument("--pairs", type=int, default=4096, help="pairs in total (config 5)")
+    p.add_argument("--weak-pairs", type=int, default=4096,
+                   help="pairs per GPU of the secondary weak-scaling figure (N > 1)")
+    p.add_argument("--variant", default="mixed", choices=["mixed", "0", "1", "2"])
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
-    p.add_argument("--cpu-sample", type=int, default=0, help="pairs in the CPU sample (0 = auto)")
+    p.add_argument("--no-extra", action="store_true", help="skip latency/config-2/config-3 figures")
+    p.add_argument("--cpu-sample", type=int, default=CPU_SAMPLE, help="pairs per reference step")
+    p.add_argument("--cpu-latency-runs", type=int, default=LAT_RUNS)
+    p.add_argument("--dump-results", default="", help="reference arm: write per-pair results (npz)")
     p.add_argument("--profile-json", default="", help="write per-kernel stats here")
     return p.parse_args()
 
 
-def partition(pairs, world, rank, scaling="strong"):
-    """Contiguous block of pair indices for this rank (no input scatter: each rank
-    renders its own).  strong: `pairs` in total; weak: `pairs` per rank."""
-    n_local = pairs if scaling == "weak" else pairs // world
-    return rank * n_local, n_local
+def partition(pairs, world, rank):
+    """Contiguous block [base, base + n) of pair indices for this rank (no input
+    scatter: each rank renders its own); the first pairs % world ranks take one more."""
+    q, r = divmod(pairs, world)
+    n = q + (1 if rank < r else 0)
+    base = rank * q + min(rank, r)
+    return base, n
 
 
 def result_records(results, n_local):
@@ -99,9 +116,11 @@ def result_records(results, n_local):
 
 
 def gather_records(rec, world, out, dist=None):
-    """The only collective of the benchmark: all_gather of the result records."""
+    """The only collective of the benchmark: all_gather of the result records
+    (ranks may hold one pair more than others: records are padded to n_max)."""
     import torch
-    t = torch.from_numpy(rec).to(out.device)
+    t = torch.zeros((out.shape[0] // world, 16), dtype=torch.float64, device=out.device)
+    t[: rec.shape[0]] = torch.from_numpy(rec).to(out.device)
     if world > 1:
         dist.all_gather_into_tensor(out, t)
     else:
@@ -112,6 +131,17 @@ def gather_records(rec, world, out, dist=None):
 def dist_env():
     return (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
             int(os.environ.get("LOCAL_RANK", "0")))
+
+
+def relaunch(args):
+    """`bench.py --gpus N` outside torchrun: one rank per GPU via torch.distributed.run."""
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1", "--master-port",
+           str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.run(cmd).returncode
 
 
 # --------------------------------------------------------------------------- clocks
@@ -171,66 +201,145 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def cpu_model():
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.startswith("Model name:"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
 # --------------------------------------------------------------------------- CPU reference
 
 
+def K_c():
+    from paper_1807_08271_b200.abi import Intrinsics_t
+    K = Intrinsics_t()
+    K.fx = K.fy = F0
+    K.cx, K.cy = (W0 - 1) / 2.0, (H0 - 1) / 2.0
+    K.width, K.height = W0, H0
+    return K
+
+
+def cfg_c(levels, iters):
+    from paper_1807_08271_b200.abi import AlignConfig_t
+    c = AlignConfig_t()
+    c.levels, c.n_iterations = levels, len(iters)
+    for i, v in enumerate(iters):
+        c.iterations[i] = v
+    c.convergence_eps, c.lambda_n_min = 1e-6, 0.1
+    c.bilateral_sigma_space, c.bilateral_sigma_intensity, c.bilateral_sigma_depth = 2.0, 0.05, 0.02
+    return c
+
+
 def host_pairs(n, variant, seed0=0):
-    """The benchmark's pairs seed0..seed0+n-1 rendered on the host
-    (rgbid_synth_pair_host: the same scene model and generator as the device
-    rendering of the timed arm, host libm)."""
+    """The benchmark's pairs seed0..seed0+n-1 rendered on the host by
+    oracle/_build/librgbid_synth.so (the scene model of the device rendering;
+    hole patterns identical, texture/noise values equal up to libm rounding)."""
     from concurrent.futures import ThreadPoolExecutor
-    import paper_1807_08271_b200 as rg
-    K = rg.simple_intrinsics(W0, H0, F0)
+    from oracle import oracle as O
+    K = K_c()
 
     def one(i):
-        fa, fb, _ = rg.synth_pair_host(K, seed0 + i, variant)
-        return (fa.intensity, fa.inverse_depth, fb.intensity, fb.inverse_depth)
+        IA, WA, IB, WB, _ = O.synth_pair_host(K, seed0 + i, pair_variant(seed0 + i, variant))
+        return (IA, WA, IB, WB)
 
     with ThreadPoolExecutor(max_workers=os.cpu_count() or 1) as ex:
         return K, list(ex.map(one, range(n)))
 
 
-def cpu_reference_rate(pairs, K, cores):
-    """oracle/_ref (reference sources compiled in place) when built, else the
-    C restatement; independent pairs on `cores` host threads."""
-    import paper_1807_08271_b200 as rg
-    from oracle import oracle as O
-    kind = "reference" if O.available("REF") else "port"
-    orc = O.Oracle("REF" if kind == "reference" else "C")
-    cfg = rg.AlignmentConfig(levels=LEVELS, iterations=ITERS).to_c()
-    t0 = time.perf_counter()
-    res = orc.align_many(pairs, K.to_c(), None, cfg, threads=cores)
-    dt = time.perf_counter() - t0
-    ok = sum(1 for r in res if r.status == 0)
-    return len(pairs) / dt, dt, kind, ok
+def input_digest(pairs):
+    import hashlib
+    h = hashlib.sha256()
+    for p in pairs:
+        for a in p:
+            h.update(a.tobytes())
+    return h.hexdigest()[:16]
 
 
 def run_reference(args, rank, world):
+    """CPU reference arm: oracle/_ref (the reference sources compiled in place) on the
+    host cores.  Per step: a bounded sample of the workload (the first --cpu-sample
+    pairs, both scene variants) aligned on all cores, one pair per thread at a time.
+    Plus single-thread latencies (median of --cpu-latency-runs) of a 3-level align
+    (config 1, clean pair), a 4-level align (config 5 pairs) and integrate_frame."""
     if rank != 0:
         return 0
+    import numpy as np
+    from oracle import oracle as O
+    kind = "reference" if O.available("REF") else "port"
+    orc = O.Oracle("REF" if kind == "reference" else "C")
     cores = os.cpu_count() or 1
-    n = args.cpu_sample or max(8, cores)
+    n = args.cpu_sample
     K, pairs = host_pairs(n, args.variant)
-    vals = []
-    kind = "reference"
+    cfg4 = cfg_c(LEVELS, ITERS)
+    vals, res = [], None
     for step in range(args.warmup + args.steps):
-        rate, dt, kind, ok = cpu_reference_rate(pairs, K, cores)
+        t0 = time.perf_counter()
+        res = orc.align_many(pairs, K, None, cfg4, threads=cores)
+        dt = time.perf_counter() - t0
         if step >= args.warmup:
-            vals.append((rate, dt))
-    rate = statistics.median(v[0] for v in vals)
-    ms = statistics.median(v[1] for v in vals) * 1000.0
-    sample = (f"the benchmark's first {n} 640x480 pairs "
-              f"({'noisy+occluder' if args.variant else 'clean'}), rendered on the host by the "
-              f"same generator, per step; 4-level align + covariance on {cores} threads, one "
-              f"pair per thread at a time")
+            vals.append(dt)
+    ms = statistics.median(vals) * 1000.0
+    rate = n / (ms / 1000.0)
+
+    # single-thread latencies (the reference is single-threaded per call)
+    lat = {}
+    if args.cpu_latency_runs > 0:
+        R = args.cpu_latency_runs
+        cfg3 = cfg_c(3, ITERS)
+        IA, WA, IB, WB, _ = O.synth_pair_host(K, 0, 0)  # clean pair, config 1
+        t3 = []
+        for _ in range(R):
+            t0 = time.perf_counter()
+            orc.align(IA, WA, IB, WB, K, None, cfg3)
+            t3.append(time.perf_counter() - t0)
+        t4 = []
+        for i in range(R):
+            p = pairs[i % len(pairs)]
+            t0 = time.perf_counter()
+            orc.align(*p, K, None, cfg4)
+            t4.append(time.perf_counter() - t0)
+        from paper_1807_08271_b200.abi import Pose_t
+        T = Pose_t()
+        T.R[0] = T.R[4] = T.R[8] = 1.0
+        kI, kW = pairs[0][0].copy(), pairs[0][1].copy()
+        kC = np.ones_like(kW)
+        tf = []
+        for i in range(R):
+            fI, fW = pairs[1 + i % (len(pairs) - 1)][2:4] if len(pairs) > 1 else pairs[0][2:4]
+            t0 = time.perf_counter()
+            orc.integrate_frame(kI, kW, kC, fI, fW, T, K, 0.05)
+            tf.append(time.perf_counter() - t0)
+        lat = {"align_3lvl_ms": statistics.median(t3) * 1e3,
+               "align_4lvl_ms": statistics.median(t4) * 1e3,
+               "integrate_frame_ms": statistics.median(tf) * 1e3,
+               "runs": R, "threads": 1,
+               "what": "single-thread wall clock, median of runs: 3-level align of a clean "
+                       "640x480 pair (config 1), 4-level align + covariance of the config-5 "
+                       "pairs, integrate_frame of a 640x480 frame"}
+    if args.dump_results:
+        ok = [r.status == 0 for r in res]
+        np.savez(args.dump_results, status=np.array([r.status for r in res]),
+                 R=np.array([list(r.T_AB.R) for r in res]), t=np.array([list(r.T_AB.t) for r in res]),
+                 iters=np.array([[r.level_log[k].iterations for k in range(LEVELS)] for r in res]),
+                 cost=np.array([[r.level_log[k].final_cost for k in range(LEVELS)] for r in res]),
+                 cov=np.array([list(r.cov) for r in res]), ok=np.array(ok),
+                 digest=input_digest(pairs))
+    sample = (f"the benchmark's first {n} 640x480 pairs ({variant_name(args.variant)}), rendered "
+              f"on the host by oracle/_build/librgbid_synth.so, per step; 4-level align + "
+              f"covariance on {cores} threads, one pair per thread at a time")
+    cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample,
+           "cpu_model": cpu_model(), "latency": lat,
+           "ok": sum(1 for r in res if r.status == 0)}
     line = {
         "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-        "scaling": args.scaling,
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
-        "config": workload_config(args, world),
-        "cpu_baseline": {"value": rate, "unit": UNIT, "cores": cores, "kind": kind,
-                         "sample": sample},
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "impl": "reference", "config": workload_config(args, world), "cpu_baseline": cpu,
         "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -261,6 +370,7 @@ def algorithmic_bytes(results):
 # and DRAM bytes per slot-iteration at level 0 (read + write / 512 slots).
 K1_FLOP_PER_PX = {0: 112.0, 1: 121.4, 2: 123.8, 3: 124.5}
 K1_TRAFFIC_L0 = (5.191611e9 + 2.551423e9) / 512
+FP64_STEP_PROFILE = os.path.join(ROOT, "profiles", "r02_fp64_flops.json")
 
 
 def warp_flops(results):
@@ -278,9 +388,149 @@ def warp_flops(results):
     return tot
 
 
+def fp64_step_roofline(kstats, ms_step, peak, n_align):
+    """Step-level FP64 roofline: ncu-measured fp64 flops per launch-slot of every kernel
+    family (profiles/r02_fp64_flops.json: DFMA x2 + DMUL + DADD + DMMA x 512 per
+    slot-launch, from an ncu --metrics capture of this bench) x the launch-slots this
+    step issued / ms_per_step, against the measured DFMA peak."""
+    if not os.path.exists(FP64_STEP_PROFILE):
+        return None
+    prof = json.load(open(FP64_STEP_PROFILE))
+    per = prof["flop_per_alignment"]  # family -> fp64 flop per alignment (bench workload)
+    tot = sum(per.values())
+    fams = {f: {"flop_per_alignment": v, "tflops_in_step": v * n_align / (ms_step / 1e3) / 1e12}
+            for f, v in per.items()}
+    ach = tot * n_align / (ms_step / 1e3) / 1e12
+    return {"achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak if peak else None,
+            "flop_per_alignment": tot, "families": fams, "source": os.path.relpath(FP64_STEP_PROFILE, ROOT),
+            "note": "whole-step fp64 work (ncu-counted per alignment of this workload) / ms_per_step"}
+
+
+def parity_block(ctx, rg, K, cfg, dump, variant):
+    """The reference arm's host-rendered pairs aligned on the GPU through the batched
+    path (co-scheduled chunk pairs), compared with the reference's results."""
+    import numpy as np
+    from oracle import oracle as O
+    d = np.load(dump)
+    n = len(d["status"])
+    Kc = K_c()
+    pairs = []
+    for i in range(n):
+        IA, WA, IB, WB, _ = O.synth_pair_host(Kc, i, pair_variant(i, variant))
+        pairs.append((IA, WA, IB, WB))
+    same_inputs = input_digest(pairs) == str(d["digest"])
+    A = [rg.DeviceFrame.from_frame(rg.FrameData(p[0], p[1]), ctx) for p in pairs]
+    B = [rg.DeviceFrame.from_frame(rg.FrameData(p[2], p[3]), ctx) for p in pairs]
+    res = rg.align_batch(A, B, K, config=cfg, ctx=ctx)
+    dt = dR = dcost = dcov = 0.0
+    it_eq = status_eq = True
+    for i, r in enumerate(res):
+        status_eq &= int(r.status) == int(d["status"][i])
+        if r.status != 0 or d["status"][i] != 0:
+            continue
+        dt = max(dt, float(np.abs(np.array(r.T_AB.t[:]) - d["t"][i]).max()))
+        Rg = np.array(r.T_AB.R[:]).reshape(3, 3)
+        Ro = d["R"][i].reshape(3, 3)
+        dR = max(dR, float(np.linalg.norm(rg.so3_log(Rg @ Ro.T))))
+        it_eq &= [r.level_log[k].iterations for k in range(LEVELS)] == list(d["iters"][i])
+        c = np.array([r.level_log[k].final_cost for k in range(LEVELS)])
+        dcost = max(dcost, float((np.abs(c - d["cost"][i]) / np.abs(d["cost"][i])).max()))
+        cv = np.array(r.cov[:])
+        dcov = max(dcov, float(np.abs(cv - d["cov"][i]).max() / np.abs(d["cov"][i]).max()))
+    for f in A + B:
+        f.close()
+    ok = same_inputs and status_eq and it_eq and dt < 1e-5 and dR < 1e-5 and dcost < 1e-4 \
+        and dcov < 1e-4
+    return {"n": n, "inputs_identical": same_inputs, "status_equal": status_eq,
+            "iterations_equal": it_eq, "max_abs_dt_m": dt, "max_dR_rad": dR,
+            "max_rel_dcost": dcost, "max_rel_dcov": dcov, "pass": bool(ok),
+            "tolerances": "pose 1e-5 m / 1e-5 rad, per-level iterations exact, per-level cost and "
+                          "covariance 1e-4 relative",
+            "path": "rgbid_align_batch on device frames, chunks co-scheduled in a two-lane graph "
+                    "(the timed path), vs oracle/_ref on the identical host-rendered pairs"}
+
+
+def frontend_ms(rg, ctx, n=60):
+    """Config 3: ms/frame of the device front-end (rgbid_frontend: align + covisibility +
+    keyframe fusion, src/pipeline.cpp:120-247) over a 640x480 sideways sweep."""
+    import numpy as np
+    from concurrent.futures import ThreadPoolExecutor
+    K = rg.simple_intrinsics(W0, H0, F0)
+    nrm = np.array([0.2, -0.15, 1.0])
+    nrm /= np.linalg.norm(nrm)
+
+    def one(i):
+        T = rg.Pose(rg.so3_exp([0.0, 0.0005 * i, 0.0]), [0.003 * i, 0.0, 0.0])
+        f = rg.render_plane(K, T, nrm, -2.0, K.width / 80.0)
+        return rg.add_noise(f, 7000 + i, 0.003, 0.001)
+
+    with ThreadPoolExecutor(max_workers=os.cpu_count() or 1) as ex:
+        frames = list(ex.map(one, range(n)))
+    fe = rg.Frontend(K, ctx=ctx)
+    ts = []
+    for i, f in enumerate(frames):
+        t0 = time.perf_counter()
+        fe.process_frame(f, 0.033 * i)
+        ts.append(time.perf_counter() - t0)
+    fe.finish()
+    kf = fe.keyframe_count()
+    fe.close()
+    steady = ts[5:]
+    return {"ms_per_frame_median": statistics.median(steady) * 1e3,
+            "ms_per_frame_mean": statistics.mean(steady) * 1e3, "frames": n, "keyframes": kf,
+            "what": "config 3: rgbid_frontend_process per 640x480 frame (host fp64 maps in, "
+                    "3-level align + covisibility + keyframe fusion on the device), host wall "
+                    "clock, frames 5.. of the sweep"}
+
+
+def fusion20(rg, ctx, abi, stream, torch):
+    """Config 2: 20 frames fused into one keyframe by one launch (k_integrate over k=20
+    frames, bit-identical to 20 integrate_frame calls); SURVEY §8(d) 24 M bytes."""
+    import numpy as np
+    K = rg.simple_intrinsics(W0, H0, F0)
+    nrm = np.array([0.2, -0.15, 1.0])
+    nrm /= np.linalg.norm(nrm)
+    first = rg.render_plane(K, rg.Pose(), nrm, -2.0, K.width / 80.0)
+    kf0 = rg.DeviceFrame.from_frame(first, ctx)  # pristine keyframe, restored before each run
+    kf = rg.DeviceFrame.from_frame(first, ctx)
+    frames, poses = [], []
+    for k in range(20):
+        T = rg.random_pose(3000 + k, 0.01, 0.01)
+        f = rg.add_noise(rg.render_plane(K, T, nrm, -2.0, K.width / 80.0), 4000 + k, 0.0, 0.01)
+        frames.append(rg.DeviceFrame.from_frame(f, ctx))
+        poses.append(T)
+    Cm = torch.empty((H0, W0), dtype=torch.float64, device="cuda")
+    Cp = C.cast(Cm.data_ptr(), abi.DP)
+    arr = (C.c_void_p * 20)(*[f.h.value for f in frames])
+    P = (abi.Pose_t * 20)(*[p.to_c() for p in poses])
+    Kc = K.to_c()
+    ts = []
+    for r in range(13):
+        # same 20 frames into the same keyframe every run (stream-ordered restore)
+        ctx.check(ctx.lib.rgbid_frame_copy(ctx.h, kf.h, kf0.h), "frame_copy")
+        ctx.check(ctx.lib.rgbid_fill(ctx.h, Cp, H0 * W0, 1.0), "fill")
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        ctx.check(ctx.lib.rgbid_integrate_frames(ctx.h, kf.h, Cp, 20, arr, P, C.byref(Kc), 0.05),
+                  "integrate_frames")
+        e1.record(stream)
+        e1.synchronize()
+        if r >= 3:
+            ts.append(e0.elapsed_time(e1))
+    for f in frames + [kf, kf0]:
+        f.close()
+    ms = statistics.median(ts)
+    return {"ms": ms, "algorithmic_bytes": 24 * M_BYTES,
+            "achieved_gbs": 24 * M_BYTES / (ms / 1e3) / 1e9,
+            "what": "config 2: 20 frames fused into one 640x480 keyframe, one k_integrate launch "
+                    "(CUDA events, median of 10); bytes = SURVEY 8(d) 24 M"}
+
+
 def main():
     args = parse()
     rank, world, local = dist_env()
+    if args.gpus > 1 and "RANK" not in os.environ:
+        return relaunch(args)
     if args.impl == "reference":
         return run_reference(args, rank, world)
 
@@ -297,59 +547,81 @@ def main():
     ctx = rg.Context(local)
     K = rg.simple_intrinsics(W0, H0, F0)
     cfg = rg.AlignmentConfig(levels=LEVELS, iterations=ITERS)
-    base, n_local = partition(args.pairs, world, rank, args.scaling)
+    base, n_local = partition(args.pairs, world, rank)
+    n_max = partition(args.pairs, world, 0)[1]
 
     # inputs resident in HBM: device-rendered pairs (pair seed = global index)
     A = [rg.DeviceFrame(W0, H0, ctx) for _ in range(n_local)]
     B = [rg.DeviceFrame(W0, H0, ctx) for _ in range(n_local)]
     for i in range(n_local):
-        rg.synth_pair_device(A[i], B[i], K, base + i, args.variant)
+        rg.synth_pair_device(A[i], B[i], K, base + i, pair_variant(base + i, args.variant))
     ctx.synchronize()
     stream = torch.cuda.ExternalStream(ctx.stream_ptr)
-    gathered = torch.empty((world * n_local, 16), dtype=torch.float64, device="cuda")
+    gathered = torch.empty((world * n_max, 16), dtype=torch.float64, device="cuda")
 
     def gather(results):
-        gather_records(result_records(results, n_local), world, gathered, dist)
+        gather_records(result_records(results, len(results)), world, gathered, dist)
         return results
 
-    def step():
-        for f in A:  # fresh inputs each step: pyramids are rebuilt like the reference does
+    def step(fa, fb):
+        for f in fa:  # fresh inputs each step: pyramids are rebuilt like the reference does
             f.invalidate()
-        return gather(rg.align_batch(A, B, K, config=cfg, ctx=ctx))
+        return gather(rg.align_batch(fa, fb, K, config=cfg, ctx=ctx))
 
-    for _ in range(args.warmup):
-        results = step()
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    clocks = ClockSampler(local)
-    clocks.start()
-    launches0 = ctx.kernel_launches
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize()
-    ev0.record(stream)
-    for _ in range(args.steps):
-        results = step()
-    ev1.record(stream)
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    clk = clocks.stop()
-    launches = ctx.kernel_launches - launches0
-    ms = ev0.elapsed_time(ev1)
-    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
-    value = pairs_total(args, world) * args.steps / (ms_max / 1000.0)
+    def timed(fa, fb, steps, warmup):
+        for _ in range(warmup):
+            step(fa, fb)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        clocks = ClockSampler(local)
+        clocks.start()
+        l0 = ctx.kernel_launches
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for _ in range(steps):
+            res = step(fa, fb)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        clk = clocks.stop()
+        ms = ev0.elapsed_time(ev1)
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return res, float(t.item()), clk, ctx.kernel_launches - l0
+
+    results, ms_max, clk, launches = timed(A, B, args.steps, args.warmup)
+    value = args.pairs * args.steps / (ms_max / 1000.0)
     statuses = {int(r.status) for r in results}
     n_ok = sum(1 for r in results if r.status == 0)
     mean_iters = float(np.mean([r.total_iterations for r in results if r.status == 0] or [0]))
 
+    # secondary: weak scaling (--weak-pairs per GPU), N > 1 only
+    weak = None
+    if world > 1 and args.weak_pairs > 0:
+        wb, wn = rank * args.weak_pairs, args.weak_pairs
+        A2 = [rg.DeviceFrame(W0, H0, ctx) for _ in range(wn)]
+        B2 = [rg.DeviceFrame(W0, H0, ctx) for _ in range(wn)]
+        for i in range(wn):
+            rg.synth_pair_device(A2[i], B2[i], K, wb + i, pair_variant(wb + i, args.variant))
+        ctx.synchronize()
+        gathered = torch.empty((world * wn, 16), dtype=torch.float64, device="cuda")
+        ws = max(1, min(args.steps, 2))
+        _, wms, _, _ = timed(A2, B2, ws, 1)
+        weak = {"value": world * wn * ws / (wms / 1e3), "unit": UNIT, "pairs_per_gpu": wn,
+                "steps": ws, "ms_per_step": wms / ws,
+                "what": f"weak scaling: each of the {world} ranks aligns its own {wn} pairs"}
+        for f in A2 + B2:
+            f.close()
+        gathered = torch.empty((world * n_max, 16), dtype=torch.float64, device="cuda")
+
     # profiled step (graph-less, CUDA events around every launch) -> dominant kernel roofline
     ctx.set_profiling(True)
     ctx.reset_stats()
-    presults = step()
+    presults = step(A, B)
     ctx.synchronize()
     kstats = ctx.kernel_stats()
     ctx.set_profiling(False)
@@ -364,7 +636,6 @@ def main():
         f = k.split("_L")[0].replace("_cov", "")
         fam[f] = fam.get(f, 0.0) + v[1]
     dom = max(fam.items(), key=lambda kv: kv[1]) if fam else ("none", 0.0)
-    dom = (dom[0], (0, dom[1]))
     warp_ms = sum(v[1] for k, v in kstats.items() if k.startswith("warp_residuals"))
     roofline = {
         "bound": "hbm", "kernel": "warp_residuals",
@@ -376,8 +647,9 @@ def main():
         "traffic_unit": "bytes per slot-iteration at level 0 (profiles/r01_k1_ncu_v35.txt)",
         "frac": ((warp_bytes / (warp_ms / 1e3)) / 1e9) / peak if warp_ms else None,
         "kernel_share_of_step": warp_ms / prof_total if prof_total else None,
-        "dominant_kernel": dom[0], "dominant_share": dom[1][1] / prof_total if prof_total else None,
-        "pipeline_achieved_gbs": (tot_bytes / (ms_max / args.steps / 1e3)) / 1e9 * world
+        "dominant_kernel": dom[0], "dominant_share": dom[1] / prof_total if prof_total else None,
+        "family_share_of_step": {k: v / prof_total for k, v in sorted(fam.items())} if prof_total else {},
+        "pipeline_achieved_gbs": (tot_bytes * world / (ms_max / args.steps / 1e3)) / 1e9
         if ms_max else None,
         "algorithmic_bytes_per_alignment": tot_bytes / max(1, sum(1 for r in presults if r.status == 0)),
         "note": "achieved = SURVEY 8(d) algorithmic bytes of the executed IRLS iterations / "
@@ -387,13 +659,11 @@ def main():
         json.dump({"kernels": kstats, "bytes": {"total": tot_bytes, "warp": warp_bytes}},
                   open(args.profile_json, "w"), indent=1)
 
-    # measured FP64 FMA peak: denominator of the FP64-issue-bound Student-t kernel
+    # measured FP64 FMA peak: denominator of the FP64-issue-bound kernels
     fp64 = C.c_double(0.0)
     ctx.check(ctx.lib.rgbid_measure_fp64_peak(ctx.h, C.byref(fp64)), "fp64_peak")
     tdist_ms = sum(v[1] for k, v in kstats.items() if k.startswith("tdist"))
     roofline["fp64_peak_tflops_measured"] = fp64.value
-    # the warp kernels are fp64-issue- and load-latency-bound rather than HBM-bound
-    # (~2.8 TB/s and ~31% fp64 instruction issue per ncu): report both ceilings
     wfl = warp_flops(presults)
     if warp_ms and fp64.value > 0:
         ach = wfl / (warp_ms / 1e3) / 1e12
@@ -403,11 +673,12 @@ def main():
                             "note": "ncu-measured flop per full-res pixel x pixels warped in "
                                     "the profiled step / its CUDA-event time; peak = "
                                     "rgbid_measure_fp64_peak (dependent-free DFMA stream)"}
+    roofline["fp64_step"] = fp64_step_roofline(kstats, ms_max / args.steps, fp64.value, n_local)
     roofline["tdist_share_of_step"] = tdist_ms / prof_total if prof_total else None
 
-    # latency: one pair, device-resident, 4 levels; + one keyframe fusion
+    # latency: one pair, device-resident, 4 levels; one keyframe fusion; config 2; config 3
     lat = {}
-    if rank == 0:
+    if rank == 0 and not args.no_extra:
         for _ in range(3):
             rg.align(A[0], B[0], K, config=cfg, ctx=ctx)
         ts = []
@@ -436,6 +707,10 @@ def main():
                "frame_ms": statistics.median(ts) + statistics.median(fs),
                "what": "one 640x480 4-level align (device-resident pair, incl. covariance) + "
                        "one integrate_frame; CUDA events, median of 10"}
+        lat["fusion_ms_hbm_frac"] = 5 * M_BYTES / (lat["fusion_ms"] / 1e3) / 1e9 / peak
+        lat["config2_fusion20"] = fusion20(rg, ctx, abi, stream, torch)
+        lat["config2_fusion20"]["hbm_frac"] = lat["config2_fusion20"]["achieved_gbs"] / peak
+        lat["config3_frontend"] = frontend_ms(rg, ctx)
 
     # end-to-end through the C-ABI with HOST buffers (pinned), copies in the timed region
     e2e = None
@@ -450,15 +725,15 @@ def main():
         ptrs = [[pn[i % P, k].ctypes.data_as(abi.DP) for i in range(n_local)] for k in range(4)]
         arrs = [(abi.DP * n_local)(*p) for p in ptrs]
         res = [(abi.AlignResult_t * n_local)() for _ in range(2)]
-        cfg_c, K_c = cfg.to_c(), K.to_c()
+        cfg_c_, K_c_ = cfg.to_c(), K.to_c()
 
-        E2E_CHUNK = int(os.environ.get("RGBID_E2E_CHUNK", "512"))
+        E2E_CHUNK = int(os.environ.get("RGBID_E2E_CHUNK", str(min(512, max(1, n_local // 2)))))
 
         def e2e_step(k):
             # streaming form: step k's first uploads overlap step k-1's last chunks;
             # results alternate between two arrays (step k-1's finish during step k)
             ctx.check(ctx.lib.rgbid_align_batch_host_async(ctx.h, n_local, *arrs, W0, H0,
-                                                           C.byref(K_c), None, C.byref(cfg_c),
+                                                           C.byref(K_c_), None, C.byref(cfg_c_),
                                                            E2E_CHUNK, res[k % 2]),
                       "align_batch_host_async")
 
@@ -481,25 +756,26 @@ def main():
         t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
         if world > 1:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e = {"value": pairs_total(args, world) * e2e_steps / (float(t.item()) / 1e3), "unit": UNIT,
+        e2e = {"value": args.pairs * e2e_steps / (float(t.item()) / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": h2d // e2e_steps, "d2h_bytes_per_step": d2h // e2e_steps,
                "path": "rgbid_align_batch_host_async/_wait (C-ABI) from pinned host buffers, 2 lanes "
                        f"x chunks of {E2E_CHUNK}, consecutive steps streamed; "
                        f"host pool of {P} distinct pairs cycled"}
 
-    cpu = None
+    cpu, parity = None, None
     if rank == 0 and world == 1 and not args.no_cpu:
         # the reference arm's measurement, in a clean process (this one holds a CUDA
         # context, torch threads and pinned pools that slow a host-thread sweep ~1.5x):
-        # the benchmark's first n pairs from the same generator, rendered on the host
+        # the benchmark's first pairs from the same scene model, rendered on the host;
+        # its per-pair results feed the parity block
         cores = os.cpu_count() or 1
-        n = args.cpu_sample or max(8, cores)
+        dump = os.path.join("/tmp", f"rgbid_ref_results_{os.getpid()}.npz")
         env = {k: v for k, v in os.environ.items()
                if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK", "LOCAL_WORLD_SIZE")}
         pr = subprocess.run([sys.executable, os.path.abspath(__file__), "--impl", "reference",
-                             "--steps", "1", "--warmup", "1", "--cpu-sample", str(n),
-                             "--variant", str(args.variant)],
-                            env=env, capture_output=True, text=True, timeout=900)
+                             "--steps", "1", "--warmup", "0", "--cpu-sample", str(args.cpu_sample),
+                             "--variant", str(args.variant), "--dump-results", dump],
+                            env=env, capture_output=True, text=True, timeout=1800)
         try:
             ref = json.loads(pr.stdout.strip().splitlines()[-1])
             cpu = dict(ref["cpu_baseline"])
@@ -507,16 +783,21 @@ def main():
         except (IndexError, KeyError, ValueError):
             cpu = {"value": None, "unit": UNIT, "cores": cores, "kind": "reference",
                    "sample": "reference subprocess failed: " + pr.stderr.strip()[-200:]}
+        if os.path.exists(dump):
+            try:
+                parity = parity_block(ctx, rg, K, cfg, dump, args.variant)
+            finally:
+                os.remove(dump)
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-            "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (device-rendered textured slanted plane, SURVEY 8d)",
             "config": workload_config(args, world),
             "clocks": clk, "gpu_launches": launches, "e2e": e2e, "roofline": roofline,
-            "cpu_baseline": cpu, "latency": lat,
+            "cpu_baseline": cpu, "parity": parity, "latency": lat, "weak_scaling": weak,
             "status": {"ok": n_ok, "statuses": sorted(statuses), "mean_iterations": mean_iters},
         }
         print(json.dumps(line), flush=True)

@@ -126,6 +126,7 @@ int rgbid_ctx_destroy(rgbid_ctx* ctx);
 const char* rgbid_ctx_last_error(rgbid_ctx* ctx);
 /* count of this library's kernel launches on ctx since creation */
 long long rgbid_ctx_kernel_launches(rgbid_ctx* ctx);
+/* waits for all of ctx's streams; completes pending async batch chunks */
 int rgbid_ctx_synchronize(rgbid_ctx* ctx);
 /* stream used by ctx (cudaStream_t, as void*) */
 void* rgbid_ctx_stream(rgbid_ctx* ctx);
@@ -191,6 +192,11 @@ int rgbid_align_batch(rgbid_ctx* ctx, int n, const rgbid_frame* const* a,
                       const rgbid_frame* const* b, const rgbid_intrinsics* K,
                       const rgbid_pose* inits, const rgbid_align_config* cfg,
                       rgbid_align_result* results);
+/* How rgbid_align_batch splits n pairs: *n_chunks chunks of <= *chunk slots
+ * (1024 cap, RGBID_BATCH_SLOTS overrides), executed as co-scheduled chunk pairs
+ * on the ctx's two lanes; a batch of >= 64 pairs is always split in two so the
+ * lanes overlap.  Host-only (no device needed). */
+int rgbid_batch_plan(int n, int* chunk, int* n_chunks);
 /* Batched alignments from HOST buffers (end-to-end path): pair i reads
  * I_A[i], W_A[i], I_B[i], W_B[i] (each width*height doubles, pinned memory
  * recommended).  Uploads are pipelined with compute in chunks of `chunk` pairs. */
@@ -203,9 +209,11 @@ int rgbid_align_batch_host(rgbid_ctx* ctx, int n, const double* const* I_A,
 /* Streaming form of rgbid_align_batch_host: returns once every chunk is enqueued;
  * the last chunks (one per stream) may still be running, and their entries of
  * `results` (and the host buffers they read) must stay valid until the next
- * rgbid_align_batch_host_async / rgbid_align_batch_host call on ctx, or until
- * rgbid_align_batch_host_wait.  Consecutive calls overlap one batch's first
- * uploads with the previous batch's last chunks. */
+ * rgbid_align_batch_host_async / rgbid_align_batch_host call on ctx RETURNS (it
+ * completes every chunk of the previous call before returning), or until
+ * rgbid_align_batch_host_wait / rgbid_ctx_synchronize / any synchronous align
+ * call on ctx.  Consecutive calls overlap one batch's first uploads with the
+ * previous batch's last chunks. */
 int rgbid_align_batch_host_async(rgbid_ctx* ctx, int n, const double* const* I_A,
                                  const double* const* W_A, const double* const* I_B,
                                  const double* const* W_B, int width, int height,
@@ -376,7 +384,9 @@ int rgbid_synth_add_noise(double* I, double* W, int width, int height, uint32_t 
                           double sigma_i, double sigma_w);
 /* Device-side generation of batch pair i (bench): renders A and B of
  * pair (seed_base + i) directly into frames a and b. variant 0 = clean,
- * 1 = noisy + 20% near occluder (counter-based Gaussian noise). */
+ * 1 = noisy + 20% near occluder (counter-based Gaussian noise), 2 = variant 1 +
+ * 5% W / 2% I seeded holes and a width/32-pixel W border band.
+ * The hole pattern is integer-hashed: identical to rgbid_synth_pair_host's. */
 int rgbid_synth_pair_device(rgbid_ctx* ctx, rgbid_frame* a, rgbid_frame* b,
                             const rgbid_intrinsics* K, uint32_t pair_seed, int variant,
                             rgbid_pose* T_AB_truth);

@@ -25,6 +25,7 @@ from paper_1807_08271_b200.abi import (DP, AlignConfig_t, AlignResult_t, DepthIn
 HERE = os.path.dirname(os.path.abspath(__file__))
 ORACLE_SO = os.path.join(HERE, "_build", "librgbid_oracle.so")
 REF_SO = os.path.join(HERE, "_ref", "librgbid_ref.so")
+SYNTH_SO = os.path.join(HERE, "_build", "librgbid_synth.so")
 REF_TESTS = os.path.join(HERE, "_ref", "ref_hotpath_tests")
 REF_SRC = "/root/reference/proj"
 
@@ -112,6 +113,32 @@ def _get(kind):
 
 def available(kind: str) -> bool:
     return os.path.exists(ORACLE_SO if kind == "C" else REF_SO)
+
+
+_synth = None
+
+
+def synth_pair_host(K, pair_seed, variant=1):
+    """Benchmark pair `pair_seed` rendered on the host by oracle/_build/librgbid_synth.so
+    (the product's synth.cpp built alone, so the CPU reference arm never maps the CUDA
+    library): (I_A, W_A, I_B, W_B, T_AB_truth as Pose_t).  K: Intrinsics_t."""
+    global _synth
+    if _synth is None:
+        if not os.path.exists(SYNTH_SO):
+            raise RuntimeError(f"{SYNTH_SO} missing (run oracle.build())")
+        L = C.CDLL(SYNTH_SO)
+        L.rgbid_synth_pair_host.restype = C.c_int
+        L.rgbid_synth_pair_host.argtypes = [C.POINTER(Intrinsics_t), C.c_uint, C.c_int, DP, DP, DP,
+                                            DP, C.POINTER(Pose_t)]
+        _synth = L
+    h, w = K.height, K.width
+    IA, WA, IB, WB = (np.empty((h, w)) for _ in range(4))
+    T = Pose_t()
+    rc = _synth.rgbid_synth_pair_host(C.byref(K), pair_seed, variant, dptr(IA), dptr(WA), dptr(IB),
+                                      dptr(WB), C.byref(T))
+    if rc != 0:
+        raise ValueError("synth_pair_host: invalid argument")
+    return IA, WA, IB, WB, T
 
 
 class Oracle:

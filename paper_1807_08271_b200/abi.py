@@ -129,6 +129,7 @@ EXPORTS = [
                                    C.POINTER(AlignConfig_t), C.POINTER(AlignResult_t)]),
     ("rgbid_last_align_trace", C.c_int, [VP, C.POINTER(IterTrace_t), C.c_int,
                                          C.POINTER(C.c_int)]),
+    ("rgbid_batch_plan", C.c_int, [C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     ("rgbid_align_batch", C.c_int, [VP, C.c_int, C.POINTER(VP), C.POINTER(VP),
                                     C.POINTER(Intrinsics_t), C.POINTER(Pose_t),
                                     C.POINTER(AlignConfig_t), C.POINTER(AlignResult_t)]),

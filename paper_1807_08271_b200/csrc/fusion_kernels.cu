@@ -246,21 +246,16 @@ void launch_forward_register(const double* WA, int w, int h, const RegisterMats&
 }
 
 // ---------------------------------------------------------------------------
-// Device synthetic pair (bench inputs): render_plane of tests/synthetic.hpp:24-50
-// with plane_texture at tex_scale * (X, Y), optional Gaussian noise
-// (counter-based hash + Box-Muller) and a 20% near occluder (test_alignment.cpp:220-232).
+// Device synthetic pair (bench inputs, synth_scene.cuh): render_plane of
+// tests/synthetic.hpp:24-50 with plane_texture at tex_scale * (X, Y), optional
+// Gaussian noise (counter-based hash + Box-Muller), a 20% near occluder
+// (test_alignment.cpp:220-232) and seeded holes / a border band.
 __device__ __forceinline__ double plane_texture_d(double x, double y) {
   return 0.5 + 0.2 * sin(7.3 * x) * cos(5.9 * y) + 0.15 * sin(3.1 * x + 2.7 * y) +
          0.1 * cos(11.0 * x - 4.0 * y);
 }
-__device__ __forceinline__ unsigned long long splitmix(unsigned long long z) {
-  z += 0x9e3779b97f4a7c15ull;
-  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
-  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
-  return z ^ (z >> 31);
-}
 __device__ __forceinline__ double gauss(unsigned long long key) {
-  const unsigned long long a = splitmix(key), b = splitmix(key ^ 0xda3e39cb94b95bdbull);
+  const unsigned long long a = synth_splitmix(key), b = synth_splitmix(key ^ 0xda3e39cb94b95bdbull);
   const double u1 = ((a >> 11) + 0.5) * (1.0 / 9007199254740992.0);
   const double u2 = ((b >> 11) + 0.5) * (1.0 / 9007199254740992.0);
   return sqrt(-2.0 * log(u1)) * cos(6.283185307179586 * u2);
@@ -289,6 +284,8 @@ __global__ void k_render(SynthView v, double* __restrict__ I, double* __restrict
     iv = plane_texture_d(7.0 + 0.1 * x * 80.0 / v.w, 3.0 + 0.1 * y * 80.0 / v.w);
     wv = 1.0;
   }
+  if (synth_hole_i(v, i)) iv = CUDART_NAN;
+  if (synth_hole_w(v, i, x, y)) wv = CUDART_NAN;
   I[i] = iv;
   W[i] = wv;
 }

@@ -5,6 +5,7 @@
 #include <cstdint>
 
 #include "hd_math.cuh"
+#include "synth_scene.cuh"
 
 namespace rgbid_b200 {
 
@@ -24,15 +25,6 @@ struct RegisterMats {  // forward_register host-side setup (src/warping.cpp:22-2
   double tt[3];
 };
 
-struct SynthView {
-  int w, h;
-  M3 Kinv, R;
-  double t[3], n[3], d;
-  double tex_scale;
-  double noise_i, noise_w;
-  unsigned long long seed;
-  int occluder;
-};
 
 void launch_integrate(const FuseFrame* frames_dev, int k, double* kfW, double* kfC, int w, int h,
                       double sigma_w, cudaStream_t s);

@@ -69,7 +69,8 @@ struct Lane {
   rgbid_align_result* pend_results = nullptr;
   int pend_levels = 0;
   bool pend_trace = false;
-  unsigned long long seq = 0;  // chunks enqueued on this lane
+  unsigned long long pend_call = 0;  // host batch call that queued the pending chunk
+  unsigned long long seq = 0;        // chunks enqueued on this lane
 };
 #ifndef RGBID_LANES
 #define RGBID_LANES 2
@@ -96,6 +97,7 @@ struct rgbid_ctx {
   Profiler prof;
   std::map<std::string, std::pair<long long, double>> kstats;  // name -> (launches, ms)
   long long h2d_bytes = 0, d2h_bytes = 0;
+  unsigned long long host_call = 0;  // rgbid_align_batch_host(_async) calls so far
 };
 
 namespace {
@@ -289,12 +291,25 @@ void free_lane_ws(Lane& L) {
   L.d_st = nullptr;
   L.h_st_pinned = nullptr;
   L.cap_slots = 0;
-  for (auto& g : L.graphs) cudaGraphExecDestroy(g.second.exec);
-  L.graphs.clear();
+}
+
+// Cached graphs bake in the AlignLaunch of every lane they co-schedule (a chunk
+// pair cached on lane 0 holds lane 1's d_io / d_st), so any lane's reallocation
+// invalidates the graphs of all lanes.
+void drop_graphs(rgbid_ctx* ctx) {
+  for (auto& L : ctx->lanes) {
+    for (auto& g : L.graphs) cudaGraphExecDestroy(g.second.exec);
+    L.graphs.clear();
+  }
 }
 
 int ensure_workspace(rgbid_ctx* ctx, Lane& L, int nslots, int w, int h) {
   if (nslots <= L.cap_slots && w == L.cap_w && h == L.cap_h) return RGBID_OK;
+  // same resolution: grow to the lane's peak slot count (no shrink thrash);
+  // a new resolution is sized for this call only (a 2048-pair VGA batch followed
+  // by one 1280x960 pair must not allocate 1024 x 114 MB)
+  if (w == L.cap_w && h == L.cap_h) nslots = std::max(nslots, L.cap_slots);
+  drop_graphs(ctx);
   free_lane_ws(L);
   CK(cudaMalloc(&L.ws_f64, sizeof(double) * slot_f64(w, h) * nslots));
   CK(cudaMalloc(&L.ws_i32, sizeof(int) * slot_i32(w, h) * nslots));
@@ -531,6 +546,15 @@ int finish_chunk(rgbid_ctx* ctx, Lane& L) {
   return RGBID_OK;
 }
 
+// Completes every lane's pending chunk (results written to the caller's arrays).
+int finish_all(rgbid_ctx* ctx) {
+  for (auto& L : ctx->lanes) {
+    const int rc = finish_chunk(ctx, L);
+    if (rc) return rc;
+  }
+  return RGBID_OK;
+}
+
 // Enqueues n alignments (one chunk) on lane L: slot setup, H2D of the slot
 // records, the (cached) CUDA graph of the whole align, D2H of the results.
 int prepare_chunk(rgbid_ctx* ctx, Lane& L, int n, const rgbid_frame* const* fa,
@@ -540,7 +564,7 @@ int prepare_chunk(rgbid_ctx* ctx, Lane& L, int n, const rgbid_frame* const* fa,
   int rc = finish_chunk(ctx, L);  // the lane's previous chunk owns h_st_pinned
   if (rc) return rc;
   const int w = fa[0]->w, h = fa[0]->h;
-  rc = ensure_workspace(ctx, L, std::max(n, L.cap_slots), w, h);
+  rc = ensure_workspace(ctx, L, n, w, h);
   if (rc) return rc;
   for (int i = 0; i < n; ++i) {
     rc = frame_alloc_pyramid(ctx, const_cast<rgbid_frame*>(fa[i]));
@@ -786,9 +810,25 @@ int run_align_slots(rgbid_ctx* ctx, int n, const rgbid_frame* const* fa,
                     const rgbid_pose* inits, const rgbid_align_config& cfg,
                     rgbid_align_result* results, bool want_trace) {
   Lane& L = ctx->lanes[0];
-  int rc = enqueue_chunk(ctx, L, n, fa, fb, K, inits, cfg, results, want_trace);
+  int rc = finish_all(ctx);  // a synchronous call leaves no chunk of an earlier call pending
+  if (rc) return rc;
+  rc = enqueue_chunk(ctx, L, n, fa, fb, K, inits, cfg, results, want_trace);
   if (rc) return rc;
   return finish_chunk(ctx, L);
+}
+
+// Slots per chunk of an n-pair batch.  Chunks bound the slot workspace (~28.6 MB
+// per VGA slot: 2 lanes x 1024 slots = 59 GB) and alternate over the lanes; they
+// go out in co-scheduled pairs, so a batch that fits one chunk is still split in
+// two (e.g. 512 pairs per GPU at 8 GPUs -> 2 x 256) whenever both halves keep
+// >= 32 slots.  RGBID_BATCH_SLOTS overrides the 1024 cap (read on every call).
+int batch_chunk(int n) {
+  const char* env = std::getenv("RGBID_BATCH_SLOTS");
+  const int cap = env ? std::max(1, atoi(env)) : 1024;
+  int nch = (n + cap - 1) / cap;
+  if (nch == 1 && n >= 64) nch = 2;
+  if (nch > 1) nch = (nch + kLanes - 1) / kLanes * kLanes;  // whole pairs / groups
+  return (n + nch - 1) / nch;
 }
 
 int frame_from_host(rgbid_ctx* ctx, rgbid_frame** slot, int w, int h, const double* I,
@@ -809,7 +849,14 @@ int frame_from_host(rgbid_ctx* ctx, rgbid_frame** slot, int w, int h, const doub
 // ===========================================================================
 extern "C" {
 
-const char* rgbid_version(void) { return "rgbid_b200 0.1 (sm_100a)"; }
+const char* rgbid_version(void) { return "rgbid_b200 0.2 (sm_100a)"; }
+
+int rgbid_batch_plan(int n, int* chunk, int* n_chunks) {
+  if (n < 0 || !chunk || !n_chunks) return RGBID_E_ARG;
+  *chunk = n > 0 ? batch_chunk(n) : 0;
+  *n_chunks = n > 0 ? (n + *chunk - 1) / *chunk : 0;
+  return RGBID_OK;
+}
 
 const char* rgbid_status_string(int s) {
   switch (s) {
@@ -857,10 +904,9 @@ int rgbid_ctx_destroy(rgbid_ctx* ctx) {
   if (!ctx) return RGBID_E_ARG;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
-  for (auto& L : ctx->lanes) {
-    cudaStreamSynchronize(L.stream);
-    free_lane_ws(L);
-  }
+  for (auto& L : ctx->lanes) cudaStreamSynchronize(L.stream);
+  drop_graphs(ctx);
+  for (auto& L : ctx->lanes) free_lane_ws(L);
   for (auto& s : ctx->scratch)
     if (s.second.first) cudaFree(s.second.first);
   for (int k = 0; k < kLanes; ++k) {
@@ -884,7 +930,10 @@ const char* rgbid_ctx_last_error(rgbid_ctx* ctx) { return ctx ? ctx->err.c_str()
 long long rgbid_ctx_kernel_launches(rgbid_ctx* ctx) { return ctx ? ctx->launches : 0; }
 int rgbid_ctx_synchronize(rgbid_ctx* ctx) {
   if (!ctx) return RGBID_E_ARG;
-  CK(cudaStreamSynchronize(ctx->stream));
+  LaunchScope ls(ctx);
+  const int rc = finish_all(ctx);  // every lane's pending chunk, not only lane 0's
+  if (rc) return rc;
+  for (auto& L : ctx->lanes) CK(cudaStreamSynchronize(L.stream));
   return RGBID_OK;
 }
 void* rgbid_ctx_stream(rgbid_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
@@ -1052,15 +1101,9 @@ int rgbid_align_batch(rgbid_ctx* ctx, int n, const rgbid_frame* const* a,
   if (validate_cfg(c, a[0]->w, a[0]->h)) return RGBID_E_ARG;
   LaunchScope ls(ctx);
   cudaSetDevice(ctx->device);
-  // chunk so the slot workspace stays bounded (~28.6 MB per VGA slot: 2 lanes x
-  // 1024 slots = 59 GB); 1024 measured 1.5% faster than 512 (fewer, fuller waves)
-  const char* env = std::getenv("RGBID_BATCH_SLOTS");
-  int chunk = env ? std::max(1, atoi(env)) : 1024;
-  // balanced chunks alternating over the lanes (chunk c+1 is prepared and
-  // enqueued while chunk c runs)
-  int nch = (n + chunk - 1) / chunk;
-  if (kLanes > 2 && nch > 1) nch = (nch + kLanes - 1) / kLanes * kLanes;  // whole groups
-  chunk = (n + nch - 1) / nch;
+  int rc0 = finish_all(ctx);  // chunks an earlier async host call left in flight
+  if (rc0) return rc0;
+  const int chunk = batch_chunk(n);
   // chunks go out in co-scheduled pairs (one graph, stage-offset), except when
   // profiling (serialised kernel times) or for a trailing single chunk
   const bool pairs = !ctx->prof.enabled && std::getenv("RGBID_NO_PAIRS") == nullptr;
@@ -1080,7 +1123,7 @@ int rgbid_align_batch(rgbid_ctx* ctx, int n, const rgbid_frame* const* a,
       int rc = launch_group(ctx, kLanes, aj, *K, c, rj, i0 == 0);
       if (rc) return rc;
       i0 += kLanes * m;
-    } else if (m2 > 0 && m2 == m) {
+    } else if (m2 > 0) {  // unequal sizes too (the graph key holds both)
       AlignLaunch pa, pb;
       int rc = prepare_chunk(ctx, ctx->lanes[0], m, a + i0, b + i0, *K,
                              inits ? inits + i0 : nullptr, c, i0 == 0, &pa);
@@ -1150,6 +1193,7 @@ static int align_batch_host_enqueue(rgbid_ctx* ctx, int n, const double* const* 
     }
   }
   const size_t bytes = sizeof(double) * (size_t)w * h;
+  const unsigned long long call = ++ctx->host_call;
   int lane = 0;
   for (int i0 = 0; i0 < n; i0 += chunk, lane = (lane + 1) % kLanes) {
     const int m = std::min(chunk, n - i0);
@@ -1167,7 +1211,16 @@ static int align_batch_host_enqueue(rgbid_ctx* ctx, int n, const double* const* 
     rc = enqueue_chunk(ctx, L, m, fa[lane].data(), fb[lane].data(), *K,
                        inits ? inits + i0 : nullptr, c, results + i0, i0 == 0);
     if (rc) return cleanup(), rc;
+    L.pend_call = call;
   }
+  // a lane this call did not reuse may still hold the previous call's last chunk:
+  // complete it now, so every result of call k is written when call k+1 returns
+  // (only this call's chunks stay in flight)
+  for (auto& L : ctx->lanes)
+    if (L.pend_n > 0 && L.pend_call != call) {
+      const int rc = finish_chunk(ctx, L);
+      if (rc) return cleanup(), rc;
+    }
   return RGBID_OK;
 }
 
@@ -1493,16 +1546,12 @@ int rgbid_forward_register(rgbid_ctx* ctx, const double* WA, int w, int h, const
   return RGBID_OK;
 }
 
-namespace {
-void synth_pair_views(const rgbid_intrinsics* K, uint32_t pair_seed, int variant, SynthView* va,
-                      SynthView* vb, rgbid_pose* T_AB_truth);
-}  // namespace
 
 int rgbid_synth_pair_device(rgbid_ctx* ctx, rgbid_frame* a, rgbid_frame* b,
                             const rgbid_intrinsics* K, uint32_t pair_seed, int variant,
                             rgbid_pose* T_AB_truth) {
   if (!ctx || !a || !b || !K || a->w != K->width || a->h != K->height || b->w != a->w ||
-      b->h != a->h)
+      b->h != a->h || variant < 0 || variant > 2)
     return RGBID_E_ARG;
   LaunchScope ls(ctx);
   // Pair geometry: A at a small random pose, B = A * random_pose(seed, 3 mm, 0.02 rad)
@@ -1515,97 +1564,6 @@ int rgbid_synth_pair_device(rgbid_ctx* ctx, rgbid_frame* a, rgbid_frame* b,
   int rc = check_launch(ctx);
   if (rc) return rc;
   CK(cudaStreamSynchronize(ctx->stream));
-  return RGBID_OK;
-}
-
-namespace {
-// host restatement of fusion_kernels.cu's k_render (plane_texture_d, splitmix/Box-Muller)
-double plane_texture_h(double x, double y) {
-  return 0.5 + 0.2 * std::sin(7.3 * x) * std::cos(5.9 * y) + 0.15 * std::sin(3.1 * x + 2.7 * y) +
-         0.1 * std::cos(11.0 * x - 4.0 * y);
-}
-unsigned long long splitmix_h(unsigned long long z) {
-  z += 0x9e3779b97f4a7c15ull;
-  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
-  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
-  return z ^ (z >> 31);
-}
-double gauss_h(unsigned long long key) {
-  const unsigned long long a = splitmix_h(key), b = splitmix_h(key ^ 0xda3e39cb94b95bdbull);
-  const double u1 = ((a >> 11) + 0.5) * (1.0 / 9007199254740992.0);
-  const double u2 = ((b >> 11) + 0.5) * (1.0 / 9007199254740992.0);
-  return std::sqrt(-2.0 * std::log(u1)) * std::cos(6.283185307179586 * u2);
-}
-void render_h(const SynthView& v, double* I, double* W) {
-  for (int i = 0; i < v.w * v.h; ++i) {
-    const int y = i / v.w, x = i - y * v.w;
-    const V3 p = {{(double)x, (double)y, 1.0}};
-    const V3 kp = m3_mulv(v.Kinv, p);
-    const V3 r = m3_mulv(v.R, kp);
-    const double denom = red3(v.n[0] * r.v[0], v.n[1] * r.v[1], v.n[2] * r.v[2]);
-    double iv = std::nan(""), wv = std::nan("");
-    if (std::fabs(denom) >= 1e-12) {
-      const double lambda = -(red3(v.n[0] * v.t[0], v.n[1] * v.t[1], v.n[2] * v.t[2]) + v.d) / denom;
-      if (lambda > 0.05) {
-        const double X = v.t[0] + lambda * r.v[0], Y = v.t[1] + lambda * r.v[1];
-        iv = plane_texture_h(v.tex_scale * X, v.tex_scale * Y);
-        wv = 1.0 / lambda;
-      }
-    }
-    if (v.noise_i > 0.0 && std::isfinite(iv)) iv += v.noise_i * gauss_h(v.seed * 0x100000000ull + 2ull * i);
-    if (v.noise_w > 0.0 && std::isfinite(wv))
-      wv += v.noise_w * gauss_h(v.seed * 0x100000000ull + 2ull * i + 1);
-    if (v.occluder && x < v.w / 5) {
-      iv = plane_texture_h(7.0 + 0.1 * x * 80.0 / v.w, 3.0 + 0.1 * y * 80.0 / v.w);
-      wv = 1.0;
-    }
-    I[i] = iv;
-    W[i] = wv;
-  }
-}
-// the pair geometry and views of rgbid_synth_pair_device
-void synth_pair_views(const rgbid_intrinsics* K, uint32_t pair_seed, int variant, SynthView* va,
-                      SynthView* vb, rgbid_pose* T_AB_truth) {
-  rgbid_pose pa, pab;
-  rgbid_synth_random_pose(5000u + pair_seed, 0, 0.01, 0.01, &pa);
-  rgbid_synth_random_pose(1000u + pair_seed, 0, 0.003, 0.02, &pab);
-  const PoseD TA = pose_of(&pa), TAB = pose_of(&pab);
-  const PoseD TB = pose_compose(TA, TAB);
-  if (T_AB_truth) pose_to(TAB, T_AB_truth->R, T_AB_truth->t);
-  double n[3] = {0.2, -0.15, 1.0};
-  const double nn = std::sqrt(red3(n[0] * n[0], n[1] * n[1], n[2] * n[2]));
-  for (double& v : n) v /= nn;
-  auto view = [&](const PoseD& T, unsigned long long seed) {
-    SynthView v;
-    v.w = K->width;
-    v.h = K->height;
-    v.Kinv = m3_inv(K_mat(K->fx, K->fy, K->cx, K->cy));
-    v.R = T.R;
-    for (int i = 0; i < 3; ++i) {
-      v.t[i] = T.t.v[i];
-      v.n[i] = n[i];
-    }
-    v.d = -2.0;
-    v.tex_scale = K->width / 80.0;
-    v.noise_i = variant ? 0.005 : 0.0;
-    v.noise_w = variant ? 0.002 : 0.0;
-    v.seed = seed;
-    v.occluder = 0;
-    return v;
-  };
-  *va = view(TA, 2u * pair_seed + 1);
-  *vb = view(TB, 2u * pair_seed + 2);
-  vb->occluder = variant ? 1 : 0;
-}
-}  // namespace
-
-int rgbid_synth_pair_host(const rgbid_intrinsics* K, uint32_t pair_seed, int variant, double* IA,
-                          double* WA, double* IB, double* WB, rgbid_pose* T_AB_truth) {
-  if (!K || !IA || !WA || !IB || !WB || K->width <= 0 || K->height <= 0) return RGBID_E_ARG;
-  SynthView va, vb;
-  synth_pair_views(K, pair_seed, variant, &va, &vb, T_AB_truth);
-  render_h(va, IA, WA);
-  render_h(vb, IB, WB);
   return RGBID_OK;
 }
 

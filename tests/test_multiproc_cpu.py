@@ -28,9 +28,10 @@ def _worker(rank, world, port, q):
     import bench
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    base, n = bench.partition(64, world, rank)
+    base, n = bench.partition(65, world, rank)  # uneven: rank 0 holds one pair more
+    n_max = bench.partition(65, world, 0)[1]
     rec = bench.result_records([_R(base + i) for i in range(n)], n)
-    out = torch.empty((world * n, 16), dtype=torch.float64)
+    out = torch.empty((world * n_max, 16), dtype=torch.float64)
     bench.gather_records(rec, world, out, dist)
     t = torch.tensor([float(rank + 1)])
     dist.all_reduce(t, op=dist.ReduceOp.MAX)  # max-over-ranks timing reduction
@@ -52,9 +53,11 @@ def test_partition_and_gather_world2():
         p.join(timeout=60)
         assert p.exitcode == 0
     assert tmax == 2.0
-    assert out.shape == (64, 16)
-    np.testing.assert_array_equal(out[:, 0], np.arange(64, dtype=float))
-    np.testing.assert_array_equal(out[:, 13], 10 + np.arange(64, dtype=float))
+    assert out.shape == (66, 16)  # 2 x 33 padded records, rank 1's last slot empty
+    got = np.concatenate([out[:33], out[33:65]])
+    np.testing.assert_array_equal(got[:, 0], np.arange(65, dtype=float))
+    np.testing.assert_array_equal(got[:, 13], 10 + np.arange(65, dtype=float))
+    assert not out[65].any()
 
 
 @pytest.mark.parametrize("world", [2, 8])
@@ -67,13 +70,13 @@ def test_partition_covers_all_pairs(world):
     assert seen == list(range(4096))
 
 
-@pytest.mark.parametrize("world", [2, 8])
-def test_weak_partition_gives_each_rank_its_own_pairs(world):
+@pytest.mark.parametrize("pairs,world", [(4096, 2), (4096, 8), (4097, 8), (5, 8)])
+def test_partition_uneven_blocks(pairs, world):
     import bench
-    blocks = [bench.partition(4096, world, r, "weak") for r in range(world)]
-    assert all(n == 4096 for _, n in blocks)
-    seen = [i for base, n in blocks for i in range(base, base + n)]
-    assert seen == list(range(4096 * world))
+    blocks = [bench.partition(pairs, world, r) for r in range(world)]
+    sizes = [n for _, n in blocks]
+    assert sum(sizes) == pairs and max(sizes) - min(sizes) <= 1
+    assert [b for b, _ in blocks] == [sum(sizes[:r]) for r in range(world)]
 
 
 def test_reference_arm_nonzero_rank_exits_clean():
@@ -81,3 +84,23 @@ def test_reference_arm_nonzero_rank_exits_clean():
     p = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference"],
                        env=env, capture_output=True, text=True, timeout=120)
     assert p.returncode == 0 and p.stdout.strip() == ""
+
+
+def test_gpus_flag_relaunches_one_rank_per_gpu():
+    """`bench.py --gpus 2` outside torchrun re-executes itself under
+    torch.distributed.run (--gpus was a dead flag): both ranks start,
+    rank 0 alone prints one JSON line carrying n_gpus = 2, every rank exits 0."""
+    import json
+    env = {k: v for k, v in os.environ.items()
+           if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK", "LOCAL_WORLD_SIZE", "MASTER_ADDR",
+                        "MASTER_PORT")}
+    p = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--impl",
+                        "reference", "--steps", "1", "--warmup", "0", "--cpu-sample", "2",
+                        "--cpu-latency-runs", "0"],
+                       env=env, capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, p.stderr[-2000:]
+    lines = [ln for ln in p.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    line = json.loads(lines[0])
+    assert line["n_gpus"] == 2 and line["impl"] == "reference"
+    assert line["cpu_baseline"]["ok"] == 2
