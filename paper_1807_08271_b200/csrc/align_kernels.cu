@@ -37,6 +37,9 @@
 #ifndef RGBID_K1_IWB
 #define RGBID_K1_IWB 1  // K1 samples frame B from an interleaved {I, W} copy (L0: -11%)
 #endif
+#ifndef RGBID_K1_SHFL
+#define RGBID_K1_SHFL 1  // levels 2-3: shuffle downsample, no per-stage block barriers
+#endif
 
 namespace rgbid_b200 {
 
@@ -360,6 +363,117 @@ __global__ void __launch_bounds__(k1_threads<L>(), RGBID_K1_THREADS_PER_SM / k1_
   }
 }
 
+// Coarse-level K1 without block barriers in the downsample (levels 2 and 3): each
+// warp owns whole level-L pixels.  A lane computes one (L = 2) or two vertically
+// adjacent (L = 3) level-1 values, each the downsample2 of its 2x2 full-res warps
+// in registers; the level-2 / level-3 downsamples combine neighbouring lanes'
+// values with shuffles, taps in the reference order (0,0),(1,0),(0,1),(1,1)
+// (inc/image.hpp:73-91).  L = 2: lanes 4q..4q+3 hold the 2x2 level-1 block of output
+// q (8 outputs per warp); L = 3: lanes 8q..8q+7 hold level-1 columns 0..3 x row
+// pairs {0,1}, {2,3} of output q (4 outputs per warp).  The tile (tx level pixels of
+// one level row, 8 warps) is the same as k_warp_residuals<L>'s, so the per-tile
+// counts and row-major validity words are unchanged; one barrier at the end
+// assembles them.
+template <int L>
+__global__ void __launch_bounds__(256, RGBID_K1_THREADS_PER_SM / 256) k_warp_residuals_shfl(
+    const SlotIO* __restrict__ io, const SlotState* __restrict__ st, LevelInfo li, int w0, int h0,
+    int phase) {
+  static_assert(L == 2 || L == 3, "shuffle downsample for levels 2 and 3");
+  constexpr int G = L == 2 ? 4 : 8;    // lanes per level-L output
+  constexpr int OPW = 32 / G;          // outputs per warp
+  constexpr int R1 = L == 2 ? 1 : 2;   // level-1 values per lane (vertical)
+  const int slot = blockIdx.y;
+  const SlotState& S = st[slot];
+  if (!slot_active(S, L, phase)) return;
+  __shared__ WarpMats wm;
+  __shared__ unsigned char sbits[2][8];
+  if (threadIdx.x < 24)
+    reinterpret_cast<double*>(&wm)[threadIdx.x] = reinterpret_cast<const double*>(&S.wm)[threadIdx.x];
+  const SlotIO& o = io[slot];
+  const double* __restrict__ WAw = phase ? o.fWA : o.WA[0];
+  const double* __restrict__ IAl = phase ? o.fIA : o.IA[L];
+  const uint8_t* __restrict__ am = o.amask[L];
+  __syncthreads();
+  const int tile = blockIdx.x;
+  const int yl = tile / li.nseg, seg = tile - yl * li.nseg;
+  const int xl0 = seg * li.tx;
+  const int nx = min(li.tx, li.w - xl0);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int q = lane / G, sub = lane % G;
+  const int ol = wid * OPW + q;  // output (level-L pixel) index within the tile
+  const bool live = ol < nx;
+  // this lane's level-1 column and first level-1 row within the output's block
+  const int c1 = L == 2 ? (sub & 1) : (sub & 3);
+  const int r1 = L == 2 ? (sub >> 1) : 2 * (sub >> 2);
+  const int X1 = ((xl0 + ol) << (L - 1)) + c1, Y1 = (yl << (L - 1)) + r1;
+  double v1i[R1], v1w[R1];
+#pragma unroll
+  for (int r = 0; r < R1; ++r) {
+    v1i[r] = v1w[r] = CUDART_NAN;
+    if (live) {
+      const int x = 2 * X1, y = 2 * (Y1 + r);
+      double vi[4], vw[4], d0, d1;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int xx = x + (k & 1), yy = y + (k >> 1);
+        warp_px_iw(wm, o.IWB, w0, h0, xx, yy, __ldg(WAw + yy * w0 + xx), vi[k], vw[k], d0, d1);
+      }
+      v1i[r] = ds4(vi[0], vi[1], vi[2], vi[3]);
+      v1w[r] = ds4(vw[0], vw[1], vw[2], vw[3]);
+    }
+  }
+  double oi, ow;
+  if (L == 2) {  // lanes 4q + {0,1,2,3} = level-1 (0,0),(1,0),(0,1),(1,1)
+    const double i1 = __shfl_down_sync(0xffffffffu, v1i[0], 1), w1 = __shfl_down_sync(0xffffffffu, v1w[0], 1);
+    const double i2 = __shfl_down_sync(0xffffffffu, v1i[0], 2), w2 = __shfl_down_sync(0xffffffffu, v1w[0], 2);
+    const double i3 = __shfl_down_sync(0xffffffffu, v1i[0], 3), w3 = __shfl_down_sync(0xffffffffu, v1w[0], 3);
+    oi = ds4(v1i[0], i1, i2, i3);
+    ow = ds4(v1w[0], w1, w2, w3);
+  } else {  // level 2 at sub 0, 2, 4, 6 from (own, lane+1) x (row pair), then level 3 at sub 0
+    const double a1 = __shfl_down_sync(0xffffffffu, v1i[0], 1), b1 = __shfl_down_sync(0xffffffffu, v1w[0], 1);
+    const double a3 = __shfl_down_sync(0xffffffffu, v1i[1], 1), b3 = __shfl_down_sync(0xffffffffu, v1w[1], 1);
+    const double l2i = ds4(v1i[0], a1, v1i[1], a3), l2w = ds4(v1w[0], b1, v1w[1], b3);
+    const double i2 = __shfl_down_sync(0xffffffffu, l2i, 2), w2 = __shfl_down_sync(0xffffffffu, l2w, 2);
+    const double i4 = __shfl_down_sync(0xffffffffu, l2i, 4), w4 = __shfl_down_sync(0xffffffffu, l2w, 4);
+    const double i6 = __shfl_down_sync(0xffffffffu, l2i, 6), w6 = __shfl_down_sync(0xffffffffu, l2w, 6);
+    oi = ds4(l2i, i2, i4, i6);
+    ow = ds4(l2w, w2, w4, w6);
+  }
+  bool jet = false, dep = false;
+  if (live && sub == 0) {
+    const int idx = yl * li.w + xl0 + ol;
+    o.ibw[idx] = make_double2(oi - __ldg(IAl + idx), ow);  // r_I (src/alignment.cpp:222), w_b
+    const unsigned a = __ldg(am + idx);
+    jet = (a & 1u) && valid(oi);
+    dep = jet && (a & 2u) && valid(ow) && ow > 0.0;
+  }
+  const unsigned bj = __ballot_sync(0xffffffffu, jet), bd = __ballot_sync(0xffffffffu, dep);
+  if (lane == 0) {  // compress bits G*k -> k
+    unsigned cj = 0, cd = 0;
+#pragma unroll
+    for (int k = 0; k < OPW; ++k) {
+      cj |= ((bj >> (G * k)) & 1u) << k;
+      cd |= ((bd >> (G * k)) & 1u) << k;
+    }
+    sbits[0][wid] = (unsigned char)cj;
+    sbits[1][wid] = (unsigned char)cd;
+  }
+  __syncthreads();
+  // row-major validity words of the tile (32 level pixels each) and the counts
+  constexpr int WPW = 32 / OPW;  // warps per word
+  const int words = (li.tx + 31) / 32;
+  if (threadIdx.x < 2 * words) {
+    const int t = threadIdx.x / words, wd = threadIdx.x % words;
+    unsigned m = 0;
+#pragma unroll
+    for (int k = 0; k < WPW; ++k) m |= (unsigned)sbits[t][wd * WPW + k] << (OPW * k);
+    (t ? o.bitsW : o.bitsI)[tile * kWordsPerTile + wd] = m;
+    const int c = __popc(m);
+    const int tot = c + __shfl_down_sync(words == 2 ? 0xfu : 0x3u, c, 1, words);
+    if (wd == 0) (t ? o.cntW : o.cntI)[tile] = words == 2 ? tot : c;
+  }
+}
+
 // Level-0 K1: 128 threads per 256-pixel tile, two independent pixels per thread
 // (x and x + 128) so their dependent load chains (W_A -> gathers) overlap.
 #ifndef RGBID_K1L0_MINB
@@ -441,7 +555,8 @@ __global__ void __launch_bounds__(128, RGBID_K1L0_MINB) k_warp_residuals_l0(cons
 // out-of-bounds hole), so every 3 x 3 stencil read is a shared load.
 constexpr int kPTW = 32, kPTH = 8, kPRW = kPTW + 2, kPRH = kPTH + 2;
 
-// gradient_at on the staged tile (same tests and expressions)
+// gradient_at on a staged tile of row stride RS (same tests and expressions)
+template <int RS = kPRW>
 __device__ __forceinline__ bool grad_sm(const double* t, int i, double& gx, double& gy) {
   const double c = t[i];
   if (!valid(c)) return false;
@@ -454,7 +569,7 @@ __device__ __forceinline__ bool grad_sm(const double* t, int i, double& gx, doub
     gx = c - l;
   else
     return false;
-  const double u = t[i - kPRW], d = t[i + kPRW];
+  const double u = t[i - RS], d = t[i + RS];
   if (valid(u) && valid(d))
     gy = (d - u) / 2.0;
   else if (valid(d))
@@ -495,9 +610,11 @@ __global__ void __launch_bounds__(kPTW * kPTH) k_prep_A(const SlotIO* __restrict
   if (valid(w_a) && w_a > 0.0 && valid(i_a) && grad_sm(tI, i, g[0], g[1])) m |= 1u;
   if (grad_sm(tW, i, g[2], g[3])) m |= 2u;
   o.amask[level][k] = (uint8_t)m;
-  double2* gp = reinterpret_cast<double2*>(o.agrad[level] + 4 * k);
-  gp[0] = make_double2(g[0], g[1]);
-  gp[1] = make_double2(g[2], g[3]);
+  if (!RGBID_K3_TILE) {
+    double2* gp = reinterpret_cast<double2*>(o.agrad[level] + 4 * k);
+    gp[0] = make_double2(g[0], g[1]);
+    gp[1] = make_double2(g[2], g[3]);
+  }
 }
 
 // frame B interleaved {I, W} for K1's taps, once per align
@@ -562,8 +679,18 @@ void launch_warp_residuals(const AlignLaunch& a, const LevelInfo& li, int phase,
   switch (li.level) {
     case 0: k_warp_residuals_l0<<<grid, 128, 0, s>>>(a.io, a.st, li, a.w0, a.h0, phase); break;
     case 1: k_warp_residuals<1><<<grid, k1_threads<1>(), 0, s>>>(a.io, a.st, li, a.w0, a.h0, phase); break;
-    case 2: k_warp_residuals<2><<<grid, k1_threads<2>(), 0, s>>>(a.io, a.st, li, a.w0, a.h0, phase); break;
-    case 3: k_warp_residuals<3><<<grid, k1_threads<3>(), 0, s>>>(a.io, a.st, li, a.w0, a.h0, phase); break;
+    case 2:
+      if (RGBID_K1_SHFL)
+        k_warp_residuals_shfl<2><<<grid, 256, 0, s>>>(a.io, a.st, li, a.w0, a.h0, phase);
+      else
+        k_warp_residuals<2><<<grid, k1_threads<2>(), 0, s>>>(a.io, a.st, li, a.w0, a.h0, phase);
+      break;
+    case 3:
+      if (RGBID_K1_SHFL)
+        k_warp_residuals_shfl<3><<<grid, 256, 0, s>>>(a.io, a.st, li, a.w0, a.h0, phase);
+      else
+        k_warp_residuals<3><<<grid, k1_threads<3>(), 0, s>>>(a.io, a.st, li, a.w0, a.h0, phase);
+      break;
     case 4: k_warp_residuals<4><<<grid, k1_threads<4>(), 0, s>>>(a.io, a.st, li, a.w0, a.h0, phase); break;
     case 5: k_warp_residuals<5><<<grid, k1_threads<5>(), 0, s>>>(a.io, a.st, li, a.w0, a.h0, phase); break;
     default: return;
@@ -1427,6 +1554,15 @@ extern "C" int rgbid_debug_tdist_phases(unsigned long long* out, int reset) {
 }
 #endif
 
+#ifndef RGBID_K3_MMA_MINB
+#define RGBID_K3_MMA_MINB 3
+#endif
+constexpr int kT3SW = kT3W + 2, kT3SH = kT3H + 2;
+constexpr int kT3Smem = 2 * kT3SW * kT3SH * 8 + (kTPB / 32) * (32 * 9 + 64) * 8;
+__global__ void __launch_bounds__(kTPB, RGBID_K3_MMA_MINB)
+    k_normal_eq_tile(const SlotIO* __restrict__ io, const SlotState* __restrict__ st, LevelInfo li,
+                     int phase, double lambda_n_min);
+
 int init_kernel_attributes() {
   const cudaError_t e =
       cudaFuncSetAttribute(k_tdist_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1439,6 +1575,7 @@ int init_kernel_attributes() {
     cudaFuncSetAttribute(k_tdist<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          kMaxSample / 4 * 8);
   cudaFuncSetAttribute(k_gather, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+  cudaFuncSetAttribute(k_normal_eq_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, kT3Smem);
   const cudaError_t e2 =
       cudaFuncSetAttribute(k_tdist_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
   if (kTdistCluster > 8)
@@ -1780,9 +1917,176 @@ __global__ void __launch_bounds__(kTPB, RGBID_K3_MMA_MINB) k_normal_eq_mma(const
   }
 }
 
+// K3 on 2-D tiles of kT3W x kT3H level pixels: the CTA stages I_A and W_A of its
+// tile plus a 1-pixel halo in shared memory (NaN outside the image = the
+// reference's out-of-bounds hole) and evaluates the A-side validity and
+// gradient_at (src/alignment.cpp:165-191,206-211,227) from it, so the only
+// per-pixel stream besides the staged A maps is K1's {r_I, w_b} pairs (32 B/px of
+// DRAM instead of 57 with a precomputed gradient stream).  Rows, weights and the
+// FP64-MMA accumulation are those of k_normal_eq_mma.  Warp w owns tile rows
+// w, w + 8, ...; each iteration is 32 consecutive pixels of one row.
+__global__ void __launch_bounds__(kTPB, RGBID_K3_MMA_MINB) k_normal_eq_tile(const SlotIO* __restrict__ io,
+                                                         const SlotState* __restrict__ st,
+                                                         LevelInfo li, int phase,
+                                                         double lambda_n_min) {
+  const int slot = blockIdx.y;
+  const SlotState& S = st[slot];
+  if (!slot_active(S, li.level, phase)) return;  // uniform over the CTA
+  const SlotIO& o = io[slot];
+  const double* __restrict__ IA = phase ? o.fIA : o.IA[li.level];
+  const double* __restrict__ WA = phase ? o.fWA : o.WA[li.level];
+  const double2* __restrict__ ibwp = o.ibw;
+  constexpr int XS = 9;  // 8 components + w per staged row
+  extern __shared__ double k3sm[];
+  double* tI = k3sm;
+  double* tW = k3sm + kT3SW * kT3SH;
+  double* xs = tW + kT3SW * kT3SH;           // [kTPB/32][32 * XS]
+  double* cst = xs + (kTPB / 32) * 32 * XS;  // [kTPB/32][64]
+  const int w = li.w, h = li.h;
+  const int ntx = (w + kT3W - 1) / kT3W;
+  const int ty0 = blockIdx.x / ntx, tx0 = blockIdx.x - ty0 * ntx;
+  const int x0 = tx0 * kT3W, y0 = ty0 * kT3H;
+  for (int i = threadIdx.x; i < kT3SW * kT3SH; i += kTPB) {
+    const int ry = i / kT3SW, rx = i - ry * kT3SW;
+    const int gx = x0 - 1 + rx, gy = y0 - 1 + ry;
+    const bool in = gx >= 0 && gx < w && gy >= 0 && gy < h;
+    const size_t k = (size_t)gy * w + gx;
+    tI[i] = in ? __ldg(IA + k) : CUDART_NAN;
+    tW[i] = in ? __ldg(WA + k) : CUDART_NAN;
+  }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double* xw = xs + wid * 32 * XS;
+  const double muI = S.tI.mu, isgI = 1.0 / S.tI.sigma, nuI = dmax_std(S.tI.nu, S.tW.nu);
+  const double muW = S.tW.mu, isgW = 1.0 / S.tW.sigma, nuW = S.tW.nu;
+  const double nuI1 = nuI + 1.0, nuW1 = nuW + 1.0;
+  const double is2i = isgI * isgI, is2w = isgW * isgW;
+  const double* Ki = li.Kinv;
+  double c0 = 0.0, c1 = 0.0;
+  auto mma_rows = [&]() {
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int row = 4 * j + (lane & 3);
+      const double xv = xw[row * XS + (lane >> 2)], wv = xw[row * XS + 8];
+      dmma884(c0, c1, wv * xv, xv);
+    }
+    __syncwarp();
+  };
+  constexpr int kIt = kT3W * kT3H / kTPB;  // 8 iterations of 32 pixels per warp
+  auto pix = [&](int it, int& x, int& y, int& r, int& c) {
+    r = wid + (kTPB / 32) * (it / (kT3W / 32));
+    c = lane + 32 * (it % (kT3W / 32));
+    x = x0 + c;
+    y = y0 + r;
+  };
+  // K1's pairs of the first iteration in flight during the staging barrier
+  int x, y, r, c;
+  pix(0, x, y, r, c);
+  bool inr = x < w && y < h;
+  double2 rw = inr ? __ldcs(ibwp + (size_t)y * w + x) : make_double2(0.0, 0.0);
+  __syncthreads();
+#pragma unroll 1
+  for (int it = 0; it < kIt; ++it) {
+    const double r_I = rw.x, w_b = rw.y;
+    const int xc = x, yc = y, rc = r, cc = c;
+    const bool inc = inr;
+    if (it + 1 < kIt) {  // prefetch the next iteration's pair
+      pix(it + 1, x, y, r, c);
+      inr = x < w && y < h;
+      rw = inr ? __ldcs(ibwp + (size_t)y * w + x) : make_double2(0.0, 0.0);
+    }
+    const int si = (rc + 1) * kT3SW + cc + 1;
+    const double w_a = tW[si], i_a = tI[si];
+    double gIx = 0.0, gIy = 0.0, gWx = 0.0, gWy = 0.0;
+    const bool okI = grad_sm<kT3SW>(tI, si, gIx, gIy);
+    const bool okW = grad_sm<kT3SW>(tW, si, gWx, gWy);
+    // jet validity (src/alignment.cpp:206-211): valid(i_a) and valid(i_b) <=> valid(r_I)
+    const bool jet = inc && valid(w_a) && w_a > 0.0 && valid(i_a) && okI && valid(r_I);
+    const bool dep = jet && okW && valid(w_b) && w_b > 0.0;
+    const double px = xc, py = yc;
+    const double ax = li.cx - px, ay = li.cy - py;
+    const double iwa = rcp_fast(jet ? w_a : 1.0);  // tolerance-checked H: MUFU + Newton
+    const double k0 = red3(Ki[0] * px, Ki[1] * py, Ki[2]), k1 = red3(Ki[3] * px, Ki[4] * py, Ki[5]),
+                 k2 = red3(Ki[6] * px, Ki[7] * py, Ki[8]);
+    const double X0 = k0 * iwa, X1 = k1 * iwa, X2 = k2 * iwa;
+    {  // photometric row
+      const double s0 = w_a * gIx, s1 = w_a * gIy;
+      const double u0 = s0 * li.fx, u1 = s1 * li.fy, u2 = s0 * ax + s1 * ay;
+      const double xi_ = (r_I - muI) * isgI;
+      const double wi = nuI1 * rcp_fast(fma(xi_, xi_, nuI)) * is2i;
+      double* rr = xw + lane * XS;
+      rr[0] = jet ? u0 : 0.0;
+      rr[1] = jet ? u1 : 0.0;
+      rr[2] = jet ? u2 : 0.0;
+      rr[3] = jet ? X1 * u2 - X2 * u1 : 0.0;
+      rr[4] = jet ? X2 * u0 - X0 * u2 : 0.0;
+      rr[5] = jet ? X0 * u1 - X1 * u0 : 0.0;
+      rr[6] = jet ? r_I : 0.0;
+      rr[7] = 0.0;
+      rr[8] = jet ? wi : 0.0;
+    }
+    mma_rows();
+    {  // geometric row
+      const double g0 = gWx * li.fx, g1 = gWy * li.fy, g2 = gWx * ax + gWy * ay;
+      const double s0 = w_a * g0, s1 = w_a * g1, s2 = w_a * (g2 + w_b);
+      double lambda = 1.0;
+      {
+        const double n0 = g0 * iwa, n1 = g1 * iwa, n2 = g2 * iwa + 1.0;
+        const double nn2 = n0 * n0 + n1 * n1 + n2 * n2;
+        if (!(nn2 < 1e-24)) {  // ||n|| < 1e-12 without the sqrt
+          const double rr2 = k0 * k0 + k1 * k1 + k2 * k2;
+          double cth = (n0 * k0 + n1 * k1 + n2 * k2) * rsqrt(nn2 * rr2);
+          if (n2 < 0) cth = -cth;
+          lambda = dmax_std(lambda_n_min, cth);
+        }
+      }
+      const double rW = w_b - w_a;
+      const double xw_ = (rW - muW) * isgW;
+      const double ww = lambda * nuW1 * rcp_fast(fma(xw_, xw_, nuW)) * is2w;
+      double* rr = xw + lane * XS;
+      rr[0] = dep ? s0 : 0.0;
+      rr[1] = dep ? s1 : 0.0;
+      rr[2] = dep ? s2 : 0.0;
+      rr[3] = dep ? X1 * s2 - X2 * s1 : 0.0;
+      rr[4] = dep ? X2 * s0 - X0 * s2 : 0.0;
+      rr[5] = dep ? X0 * s1 - X1 * s0 : 0.0;
+      rr[6] = dep ? rW : 0.0;
+      rr[7] = 0.0;
+      rr[8] = dep ? ww : 0.0;
+    }
+    mma_rows();
+  }
+  double* cw = cst + wid * 64;
+  cw[(lane >> 2) * 8 + 2 * (lane & 3)] = c0;
+  cw[(lane >> 2) * 8 + 2 * (lane & 3) + 1] = c1;
+  __syncthreads();
+  if (threadIdx.x < kNPart) {  // partial q in k_normal_eq's order
+    const int q = threadIdx.x;
+    int rr, cc;
+    if (q < 21) {
+      rr = 0;
+      while ((rr + 1) * (rr + 2) / 2 <= q) ++rr;
+      cc = q - rr * (rr + 1) / 2;
+    } else if (q < 27) {
+      rr = q - 21;
+      cc = 6;
+    } else {
+      rr = 6;
+      cc = 6;
+    }
+    double t = 0.0;
+#pragma unroll
+    for (int wv = 0; wv < kTPB / 32; ++wv) t += cst[wv * 64 + rr * 8 + cc];
+    o.part[(size_t)blockIdx.x * kNPart + q] = t;
+  }
+}
+
 void launch_normal_equations(const AlignLaunch& a, const LevelInfo& li, int phase, cudaStream_t s) {
   KScope ks_(phase ? "normal_eq_cov" : kNeNames[li.level], s);
-  if (RGBID_K3_MMA)
+  if (RGBID_K3_TILE)
+    k_normal_eq_tile<<<dim3(li.ntiles3, a.nslots), kTPB, kT3Smem, s>>>(a.io, a.st, li, phase,
+                                                                    a.lambda_n_min);
+  else if (RGBID_K3_MMA)
     k_normal_eq_mma<<<dim3(li.ntiles3, a.nslots), kTPB, 0, s>>>(a.io, a.st, li, phase,
                                                                 a.lambda_n_min);
   else

@@ -32,6 +32,16 @@ constexpr int kTdistClusterMaxSlots = 8; // batches up to this size use the clus
 #endif
 constexpr int kTdistClusterThreads = RGBID_TDIST_CLUSTER_THREADS;
 constexpr int kPixK3 = 8;           // pixels per thread in the normal-equation kernel
+#ifndef RGBID_K3_TILE
+#define RGBID_K3_TILE 1  // K3 on 2-D tiles: A-side gradients from a shared-memory halo tile
+#endif
+// K3 tiles: kT3W x kT3H level pixels (2048 = kTPB * kPixK3), gradients from the
+// staged (kT3W + 2) x (kT3H + 2) halo of I_A, W_A
+constexpr int kT3W = 64, kT3H = 32;
+__host__ __device__ constexpr int k3_tiles(int w, int h) {
+  return RGBID_K3_TILE ? ((w + kT3W - 1) / kT3W) * ((h + kT3H - 1) / kT3H)
+                       : (w * h + kTPB * kPixK3 - 1) / (kTPB * kPixK3);
+}
 
 // K1 tiling of level l: tile = (level row, segment of tx level pixels).
 // Full-res pixels per tile = tx * 4^l <= 2048 (smem staging of the warp).

@@ -228,7 +228,7 @@ LevelInfo make_level(const rgbid_intrinsics& K0, int w0, int h0, int level) {
   li.tx = k1_tx(level);
   li.nseg = (li.w + li.tx - 1) / li.tx;
   li.ntiles = li.nseg * li.h;
-  li.ntiles3 = (li.w * li.h + kTPB * kPixK3 - 1) / (kTPB * kPixK3);
+  li.ntiles3 = k3_tiles(li.w, li.h);
   rgbid_intrinsics k;
   level_intrinsics(K0, level, &k);
   li.fx = k.fx;
@@ -269,9 +269,10 @@ size_t pyr_pixels(int w, int h) {
 }
 size_t slot_f64(int w, int h) {
   const size_t N = (size_t)w * h;
-  const size_t part = (size_t)((N + kTPB * kPixK3 - 1) / (kTPB * kPixK3)) * kNPart;
+  const size_t part = (size_t)k3_tiles(w, h) * kNPart;
   // ... + K2 samples + interleaved frame B (16-byte aligned: the total stays even)
-  const size_t f = 4 * N + 4 * pyr_pixels(w, h) + part + 2 * (size_t)kMaxSample;
+  const size_t grad = RGBID_K3_TILE ? 0 : 4 * pyr_pixels(w, h);
+  const size_t f = 4 * N + grad + part + 2 * (size_t)kMaxSample;
   return ((f + 1) & ~(size_t)1) + 2 * N;
 }
 size_t slot_u8(int w, int h) { return (pyr_pixels(w, h) + 255) & ~(size_t)255; }
@@ -592,8 +593,8 @@ int prepare_chunk(rgbid_ctx* ctx, Lane& L, int n, const rgbid_frame* const* fa,
     o.fWA = base + 3 * N;
     double* g = base + 4 * N;
     for (int l = 0; l < kMaxLevels; ++l) {
-      o.agrad[l] = g;
-      g += 4 * (size_t)(w >> l) * (h >> l);
+      o.agrad[l] = RGBID_K3_TILE ? nullptr : g;
+      if (!RGBID_K3_TILE) g += 4 * (size_t)(w >> l) * (h >> l);
     }
     o.part = g;
     o.IWB = reinterpret_cast<double2*>(base + (sf - 2 * N));  // sf and N*2 even: 16-B aligned
