@@ -33,7 +33,7 @@ constexpr int kTdistClusterMaxSlots = 8; // batches up to this size use the clus
 constexpr int kTdistClusterThreads = RGBID_TDIST_CLUSTER_THREADS;
 constexpr int kPixK3 = 8;           // pixels per thread in the normal-equation kernel
 #ifndef RGBID_K3_TILE
-#define RGBID_K3_TILE 1  // K3 on 2-D tiles: A-side gradients from a shared-memory halo tile
+#define RGBID_K3_TILE 0  // 1: K3 on 2-D tiles, A-side gradients from a shared-memory halo tile (measured 14% slower per L0 launch)
 #endif
 // K3 tiles: kT3W x kT3H level pixels (2048 = kTPB * kPixK3), gradients from the
 // staged (kT3W + 2) x (kT3H + 2) halo of I_A, W_A
