@@ -37,9 +37,6 @@
 #ifndef RGBID_K1_IWB
 #define RGBID_K1_IWB 1  // K1 samples frame B from an interleaved {I, W} copy (L0: -11%)
 #endif
-#ifndef RGBID_K1_FAST
-#define RGBID_K1_FAST 1  // K1 warps with fast reciprocals + guard bands (exact fallback)
-#endif
 #ifndef RGBID_K1_SHFL
 #define RGBID_K1_SHFL 0  // 1: levels 2-3 shuffle downsample, no per-stage block barriers (measured 1-3% slower)
 #endif
@@ -83,15 +80,6 @@ __device__ __forceinline__ double div_rcp(double a, double b, double r) {
   const double q = a * r;
   const double e = fma(-b, q, a);
   return fma(e, r, q);
-}
-
-// 1/q for normal q (|q| in ~[1e-300, 1e300]): MUFU seed + cubic Newton step, within
-// ~1 ulp of the IEEE reciprocal (no range checks, no slow path).
-__device__ __forceinline__ double rcp_fast(double q) {
-  double r;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(q));
-  const double e = fma(-q, r, 1.0);
-  return fma(r, fma(e, e, e), r);
 }
 
 // bilinear — inc/image.hpp:51-62
@@ -201,106 +189,6 @@ __device__ __forceinline__ void warp_px_iw(const WarpMats& m, const double2* __r
   oW = v3 ? __drcp_rn(za) : CUDART_NAN;  // == 1.0 / za
 }
 
-// The same pixel of inverse_geometric_warp with fast reciprocals (rcp_fast, plain
-// products instead of correctly rounded quotients): the warped VALUES are within a
-// few ulps of the reference's (they only feed the tolerance-checked residuals,
-// Student-t fit and normal equations), while every DECISION the reference takes on
-// this pixel -- x_B.z > 1e-12, the bounds and floor() of p_b, the taps' validity,
-// w_m > 0, z_A > 1e-12 -- is guaranteed identical: the fast quantities are within
-// ~1e-12 (absolute, p_b in pixels; relative elsewhere) of the exact ones, and any
-// pixel whose fast p_b lies within 1e-9 (1 + |p_b|) of an integer, or whose x_B.z,
-// w_m or z_A lies within a guard band of its threshold, or whose w_a is outside
-// the reciprocal's safe range, returns `risky` and is recomputed by the exact
-// warp_px_iw.  Masks therefore stay bit-exact (tests: per-iteration jet counts).
-__device__ __forceinline__ bool warp_px_fast(const WarpMats& m, const double2* __restrict__ IWB,
-                                             int wb, int hb, int x, int y, double w_a, double& oI,
-                                             double& oW) {
-  const bool v0 = valid(w_a) && w_a > 0.0;
-  bool risky = v0 && !(w_a > 1e-290 && w_a < 1e290);
-  const double wa = v0 && !risky ? w_a : 1.0;
-  const double qz = rcp_fast(wa);
-  const double qx = x * qz, qy = y * qz;
-  const double xb0 = red3(m.Rt_BA[0] * qx, m.Rt_BA[1] * qy, m.Rt_BA[2] * qz) + m.tt_BA[0];
-  const double xb1 = red3(m.Rt_BA[3] * qx, m.Rt_BA[4] * qy, m.Rt_BA[5] * qz) + m.tt_BA[1];
-  const double xb2 = red3(m.Rt_BA[6] * qx, m.Rt_BA[7] * qy, m.Rt_BA[8] * qz) + m.tt_BA[2];
-  risky |= v0 && xb2 < 1e-6 && xb2 > -1e-6;  // near the x_B.z > 1e-12 threshold
-  const bool v1 = v0 && xb2 > 1e-12;
-  const double rz2 = rcp_fast(v1 ? xb2 : 1.0);
-  const double px = xb0 * rz2, py = xb1 * rz2;
-  // p_b near an integer: bounds (0, w - 1) and floor() could differ from the exact p_b
-  const double fpx = px - floor(px), fpy = py - floor(py);
-  const double dx_ = 1e-9 * (1.0 + fabs(px)), dy_ = 1e-9 * (1.0 + fabs(py));
-  risky |= v1 && (fpx < dx_ || fpx > 1.0 - dx_ || fpy < dy_ || fpy > 1.0 - dy_);
-  const bool inb = v1 && (px >= 0.0 && px <= wb - 1.0 && py >= 0.0 && py <= hb - 1.0);
-  const double sx = inb ? px : 0.0, sy = inb ? py : 0.0;
-  const int x0 = (int)floor(sx), y0 = (int)floor(sy);
-  const int dx = x0 + 1 < wb ? 1 : 0;
-  const int dy = y0 + 1 < hb ? wb : 0;
-  const double fx = sx - x0, fy = sy - y0, gx = 1 - fx, gy = 1 - fy;
-  const int i00 = y0 * wb + x0;
-  const double2 t00 = __ldg(IWB + i00), t10 = __ldg(IWB + i00 + dx), t01 = __ldg(IWB + i00 + dy),
-                t11 = __ldg(IWB + i00 + dy + dx);
-  const double a00 = t00.x, a10 = t10.x, a01 = t01.x, a11 = t11.x;
-  const double b00 = t00.y, b10 = t10.y, b01 = t01.y, b11 = t11.y;
-  const double ri = gy * (gx * a00 + fx * a10) + fy * (gx * a01 + fx * a11);
-  const double w_meas = gy * (gx * b00 + fx * b10) + fy * (gx * b01 + fx * b11);
-  // a non-finite formula value: the taps decide (bilin_fix), exactly as the reference
-  const double riv = bilin_fix(ri, a00, a10, a01, a11);
-  const double wmv = bilin_fix(w_meas, b00, b10, b01, b11);
-  oI = inb ? riv : CUDART_NAN;
-  // w_m > 0 decided by the same taps; guard |w_m| against the weights' ~1e-12 error
-  const double bsum = fabs(b00) + fabs(b10) + fabs(b01) + fabs(b11);
-  risky |= inb && valid(wmv) && (fabs(wmv) <= 1e-9 * bsum || fabs(wmv) > 1e300);
-  const bool v2 = inb && valid(wmv) && wmv > 0.0;
-  const double rz = red3(m.Rt_AB[6] * px, m.Rt_AB[7] * py, m.Rt_AB[8] * 1.0);
-  const double za = rz * rcp_fast(v2 ? wmv : 1.0) + m.tt_AB[2];
-  risky |= v2 && za < 1e-6 && za > -1e-6;  // near the z_A > 1e-12 threshold
-  const bool v3 = v2 && za > 1e-12;
-  oW = v3 ? rcp_fast(za) : CUDART_NAN;
-  return risky;
-}
-
-// K1's warps of NP pixels: pixel k at coord(k) -> (x, y), w_a = W_A[y * wb + x] (or a
-// hole when !in(k)).  The fast path for all of them, then the exact warp for the
-// (rare) risky ones in a separate, non-unrolled loop that reloads its inputs, so
-// only the risky bits stay live across the fast path.
-template <int NP, typename Coord, typename In>
-__device__ __forceinline__ void warp_px_k1(const WarpMats& m, const double2* __restrict__ IWB,
-                                           const double* __restrict__ WA, int wb, int hb,
-                                           Coord coord, In in, double (&oI)[NP], double (&oW)[NP]) {
-#if RGBID_K1_FAST
-  unsigned risky = 0;
-#pragma unroll
-  for (int k = 0; k < NP; ++k) {
-    int x, y;
-    coord(k, x, y);
-    const double w_a = in(k) ? __ldg(WA + y * wb + x) : CUDART_NAN;
-    risky |= (unsigned)warp_px_fast(m, IWB, wb, hb, x, y, w_a, oI[k], oW[k]) << k;
-  }
-  if (risky) {
-#pragma unroll 1
-    for (int k = 0; k < NP; ++k)
-      if (risky >> k & 1u) {
-        int x, y;
-        coord(k, x, y);
-        double d0, d1, i_, w_;
-        warp_px_iw(m, IWB, wb, hb, x, y, __ldg(WA + y * wb + x), i_, w_, d0, d1);
-        oI[k] = i_;
-        oW[k] = w_;
-      }
-  }
-#else
-#pragma unroll
-  for (int k = 0; k < NP; ++k) {
-    int x, y;
-    coord(k, x, y);
-    const double w_a = in(k) ? __ldg(WA + y * wb + x) : CUDART_NAN;
-    double d0, d1;
-    warp_px_iw(m, IWB, wb, hb, x, y, w_a, oI[k], oW[k], d0, d1);
-  }
-#endif
-}
-
 __device__ __forceinline__ double px_or_nan(const double* img, int w, int h, int x, int y) {
   return (x >= 0 && x < w && y >= 0 && y < h) ? __ldg(img + (size_t)y * w + x) : CUDART_NAN;
 }
@@ -406,14 +294,15 @@ __global__ void __launch_bounds__(k1_threads<L>(), RGBID_K1_THREADS_PER_SM / k1_
     for (int rr = 0; rr < (1 << (L - 1)) / NG; ++rr) {
       const int r = rr * NG + grp;
       const int y = (yl << L) + 2 * r;
-      double vi[4], vw[4];
-      warp_px_k1<4>(
-          wm, o.IWB, WAw, w0, h0,
-          [&](int q, int& xx, int& yy) {
-            xx = x + (q & 1);
-            yy = y + (q >> 1);
-          },
-          [](int) { return true; }, vi, vw);
+      double vi[4], vw[4], d0, d1;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int xx = x + (q & 1), yy = y + (q >> 1);
+        if (RGBID_K1_IWB_LEVELS)
+          warp_px_iw(wm, o.IWB, w0, h0, xx, yy, __ldg(WAw + yy * w0 + xx), vi[q], vw[q], d0, d1);
+        else
+          warp_px(wm, IB, WB, w0, h0, xx, yy, __ldg(WAw + yy * w0 + xx), vi[q], vw[q], d0, d1);
+      }
       sI[r * cw + col] = ds4(vi[0], vi[1], vi[2], vi[3]);
       sW[r * cw + col] = ds4(vw[0], vw[1], vw[2], vw[3]);
     }
@@ -523,14 +412,12 @@ __global__ void __launch_bounds__(256, RGBID_K1_THREADS_PER_SM / 256) k_warp_res
     v1i[r] = v1w[r] = CUDART_NAN;
     if (live) {
       const int x = 2 * X1, y = 2 * (Y1 + r);
-      double vi[4], vw[4];
-      warp_px_k1<4>(
-          wm, o.IWB, WAw, w0, h0,
-          [&](int k, int& xx, int& yy) {
-            xx = x + (k & 1);
-            yy = y + (k >> 1);
-          },
-          [](int) { return true; }, vi, vw);
+      double vi[4], vw[4], d0, d1;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int xx = x + (k & 1), yy = y + (k >> 1);
+        warp_px_iw(wm, o.IWB, w0, h0, xx, yy, __ldg(WAw + yy * w0 + xx), vi[k], vw[k], d0, d1);
+      }
       v1i[r] = ds4(vi[0], vi[1], vi[2], vi[3]);
       v1w[r] = ds4(vw[0], vw[1], vw[2], vw[3]);
     }
@@ -615,15 +502,6 @@ __global__ void __launch_bounds__(128, RGBID_K1L0_MINB) k_warp_residuals_l0(cons
   const int xl0 = seg * li.tx;
   const int nx = min(li.tx, li.w - xl0);
   bool jet[2], dep[2];
-  double ib[2], wb[2];
-  // pixels past the tile warp a hole (w_a = NaN): no taps, never risky
-  warp_px_k1<2>(
-      wm, o.IWB, WAw, w0, h0,
-      [&](int q, int& x, int& y) {
-        x = xl0 + tid + 128 * q;
-        y = yl;
-      },
-      [&](int q) { return tid + 128 * q < nx; }, ib, wb);
 #pragma unroll
   for (int q = 0; q < 2; ++q) {
     const int lx = tid + 128 * q;
@@ -632,9 +510,14 @@ __global__ void __launch_bounds__(128, RGBID_K1L0_MINB) k_warp_residuals_l0(cons
       const int idx = yl * w0 + xl0 + lx;
       const unsigned a = __ldg(am + idx);
       const double ia = __ldg(IA0 + idx);
-      o.ibw[idx] = make_double2(ib[q] - ia, wb[q]);  // r_I (src/alignment.cpp:222), w_b: K2, K3
-      jet[q] = (a & 1u) && valid(ib[q]);
-      dep[q] = jet[q] && (a & 2u) && valid(wb[q]) && wb[q] > 0.0;
+      double ib, wb, d0, d1;
+      if (RGBID_K1_IWB)
+        warp_px_iw(wm, o.IWB, w0, h0, xl0 + lx, yl, __ldg(WAw + idx), ib, wb, d0, d1);
+      else
+        warp_px(wm, IB, WB, w0, h0, xl0 + lx, yl, __ldg(WAw + idx), ib, wb, d0, d1);
+      o.ibw[idx] = make_double2(ib - ia, wb);  // r_I (src/alignment.cpp:222), w_b: K2, K3
+      jet[q] = (a & 1u) && valid(ib);
+      dep[q] = jet[q] && (a & 2u) && valid(wb) && wb > 0.0;
     }
   }
   __shared__ int wcnt[2][8];
@@ -875,6 +758,13 @@ __device__ __forceinline__ void sample_allsum(double (&v)[NV], Sample& S);
 
 __device__ __forceinline__ double t_weight(double x, double nu) { return (nu + 1.0) / (nu + x * x); }
 
+// 1/q for q >= 1 (t_weight denominators): MUFU seed + cubic Newton step (full precision).
+__device__ __forceinline__ double rcp_fast(double q) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(q));
+  const double e = fma(-q, r, 1.0);
+  return fma(r, fma(e, e, e), r);
+}
 // 1/q for normal positive q: MUFU seed + one quadratic Newton step (~1e-12 relative;
 // used only inside sums whose order already differs from the reference).
 __device__ __forceinline__ double rcp_q(double q) {
