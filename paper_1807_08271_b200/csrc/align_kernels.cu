@@ -546,6 +546,97 @@ __global__ void __launch_bounds__(128, RGBID_K1L0_MINB) k_warp_residuals_l0(cons
   }
 }
 
+// Level-0 K1, persistent over tiles (RGBID_K1L0_PERSIST = tiles per CTA): the CTA
+// walks tiles blockIdx.x, + gridDim.x, ... of its slot and loads the NEXT tile's
+// W_A, I_A and mask bytes before warping the current one, so the first link of
+// the per-pixel dependent chain (W_A -> taps) is off the critical path.  Same
+// per-pixel arithmetic, outputs and per-tile ballots as k_warp_residuals_l0.
+#ifndef RGBID_ALLSUM_SMEM
+#define RGBID_ALLSUM_SMEM 0
+#endif
+#ifndef RGBID_K1L0_PERSIST
+#define RGBID_K1L0_PERSIST 0
+#endif
+__global__ void __launch_bounds__(128, RGBID_K1L0_MINB) k_warp_residuals_l0p(const SlotIO* __restrict__ io,
+                                                                 const SlotState* __restrict__ st,
+                                                                 LevelInfo li, int w0, int h0,
+                                                                 int phase) {
+  const int slot = blockIdx.y;
+  const SlotState& S = st[slot];
+  if (!slot_active(S, 0, phase)) return;
+  __shared__ WarpMats wm;
+  __shared__ int wcnt[2][2][8];  // [tile parity][type][word]
+  if (threadIdx.x < 24)
+    reinterpret_cast<double*>(&wm)[threadIdx.x] = reinterpret_cast<const double*>(&S.wm)[threadIdx.x];
+  const SlotIO& o = io[slot];
+  const double* __restrict__ WAw = phase ? o.fWA : o.WA[0];
+  const double* __restrict__ IA0 = phase ? o.fIA : o.IA[0];
+  const uint8_t* __restrict__ am = o.amask[0];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int nt = li.ntiles;
+  double pwa[2], pia[2];
+  unsigned pam[2];
+  auto prefetch = [&](int tile) {
+    const int yl = tile / li.nseg, seg = tile - yl * li.nseg;
+    const int xl0 = seg * li.tx, nx = min(li.tx, li.w - xl0);
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int lx = tid + 128 * q;
+      const bool in = tile < nt && lx < nx;
+      const int idx = yl * w0 + xl0 + lx;
+      pwa[q] = in ? __ldg(WAw + idx) : CUDART_NAN;
+      pia[q] = in ? __ldg(IA0 + idx) : 0.0;
+      pam[q] = in ? __ldg(am + idx) : 0u;
+    }
+  };
+  prefetch(blockIdx.x);
+  __syncthreads();
+  int par = 0;
+  for (int tile = blockIdx.x; tile < nt; tile += gridDim.x, par ^= 1) {
+    const double cwa[2] = {pwa[0], pwa[1]}, cia[2] = {pia[0], pia[1]};
+    const unsigned cam[2] = {pam[0], pam[1]};
+    prefetch(tile + gridDim.x);
+    const int yl = tile / li.nseg, seg = tile - yl * li.nseg;
+    const int xl0 = seg * li.tx, nx = min(li.tx, li.w - xl0);
+    bool jet[2], dep[2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int lx = tid + 128 * q;
+      jet[q] = dep[q] = false;
+      if (lx < nx) {
+        const int idx = yl * w0 + xl0 + lx;
+        double ib, wb, d0, d1;
+        warp_px_iw(wm, o.IWB, w0, h0, xl0 + lx, yl, cwa[q], ib, wb, d0, d1);
+        o.ibw[idx] = make_double2(ib - cia[q], wb);  // r_I (src/alignment.cpp:222), w_b
+        jet[q] = (cam[q] & 1u) && valid(ib);
+        dep[q] = jet[q] && (cam[q] & 2u) && valid(wb) && wb > 0.0;
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const unsigned bj = __ballot_sync(0xffffffffu, jet[q]), bd = __ballot_sync(0xffffffffu, dep[q]);
+      if (lane == 0) {
+        const int word = wid + 4 * q;
+        wcnt[par][0][word] = __popc(bj);
+        wcnt[par][1][word] = __popc(bd);
+        o.bitsI[tile * kWordsPerTile + word] = bj;
+        o.bitsW[tile * kWordsPerTile + word] = bd;
+      }
+    }
+    __syncthreads();  // double-buffered counts: one barrier per tile
+    if (tid == 0) {
+      int tI = 0, tW = 0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        tI += wcnt[par][0][k];
+        tW += wcnt[par][1][k];
+      }
+      o.cntI[tile] = tI;
+      o.cntW[tile] = tW;
+    }
+  }
+}
+
 // A-side part of residuals_and_jacobians, constant over the IRLS iterations:
 // validity (src/alignment.cpp:209-211,227) and gradient_at of I_A and W_A
 // (src/alignment.cpp:165-191) per level pixel.  phase 1 = from the filtered A
@@ -677,7 +768,14 @@ void launch_warp_residuals(const AlignLaunch& a, const LevelInfo& li, int phase,
   KScope ks_(kLevelNames[phase ? 1 : 0][li.level], s);
   dim3 grid(li.ntiles, a.nslots);
   switch (li.level) {
-    case 0: k_warp_residuals_l0<<<grid, 128, 0, s>>>(a.io, a.st, li, a.w0, a.h0, phase); break;
+    case 0:
+      if (RGBID_K1L0_PERSIST > 1)
+        k_warp_residuals_l0p<<<dim3((li.ntiles + RGBID_K1L0_PERSIST - 1) / RGBID_K1L0_PERSIST,
+                                    a.nslots),
+                               128, 0, s>>>(a.io, a.st, li, a.w0, a.h0, phase);
+      else
+        k_warp_residuals_l0<<<grid, 128, 0, s>>>(a.io, a.st, li, a.w0, a.h0, phase);
+      break;
     case 1: k_warp_residuals<1><<<grid, k1_threads<1>(), 0, s>>>(a.io, a.st, li, a.w0, a.h0, phase); break;
     case 2:
       if (RGBID_K1_SHFL)
@@ -725,12 +823,28 @@ __device__ __forceinline__ void block_allsum(double (&v)[NV], double* scratch2, 
 #pragma unroll
     for (int i = 0; i < NV; ++i) scratch[wid * NV + i] = v[i];
   __syncthreads();
+#if RGBID_ALLSUM_SMEM
+  // every thread sums the NW warp partials itself (broadcast shared loads, fixed
+  // pairwise tree: bit-identical everywhere) instead of a second shuffle butterfly
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    double t[NW];
+#pragma unroll
+    for (int k = 0; k < NW; ++k) t[k] = scratch[k * NV + i];
+#pragma unroll
+    for (int wdt = NW / 2; wdt > 0; wdt >>= 1)
+#pragma unroll
+      for (int k = 0; k < wdt; ++k) t[k] = t[2 * k] + t[2 * k + 1];
+    v[i] = t[0];
+  }
+#else
 #pragma unroll
   for (int i = 0; i < NV; ++i) v[i] = lane < NW ? scratch[lane * NV + i] : 0.0;
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1)
 #pragma unroll
     for (int i = 0; i < NV; ++i) v[i] += __shfl_xor_sync(0xffffffffu, v[i], off);
+#endif
 }
 
 struct TD {
