@@ -36,50 +36,138 @@ __device__ __forceinline__ double bilinear_f(const double* __restrict__ img, int
 
 // ---------------------------------------------------------------------------
 // integrate_frame over k frames (frames in call order).
-__global__ void __launch_bounds__(256) k_integrate(const FuseFrame* __restrict__ frames, int k,
-                                                   double* __restrict__ kfW,
-                                                   double* __restrict__ kfC, int w, int h,
-                                                   double sigma_w) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= w * h) return;
-  const int y = i / w, x = i - y * w;
-  double w_kf = kfW[i], c_kf = kfC[i];
-  const double gate = 3.0 * sigma_w;
-  for (int f = 0; f < k; ++f) {
-    const FuseFrame& F = frames[f];
-    const WarpMats& m = F.wm;
-    // inverse_geometric_warp inverse depth at this pixel, W_A = current kf W
-    if (!fvalid(w_kf) || w_kf <= 0.0) continue;
-    const double qx = x / w_kf, qy = y / w_kf, qz = 1.0 / w_kf;
-    const double xb0 = red3(m.Rt_BA[0] * qx, m.Rt_BA[1] * qy, m.Rt_BA[2] * qz) + m.tt_BA[0];
-    const double xb1 = red3(m.Rt_BA[3] * qx, m.Rt_BA[4] * qy, m.Rt_BA[5] * qz) + m.tt_BA[1];
-    const double xb2 = red3(m.Rt_BA[6] * qx, m.Rt_BA[7] * qy, m.Rt_BA[8] * qz) + m.tt_BA[2];
-    if (xb2 <= 1e-12) continue;
-    const double bx = xb0 / xb2, by = xb1 / xb2;
-    const double w_meas = bilinear_f(F.W, w, h, bx, by);
-    if (!fvalid(w_meas) || w_meas <= 0.0) continue;
-    const double rz = red3(m.Rt_AB[6] * bx, m.Rt_AB[7] * by, m.Rt_AB[8] * 1.0);
-    const double za = rz / w_meas + m.tt_AB[2];
-    if (za <= 1e-12) continue;
-    const double w_new = 1.0 / za;
-    // fusion update — src/fusion.cpp:78-92 (w_b == w_meas: same bilinear call)
-    if (fabs(w_new - w_kf) >= gate) continue;
-    const double w_b = w_meas;
-    const double num = 1.0 - w_b * m.tt_BA[2];
-    const double den = red3(m.Rt_BA[6] * x, m.Rt_BA[7] * y, m.Rt_BA[8] * 1.0);
-    const double c_k = (num * num / den) * (num * num / den);
-    if (!isfinite(c_k) || c_k <= 0.0) continue;
-    w_kf = (w_kf * c_kf + c_k * w_new) / (c_kf + c_k);
+//
+// Correctly rounded a / b from r = RN(1/b) (Markstein; bit-identical to IEEE a / b
+// for normal operands, rgbid_selftest_division): the quotients sharing a divisor
+// (p / w_kf, x_B / z) cost one reciprocal.  Divisors outside [1e-300, 1e300] take
+// the IEEE division.
+__device__ __forceinline__ double fdiv_rcp(double a, double b, double r) {
+  const double q = a * r;
+  const double e = fma(-b, q, a);
+  return fma(e, r, q);
+}
+__device__ __forceinline__ bool rcp_safe(double b) {
+  const double m = fabs(b);
+  return m > 1e-300 && m < 1e300;
+}
+
+// one frame into one keyframe pixel (x, y): src/fusion.cpp:68-95 with W_A = the
+// keyframe's current W (the per-pixel state depends only on this pixel).  Written
+// branch-free (a validity predicate, safe operands, always-issued tap loads) so the
+// chains of several pixels interleave; every test and expression is the
+// reference's, in its order.
+__device__ __forceinline__ void integrate_px(const FuseFrame& F, int x, int y, int w, int h,
+                                             double gate, double& w_kf, double& c_kf) {
+  const WarpMats& m = F.wm;
+  // inverse_geometric_warp inverse depth at this pixel (src/warping.cpp:96-111)
+  bool ok = fvalid(w_kf) && w_kf > 0.0;
+  const double wa = ok ? w_kf : 1.0;
+  double qx, qy, qz;
+  if (rcp_safe(wa)) {
+    qz = __drcp_rn(wa);
+    qx = fdiv_rcp((double)x, wa, qz);
+    qy = fdiv_rcp((double)y, wa, qz);
+  } else {
+    qx = x / wa;
+    qy = y / wa;
+    qz = 1.0 / wa;
+  }
+  const double xb0 = red3(m.Rt_BA[0] * qx, m.Rt_BA[1] * qy, m.Rt_BA[2] * qz) + m.tt_BA[0];
+  const double xb1 = red3(m.Rt_BA[3] * qx, m.Rt_BA[4] * qy, m.Rt_BA[5] * qz) + m.tt_BA[1];
+  const double xb2 = red3(m.Rt_BA[6] * qx, m.Rt_BA[7] * qy, m.Rt_BA[8] * qz) + m.tt_BA[2];
+  ok = ok && xb2 > 1e-12;
+  const double z = ok ? xb2 : 1.0;
+  double bx, by;
+  if (rcp_safe(z)) {
+    const double r = __drcp_rn(z);
+    bx = fdiv_rcp(xb0, z, r);
+    by = fdiv_rcp(xb1, z, r);
+  } else {
+    bx = xb0 / z;
+    by = xb1 / z;
+  }
+  // bilinear(frame.W, b) — inc/image.hpp:51-62
+  const bool inb = ok && (bx >= 0.0 && bx <= w - 1.0 && by >= 0.0 && by <= h - 1.0);
+  const double sx = inb ? bx : 0.0, sy = inb ? by : 0.0;
+  const int x0 = (int)floor(sx), y0 = (int)floor(sy);
+  const int dx = x0 + 1 < w ? 1 : 0, dy = y0 + 1 < h ? w : 0;
+  const double fx = sx - x0, fy = sy - y0;
+  const double* __restrict__ Wf = F.W;
+  const int i00 = y0 * w + x0;
+  const double v00 = __ldg(Wf + i00), v10 = __ldg(Wf + i00 + dx), v01 = __ldg(Wf + i00 + dy),
+               v11 = __ldg(Wf + i00 + dy + dx);
+  const double w_meas = (1 - fy) * ((1 - fx) * v00 + fx * v10) + fy * ((1 - fx) * v01 + fx * v11);
+  ok = inb && fvalid(v00) && fvalid(v10) && fvalid(v01) && fvalid(v11) && fvalid(w_meas) &&
+       w_meas > 0.0;
+  const double rz = red3(m.Rt_AB[6] * bx, m.Rt_AB[7] * by, m.Rt_AB[8] * 1.0);
+  const double za = rz / (ok ? w_meas : 1.0) + m.tt_AB[2];
+  ok = ok && za > 1e-12;
+  const double w_new = 1.0 / (ok ? za : 1.0);
+  // fusion update — src/fusion.cpp:78-92 (w_b == w_meas: same bilinear call)
+  ok = ok && fabs(w_new - w_kf) < gate;
+  const double num = 1.0 - w_meas * m.tt_BA[2];
+  const double den = red3(m.Rt_BA[6] * x, m.Rt_BA[7] * y, m.Rt_BA[8] * 1.0);
+  const double t = num * num / den;
+  const double c_k = t * t;
+  ok = ok && isfinite(c_k) && c_k > 0.0;
+  const double wn = (w_kf * c_kf + c_k * w_new) / (c_kf + c_k);
+  if (ok) {
+    w_kf = wn;
     c_kf = c_kf + c_k;
   }
-  kfW[i] = w_kf;
-  kfC[i] = c_kf;
+}
+
+// k frames, kIntPx pixels per thread (independent chains interleaved: the
+// per-frame chain 1/w_kf -> x_B -> taps -> z_A -> update is serial per pixel), so
+// that every keyframe pixel of a VGA frame is resident in one wave; the frames'
+// warp matrices are staged in shared memory, kIntStage frames at a time.
+constexpr int kIntPx = 2, kIntThreads = 256, kIntStage = 32;
+__global__ void __launch_bounds__(kIntThreads) k_integrate(const FuseFrame* __restrict__ frames,
+                                                           int k, double* __restrict__ kfW,
+                                                           double* __restrict__ kfC, int w, int h,
+                                                           double sigma_w) {
+  __shared__ FuseFrame sf[kIntStage];
+  const int n = w * h;
+  const int base = blockIdx.x * (kIntThreads * kIntPx) + threadIdx.x;
+  double wk[kIntPx], ck[kIntPx];
+  int px[kIntPx], py[kIntPx];
+#pragma unroll
+  for (int j = 0; j < kIntPx; ++j) {
+    const int i = base + j * kIntThreads;
+    const bool in = i < n;
+    wk[j] = in ? kfW[i] : CUDART_NAN;  // out-of-range pixels: holes, never updated
+    ck[j] = in ? kfC[i] : 0.0;
+    py[j] = in ? i / w : 0;
+    px[j] = in ? i - py[j] * w : 0;
+  }
+  const double gate = 3.0 * sigma_w;
+  for (int f0 = 0; f0 < k; f0 += kIntStage) {
+    const int nf = min(kIntStage, k - f0);
+    __syncthreads();
+    for (int t = threadIdx.x; t < nf * (int)(sizeof(FuseFrame) / 8); t += kIntThreads)
+      reinterpret_cast<double*>(sf)[t] = reinterpret_cast<const double*>(frames + f0)[t];
+    __syncthreads();
+    for (int f = 0; f < nf; ++f) {
+#pragma unroll
+      for (int j = 0; j < kIntPx; ++j) integrate_px(sf[f], px[j], py[j], w, h, gate, wk[j], ck[j]);
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < kIntPx; ++j) {
+    const int i = base + j * kIntThreads;
+    if (i < n) {
+      kfW[i] = wk[j];
+      kfC[i] = ck[j];
+    }
+  }
 }
 
 void launch_integrate(const FuseFrame* frames_dev, int k, double* kfW, double* kfC, int w, int h,
                       double sigma_w, cudaStream_t s) {
   KScope ks_("integrate", s);
-  k_integrate<<<(w * h + 255) / 256, 256, 0, s>>>(frames_dev, k, kfW, kfC, w, h, sigma_w);
+  const int per = kIntThreads * kIntPx;
+  k_integrate<<<(w * h + per - 1) / per, kIntThreads, 0, s>>>(frames_dev, k, kfW, kfC, w, h,
+                                                              sigma_w);
 }
 
 // ---------------------------------------------------------------------------
