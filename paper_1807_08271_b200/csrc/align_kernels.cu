@@ -13,11 +13,12 @@
 //                        K2a+K2b for <= 8 pairs over an 8-CTA cluster (latency mode).
 //   K3  k_normal_eq_mma  jets (src/alignment.cpp:212-244), robust weights and the
 //                        21+6+1 fp64 sums (src/alignment.cpp:321-335) on the FP64
-//                        tensor cores (k_normal_eq: the FMA version).
-//   K4  k_solve          fixed-order reduce, rank test, LDLT, SE(3) update, convergence
-//                        (src/alignment.cpp:387-401) — no host round trip.
+//                        tensor cores; the slot's last CTA then runs
+//   K4  solve_slot       fixed-order reduce, rank test, LDLT, SE(3) update, convergence
+//                        (src/alignment.cpp:387-401) — no host round trip, no launch;
+//                        for a single pair it also writes the level's WHILE condition.
 // Once per align: k_pyramid_slots, k_prep_A (A-side validity + gradients); the
-// covariance pass adds k_bilateral_slots and k_covariance.
+// covariance pass adds k_bilateral_slots, and K3's last CTA runs covariance_slot.
 // Compiled with --fmad=false: mask-deciding arithmetic rounds exactly like the
 // reference; reductions use a fixed tree (bit-reproducible run to run).
 #include <cooperative_groups.h>
@@ -30,16 +31,6 @@
 
 #include "align_kernels.cuh"
 
-#ifndef RGBID_K1_IWB_LEVELS
-#define RGBID_K1_IWB_LEVELS 1  // levels >= 1 too (with the 1536-thread cap below; at 32
-                               // registers the register pairs spill and it measured slower)
-#endif
-#ifndef RGBID_K1_IWB
-#define RGBID_K1_IWB 1  // K1 samples frame B from an interleaved {I, W} copy (L0: -11%)
-#endif
-#ifndef RGBID_K1_SHFL
-#define RGBID_K1_SHFL 0  // 1: levels 2-3 shuffle downsample, no per-stage block barriers (measured 1-3% slower)
-#endif
 
 namespace rgbid_b200 {
 
@@ -106,50 +97,9 @@ __device__ __forceinline__ double bilin_fix(double r, double a, double b, double
   return (valid(a) && valid(b) && valid(c) && valid(d)) ? r : CUDART_NAN;
 }
 
-// one A pixel of inverse_geometric_warp — src/warping.cpp:96-111 (bit-identical).
-// Written branch-free (predicates + clamped, always-issued tap loads) so that
-// several pixels unrolled in one thread overlap their gathers.
-__device__ __forceinline__ void warp_px(const WarpMats& m, const double* __restrict__ IB,
-                                        const double* __restrict__ WB, int wb, int hb, int x,
-                                        int y, double w_a, double& oI, double& oW, double& mx,
-                                        double& my) {
-  const bool v0 = valid(w_a) && w_a > 0.0;
-  const double wa = v0 ? w_a : 1.0;
-  const double qz = __drcp_rn(wa);  // == 1.0 / w_a
-  const double qx = div_rcp((double)x, wa, qz), qy = div_rcp((double)y, wa, qz);
-  const double xb0 = red3(m.Rt_BA[0] * qx, m.Rt_BA[1] * qy, m.Rt_BA[2] * qz) + m.tt_BA[0];
-  const double xb1 = red3(m.Rt_BA[3] * qx, m.Rt_BA[4] * qy, m.Rt_BA[5] * qz) + m.tt_BA[1];
-  const double xb2 = red3(m.Rt_BA[6] * qx, m.Rt_BA[7] * qy, m.Rt_BA[8] * qz) + m.tt_BA[2];
-  const bool v1 = v0 && xb2 > 1e-12;
-  const double z = v1 ? xb2 : 1.0;
-  const double rz2 = __drcp_rn(z);
-  const double px = div_rcp(xb0, z, rz2), py = div_rcp(xb1, z, rz2);
-  mx = v1 ? px : CUDART_NAN;
-  my = v1 ? py : CUDART_NAN;
-  const bool inb = v1 && (px >= 0.0 && px <= wb - 1.0 && py >= 0.0 && py <= hb - 1.0);
-  const double sx = inb ? px : 0.0, sy = inb ? py : 0.0;
-  const int x0 = (int)floor(sx), y0 = (int)floor(sy);
-  const int dx = x0 + 1 < wb ? 1 : 0;  // x1 = min(x0 + 1, w - 1)
-  const int dy = y0 + 1 < hb ? wb : 0; // y1 = min(y0 + 1, h - 1)
-  const double fx = sx - x0, fy = sy - y0, gx = 1 - fx, gy = 1 - fy;
-  const int i00 = y0 * wb + x0;
-  const double a00 = __ldg(IB + i00), a10 = __ldg(IB + i00 + dx), a01 = __ldg(IB + i00 + dy),
-               a11 = __ldg(IB + i00 + dy + dx);
-  const double b00 = __ldg(WB + i00), b10 = __ldg(WB + i00 + dx), b01 = __ldg(WB + i00 + dy),
-               b11 = __ldg(WB + i00 + dy + dx);
-  const double ri = bilin_fix(gy * (gx * a00 + fx * a10) + fy * (gx * a01 + fx * a11), a00, a10, a01, a11);
-  const double w_meas = bilin_fix(gy * (gx * b00 + fx * b10) + fy * (gx * b01 + fx * b11), b00, b10, b01, b11);
-  oI = inb ? ri : CUDART_NAN;
-  const bool v2 = inb && valid(w_meas) && w_meas > 0.0;
-  const double rz = red3(m.Rt_AB[6] * px, m.Rt_AB[7] * py, m.Rt_AB[8] * 1.0);
-  const double za = rz / (v2 ? w_meas : 1.0) + m.tt_AB[2];
-  const bool v3 = v2 && za > 1e-12;
-  oW = v3 ? __drcp_rn(za) : CUDART_NAN;  // == 1.0 / za
-}
-
-// warp_px on frame B stored interleaved {I, W}: the four bilinear taps are four
-// 16-byte loads instead of eight 8-byte loads (same values, same arithmetic).
-// Written branch-free (predicates + clamped, always-issued tap loads) so that
+// one A pixel of inverse_geometric_warp — src/warping.cpp:96-111 (bit-identical),
+// on frame B stored interleaved {I, W}: the four bilinear taps are four 16-byte
+// loads instead of eight 8-byte loads (-11% per level-0 launch).  Written branch-free (predicates + clamped, always-issued tap loads) so that
 // several pixels unrolled in one thread overlap their gathers.
 __device__ __forceinline__ void warp_px_iw(const WarpMats& m, const double2* __restrict__ IWB,
                                            int wb, int hb, int x,
@@ -179,6 +129,46 @@ __device__ __forceinline__ void warp_px_iw(const WarpMats& m, const double2* __r
                 t11 = __ldg(IWB + i00 + dy + dx);
   const double a00 = t00.x, a10 = t10.x, a01 = t01.x, a11 = t11.x;
   const double b00 = t00.y, b10 = t10.y, b01 = t01.y, b11 = t11.y;
+  const double ri = bilin_fix(gy * (gx * a00 + fx * a10) + fy * (gx * a01 + fx * a11), a00, a10, a01, a11);
+  const double w_meas = bilin_fix(gy * (gx * b00 + fx * b10) + fy * (gx * b01 + fx * b11), b00, b10, b01, b11);
+  oI = inb ? ri : CUDART_NAN;
+  const bool v2 = inb && valid(w_meas) && w_meas > 0.0;
+  const double rz = red3(m.Rt_AB[6] * px, m.Rt_AB[7] * py, m.Rt_AB[8] * 1.0);
+  const double za = rz / (v2 ? w_meas : 1.0) + m.tt_AB[2];
+  const bool v3 = v2 && za > 1e-12;
+  oW = v3 ? __drcp_rn(za) : CUDART_NAN;  // == 1.0 / za
+}
+
+// warp_px_iw on separate I_B, W_B maps (k_warp_maps: the C-ABI inverse_geometric_warp,
+// whose frame B may differ in size from A).
+__device__ __forceinline__ void warp_px(const WarpMats& m, const double* __restrict__ IB,
+                                        const double* __restrict__ WB, int wb, int hb, int x,
+                                        int y, double w_a, double& oI, double& oW, double& mx,
+                                        double& my) {
+  const bool v0 = valid(w_a) && w_a > 0.0;
+  const double wa = v0 ? w_a : 1.0;
+  const double qz = __drcp_rn(wa);  // == 1.0 / w_a
+  const double qx = div_rcp((double)x, wa, qz), qy = div_rcp((double)y, wa, qz);
+  const double xb0 = red3(m.Rt_BA[0] * qx, m.Rt_BA[1] * qy, m.Rt_BA[2] * qz) + m.tt_BA[0];
+  const double xb1 = red3(m.Rt_BA[3] * qx, m.Rt_BA[4] * qy, m.Rt_BA[5] * qz) + m.tt_BA[1];
+  const double xb2 = red3(m.Rt_BA[6] * qx, m.Rt_BA[7] * qy, m.Rt_BA[8] * qz) + m.tt_BA[2];
+  const bool v1 = v0 && xb2 > 1e-12;
+  const double z = v1 ? xb2 : 1.0;
+  const double rz2 = __drcp_rn(z);
+  const double px = div_rcp(xb0, z, rz2), py = div_rcp(xb1, z, rz2);
+  mx = v1 ? px : CUDART_NAN;
+  my = v1 ? py : CUDART_NAN;
+  const bool inb = v1 && (px >= 0.0 && px <= wb - 1.0 && py >= 0.0 && py <= hb - 1.0);
+  const double sx = inb ? px : 0.0, sy = inb ? py : 0.0;
+  const int x0 = (int)floor(sx), y0 = (int)floor(sy);
+  const int dx = x0 + 1 < wb ? 1 : 0;  // x1 = min(x0 + 1, w - 1)
+  const int dy = y0 + 1 < hb ? wb : 0; // y1 = min(y0 + 1, h - 1)
+  const double fx = sx - x0, fy = sy - y0, gx = 1 - fx, gy = 1 - fy;
+  const int i00 = y0 * wb + x0;
+  const double a00 = __ldg(IB + i00), a10 = __ldg(IB + i00 + dx), a01 = __ldg(IB + i00 + dy),
+               a11 = __ldg(IB + i00 + dy + dx);
+  const double b00 = __ldg(WB + i00), b10 = __ldg(WB + i00 + dx), b01 = __ldg(WB + i00 + dy),
+               b11 = __ldg(WB + i00 + dy + dx);
   const double ri = bilin_fix(gy * (gx * a00 + fx * a10) + fy * (gx * a01 + fx * a11), a00, a10, a01, a11);
   const double w_meas = bilin_fix(gy * (gx * b00 + fx * b10) + fy * (gx * b01 + fx * b11), b00, b10, b01, b11);
   oI = inb ? ri : CUDART_NAN;
@@ -271,8 +261,6 @@ __global__ void __launch_bounds__(k1_threads<L>(), RGBID_K1_THREADS_PER_SM / k1_
   const double* __restrict__ WAw = phase ? o.fWA : o.WA[0];
   const double* __restrict__ IAl = phase ? o.fIA : o.IA[L];
   const uint8_t* __restrict__ am = o.amask[L];
-  const double* __restrict__ IB = o.IB;
-  const double* __restrict__ WB = o.WB;
   __syncthreads();
 
   const int tid = threadIdx.x;
@@ -298,10 +286,7 @@ __global__ void __launch_bounds__(k1_threads<L>(), RGBID_K1_THREADS_PER_SM / k1_
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const int xx = x + (q & 1), yy = y + (q >> 1);
-        if (RGBID_K1_IWB_LEVELS)
-          warp_px_iw(wm, o.IWB, w0, h0, xx, yy, __ldg(WAw + yy * w0 + xx), vi[q], vw[q], d0, d1);
-        else
-          warp_px(wm, IB, WB, w0, h0, xx, yy, __ldg(WAw + yy * w0 + xx), vi[q], vw[q], d0, d1);
+        warp_px_iw(wm, o.IWB, w0, h0, xx, yy, __ldg(WAw + yy * w0 + xx), vi[q], vw[q], d0, d1);
       }
       sI[r * cw + col] = ds4(vi[0], vi[1], vi[2], vi[3]);
       sW[r * cw + col] = ds4(vw[0], vw[1], vw[2], vw[3]);
@@ -363,117 +348,6 @@ __global__ void __launch_bounds__(k1_threads<L>(), RGBID_K1_THREADS_PER_SM / k1_
   }
 }
 
-// Coarse-level K1 without block barriers in the downsample (levels 2 and 3): each
-// warp owns whole level-L pixels.  A lane computes one (L = 2) or two vertically
-// adjacent (L = 3) level-1 values, each the downsample2 of its 2x2 full-res warps
-// in registers; the level-2 / level-3 downsamples combine neighbouring lanes'
-// values with shuffles, taps in the reference order (0,0),(1,0),(0,1),(1,1)
-// (inc/image.hpp:73-91).  L = 2: lanes 4q..4q+3 hold the 2x2 level-1 block of output
-// q (8 outputs per warp); L = 3: lanes 8q..8q+7 hold level-1 columns 0..3 x row
-// pairs {0,1}, {2,3} of output q (4 outputs per warp).  The tile (tx level pixels of
-// one level row, 8 warps) is the same as k_warp_residuals<L>'s, so the per-tile
-// counts and row-major validity words are unchanged; one barrier at the end
-// assembles them.
-template <int L>
-__global__ void __launch_bounds__(256, RGBID_K1_THREADS_PER_SM / 256) k_warp_residuals_shfl(
-    const SlotIO* __restrict__ io, const SlotState* __restrict__ st, LevelInfo li, int w0, int h0,
-    int phase) {
-  static_assert(L == 2 || L == 3, "shuffle downsample for levels 2 and 3");
-  constexpr int G = L == 2 ? 4 : 8;    // lanes per level-L output
-  constexpr int OPW = 32 / G;          // outputs per warp
-  constexpr int R1 = L == 2 ? 1 : 2;   // level-1 values per lane (vertical)
-  const int slot = blockIdx.y;
-  const SlotState& S = st[slot];
-  if (!slot_active(S, L, phase)) return;
-  __shared__ WarpMats wm;
-  __shared__ unsigned char sbits[2][8];
-  if (threadIdx.x < 24)
-    reinterpret_cast<double*>(&wm)[threadIdx.x] = reinterpret_cast<const double*>(&S.wm)[threadIdx.x];
-  const SlotIO& o = io[slot];
-  const double* __restrict__ WAw = phase ? o.fWA : o.WA[0];
-  const double* __restrict__ IAl = phase ? o.fIA : o.IA[L];
-  const uint8_t* __restrict__ am = o.amask[L];
-  __syncthreads();
-  const int tile = blockIdx.x;
-  const int yl = tile / li.nseg, seg = tile - yl * li.nseg;
-  const int xl0 = seg * li.tx;
-  const int nx = min(li.tx, li.w - xl0);
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int q = lane / G, sub = lane % G;
-  const int ol = wid * OPW + q;  // output (level-L pixel) index within the tile
-  const bool live = ol < nx;
-  // this lane's level-1 column and first level-1 row within the output's block
-  const int c1 = L == 2 ? (sub & 1) : (sub & 3);
-  const int r1 = L == 2 ? (sub >> 1) : 2 * (sub >> 2);
-  const int X1 = ((xl0 + ol) << (L - 1)) + c1, Y1 = (yl << (L - 1)) + r1;
-  double v1i[R1], v1w[R1];
-#pragma unroll
-  for (int r = 0; r < R1; ++r) {
-    v1i[r] = v1w[r] = CUDART_NAN;
-    if (live) {
-      const int x = 2 * X1, y = 2 * (Y1 + r);
-      double vi[4], vw[4], d0, d1;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const int xx = x + (k & 1), yy = y + (k >> 1);
-        warp_px_iw(wm, o.IWB, w0, h0, xx, yy, __ldg(WAw + yy * w0 + xx), vi[k], vw[k], d0, d1);
-      }
-      v1i[r] = ds4(vi[0], vi[1], vi[2], vi[3]);
-      v1w[r] = ds4(vw[0], vw[1], vw[2], vw[3]);
-    }
-  }
-  double oi, ow;
-  if (L == 2) {  // lanes 4q + {0,1,2,3} = level-1 (0,0),(1,0),(0,1),(1,1)
-    const double i1 = __shfl_down_sync(0xffffffffu, v1i[0], 1), w1 = __shfl_down_sync(0xffffffffu, v1w[0], 1);
-    const double i2 = __shfl_down_sync(0xffffffffu, v1i[0], 2), w2 = __shfl_down_sync(0xffffffffu, v1w[0], 2);
-    const double i3 = __shfl_down_sync(0xffffffffu, v1i[0], 3), w3 = __shfl_down_sync(0xffffffffu, v1w[0], 3);
-    oi = ds4(v1i[0], i1, i2, i3);
-    ow = ds4(v1w[0], w1, w2, w3);
-  } else {  // level 2 at sub 0, 2, 4, 6 from (own, lane+1) x (row pair), then level 3 at sub 0
-    const double a1 = __shfl_down_sync(0xffffffffu, v1i[0], 1), b1 = __shfl_down_sync(0xffffffffu, v1w[0], 1);
-    const double a3 = __shfl_down_sync(0xffffffffu, v1i[1], 1), b3 = __shfl_down_sync(0xffffffffu, v1w[1], 1);
-    const double l2i = ds4(v1i[0], a1, v1i[1], a3), l2w = ds4(v1w[0], b1, v1w[1], b3);
-    const double i2 = __shfl_down_sync(0xffffffffu, l2i, 2), w2 = __shfl_down_sync(0xffffffffu, l2w, 2);
-    const double i4 = __shfl_down_sync(0xffffffffu, l2i, 4), w4 = __shfl_down_sync(0xffffffffu, l2w, 4);
-    const double i6 = __shfl_down_sync(0xffffffffu, l2i, 6), w6 = __shfl_down_sync(0xffffffffu, l2w, 6);
-    oi = ds4(l2i, i2, i4, i6);
-    ow = ds4(l2w, w2, w4, w6);
-  }
-  bool jet = false, dep = false;
-  if (live && sub == 0) {
-    const int idx = yl * li.w + xl0 + ol;
-    o.ibw[idx] = make_double2(oi - __ldg(IAl + idx), ow);  // r_I (src/alignment.cpp:222), w_b
-    const unsigned a = __ldg(am + idx);
-    jet = (a & 1u) && valid(oi);
-    dep = jet && (a & 2u) && valid(ow) && ow > 0.0;
-  }
-  const unsigned bj = __ballot_sync(0xffffffffu, jet), bd = __ballot_sync(0xffffffffu, dep);
-  if (lane == 0) {  // compress bits G*k -> k
-    unsigned cj = 0, cd = 0;
-#pragma unroll
-    for (int k = 0; k < OPW; ++k) {
-      cj |= ((bj >> (G * k)) & 1u) << k;
-      cd |= ((bd >> (G * k)) & 1u) << k;
-    }
-    sbits[0][wid] = (unsigned char)cj;
-    sbits[1][wid] = (unsigned char)cd;
-  }
-  __syncthreads();
-  // row-major validity words of the tile (32 level pixels each) and the counts
-  constexpr int WPW = 32 / OPW;  // warps per word
-  const int words = (li.tx + 31) / 32;
-  if (threadIdx.x < 2 * words) {
-    const int t = threadIdx.x / words, wd = threadIdx.x % words;
-    unsigned m = 0;
-#pragma unroll
-    for (int k = 0; k < WPW; ++k) m |= (unsigned)sbits[t][wd * WPW + k] << (OPW * k);
-    (t ? o.bitsW : o.bitsI)[tile * kWordsPerTile + wd] = m;
-    const int c = __popc(m);
-    const int tot = c + __shfl_down_sync(words == 2 ? 0xfu : 0x3u, c, 1, words);
-    if (wd == 0) (t ? o.cntW : o.cntI)[tile] = words == 2 ? tot : c;
-  }
-}
-
 // Level-0 K1: 128 threads per 256-pixel tile, two independent pixels per thread
 // (x and x + 128) so their dependent load chains (W_A -> gathers) overlap.
 #ifndef RGBID_K1L0_MINB
@@ -493,8 +367,6 @@ __global__ void __launch_bounds__(128, RGBID_K1L0_MINB) k_warp_residuals_l0(cons
   const double* __restrict__ WAw = phase ? o.fWA : o.WA[0];
   const double* __restrict__ IA0 = phase ? o.fIA : o.IA[0];
   const uint8_t* __restrict__ am = o.amask[0];
-  const double* __restrict__ IB = o.IB;
-  const double* __restrict__ WB = o.WB;
   __syncthreads();
   const int tid = threadIdx.x;
   const int tile = blockIdx.x;
@@ -511,10 +383,7 @@ __global__ void __launch_bounds__(128, RGBID_K1L0_MINB) k_warp_residuals_l0(cons
       const unsigned a = __ldg(am + idx);
       const double ia = __ldg(IA0 + idx);
       double ib, wb, d0, d1;
-      if (RGBID_K1_IWB)
-        warp_px_iw(wm, o.IWB, w0, h0, xl0 + lx, yl, __ldg(WAw + idx), ib, wb, d0, d1);
-      else
-        warp_px(wm, IB, WB, w0, h0, xl0 + lx, yl, __ldg(WAw + idx), ib, wb, d0, d1);
+      warp_px_iw(wm, o.IWB, w0, h0, xl0 + lx, yl, __ldg(WAw + idx), ib, wb, d0, d1);
       o.ibw[idx] = make_double2(ib - ia, wb);  // r_I (src/alignment.cpp:222), w_b: K2, K3
       jet[q] = (a & 1u) && valid(ib);
       dep[q] = jet[q] && (a & 2u) && valid(wb) && wb > 0.0;
@@ -546,97 +415,6 @@ __global__ void __launch_bounds__(128, RGBID_K1L0_MINB) k_warp_residuals_l0(cons
   }
 }
 
-// Level-0 K1, persistent over tiles (RGBID_K1L0_PERSIST = tiles per CTA): the CTA
-// walks tiles blockIdx.x, + gridDim.x, ... of its slot and loads the NEXT tile's
-// W_A, I_A and mask bytes before warping the current one, so the first link of
-// the per-pixel dependent chain (W_A -> taps) is off the critical path.  Same
-// per-pixel arithmetic, outputs and per-tile ballots as k_warp_residuals_l0.
-#ifndef RGBID_ALLSUM_SMEM
-#define RGBID_ALLSUM_SMEM 0
-#endif
-#ifndef RGBID_K1L0_PERSIST
-#define RGBID_K1L0_PERSIST 0
-#endif
-__global__ void __launch_bounds__(128, RGBID_K1L0_MINB) k_warp_residuals_l0p(const SlotIO* __restrict__ io,
-                                                                 const SlotState* __restrict__ st,
-                                                                 LevelInfo li, int w0, int h0,
-                                                                 int phase) {
-  const int slot = blockIdx.y;
-  const SlotState& S = st[slot];
-  if (!slot_active(S, 0, phase)) return;
-  __shared__ WarpMats wm;
-  __shared__ int wcnt[2][2][8];  // [tile parity][type][word]
-  if (threadIdx.x < 24)
-    reinterpret_cast<double*>(&wm)[threadIdx.x] = reinterpret_cast<const double*>(&S.wm)[threadIdx.x];
-  const SlotIO& o = io[slot];
-  const double* __restrict__ WAw = phase ? o.fWA : o.WA[0];
-  const double* __restrict__ IA0 = phase ? o.fIA : o.IA[0];
-  const uint8_t* __restrict__ am = o.amask[0];
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int nt = li.ntiles;
-  double pwa[2], pia[2];
-  unsigned pam[2];
-  auto prefetch = [&](int tile) {
-    const int yl = tile / li.nseg, seg = tile - yl * li.nseg;
-    const int xl0 = seg * li.tx, nx = min(li.tx, li.w - xl0);
-#pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      const int lx = tid + 128 * q;
-      const bool in = tile < nt && lx < nx;
-      const int idx = yl * w0 + xl0 + lx;
-      pwa[q] = in ? __ldg(WAw + idx) : CUDART_NAN;
-      pia[q] = in ? __ldg(IA0 + idx) : 0.0;
-      pam[q] = in ? __ldg(am + idx) : 0u;
-    }
-  };
-  prefetch(blockIdx.x);
-  __syncthreads();
-  int par = 0;
-  for (int tile = blockIdx.x; tile < nt; tile += gridDim.x, par ^= 1) {
-    const double cwa[2] = {pwa[0], pwa[1]}, cia[2] = {pia[0], pia[1]};
-    const unsigned cam[2] = {pam[0], pam[1]};
-    prefetch(tile + gridDim.x);
-    const int yl = tile / li.nseg, seg = tile - yl * li.nseg;
-    const int xl0 = seg * li.tx, nx = min(li.tx, li.w - xl0);
-    bool jet[2], dep[2];
-#pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      const int lx = tid + 128 * q;
-      jet[q] = dep[q] = false;
-      if (lx < nx) {
-        const int idx = yl * w0 + xl0 + lx;
-        double ib, wb, d0, d1;
-        warp_px_iw(wm, o.IWB, w0, h0, xl0 + lx, yl, cwa[q], ib, wb, d0, d1);
-        o.ibw[idx] = make_double2(ib - cia[q], wb);  // r_I (src/alignment.cpp:222), w_b
-        jet[q] = (cam[q] & 1u) && valid(ib);
-        dep[q] = jet[q] && (cam[q] & 2u) && valid(wb) && wb > 0.0;
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      const unsigned bj = __ballot_sync(0xffffffffu, jet[q]), bd = __ballot_sync(0xffffffffu, dep[q]);
-      if (lane == 0) {
-        const int word = wid + 4 * q;
-        wcnt[par][0][word] = __popc(bj);
-        wcnt[par][1][word] = __popc(bd);
-        o.bitsI[tile * kWordsPerTile + word] = bj;
-        o.bitsW[tile * kWordsPerTile + word] = bd;
-      }
-    }
-    __syncthreads();  // double-buffered counts: one barrier per tile
-    if (tid == 0) {
-      int tI = 0, tW = 0;
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        tI += wcnt[par][0][k];
-        tW += wcnt[par][1][k];
-      }
-      o.cntI[tile] = tI;
-      o.cntW[tile] = tW;
-    }
-  }
-}
-
 // A-side part of residuals_and_jacobians, constant over the IRLS iterations:
 // validity (src/alignment.cpp:209-211,227) and gradient_at of I_A and W_A
 // (src/alignment.cpp:165-191) per level pixel.  phase 1 = from the filtered A
@@ -646,8 +424,7 @@ __global__ void __launch_bounds__(128, RGBID_K1L0_MINB) k_warp_residuals_l0p(con
 // out-of-bounds hole), so every 3 x 3 stencil read is a shared load.
 constexpr int kPTW = 32, kPTH = 8, kPRW = kPTW + 2, kPRH = kPTH + 2;
 
-// gradient_at on a staged tile of row stride RS (same tests and expressions)
-template <int RS = kPRW>
+// gradient_at on the staged tile (same tests and expressions)
 __device__ __forceinline__ bool grad_sm(const double* t, int i, double& gx, double& gy) {
   const double c = t[i];
   if (!valid(c)) return false;
@@ -660,7 +437,7 @@ __device__ __forceinline__ bool grad_sm(const double* t, int i, double& gx, doub
     gx = c - l;
   else
     return false;
-  const double u = t[i - RS], d = t[i + RS];
+  const double u = t[i - kPRW], d = t[i + kPRW];
   if (valid(u) && valid(d))
     gy = (d - u) / 2.0;
   else if (valid(d))
@@ -701,11 +478,9 @@ __global__ void __launch_bounds__(kPTW * kPTH) k_prep_A(const SlotIO* __restrict
   if (valid(w_a) && w_a > 0.0 && valid(i_a) && grad_sm(tI, i, g[0], g[1])) m |= 1u;
   if (grad_sm(tW, i, g[2], g[3])) m |= 2u;
   o.amask[level][k] = (uint8_t)m;
-  if (!RGBID_K3_TILE) {
-    double2* gp = reinterpret_cast<double2*>(o.agrad[level] + 4 * k);
-    gp[0] = make_double2(g[0], g[1]);
-    gp[1] = make_double2(g[2], g[3]);
-  }
+  double2* gp = reinterpret_cast<double2*>(o.agrad[level] + 4 * k);
+  gp[0] = make_double2(g[0], g[1]);
+  gp[1] = make_double2(g[2], g[3]);
 }
 
 // frame B interleaved {I, W} for K1's taps, once per align
@@ -719,7 +494,6 @@ __global__ void k_interleave_B(const SlotIO* __restrict__ io, const SlotState* _
 }
 
 void launch_interleave_B(const AlignLaunch& a, cudaStream_t s) {
-  if (!RGBID_K1_IWB) return;
   KScope ks_("interleave_B", s);
   const int n = a.w0 * a.h0;
   k_interleave_B<<<dim3((n + 255) / 256, a.nslots), 256, 0, s>>>(a.io, a.st, n);
@@ -768,27 +542,10 @@ void launch_warp_residuals(const AlignLaunch& a, const LevelInfo& li, int phase,
   KScope ks_(kLevelNames[phase ? 1 : 0][li.level], s);
   dim3 grid(li.ntiles, a.nslots);
   switch (li.level) {
-    case 0:
-      if (RGBID_K1L0_PERSIST > 1)
-        k_warp_residuals_l0p<<<dim3((li.ntiles + RGBID_K1L0_PERSIST - 1) / RGBID_K1L0_PERSIST,
-                                    a.nslots),
-                               128, 0, s>>>(a.io, a.st, li, a.w0, a.h0, phase);
-      else
-        k_warp_residuals_l0<<<grid, 128, 0, s>>>(a.io, a.st, li, a.w0, a.h0, phase);
-      break;
+    case 0: k_warp_residuals_l0<<<grid, 128, 0, s>>>(a.io, a.st, li, a.w0, a.h0, phase); break;
     case 1: k_warp_residuals<1><<<grid, k1_threads<1>(), 0, s>>>(a.io, a.st, li, a.w0, a.h0, phase); break;
-    case 2:
-      if (RGBID_K1_SHFL)
-        k_warp_residuals_shfl<2><<<grid, 256, 0, s>>>(a.io, a.st, li, a.w0, a.h0, phase);
-      else
-        k_warp_residuals<2><<<grid, k1_threads<2>(), 0, s>>>(a.io, a.st, li, a.w0, a.h0, phase);
-      break;
-    case 3:
-      if (RGBID_K1_SHFL)
-        k_warp_residuals_shfl<3><<<grid, 256, 0, s>>>(a.io, a.st, li, a.w0, a.h0, phase);
-      else
-        k_warp_residuals<3><<<grid, k1_threads<3>(), 0, s>>>(a.io, a.st, li, a.w0, a.h0, phase);
-      break;
+    case 2: k_warp_residuals<2><<<grid, k1_threads<2>(), 0, s>>>(a.io, a.st, li, a.w0, a.h0, phase); break;
+    case 3: k_warp_residuals<3><<<grid, k1_threads<3>(), 0, s>>>(a.io, a.st, li, a.w0, a.h0, phase); break;
     case 4: k_warp_residuals<4><<<grid, k1_threads<4>(), 0, s>>>(a.io, a.st, li, a.w0, a.h0, phase); break;
     case 5: k_warp_residuals<5><<<grid, k1_threads<5>(), 0, s>>>(a.io, a.st, li, a.w0, a.h0, phase); break;
     default: return;
@@ -823,28 +580,12 @@ __device__ __forceinline__ void block_allsum(double (&v)[NV], double* scratch2, 
 #pragma unroll
     for (int i = 0; i < NV; ++i) scratch[wid * NV + i] = v[i];
   __syncthreads();
-#if RGBID_ALLSUM_SMEM
-  // every thread sums the NW warp partials itself (broadcast shared loads, fixed
-  // pairwise tree: bit-identical everywhere) instead of a second shuffle butterfly
-#pragma unroll
-  for (int i = 0; i < NV; ++i) {
-    double t[NW];
-#pragma unroll
-    for (int k = 0; k < NW; ++k) t[k] = scratch[k * NV + i];
-#pragma unroll
-    for (int wdt = NW / 2; wdt > 0; wdt >>= 1)
-#pragma unroll
-      for (int k = 0; k < wdt; ++k) t[k] = t[2 * k] + t[2 * k + 1];
-    v[i] = t[0];
-  }
-#else
 #pragma unroll
   for (int i = 0; i < NV; ++i) v[i] = lane < NW ? scratch[lane * NV + i] : 0.0;
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1)
 #pragma unroll
     for (int i = 0; i < NV; ++i) v[i] += __shfl_xor_sync(0xffffffffu, v[i], off);
-#endif
 }
 
 struct TD {
@@ -1668,15 +1409,6 @@ extern "C" int rgbid_debug_tdist_phases(unsigned long long* out, int reset) {
 }
 #endif
 
-#ifndef RGBID_K3_MMA_MINB
-#define RGBID_K3_MMA_MINB 3
-#endif
-constexpr int kT3SW = kT3W + 2, kT3SH = kT3H + 2;
-constexpr int kT3Smem = 2 * kT3SW * kT3SH * 8 + (kTPB / 32) * (32 * 9 + 64) * 8;
-__global__ void __launch_bounds__(kTPB, RGBID_K3_MMA_MINB)
-    k_normal_eq_tile(const SlotIO* __restrict__ io, const SlotState* __restrict__ st, LevelInfo li,
-                     int phase, double lambda_n_min);
-
 int init_kernel_attributes() {
   const cudaError_t e =
       cudaFuncSetAttribute(k_tdist_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1689,7 +1421,6 @@ int init_kernel_attributes() {
     cudaFuncSetAttribute(k_tdist<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          kMaxSample / 4 * 8);
   cudaFuncSetAttribute(k_gather, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-  cudaFuncSetAttribute(k_normal_eq_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, kT3Smem);
   const cudaError_t e2 =
       cudaFuncSetAttribute(k_tdist_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
   if (kTdistCluster > 8)
@@ -1774,120 +1505,9 @@ __device__ __forceinline__ void block_sum_to(double (&v)[kNPart], double* out, d
   }
 }
 
-__device__ __forceinline__ void accum(double (&acc)[kNPart], const double (&J)[6], double w,
-                                      double r) {
-  int q = 0;
-#pragma unroll
-  for (int a = 0; a < 6; ++a) {
-    const double va = w * J[a];
-#pragma unroll
-    for (int c = 0; c <= a; ++c) {
-      acc[q] = fma(va, J[c], acc[q]);
-      ++q;
-    }
-    acc[21 + a] = fma(va, r, acc[21 + a]);
-  }
-  acc[27] = fma(w * r, r, acc[27]);
-}
-
-#ifndef RGBID_K3_MINBLOCKS
-#define RGBID_K3_MINBLOCKS 2
-#endif
-__global__ void __launch_bounds__(kTPB, RGBID_K3_MINBLOCKS) k_normal_eq(const SlotIO* __restrict__ io,
-                                                    const SlotState* __restrict__ st, LevelInfo li,
-                                                    int phase, double lambda_n_min) {
-  const int slot = blockIdx.y;
-  const SlotState& S = st[slot];
-  if (!slot_active(S, li.level, phase)) return;
-  const SlotIO& o = io[slot];
-  const double* __restrict__ WA = phase ? o.fWA : o.WA[li.level];
-  const uint8_t* __restrict__ am = o.amask[li.level];
-  const double2* __restrict__ ag = reinterpret_cast<const double2*>(o.agrad[li.level]);
-  const double2* __restrict__ ibwp = o.ibw;
-  __shared__ double scratch[(kTPB / 32) * kNPart];
-  const double muI = S.tI.mu, isgI = 1.0 / S.tI.sigma, nuI = dmax_std(S.tI.nu, S.tW.nu);
-  const double muW = S.tW.mu, isgW = 1.0 / S.tW.sigma, nuW = S.tW.nu;
-  const double nuI1 = nuI + 1.0, nuW1 = nuW + 1.0;
-  const double is2i = isgI * isgI, is2w = isgW * isgW;
-  const int w = li.w;
-  const double* Ki = li.Kinv;
-  double acc[kNPart];
-#pragma unroll
-  for (int i = 0; i < kNPart; ++i) acc[i] = 0.0;
-  const int N = li.w * li.h;
-#pragma unroll 1
-  for (int p = 0; p < kPixK3; ++p) {
-    const int k = (blockIdx.x * kPixK3 + p) * kTPB + threadIdx.x;
-    if (k >= N) break;
-    // every load of the pixel issued at once (one memory round trip; the
-    // validity tests below only select)
-    const unsigned a = __ldg(am + k);
-    const double2 rw = __ldcs(ibwp + k);  // {r_I = i_b - i_a, w_b} (K1)
-    const double r_I = rw.x, w_b = rw.y;
-    const double w_a = __ldg(WA + k);
-    const double2 gI = __ldg(ag + 2 * k), gW = __ldg(ag + 2 * k + 1);
-    if (!(a & 1u) || !valid(r_I)) continue;  // bit0 implies valid(i_a): valid(r_I) == valid(i_b)
-    const int y = k / w, x = k - y * w;
-    const double px = x, py = y;
-    const double ax = li.cx - px, ay = li.cy - py;  // A(0,2), A(1,2)
-    const double iwa = rcp_fast(w_a);  // H is tolerance-checked: MUFU + Newton, no IEEE divide
-    const double k0 = red3(Ki[0] * px, Ki[1] * py, Ki[2]), k1 = red3(Ki[3] * px, Ki[4] * py, Ki[5]),
-                 k2 = red3(Ki[6] * px, Ki[7] * py, Ki[8]);
-    const double X0 = k0 * iwa, X1 = k1 * iwa, X2 = k2 * iwa;
-    // photometric row: u = w_a (gix, giy, 0) A ; J_I = (u, X x u)
-    double J[6];
-    {
-      const double s0 = w_a * gI.x, s1 = w_a * gI.y;
-      const double u0 = s0 * li.fx, u1 = s1 * li.fy, u2 = s0 * ax + s1 * ay;
-      J[0] = u0;
-      J[1] = u1;
-      J[2] = u2;
-      J[3] = X1 * u2 - X2 * u1;
-      J[4] = X2 * u0 - X0 * u2;
-      J[5] = X0 * u1 - X1 * u0;
-      const double rI = r_I;
-      const double xi_ = (rI - muI) * isgI;
-      const double wi = nuI1 * rcp_fast(fma(xi_, xi_, nuI)) * is2i;
-      accum(acc, J, wi, rI);
-    }
-    if (!((a & 2u) && valid(w_b) && w_b > 0.0)) continue;
-    // geometric row: s = w_a (g_W A + w_b e_z) ; J_W = (s, X x s)
-    const double g0 = gW.x * li.fx, g1 = gW.y * li.fy, g2 = gW.x * ax + gW.y * ay;
-    {
-      const double s0 = w_a * g0, s1 = w_a * g1, s2 = w_a * (g2 + w_b);
-      J[0] = s0;
-      J[1] = s1;
-      J[2] = s2;
-      J[3] = X1 * s2 - X2 * s1;
-      J[4] = X2 * s0 - X0 * s2;
-      J[5] = X0 * s1 - X1 * s0;
-    }
-    // lambda_n: normal of the inverse-depth surface vs the viewing ray
-    double lambda = 1.0;
-    {
-      const double n0 = g0 * iwa, n1 = g1 * iwa, n2 = g2 * iwa + 1.0;
-      const double nn2 = n0 * n0 + n1 * n1 + n2 * n2;
-      if (!(nn2 < 1e-24)) {  // ||n|| < 1e-12 without the sqrt
-        const double rr2 = k0 * k0 + k1 * k1 + k2 * k2;
-        double c = (n0 * k0 + n1 * k1 + n2 * k2) * rsqrt(nn2 * rr2);
-        if (n2 < 0) c = -c;
-        lambda = dmax_std(lambda_n_min, c);
-      }
-    }
-    const double rW = w_b - w_a;
-    const double xw = (rW - muW) * isgW;
-    const double ww = lambda * nuW1 * rcp_fast(fma(xw, xw, nuW)) * is2w;
-    accum(acc, J, ww, rW);
-  }
-  block_sum_to<kTPB>(acc, o.part + (size_t)blockIdx.x * kNPart, scratch);
-}
-
 static const char* kNeNames[kMaxLevels] = {"normal_eq_L0", "normal_eq_L1", "normal_eq_L2",
                                             "normal_eq_L3", "normal_eq_L4", "normal_eq_L5"};
 
-#ifndef RGBID_K3_MMA
-#define RGBID_K3_MMA 1
-#endif
 
 // D = A B + C, one m8n8k4 fp64 tensor-core MMA (A row-major 8x4, B col-major 4x8;
 // lane l holds A[l/4][l%4], B[l%4][l/4], C[l/4][2(l%4) + {0,1}])
@@ -1902,16 +1522,30 @@ __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double
 // C += sum_k w_k x_k x_k^T with 8 MMAs per row type, so the 8x8 system (H, the
 // J^T W r column, the cost) lives in two fp64 registers per lane instead of 28 --
 // the register file no longer caps occupancy.  Invalid rows are zeroed (w and x).
+// Sets the level's WHILE-loop condition (single-pair conditional graph) if any.
+__device__ __forceinline__ void set_cond(unsigned long long cond, unsigned v) {
+  if (cond) cudaGraphSetConditional((cudaGraphConditionalHandle)cond, v);
+}
+__device__ __noinline__ void solve_slot(const SlotIO& o, SlotState& S, int slot, const LevelInfo& li,
+                                        const AlignLaunch& a, int max_iters,
+                                        unsigned long long cond);
+__device__ __noinline__ void covariance_slot(const SlotIO& o, SlotState& S, int ntiles3);
+
 #ifndef RGBID_K3_MMA_MINB
 #define RGBID_K3_MMA_MINB 3
 #endif
 __global__ void __launch_bounds__(kTPB, RGBID_K3_MMA_MINB) k_normal_eq_mma(const SlotIO* __restrict__ io,
-                                                        const SlotState* __restrict__ st,
+                                                        SlotState* __restrict__ st,
                                                         LevelInfo li, int phase,
-                                                        double lambda_n_min) {
+                                                        AlignLaunch al, int max_iters,
+                                                        unsigned long long cond) {
+  const double lambda_n_min = al.lambda_n_min;
   const int slot = blockIdx.y;
-  const SlotState& S = st[slot];
-  if (!slot_active(S, li.level, phase)) return;  // uniform over the CTA
+  SlotState& S = st[slot];
+  if (!slot_active(S, li.level, phase)) {  // uniform over the CTA
+    if (blockIdx.x == 0 && threadIdx.x == 0) set_cond(cond, 0);
+    return;
+  }
   const SlotIO& o = io[slot];
   const double* __restrict__ WA = phase ? o.fWA : o.WA[li.level];
   const uint8_t* __restrict__ am = o.amask[li.level];
@@ -2028,184 +1662,28 @@ __global__ void __launch_bounds__(kTPB, RGBID_K3_MMA_MINB) k_normal_eq_mma(const
 #pragma unroll
     for (int wv = 0; wv < kTPB / 32; ++wv) t += cst[wv][r * 8 + c];
     o.part[(size_t)blockIdx.x * kNPart + q] = t;
+    __threadfence();
   }
-}
-
-// K3 on 2-D tiles of kT3W x kT3H level pixels: the CTA stages I_A and W_A of its
-// tile plus a 1-pixel halo in shared memory (NaN outside the image = the
-// reference's out-of-bounds hole) and evaluates the A-side validity and
-// gradient_at (src/alignment.cpp:165-191,206-211,227) from it, so the only
-// per-pixel stream besides the staged A maps is K1's {r_I, w_b} pairs (32 B/px of
-// DRAM instead of 57 with a precomputed gradient stream).  Rows, weights and the
-// FP64-MMA accumulation are those of k_normal_eq_mma.  Warp w owns tile rows
-// w, w + 8, ...; each iteration is 32 consecutive pixels of one row.
-__global__ void __launch_bounds__(kTPB, RGBID_K3_MMA_MINB) k_normal_eq_tile(const SlotIO* __restrict__ io,
-                                                         const SlotState* __restrict__ st,
-                                                         LevelInfo li, int phase,
-                                                         double lambda_n_min) {
-  const int slot = blockIdx.y;
-  const SlotState& S = st[slot];
-  if (!slot_active(S, li.level, phase)) return;  // uniform over the CTA
-  const SlotIO& o = io[slot];
-  const double* __restrict__ IA = phase ? o.fIA : o.IA[li.level];
-  const double* __restrict__ WA = phase ? o.fWA : o.WA[li.level];
-  const double2* __restrict__ ibwp = o.ibw;
-  constexpr int XS = 9;  // 8 components + w per staged row
-  extern __shared__ double k3sm[];
-  double* tI = k3sm;
-  double* tW = k3sm + kT3SW * kT3SH;
-  double* xs = tW + kT3SW * kT3SH;           // [kTPB/32][32 * XS]
-  double* cst = xs + (kTPB / 32) * 32 * XS;  // [kTPB/32][64]
-  const int w = li.w, h = li.h;
-  const int ntx = (w + kT3W - 1) / kT3W;
-  const int ty0 = blockIdx.x / ntx, tx0 = blockIdx.x - ty0 * ntx;
-  const int x0 = tx0 * kT3W, y0 = ty0 * kT3H;
-  for (int i = threadIdx.x; i < kT3SW * kT3SH; i += kTPB) {
-    const int ry = i / kT3SW, rx = i - ry * kT3SW;
-    const int gx = x0 - 1 + rx, gy = y0 - 1 + ry;
-    const bool in = gx >= 0 && gx < w && gy >= 0 && gy < h;
-    const size_t k = (size_t)gy * w + gx;
-    tI[i] = in ? __ldg(IA + k) : CUDART_NAN;
-    tW[i] = in ? __ldg(WA + k) : CUDART_NAN;
-  }
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  double* xw = xs + wid * 32 * XS;
-  const double muI = S.tI.mu, isgI = 1.0 / S.tI.sigma, nuI = dmax_std(S.tI.nu, S.tW.nu);
-  const double muW = S.tW.mu, isgW = 1.0 / S.tW.sigma, nuW = S.tW.nu;
-  const double nuI1 = nuI + 1.0, nuW1 = nuW + 1.0;
-  const double is2i = isgI * isgI, is2w = isgW * isgW;
-  const double* Ki = li.Kinv;
-  double c0 = 0.0, c1 = 0.0;
-  auto mma_rows = [&]() {
-    __syncwarp();
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int row = 4 * j + (lane & 3);
-      const double xv = xw[row * XS + (lane >> 2)], wv = xw[row * XS + 8];
-      dmma884(c0, c1, wv * xv, xv);
-    }
-    __syncwarp();
-  };
-  constexpr int kIt = kT3W * kT3H / kTPB;  // 8 iterations of 32 pixels per warp
-  auto pix = [&](int it, int& x, int& y, int& r, int& c) {
-    r = wid + (kTPB / 32) * (it / (kT3W / 32));
-    c = lane + 32 * (it % (kT3W / 32));
-    x = x0 + c;
-    y = y0 + r;
-  };
-  // K1's pairs of the first iteration in flight during the staging barrier
-  int x, y, r, c;
-  pix(0, x, y, r, c);
-  bool inr = x < w && y < h;
-  double2 rw = inr ? __ldcs(ibwp + (size_t)y * w + x) : make_double2(0.0, 0.0);
+  // the slot's last CTA to finish reduces every tile's partials in a fixed order and
+  // runs K4 (solve + update) or K5 (covariance): no separate per-iteration launch
+  __shared__ bool last;
   __syncthreads();
-#pragma unroll 1
-  for (int it = 0; it < kIt; ++it) {
-    const double r_I = rw.x, w_b = rw.y;
-    const int xc = x, yc = y, rc = r, cc = c;
-    const bool inc = inr;
-    if (it + 1 < kIt) {  // prefetch the next iteration's pair
-      pix(it + 1, x, y, r, c);
-      inr = x < w && y < h;
-      rw = inr ? __ldcs(ibwp + (size_t)y * w + x) : make_double2(0.0, 0.0);
-    }
-    const int si = (rc + 1) * kT3SW + cc + 1;
-    const double w_a = tW[si], i_a = tI[si];
-    double gIx = 0.0, gIy = 0.0, gWx = 0.0, gWy = 0.0;
-    const bool okI = grad_sm<kT3SW>(tI, si, gIx, gIy);
-    const bool okW = grad_sm<kT3SW>(tW, si, gWx, gWy);
-    // jet validity (src/alignment.cpp:206-211): valid(i_a) and valid(i_b) <=> valid(r_I)
-    const bool jet = inc && valid(w_a) && w_a > 0.0 && valid(i_a) && okI && valid(r_I);
-    const bool dep = jet && okW && valid(w_b) && w_b > 0.0;
-    const double px = xc, py = yc;
-    const double ax = li.cx - px, ay = li.cy - py;
-    const double iwa = rcp_fast(jet ? w_a : 1.0);  // tolerance-checked H: MUFU + Newton
-    const double k0 = red3(Ki[0] * px, Ki[1] * py, Ki[2]), k1 = red3(Ki[3] * px, Ki[4] * py, Ki[5]),
-                 k2 = red3(Ki[6] * px, Ki[7] * py, Ki[8]);
-    const double X0 = k0 * iwa, X1 = k1 * iwa, X2 = k2 * iwa;
-    {  // photometric row
-      const double s0 = w_a * gIx, s1 = w_a * gIy;
-      const double u0 = s0 * li.fx, u1 = s1 * li.fy, u2 = s0 * ax + s1 * ay;
-      const double xi_ = (r_I - muI) * isgI;
-      const double wi = nuI1 * rcp_fast(fma(xi_, xi_, nuI)) * is2i;
-      double* rr = xw + lane * XS;
-      rr[0] = jet ? u0 : 0.0;
-      rr[1] = jet ? u1 : 0.0;
-      rr[2] = jet ? u2 : 0.0;
-      rr[3] = jet ? X1 * u2 - X2 * u1 : 0.0;
-      rr[4] = jet ? X2 * u0 - X0 * u2 : 0.0;
-      rr[5] = jet ? X0 * u1 - X1 * u0 : 0.0;
-      rr[6] = jet ? r_I : 0.0;
-      rr[7] = 0.0;
-      rr[8] = jet ? wi : 0.0;
-    }
-    mma_rows();
-    {  // geometric row
-      const double g0 = gWx * li.fx, g1 = gWy * li.fy, g2 = gWx * ax + gWy * ay;
-      const double s0 = w_a * g0, s1 = w_a * g1, s2 = w_a * (g2 + w_b);
-      double lambda = 1.0;
-      {
-        const double n0 = g0 * iwa, n1 = g1 * iwa, n2 = g2 * iwa + 1.0;
-        const double nn2 = n0 * n0 + n1 * n1 + n2 * n2;
-        if (!(nn2 < 1e-24)) {  // ||n|| < 1e-12 without the sqrt
-          const double rr2 = k0 * k0 + k1 * k1 + k2 * k2;
-          double cth = (n0 * k0 + n1 * k1 + n2 * k2) * rsqrt(nn2 * rr2);
-          if (n2 < 0) cth = -cth;
-          lambda = dmax_std(lambda_n_min, cth);
-        }
-      }
-      const double rW = w_b - w_a;
-      const double xw_ = (rW - muW) * isgW;
-      const double ww = lambda * nuW1 * rcp_fast(fma(xw_, xw_, nuW)) * is2w;
-      double* rr = xw + lane * XS;
-      rr[0] = dep ? s0 : 0.0;
-      rr[1] = dep ? s1 : 0.0;
-      rr[2] = dep ? s2 : 0.0;
-      rr[3] = dep ? X1 * s2 - X2 * s1 : 0.0;
-      rr[4] = dep ? X2 * s0 - X0 * s2 : 0.0;
-      rr[5] = dep ? X0 * s1 - X1 * s0 : 0.0;
-      rr[6] = dep ? rW : 0.0;
-      rr[7] = 0.0;
-      rr[8] = dep ? ww : 0.0;
-    }
-    mma_rows();
-  }
-  double* cw = cst + wid * 64;
-  cw[(lane >> 2) * 8 + 2 * (lane & 3)] = c0;
-  cw[(lane >> 2) * 8 + 2 * (lane & 3) + 1] = c1;
+  if (threadIdx.x == 0) last = atomicAdd(o.ticket, 1u) == gridDim.x - 1;
   __syncthreads();
-  if (threadIdx.x < kNPart) {  // partial q in k_normal_eq's order
-    const int q = threadIdx.x;
-    int rr, cc;
-    if (q < 21) {
-      rr = 0;
-      while ((rr + 1) * (rr + 2) / 2 <= q) ++rr;
-      cc = q - rr * (rr + 1) / 2;
-    } else if (q < 27) {
-      rr = q - 21;
-      cc = 6;
-    } else {
-      rr = 6;
-      cc = 6;
-    }
-    double t = 0.0;
-#pragma unroll
-    for (int wv = 0; wv < kTPB / 32; ++wv) t += cst[wv * 64 + rr * 8 + cc];
-    o.part[(size_t)blockIdx.x * kNPart + q] = t;
-  }
-}
-
-void launch_normal_equations(const AlignLaunch& a, const LevelInfo& li, int phase, cudaStream_t s) {
-  KScope ks_(phase ? "normal_eq_cov" : kNeNames[li.level], s);
-  if (RGBID_K3_TILE)
-    k_normal_eq_tile<<<dim3(li.ntiles3, a.nslots), kTPB, kT3Smem, s>>>(a.io, a.st, li, phase,
-                                                                    a.lambda_n_min);
-  else if (RGBID_K3_MMA)
-    k_normal_eq_mma<<<dim3(li.ntiles3, a.nslots), kTPB, 0, s>>>(a.io, a.st, li, phase,
-                                                                a.lambda_n_min);
+  if (!last) return;
+  __threadfence();
+  if (threadIdx.x == 0) *o.ticket = 0u;  // ready for the next launch
+  if (phase)
+    covariance_slot(o, S, li.ntiles3);
   else
-    k_normal_eq<<<dim3(li.ntiles3, a.nslots), kTPB, 0, s>>>(a.io, a.st, li, phase,
-                                                            a.lambda_n_min);
+    solve_slot(o, S, slot, li, al, max_iters, cond);
+}
+
+void launch_normal_equations(const AlignLaunch& a, const LevelInfo& li, int phase, cudaStream_t s,
+                             int max_iters, unsigned long long cond) {
+  KScope ks_(phase ? "normal_eq_cov" : kNeNames[li.level], s);
+  k_normal_eq_mma<<<dim3(li.ntiles3, a.nslots), kTPB, 0, s>>>(a.io, a.st, li, phase, a, max_iters,
+                                                              cond);
 }
 
 // fixed-order reduction of the per-tile partials into H (full, mirrored), b, cost
@@ -2216,7 +1694,7 @@ __device__ void reduce_partials(const double* part, int ntiles, double* H, doubl
   for (int i = 0; i < kNPart; ++i) acc[i] = 0.0;
   for (int t = threadIdx.x; t < ntiles; t += kTPB)
 #pragma unroll
-    for (int i = 0; i < kNPart; ++i) acc[i] += part[(size_t)t * kNPart + i];
+    for (int i = 0; i < kNPart; ++i) acc[i] += __ldcg(part + (size_t)t * kNPart + i);
   __shared__ double tot[kNPart];
   block_sum_to<kTPB>(acc, tot, sh);
   __syncthreads();
@@ -2233,37 +1711,36 @@ __device__ void reduce_partials(const double* part, int ntiles, double* H, doubl
   }
 }
 
-// K4: solve + pose update + convergence — src/alignment.cpp:387-401
-__global__ void __launch_bounds__(kTPB) k_solve(const SlotIO* __restrict__ io,
-                                                SlotState* __restrict__ st,
-                                                rgbid_iter_trace* __restrict__ trace, LevelInfo li,
-                                                int w0, int h0, double fx0, double fy0, double cx0,
-                                                double cy0, double eps) {
-  const int slot = blockIdx.x;
-  SlotState& S = st[slot];
-  if (!slot_active(S, li.level, 0)) return;
+// K4: solve + pose update + convergence — src/alignment.cpp:387-401.  Run by the
+// last CTA of the slot's K3 launch (all its threads) after the fixed-order reduction
+// of the tile partials; out of line so K3's register budget is unaffected.
+__device__ __noinline__ void solve_slot(const SlotIO& o, SlotState& S, int slot, const LevelInfo& li,
+                                        const AlignLaunch& a, int max_iters,
+                                        unsigned long long cond) {
+  const int L = li.level;
   if (S.nI < 6) {  // jets.size() < 6 -> DegenerateAlignmentError(zero spectrum)
     if (threadIdx.x == 0) {
       S.status = RGBID_E_DEGENERATE;
       for (int i = 0; i < 36; ++i) S.H[i] = 0.0;
+      set_cond(cond, 0);
     }
     return;
   }
   __shared__ double sh[(kTPB / 32) * kNPart];
   __shared__ double H[36], b[6], cost;
-  reduce_partials(io[slot].part, li.ntiles3, H, b, &cost, sh);
+  reduce_partials(o.part, li.ntiles3, H, b, &cost, sh);
   if (threadIdx.x != 0) return;
   for (int i = 0; i < 36; ++i) S.H[i] = H[i];
   if (rank_deficient6(H)) {
     S.status = RGBID_E_DEGENERATE;
+    set_cond(cond, 0);
     return;
   }
   double xi[6];
   ldlt_solve6(H, b, xi);
   const PoseD T = pose_update(xi, pose_from(S.R, S.t));
   pose_to(T, S.R, S.t);
-  S.wm = warp_mats(T, fx0, fy0, cx0, cy0);
-  const int L = li.level;
+  S.wm = warp_mats(T, a.fx0, a.fy0, a.cx0, a.cy0);
   S.iters[L] += 1;
   S.cost[L] = cost;
   S.total_iters += 1;
@@ -2273,8 +1750,8 @@ __global__ void __launch_bounds__(kTPB) k_solve(const SlotIO* __restrict__ io,
     S.finI = tI;
     S.finW = S.tW;
   }
-  if (trace && slot == 0 && S.trace_n < kTraceMax) {
-    rgbid_iter_trace& e = trace[S.trace_n++];
+  if (a.trace && slot == 0 && S.trace_n < kTraceMax) {
+    rgbid_iter_trace& e = a.trace[S.trace_n++];
     e.level = L;
     e.iter = S.iters[L] - 1;
     e.n_jets = S.nI;
@@ -2291,17 +1768,12 @@ __global__ void __launch_bounds__(kTPB) k_solve(const SlotIO* __restrict__ io,
   }
   const double xn = sqrt(red3(xi[0] * xi[0], xi[1] * xi[1], xi[2] * xi[2]) +
                          red3(xi[3] * xi[3], xi[4] * xi[4], xi[5] * xi[5]));
-  if (xn < eps) S.done_level = L;
-  (void)w0;
-  (void)h0;
+  if (xn < a.eps) S.done_level = L;
+  set_cond(cond, S.done_level != L && S.iters[L] < max_iters ? 1u : 0u);
 }
 
-// K5: filtered-Hessian covariance — src/alignment.cpp:422-435
-__global__ void __launch_bounds__(kTPB) k_covariance(const SlotIO* __restrict__ io,
-                                                     SlotState* __restrict__ st, int ntiles3) {
-  const int slot = blockIdx.x;
-  SlotState& S = st[slot];
-  if (S.status != RGBID_OK) return;
+// K5: filtered-Hessian covariance — src/alignment.cpp:422-435 (K3's last CTA, phase 1)
+__device__ __noinline__ void covariance_slot(const SlotIO& o, SlotState& S, int ntiles3) {
   if (S.nI < 6) {
     if (threadIdx.x < 36) S.cov[threadIdx.x] = (threadIdx.x % 7 == 0) ? 1e6 : 0.0;
     if (threadIdx.x == 0) S.cov_degenerate = 1;
@@ -2309,7 +1781,7 @@ __global__ void __launch_bounds__(kTPB) k_covariance(const SlotIO* __restrict__ 
   }
   __shared__ double sh[(kTPB / 32) * kNPart];
   __shared__ double H[36], b[6], cost;
-  reduce_partials(io[slot].part, ntiles3, H, b, &cost, sh);
+  reduce_partials(o.part, ntiles3, H, b, &cost, sh);
   if (threadIdx.x != 0) return;
   double Hs[36], inv[36];
   for (int r = 0; r < 6; ++r)
@@ -2325,16 +1797,6 @@ __global__ void __launch_bounds__(kTPB) k_covariance(const SlotIO* __restrict__ 
   S.cov_degenerate = 0;
 }
 
-void launch_covariance(const AlignLaunch& a, const LevelInfo& li, cudaStream_t s) {
-  KScope ks_("covariance", s);
-  k_covariance<<<a.nslots, kTPB, 0, s>>>(a.io, a.st, li.ntiles3);
-}
-
-void launch_solve(const AlignLaunch& a, const LevelInfo& li, const LevelInfo& li0, cudaStream_t s) {
-  KScope ks_("solve", s);
-  k_solve<<<a.nslots, kTPB, 0, s>>>(a.io, a.st, a.trace, li, a.w0, a.h0, li0.fx, li0.fy, li0.cx,
-                                    li0.cy, a.eps);
-}
 
 // ---------------------------------------------------------------------------
 // pyramid level: downsample2 of I and W — inc/image.hpp:73-91

@@ -32,15 +32,9 @@ constexpr int kTdistClusterMaxSlots = 8; // batches up to this size use the clus
 #endif
 constexpr int kTdistClusterThreads = RGBID_TDIST_CLUSTER_THREADS;
 constexpr int kPixK3 = 8;           // pixels per thread in the normal-equation kernel
-#ifndef RGBID_K3_TILE
-#define RGBID_K3_TILE 0  // 1: K3 on 2-D tiles, A-side gradients from a shared-memory halo tile (measured 14% slower per L0 launch)
-#endif
-// K3 tiles: kT3W x kT3H level pixels (2048 = kTPB * kPixK3), gradients from the
-// staged (kT3W + 2) x (kT3H + 2) halo of I_A, W_A
-constexpr int kT3W = 64, kT3H = 32;
+// K3 tiles: kTPB * kPixK3 consecutive level pixels
 __host__ __device__ constexpr int k3_tiles(int w, int h) {
-  return RGBID_K3_TILE ? ((w + kT3W - 1) / kT3W) * ((h + kT3H - 1) / kT3H)
-                       : (w * h + kTPB * kPixK3 - 1) / (kTPB * kPixK3);
+  return (w * h + kTPB * kPixK3 - 1) / (kTPB * kPixK3);
 }
 
 // K1 tiling of level l: tile = (level row, segment of tx level pixels).
@@ -83,6 +77,7 @@ struct SlotIO {
   double* part;                  // K3 partial sums [ntiles3][kNPart]
   double* smp;                   // K2 systematic samples [2][kMaxSample] (r_I, r_W; k_gather)
   int* nsmp;                     // K2 valid residual counts [2] (k_gather)
+  unsigned* ticket;              // K3 CTAs finished (the last one runs K4 / K5); 0 between launches
   int build_pyr;                 // 1: this slot builds frame A's pyramid levels >= 1
 };
 
@@ -116,14 +111,16 @@ struct AlignLaunch {
   int w0, h0;
   double eps;
   double lambda_n_min;
+  double fx0, fy0, cx0, cy0;  // level-0 intrinsics (K4's warp matrices)
 };
 
 // Kernel launchers (align_kernels.cu); all asynchronous on `stream`.
 void launch_warp_residuals(const AlignLaunch& a, const LevelInfo& li, int phase, cudaStream_t s);
 void launch_tdist(const AlignLaunch& a, const LevelInfo& li, int phase, cudaStream_t s);
-void launch_normal_equations(const AlignLaunch& a, const LevelInfo& li, int phase, cudaStream_t s);
-void launch_solve(const AlignLaunch& a, const LevelInfo& li, const LevelInfo& li0, cudaStream_t s);
-void launch_covariance(const AlignLaunch& a, const LevelInfo& li, cudaStream_t s);
+// K3 + (in its last CTA per slot) K4 solve/update (phase 0) or K5 covariance (phase 1);
+// cond: the level's WHILE-loop handle of a conditional graph (0 = none)
+void launch_normal_equations(const AlignLaunch& a, const LevelInfo& li, int phase, cudaStream_t s,
+                             int max_iters = 0, unsigned long long cond = 0);
 void launch_downsample2(const double* I, const double* W, int w, int h, double* oI, double* oW,
                         cudaStream_t s);
 void launch_pyramid_slots(const AlignLaunch& a, int levels, cudaStream_t s);
