@@ -13,12 +13,11 @@
 //                        K2a+K2b for <= 8 pairs over an 8-CTA cluster (latency mode).
 //   K3  k_normal_eq_mma  jets (src/alignment.cpp:212-244), robust weights and the
 //                        21+6+1 fp64 sums (src/alignment.cpp:321-335) on the FP64
-//                        tensor cores; the slot's last CTA then runs
-//   K4  solve_slot       fixed-order reduce, rank test, LDLT, SE(3) update, convergence
-//                        (src/alignment.cpp:387-401) — no host round trip, no launch;
-//                        for a single pair it also writes the level's WHILE condition.
+//                        tensor cores (k_normal_eq: the FMA version).
+//   K4  k_solve          fixed-order reduce, rank test, LDLT, SE(3) update, convergence
+//                        (src/alignment.cpp:387-401) — no host round trip.
 // Once per align: k_pyramid_slots, k_prep_A (A-side validity + gradients); the
-// covariance pass adds k_bilateral_slots, and K3's last CTA runs covariance_slot.
+// covariance pass adds k_bilateral_slots and k_covariance.
 // Compiled with --fmad=false: mask-deciding arithmetic rounds exactly like the
 // reference; reductions use a fixed tree (bit-reproducible run to run).
 #include <cooperative_groups.h>
@@ -97,6 +96,46 @@ __device__ __forceinline__ double bilin_fix(double r, double a, double b, double
   return (valid(a) && valid(b) && valid(c) && valid(d)) ? r : CUDART_NAN;
 }
 
+// warp_px_iw on separate I_B, W_B maps (k_warp_maps: the C-ABI inverse_geometric_warp,
+// whose frame B may differ in size from A).
+__device__ __forceinline__ void warp_px(const WarpMats& m, const double* __restrict__ IB,
+                                        const double* __restrict__ WB, int wb, int hb, int x,
+                                        int y, double w_a, double& oI, double& oW, double& mx,
+                                        double& my) {
+  const bool v0 = valid(w_a) && w_a > 0.0;
+  const double wa = v0 ? w_a : 1.0;
+  const double qz = __drcp_rn(wa);  // == 1.0 / w_a
+  const double qx = div_rcp((double)x, wa, qz), qy = div_rcp((double)y, wa, qz);
+  const double xb0 = red3(m.Rt_BA[0] * qx, m.Rt_BA[1] * qy, m.Rt_BA[2] * qz) + m.tt_BA[0];
+  const double xb1 = red3(m.Rt_BA[3] * qx, m.Rt_BA[4] * qy, m.Rt_BA[5] * qz) + m.tt_BA[1];
+  const double xb2 = red3(m.Rt_BA[6] * qx, m.Rt_BA[7] * qy, m.Rt_BA[8] * qz) + m.tt_BA[2];
+  const bool v1 = v0 && xb2 > 1e-12;
+  const double z = v1 ? xb2 : 1.0;
+  const double rz2 = __drcp_rn(z);
+  const double px = div_rcp(xb0, z, rz2), py = div_rcp(xb1, z, rz2);
+  mx = v1 ? px : CUDART_NAN;
+  my = v1 ? py : CUDART_NAN;
+  const bool inb = v1 && (px >= 0.0 && px <= wb - 1.0 && py >= 0.0 && py <= hb - 1.0);
+  const double sx = inb ? px : 0.0, sy = inb ? py : 0.0;
+  const int x0 = (int)floor(sx), y0 = (int)floor(sy);
+  const int dx = x0 + 1 < wb ? 1 : 0;  // x1 = min(x0 + 1, w - 1)
+  const int dy = y0 + 1 < hb ? wb : 0; // y1 = min(y0 + 1, h - 1)
+  const double fx = sx - x0, fy = sy - y0, gx = 1 - fx, gy = 1 - fy;
+  const int i00 = y0 * wb + x0;
+  const double a00 = __ldg(IB + i00), a10 = __ldg(IB + i00 + dx), a01 = __ldg(IB + i00 + dy),
+               a11 = __ldg(IB + i00 + dy + dx);
+  const double b00 = __ldg(WB + i00), b10 = __ldg(WB + i00 + dx), b01 = __ldg(WB + i00 + dy),
+               b11 = __ldg(WB + i00 + dy + dx);
+  const double ri = bilin_fix(gy * (gx * a00 + fx * a10) + fy * (gx * a01 + fx * a11), a00, a10, a01, a11);
+  const double w_meas = bilin_fix(gy * (gx * b00 + fx * b10) + fy * (gx * b01 + fx * b11), b00, b10, b01, b11);
+  oI = inb ? ri : CUDART_NAN;
+  const bool v2 = inb && valid(w_meas) && w_meas > 0.0;
+  const double rz = red3(m.Rt_AB[6] * px, m.Rt_AB[7] * py, m.Rt_AB[8] * 1.0);
+  const double za = rz / (v2 ? w_meas : 1.0) + m.tt_AB[2];
+  const bool v3 = v2 && za > 1e-12;
+  oW = v3 ? __drcp_rn(za) : CUDART_NAN;  // == 1.0 / za
+}
+
 // one A pixel of inverse_geometric_warp — src/warping.cpp:96-111 (bit-identical),
 // on frame B stored interleaved {I, W}: the four bilinear taps are four 16-byte
 // loads instead of eight 8-byte loads (-11% per level-0 launch).  Written branch-free (predicates + clamped, always-issued tap loads) so that
@@ -129,46 +168,6 @@ __device__ __forceinline__ void warp_px_iw(const WarpMats& m, const double2* __r
                 t11 = __ldg(IWB + i00 + dy + dx);
   const double a00 = t00.x, a10 = t10.x, a01 = t01.x, a11 = t11.x;
   const double b00 = t00.y, b10 = t10.y, b01 = t01.y, b11 = t11.y;
-  const double ri = bilin_fix(gy * (gx * a00 + fx * a10) + fy * (gx * a01 + fx * a11), a00, a10, a01, a11);
-  const double w_meas = bilin_fix(gy * (gx * b00 + fx * b10) + fy * (gx * b01 + fx * b11), b00, b10, b01, b11);
-  oI = inb ? ri : CUDART_NAN;
-  const bool v2 = inb && valid(w_meas) && w_meas > 0.0;
-  const double rz = red3(m.Rt_AB[6] * px, m.Rt_AB[7] * py, m.Rt_AB[8] * 1.0);
-  const double za = rz / (v2 ? w_meas : 1.0) + m.tt_AB[2];
-  const bool v3 = v2 && za > 1e-12;
-  oW = v3 ? __drcp_rn(za) : CUDART_NAN;  // == 1.0 / za
-}
-
-// warp_px_iw on separate I_B, W_B maps (k_warp_maps: the C-ABI inverse_geometric_warp,
-// whose frame B may differ in size from A).
-__device__ __forceinline__ void warp_px(const WarpMats& m, const double* __restrict__ IB,
-                                        const double* __restrict__ WB, int wb, int hb, int x,
-                                        int y, double w_a, double& oI, double& oW, double& mx,
-                                        double& my) {
-  const bool v0 = valid(w_a) && w_a > 0.0;
-  const double wa = v0 ? w_a : 1.0;
-  const double qz = __drcp_rn(wa);  // == 1.0 / w_a
-  const double qx = div_rcp((double)x, wa, qz), qy = div_rcp((double)y, wa, qz);
-  const double xb0 = red3(m.Rt_BA[0] * qx, m.Rt_BA[1] * qy, m.Rt_BA[2] * qz) + m.tt_BA[0];
-  const double xb1 = red3(m.Rt_BA[3] * qx, m.Rt_BA[4] * qy, m.Rt_BA[5] * qz) + m.tt_BA[1];
-  const double xb2 = red3(m.Rt_BA[6] * qx, m.Rt_BA[7] * qy, m.Rt_BA[8] * qz) + m.tt_BA[2];
-  const bool v1 = v0 && xb2 > 1e-12;
-  const double z = v1 ? xb2 : 1.0;
-  const double rz2 = __drcp_rn(z);
-  const double px = div_rcp(xb0, z, rz2), py = div_rcp(xb1, z, rz2);
-  mx = v1 ? px : CUDART_NAN;
-  my = v1 ? py : CUDART_NAN;
-  const bool inb = v1 && (px >= 0.0 && px <= wb - 1.0 && py >= 0.0 && py <= hb - 1.0);
-  const double sx = inb ? px : 0.0, sy = inb ? py : 0.0;
-  const int x0 = (int)floor(sx), y0 = (int)floor(sy);
-  const int dx = x0 + 1 < wb ? 1 : 0;  // x1 = min(x0 + 1, w - 1)
-  const int dy = y0 + 1 < hb ? wb : 0; // y1 = min(y0 + 1, h - 1)
-  const double fx = sx - x0, fy = sy - y0, gx = 1 - fx, gy = 1 - fy;
-  const int i00 = y0 * wb + x0;
-  const double a00 = __ldg(IB + i00), a10 = __ldg(IB + i00 + dx), a01 = __ldg(IB + i00 + dy),
-               a11 = __ldg(IB + i00 + dy + dx);
-  const double b00 = __ldg(WB + i00), b10 = __ldg(WB + i00 + dx), b01 = __ldg(WB + i00 + dy),
-               b11 = __ldg(WB + i00 + dy + dx);
   const double ri = bilin_fix(gy * (gx * a00 + fx * a10) + fy * (gx * a01 + fx * a11), a00, a10, a01, a11);
   const double w_meas = bilin_fix(gy * (gx * b00 + fx * b10) + fy * (gx * b01 + fx * b11), b00, b10, b01, b11);
   oI = inb ? ri : CUDART_NAN;
@@ -1522,30 +1521,16 @@ __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double
 // C += sum_k w_k x_k x_k^T with 8 MMAs per row type, so the 8x8 system (H, the
 // J^T W r column, the cost) lives in two fp64 registers per lane instead of 28 --
 // the register file no longer caps occupancy.  Invalid rows are zeroed (w and x).
-// Sets the level's WHILE-loop condition (single-pair conditional graph) if any.
-__device__ __forceinline__ void set_cond(unsigned long long cond, unsigned v) {
-  if (cond) cudaGraphSetConditional((cudaGraphConditionalHandle)cond, v);
-}
-__device__ __noinline__ void solve_slot(const SlotIO& o, SlotState& S, int slot, const LevelInfo& li,
-                                        const AlignLaunch& a, int max_iters,
-                                        unsigned long long cond);
-__device__ __noinline__ void covariance_slot(const SlotIO& o, SlotState& S, int ntiles3);
-
 #ifndef RGBID_K3_MMA_MINB
 #define RGBID_K3_MMA_MINB 3
 #endif
 __global__ void __launch_bounds__(kTPB, RGBID_K3_MMA_MINB) k_normal_eq_mma(const SlotIO* __restrict__ io,
-                                                        SlotState* __restrict__ st,
+                                                        const SlotState* __restrict__ st,
                                                         LevelInfo li, int phase,
-                                                        AlignLaunch al, int max_iters,
-                                                        unsigned long long cond) {
-  const double lambda_n_min = al.lambda_n_min;
+                                                        double lambda_n_min) {
   const int slot = blockIdx.y;
-  SlotState& S = st[slot];
-  if (!slot_active(S, li.level, phase)) {  // uniform over the CTA
-    if (blockIdx.x == 0 && threadIdx.x == 0) set_cond(cond, 0);
-    return;
-  }
+  const SlotState& S = st[slot];
+  if (!slot_active(S, li.level, phase)) return;  // uniform over the CTA
   const SlotIO& o = io[slot];
   const double* __restrict__ WA = phase ? o.fWA : o.WA[li.level];
   const uint8_t* __restrict__ am = o.amask[li.level];
@@ -1662,28 +1647,13 @@ __global__ void __launch_bounds__(kTPB, RGBID_K3_MMA_MINB) k_normal_eq_mma(const
 #pragma unroll
     for (int wv = 0; wv < kTPB / 32; ++wv) t += cst[wv][r * 8 + c];
     o.part[(size_t)blockIdx.x * kNPart + q] = t;
-    __threadfence();
   }
-  // the slot's last CTA to finish reduces every tile's partials in a fixed order and
-  // runs K4 (solve + update) or K5 (covariance): no separate per-iteration launch
-  __shared__ bool last;
-  __syncthreads();
-  if (threadIdx.x == 0) last = atomicAdd(o.ticket, 1u) == gridDim.x - 1;
-  __syncthreads();
-  if (!last) return;
-  __threadfence();
-  if (threadIdx.x == 0) *o.ticket = 0u;  // ready for the next launch
-  if (phase)
-    covariance_slot(o, S, li.ntiles3);
-  else
-    solve_slot(o, S, slot, li, al, max_iters, cond);
 }
 
-void launch_normal_equations(const AlignLaunch& a, const LevelInfo& li, int phase, cudaStream_t s,
-                             int max_iters, unsigned long long cond) {
+void launch_normal_equations(const AlignLaunch& a, const LevelInfo& li, int phase, cudaStream_t s) {
   KScope ks_(phase ? "normal_eq_cov" : kNeNames[li.level], s);
-  k_normal_eq_mma<<<dim3(li.ntiles3, a.nslots), kTPB, 0, s>>>(a.io, a.st, li, phase, a, max_iters,
-                                                              cond);
+  k_normal_eq_mma<<<dim3(li.ntiles3, a.nslots), kTPB, 0, s>>>(a.io, a.st, li, phase,
+                                                              a.lambda_n_min);
 }
 
 // fixed-order reduction of the per-tile partials into H (full, mirrored), b, cost
@@ -1694,7 +1664,7 @@ __device__ void reduce_partials(const double* part, int ntiles, double* H, doubl
   for (int i = 0; i < kNPart; ++i) acc[i] = 0.0;
   for (int t = threadIdx.x; t < ntiles; t += kTPB)
 #pragma unroll
-    for (int i = 0; i < kNPart; ++i) acc[i] += __ldcg(part + (size_t)t * kNPart + i);
+    for (int i = 0; i < kNPart; ++i) acc[i] += part[(size_t)t * kNPart + i];
   __shared__ double tot[kNPart];
   block_sum_to<kTPB>(acc, tot, sh);
   __syncthreads();
@@ -1711,36 +1681,37 @@ __device__ void reduce_partials(const double* part, int ntiles, double* H, doubl
   }
 }
 
-// K4: solve + pose update + convergence — src/alignment.cpp:387-401.  Run by the
-// last CTA of the slot's K3 launch (all its threads) after the fixed-order reduction
-// of the tile partials; out of line so K3's register budget is unaffected.
-__device__ __noinline__ void solve_slot(const SlotIO& o, SlotState& S, int slot, const LevelInfo& li,
-                                        const AlignLaunch& a, int max_iters,
-                                        unsigned long long cond) {
-  const int L = li.level;
+// K4: solve + pose update + convergence — src/alignment.cpp:387-401
+__global__ void __launch_bounds__(kTPB) k_solve(const SlotIO* __restrict__ io,
+                                                SlotState* __restrict__ st,
+                                                rgbid_iter_trace* __restrict__ trace, LevelInfo li,
+                                                int w0, int h0, double fx0, double fy0, double cx0,
+                                                double cy0, double eps) {
+  const int slot = blockIdx.x;
+  SlotState& S = st[slot];
+  if (!slot_active(S, li.level, 0)) return;
   if (S.nI < 6) {  // jets.size() < 6 -> DegenerateAlignmentError(zero spectrum)
     if (threadIdx.x == 0) {
       S.status = RGBID_E_DEGENERATE;
       for (int i = 0; i < 36; ++i) S.H[i] = 0.0;
-      set_cond(cond, 0);
     }
     return;
   }
   __shared__ double sh[(kTPB / 32) * kNPart];
   __shared__ double H[36], b[6], cost;
-  reduce_partials(o.part, li.ntiles3, H, b, &cost, sh);
+  reduce_partials(io[slot].part, li.ntiles3, H, b, &cost, sh);
   if (threadIdx.x != 0) return;
   for (int i = 0; i < 36; ++i) S.H[i] = H[i];
   if (rank_deficient6(H)) {
     S.status = RGBID_E_DEGENERATE;
-    set_cond(cond, 0);
     return;
   }
   double xi[6];
   ldlt_solve6(H, b, xi);
   const PoseD T = pose_update(xi, pose_from(S.R, S.t));
   pose_to(T, S.R, S.t);
-  S.wm = warp_mats(T, a.fx0, a.fy0, a.cx0, a.cy0);
+  S.wm = warp_mats(T, fx0, fy0, cx0, cy0);
+  const int L = li.level;
   S.iters[L] += 1;
   S.cost[L] = cost;
   S.total_iters += 1;
@@ -1750,8 +1721,8 @@ __device__ __noinline__ void solve_slot(const SlotIO& o, SlotState& S, int slot,
     S.finI = tI;
     S.finW = S.tW;
   }
-  if (a.trace && slot == 0 && S.trace_n < kTraceMax) {
-    rgbid_iter_trace& e = a.trace[S.trace_n++];
+  if (trace && slot == 0 && S.trace_n < kTraceMax) {
+    rgbid_iter_trace& e = trace[S.trace_n++];
     e.level = L;
     e.iter = S.iters[L] - 1;
     e.n_jets = S.nI;
@@ -1768,12 +1739,17 @@ __device__ __noinline__ void solve_slot(const SlotIO& o, SlotState& S, int slot,
   }
   const double xn = sqrt(red3(xi[0] * xi[0], xi[1] * xi[1], xi[2] * xi[2]) +
                          red3(xi[3] * xi[3], xi[4] * xi[4], xi[5] * xi[5]));
-  if (xn < a.eps) S.done_level = L;
-  set_cond(cond, S.done_level != L && S.iters[L] < max_iters ? 1u : 0u);
+  if (xn < eps) S.done_level = L;
+  (void)w0;
+  (void)h0;
 }
 
-// K5: filtered-Hessian covariance — src/alignment.cpp:422-435 (K3's last CTA, phase 1)
-__device__ __noinline__ void covariance_slot(const SlotIO& o, SlotState& S, int ntiles3) {
+// K5: filtered-Hessian covariance — src/alignment.cpp:422-435
+__global__ void __launch_bounds__(kTPB) k_covariance(const SlotIO* __restrict__ io,
+                                                     SlotState* __restrict__ st, int ntiles3) {
+  const int slot = blockIdx.x;
+  SlotState& S = st[slot];
+  if (S.status != RGBID_OK) return;
   if (S.nI < 6) {
     if (threadIdx.x < 36) S.cov[threadIdx.x] = (threadIdx.x % 7 == 0) ? 1e6 : 0.0;
     if (threadIdx.x == 0) S.cov_degenerate = 1;
@@ -1781,7 +1757,7 @@ __device__ __noinline__ void covariance_slot(const SlotIO& o, SlotState& S, int 
   }
   __shared__ double sh[(kTPB / 32) * kNPart];
   __shared__ double H[36], b[6], cost;
-  reduce_partials(o.part, ntiles3, H, b, &cost, sh);
+  reduce_partials(io[slot].part, ntiles3, H, b, &cost, sh);
   if (threadIdx.x != 0) return;
   double Hs[36], inv[36];
   for (int r = 0; r < 6; ++r)
@@ -1797,6 +1773,16 @@ __device__ __noinline__ void covariance_slot(const SlotIO& o, SlotState& S, int 
   S.cov_degenerate = 0;
 }
 
+void launch_covariance(const AlignLaunch& a, const LevelInfo& li, cudaStream_t s) {
+  KScope ks_("covariance", s);
+  k_covariance<<<a.nslots, kTPB, 0, s>>>(a.io, a.st, li.ntiles3);
+}
+
+void launch_solve(const AlignLaunch& a, const LevelInfo& li, const LevelInfo& li0, cudaStream_t s) {
+  KScope ks_("solve", s);
+  k_solve<<<a.nslots, kTPB, 0, s>>>(a.io, a.st, a.trace, li, a.w0, a.h0, li0.fx, li0.fy, li0.cx,
+                                    li0.cy, a.eps);
+}
 
 // ---------------------------------------------------------------------------
 // pyramid level: downsample2 of I and W — inc/image.hpp:73-91

@@ -77,7 +77,6 @@ struct SlotIO {
   double* part;                  // K3 partial sums [ntiles3][kNPart]
   double* smp;                   // K2 systematic samples [2][kMaxSample] (r_I, r_W; k_gather)
   int* nsmp;                     // K2 valid residual counts [2] (k_gather)
-  unsigned* ticket;              // K3 CTAs finished (the last one runs K4 / K5); 0 between launches
   int build_pyr;                 // 1: this slot builds frame A's pyramid levels >= 1
 };
 
@@ -111,16 +110,14 @@ struct AlignLaunch {
   int w0, h0;
   double eps;
   double lambda_n_min;
-  double fx0, fy0, cx0, cy0;  // level-0 intrinsics (K4's warp matrices)
 };
 
 // Kernel launchers (align_kernels.cu); all asynchronous on `stream`.
 void launch_warp_residuals(const AlignLaunch& a, const LevelInfo& li, int phase, cudaStream_t s);
 void launch_tdist(const AlignLaunch& a, const LevelInfo& li, int phase, cudaStream_t s);
-// K3 + (in its last CTA per slot) K4 solve/update (phase 0) or K5 covariance (phase 1);
-// cond: the level's WHILE-loop handle of a conditional graph (0 = none)
-void launch_normal_equations(const AlignLaunch& a, const LevelInfo& li, int phase, cudaStream_t s,
-                             int max_iters = 0, unsigned long long cond = 0);
+void launch_normal_equations(const AlignLaunch& a, const LevelInfo& li, int phase, cudaStream_t s);
+void launch_solve(const AlignLaunch& a, const LevelInfo& li, const LevelInfo& li0, cudaStream_t s);
+void launch_covariance(const AlignLaunch& a, const LevelInfo& li, cudaStream_t s);
 void launch_downsample2(const double* I, const double* W, int w, int h, double* oI, double* oW,
                         cudaStream_t s);
 void launch_pyramid_slots(const AlignLaunch& a, int levels, cudaStream_t s);

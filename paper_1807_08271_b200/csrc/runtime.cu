@@ -86,7 +86,6 @@ struct rgbid_ctx {
   rgbid_iter_trace* d_trace = nullptr;
   std::vector<rgbid_iter_trace> last_trace;
   bool use_graphs = true;
-  bool use_cond = true;  // single alignments as conditional (WHILE-per-level) graphs
   std::vector<cudaEvent_t> pair_events;  // stage events of co-scheduled chunk pairs
   // scratch device buffers for the one-shot host APIs
   std::map<std::string, std::pair<void*, size_t>> scratch;
@@ -276,7 +275,7 @@ size_t slot_f64(int w, int h) {
   return ((f + 1) & ~(size_t)1) + 2 * N;
 }
 size_t slot_u8(int w, int h) { return (pyr_pixels(w, h) + 255) & ~(size_t)255; }
-size_t slot_i32(int w, int h) { return 2 * max_tiles(w, h) * (1 + kWordsPerTile) + 4; }
+size_t slot_i32(int w, int h) { return 2 * max_tiles(w, h) * (1 + kWordsPerTile) + 2; }
 
 void free_lane_ws(Lane& L) {
   if (L.ws_f64) cudaFree(L.ws_f64);
@@ -314,7 +313,6 @@ int ensure_workspace(rgbid_ctx* ctx, Lane& L, int nslots, int w, int h) {
   free_lane_ws(L);
   CK(cudaMalloc(&L.ws_f64, sizeof(double) * slot_f64(w, h) * nslots));
   CK(cudaMalloc(&L.ws_i32, sizeof(int) * slot_i32(w, h) * nslots));
-  CK(cudaMemset(L.ws_i32, 0, sizeof(int) * slot_i32(w, h) * nslots));  // K3 tickets start at 0
   CK(cudaMalloc(&L.ws_u8, slot_u8(w, h) * nslots));
   CK(cudaMalloc(&L.d_io, sizeof(SlotIO) * nslots));
   CK(cudaMalloc(&L.d_st, sizeof(SlotState) * nslots));
@@ -414,60 +412,41 @@ int validate_cfg(const rgbid_align_config& c, int w, int h) {
 // pair the FP64-bound Student-t kernel with a memory-bound kernel.
 using Stage = std::function<void(cudaStream_t)>;
 
-// The launches of one IRLS iteration at `li` (src/alignment.cpp:378-401): K1 | K2 |
-// K3 (+ K4 in K3's last CTA per slot); cond = the level's WHILE handle, if any.
-Stage iteration_stage(const AlignLaunch& a, const LevelInfo& li, int part, int max_iters,
-                      unsigned long long cond) {
-  switch (part) {
-    case 0: return [a, li](cudaStream_t s) { launch_warp_residuals(a, li, 0, s); };
-    case 1: return [a, li](cudaStream_t s) { launch_tdist(a, li, 0, s); };
-    default:
-      return [a, li, max_iters, cond](cudaStream_t s) {
-        launch_normal_equations(a, li, 0, s, max_iters, cond);
-      };
-  }
-}
-
-Stage prologue_stage(const AlignLaunch& a, int levels) {
-  return [a, levels](cudaStream_t s) {
+std::vector<Stage> align_stages(const AlignLaunch& a, const rgbid_intrinsics& K,
+                                const rgbid_align_config& cfg) {
+  std::vector<Stage> st;
+  const LevelInfo li0 = make_level(K, a.w0, a.h0, 0);
+  const int levels = cfg.levels;
+  st.push_back([a, levels](cudaStream_t s) {
     launch_pyramid_slots(a, levels, s);  // build_pyramid (src/alignment.cpp:369)
     launch_amask(a, levels, 0, s);       // A-side validity + gradients, once per align
     launch_interleave_B(a, s);           // B as {I, W} pairs for K1's bilinear taps
-  };
-}
-
-// filtered_hessian_covariance — src/alignment.cpp:406-407, 411-436 (three stages)
-std::vector<Stage> covariance_stages(const AlignLaunch& a, const LevelInfo& li0,
-                                     const rgbid_align_config& cfg) {
+  });
+  for (int level = cfg.levels - 1; level >= 0; --level) {
+    const LevelInfo li = make_level(K, a.w0, a.h0, level);
+    const int iters = level_iters(cfg, level);
+    for (int it = 0; it < iters; ++it) {
+      st.push_back([a, li](cudaStream_t s) { launch_warp_residuals(a, li, 0, s); });
+      st.push_back([a, li](cudaStream_t s) { launch_tdist(a, li, 0, s); });
+      st.push_back([a, li, li0](cudaStream_t s) {
+        launch_normal_equations(a, li, 0, s);
+        launch_solve(a, li, li0, s);
+      });
+    }
+  }
+  // filtered_hessian_covariance — src/alignment.cpp:406-407, 411-436
   const double ss = cfg.bilateral_sigma_space, si = cfg.bilateral_sigma_intensity,
                sd = cfg.bilateral_sigma_depth;
-  std::vector<Stage> st;
   st.push_back([a, li0, ss, si, sd](cudaStream_t s) {
     launch_bilateral_pair(a, ss, si, sd, s);
     launch_amask(a, 1, 1, s);
     launch_warp_residuals(a, li0, 1, s);
   });
   st.push_back([a, li0](cudaStream_t s) { launch_tdist(a, li0, 1, s); });
-  st.push_back([a, li0](cudaStream_t s) { launch_normal_equations(a, li0, 1, s); });  // + K5
-  return st;
-}
-
-// The whole align (all levels + covariance pass) as a list of stages; a stage
-// is one or more dependent kernel launches on one stream.  Stages cycle
-// K1 | K2 | K3(+K4) per IRLS iteration so that two chunks offset by one stage
-// pair the FP64-bound Student-t kernel with a memory-bound kernel.
-std::vector<Stage> align_stages(const AlignLaunch& a, const rgbid_intrinsics& K,
-                                const rgbid_align_config& cfg) {
-  std::vector<Stage> st;
-  const LevelInfo li0 = make_level(K, a.w0, a.h0, 0);
-  st.push_back(prologue_stage(a, cfg.levels));
-  for (int level = cfg.levels - 1; level >= 0; --level) {
-    const LevelInfo li = make_level(K, a.w0, a.h0, level);
-    const int iters = level_iters(cfg, level);
-    for (int it = 0; it < iters; ++it)
-      for (int part = 0; part < 3; ++part) st.push_back(iteration_stage(a, li, part, iters, 0));
-  }
-  for (auto& f : covariance_stages(a, li0, cfg)) st.push_back(f);
+  st.push_back([a, li0](cudaStream_t s) {
+    launch_normal_equations(a, li0, 1, s);
+    launch_covariance(a, li0, s);
+  });
   return st;
 }
 
@@ -501,66 +480,6 @@ void enqueue_align_group(const std::vector<cudaStream_t>& sj, const std::vector<
       cudaEventRecord(ev[j * n + i], sj[j]);
     }
   cudaStreamWaitEvent(sj[0], ev[(G - 1) * n + n - 1], 0);  // join
-}
-
-// A single alignment as a conditional graph: per level one WHILE node whose body
-// is ONE IRLS iteration (K1 | K2 | K3 + K4), the loop condition written by K4
-// (cudaGraphSetConditional: continue while not converged, below the level's
-// iteration count and not degenerate), so converged iterations issue no launches
-// (src/alignment.cpp:376-402: `for (it < iters) { ...; if (|xi| < eps) break; }`).
-// Returns the instantiated graph; *launches = kernel launches of a full run.
-int build_conditional_graph(rgbid_ctx* ctx, cudaStream_t st, const AlignLaunch& a,
-                            const rgbid_intrinsics& K, const rgbid_align_config& cfg,
-                            cudaGraphExec_t* exec, long long* launches) {
-  cudaGraph_t g;
-  CK(cudaGraphCreate(&g, 0));
-  const long long before = ctx->launches;
-  // prologue, captured into g
-  std::vector<cudaGraphNode_t> deps;
-  auto capture_into = [&](cudaGraph_t target, const std::vector<cudaGraphNode_t>& d,
-                          const std::vector<Stage>& stages, std::vector<cudaGraphNode_t>* leaves) {
-    cudaError_t e = cudaStreamBeginCaptureToGraph(st, target, d.empty() ? nullptr : d.data(),
-                                                  nullptr, d.size(),
-                                                  cudaStreamCaptureModeThreadLocal);
-    if (e != cudaSuccess) return e;
-    for (auto& f : stages) f(st);
-    if (leaves) {
-      cudaStreamCaptureStatus cs;
-      const cudaGraphNode_t* ld = nullptr;
-      size_t nl = 0;
-      e = cudaStreamGetCaptureInfo(st, &cs, nullptr, nullptr, &ld, &nl);
-      if (e != cudaSuccess) return e;
-      leaves->assign(ld, ld + nl);
-    }
-    cudaGraph_t out;
-    return cudaStreamEndCapture(st, &out);
-  };
-  CK(capture_into(g, {}, {prologue_stage(a, cfg.levels)}, &deps));
-  for (int level = cfg.levels - 1; level >= 0; --level) {
-    const LevelInfo li = make_level(K, a.w0, a.h0, level);
-    const int iters = level_iters(cfg, level);
-    cudaGraphConditionalHandle h;
-    CK(cudaGraphConditionalHandleCreate(&h, g, iters > 0 ? 1u : 0u, cudaGraphCondAssignDefault));
-    cudaGraphNodeParams cp = {};
-    cp.type = cudaGraphNodeTypeConditional;
-    cp.conditional.handle = h;
-    cp.conditional.type = cudaGraphCondTypeWhile;
-    cp.conditional.size = 1;
-    cudaGraphNode_t node;
-    CK(cudaGraphAddNode(&node, g, deps.empty() ? nullptr : deps.data(), deps.size(), &cp));
-    std::vector<Stage> body;
-    for (int part = 0; part < 3; ++part)
-      body.push_back(iteration_stage(a, li, part, iters, (unsigned long long)h));
-    CK(capture_into(cp.conditional.phGraph_out[0], {}, body, nullptr));
-    deps.assign(1, node);
-  }
-  CK(capture_into(g, deps, covariance_stages(a, make_level(K, a.w0, a.h0, 0), cfg), nullptr));
-  *launches = ctx->launches - before;  // prologue + one iteration per level + covariance
-  ctx->launches = before;
-  const cudaError_t e = cudaGraphInstantiateWithFlags(exec, g, 0);
-  cudaGraphDestroy(g);
-  CK(e);
-  return RGBID_OK;
 }
 
 // Two chunks in one launch sequence: stage s of B after stage s of A, stage
@@ -685,7 +604,6 @@ int prepare_chunk(rgbid_ctx* ctx, Lane& L, int n, const rgbid_frame* const* fa,
     o.bitsI = reinterpret_cast<unsigned*>(ib32 + 2 * mt);
     o.bitsW = o.bitsI + mt * kWordsPerTile;
     o.nsmp = ib32 + 2 * mt * (1 + kWordsPerTile);
-    o.ticket = reinterpret_cast<unsigned*>(ib32 + 2 * mt * (1 + kWordsPerTile) + 2);
     uint8_t* u8 = L.ws_u8 + su * i;
     for (int l = 0; l < kMaxLevels; ++l) {
       o.amask[l] = u8;
@@ -729,10 +647,6 @@ int prepare_chunk(rgbid_ctx* ctx, Lane& L, int n, const rgbid_frame* const* fa,
   a.h0 = h;
   a.eps = cfg.convergence_eps;
   a.lambda_n_min = cfg.lambda_n_min;
-  a.fx0 = li0.fx;
-  a.fy0 = li0.fy;
-  a.cx0 = li0.cx;
-  a.cy0 = li0.cy;
 
   *out_a = a;
   // remember what finish_chunk / the pyramid bookkeeping need
@@ -784,24 +698,19 @@ int launch_prepared(rgbid_ctx* ctx, Lane& L, const AlignLaunch& a, Lane* LB,
   if (ctx->use_graphs && !ctx->prof.enabled) {
     auto it = L.graphs.find(key);
     if (it == L.graphs.end()) {
+      cudaGraph_t g;
+      CK(cudaStreamBeginCapture(L.stream, cudaStreamCaptureModeThreadLocal));
+      const long long before = ctx->launches;
+      if (LB)
+        enqueue_align_pair(L.stream, LB->stream, a, *b, K, cfg, ctx->pair_events);
+      else
+        enqueue_align(L.stream, a, K, cfg);
       CachedGraph cg;
-      if (!LB && a.nslots == 1 && ctx->use_cond) {  // single pair: WHILE node per level
-        const int rc = build_conditional_graph(ctx, L.stream, a, K, cfg, &cg.exec, &cg.launches);
-        if (rc) return rc;
-      } else {
-        cudaGraph_t g;
-        CK(cudaStreamBeginCapture(L.stream, cudaStreamCaptureModeThreadLocal));
-        const long long before = ctx->launches;
-        if (LB)
-          enqueue_align_pair(L.stream, LB->stream, a, *b, K, cfg, ctx->pair_events);
-        else
-          enqueue_align(L.stream, a, K, cfg);
-        cg.launches = ctx->launches - before;
-        ctx->launches = before;
-        CK(cudaStreamEndCapture(L.stream, &g));
-        CK(cudaGraphInstantiateWithFlags(&cg.exec, g, cudaGraphInstantiateFlagUseNodePriority));
-        cudaGraphDestroy(g);
-      }
+      cg.launches = ctx->launches - before;
+      ctx->launches = before;
+      CK(cudaStreamEndCapture(L.stream, &g));
+      CK(cudaGraphInstantiateWithFlags(&cg.exec, g, cudaGraphInstantiateFlagUseNodePriority));
+      cudaGraphDestroy(g);
       it = L.graphs.emplace(key, cg).first;
     }
     CK(cudaGraphLaunch(it->second.exec, L.stream));
@@ -987,8 +896,6 @@ int rgbid_ctx_create(int device, rgbid_ctx** out) {
   }
   const char* g = std::getenv("RGBID_NO_GRAPHS");
   ctx->use_graphs = !(g && g[0] == '1');
-  const char* gc = std::getenv("RGBID_NO_COND_GRAPHS");
-  ctx->use_cond = !(gc && gc[0] == '1');
   *out = ctx;
   return RGBID_OK;
 }
