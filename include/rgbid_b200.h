@@ -262,6 +262,21 @@ int rgbid_forward_register(rgbid_ctx* ctx, const double* W_A, int width, int hei
                            const rgbid_pose* T_BA, const rgbid_intrinsics* K_A,
                            const rgbid_intrinsics* K_B, double* out);
 
+/* ---- distorted sensors (config 4 with k != 0) ---------------------------- */
+/* Image<double> inverse_warp(src, f_w, w, h) (src/warping.cpp:8-18) with the
+ * rectification map f_w(p) = project(K, ((x - cx) / fx, (y - cy) / fy, 1)) =
+ * K distort(K^-1 p) (src/camera.cpp:11-22,41-45), applied to both maps
+ * of a device frame (dst != src, both K->width x K->height). */
+int rgbid_rectify_frame(rgbid_ctx* ctx, const rgbid_frame* src, const rgbid_intrinsics* K,
+                        rgbid_frame* dst);
+/* The same for one host image. */
+int rgbid_rectify(rgbid_ctx* ctx, const double* src, int width, int height,
+                  const rgbid_intrinsics* K, double* out);
+/* std::optional<Vec2> undistort(K, m_d) (src/camera.cpp:24-39) for n normalized points
+ * m_d[2i], m_d[2i+1]; ok[i] = 0 where the reference returns std::nullopt. */
+int rgbid_undistort_points(rgbid_ctx* ctx, const double* m_d, long long n,
+                           const rgbid_intrinsics* K, double* m_u, unsigned char* ok);
+
 /* ---- front-end odometry driver (config 3) -------------------------------- */
 /* Restates Pipeline::process_frame / track / fuse_and_maybe_switch
  * (src/pipeline.cpp:120-247) without the back-end; frames, reference and

@@ -90,6 +90,8 @@ def _sig(L, prefix):
         sigs["covisibility_ratio"] = (C.c_int, [DP, DP, DP, DP, C.c_int, C.c_int, P(Pose_t),
                                                 P(Intrinsics_t), C.c_double, DP, P(C.c_int)])
         sigs["so3_exp"] = (C.c_int, [DP, DP])
+        sigs["rectify"] = (C.c_int, [DP, C.c_int, C.c_int, P(Intrinsics_t), DP])
+        sigs["undistort"] = (C.c_int, [DP, C.c_longlong, P(Intrinsics_t), DP, P(C.c_ubyte)])
         sigs["render_plane"] = (C.c_int, [P(Intrinsics_t), P(Pose_t), DP, C.c_double, DP, DP])
         sigs["random_pose"] = (C.c_int, [C.c_uint, C.c_int, C.c_double, C.c_double, P(Pose_t)])
     for name, (res, args) in sigs.items():
@@ -317,6 +319,24 @@ class Oracle:
         bgr = np.ascontiguousarray(bgr, dtype=np.uint8)
         self._f("decode_frame")(bgr.ctypes.data, depth.ctypes.data, w, h, scale, dptr(I), dptr(W))
         return I, W
+
+    # reference-only: the distorted-sensor path (src/camera.cpp:11-45, src/warping.cpp:8-18)
+    def rectify(self, img, K):
+        assert self.kind == "REF", "rectify composes the reference's own project/inverse_warp"
+        h, w = img.shape
+        out = np.empty_like(img)
+        self._f("rectify")(dptr(np.ascontiguousarray(img)), w, h, C.byref(K), dptr(out))
+        return out
+
+    def undistort(self, m_d, K):
+        assert self.kind == "REF"
+        m_d = np.ascontiguousarray(m_d, dtype=np.float64).reshape(-1, 2)
+        n = len(m_d)
+        m_u = np.empty_like(m_d)
+        ok = np.zeros(n, dtype=np.uint8)
+        self._f("undistort")(dptr(m_d), n, C.byref(K), dptr(m_u),
+                             ok.ctypes.data_as(C.POINTER(C.c_ubyte)))
+        return m_u, ok.astype(bool)
 
     # reference-only fixtures (tests/synthetic.hpp)
     def render_plane(self, K, T_WC, n=(0.0, 0.0, 1.0), d=-2.0):

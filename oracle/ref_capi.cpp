@@ -298,6 +298,33 @@ int ref_forward_register(const double* WA, int w, int h, const rgbid_pose* T_BA,
 }
 
 // geometry: src/geometry.cpp:15-28, :56, inc/geometry.hpp:30-31
+// inverse_warp (src/warping.cpp:8-18) with the rectification map of a distorted
+// sensor: f_w(p) = project(K, ((x - cx) / fx, (y - cy) / fy, 1)) = K distort(K^-1 p)
+// (src/camera.cpp:11-22,41-45) — the reference's own functions composed
+int ref_rectify(const double* src, int w, int h, const rgbid_intrinsics* K, double* out) {
+  const Intrinsics intr = to_K(K);
+  const Image<double> im = to_img(src, w, h);
+  const auto f_w = [&](const Vec2& p) {
+    const auto q = project(intr, Vec3((p.x() - intr.cx) / intr.fx, (p.y() - intr.cy) / intr.fy, 1.0));
+    return q ? *q : Vec2(-1.0, -1.0);
+  };
+  from_img(inverse_warp(im, f_w, w, h), out);
+  return 0;
+}
+
+// undistort (src/camera.cpp:24-39) of n normalized points; ok[i] = 0 for std::nullopt
+int ref_undistort(const double* m_d, long long n, const rgbid_intrinsics* K, double* m_u,
+                  unsigned char* ok) {
+  const Intrinsics intr = to_K(K);
+  for (long long i = 0; i < n; ++i) {
+    const auto u = undistort(intr, Vec2(m_d[2 * i], m_d[2 * i + 1]));
+    ok[i] = u ? 1 : 0;
+    m_u[2 * i] = u ? u->x() : 0.0;
+    m_u[2 * i + 1] = u ? u->y() : 0.0;
+  }
+  return 0;
+}
+
 int ref_so3_exp(const double theta[3], double R[9]) {
   const Mat3 m = so3_exp(Vec3(theta[0], theta[1], theta[2]));
   for (int r = 0; r < 3; ++r)

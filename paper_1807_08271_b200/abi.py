@@ -130,6 +130,10 @@ EXPORTS = [
     ("rgbid_last_align_trace", C.c_int, [VP, C.POINTER(IterTrace_t), C.c_int,
                                          C.POINTER(C.c_int)]),
     ("rgbid_batch_plan", C.c_int, [C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    ("rgbid_rectify_frame", C.c_int, [VP, VP, C.POINTER(Intrinsics_t), VP]),
+    ("rgbid_rectify", C.c_int, [VP, DP, C.c_int, C.c_int, C.POINTER(Intrinsics_t), DP]),
+    ("rgbid_undistort_points", C.c_int, [VP, DP, C.c_longlong, C.POINTER(Intrinsics_t), DP,
+                                         C.POINTER(C.c_ubyte)]),
     ("rgbid_align_batch", C.c_int, [VP, C.c_int, C.POINTER(VP), C.POINTER(VP),
                                     C.POINTER(Intrinsics_t), C.POINTER(Pose_t),
                                     C.POINTER(AlignConfig_t), C.POINTER(AlignResult_t)]),

@@ -7,10 +7,14 @@
 // B200 layout: every frame, the tracking reference, the keyframe source and
 // the fused keyframe maps (W, C) stay resident in HBM; the reference frame's
 // pyramid is built once and reused for every frame tracked against it (the
-// reference rebuilds it per align call, src/alignment.cpp:369).  Per frame the
-// host only does the 6x6 covariance composition and the switch decisions; the
-// compute is 1 align + 2 covisibility + 1 fusion launch sequence on the ctx
-// stream.
+// reference rebuilds it per align call, src/alignment.cpp:369).  Device frames
+// come from a pool recycled when the last reference (tracking reference,
+// keyframe source, fusion buffer) drops, so steady state allocates nothing.  Per
+// frame the host only does the 6x6 covariance composition and the switch
+// decisions; the device work is one stream-ordered sequence -- upload, align,
+// both covisibility ratios, one fusion step -- with two host waits: the align
+// result (the covisibility transforms and sigma_w depend on it) and the four
+// covisibility counts, read back together.
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -21,6 +25,7 @@
 
 #include "../../include/rgbid_b200.h"
 #include "hd_math.cuh"
+#include "runtime_internal.cuh"
 
 using namespace rgbid_b200;
 
@@ -90,9 +95,9 @@ rgbid_pose to_c(const PoseD& p) {
 }
 
 struct FrameRef {  // immutable device frame shared by reference / keyframe source / buffer
-  rgbid_ctx* ctx;
+  std::vector<rgbid_frame*>* pool;
   rgbid_frame* f;
-  ~FrameRef() { rgbid_frame_destroy(ctx, f); }
+  ~FrameRef() { pool->push_back(f); }  // recycled, not freed
 };
 using FramePtr = std::shared_ptr<FrameRef>;
 
@@ -129,6 +134,9 @@ struct rgbid_frontend {
   std::vector<rgbid_frame_estimate> traj;
   std::vector<int> keyframe_frame_index;
   int emitted = 0;
+  std::vector<rgbid_frame*> pool;            // free device frames
+  unsigned long long* counts_dev = nullptr;  // [8]: reference and keyframe covisibility counts
+  unsigned long long* counts_host = nullptr; // pinned
 };
 
 namespace {
@@ -165,7 +173,7 @@ int drain_buffer_step(rgbid_frontend* fe) {
   fe->buffer.erase(fe->buffer.begin() + (long)best);
   const rgbid_pose T = to_c(pose_compose(pose_inverse(fe->T_W_kf), b.T_W_frame));
   const rgbid_frame* fr = b.frame->f;
-  return rgbid_integrate_frames(fe->ctx, fe->kf, fe->kf_C, 1, &fr, &T, &fe->K, fe->sigma_w);
+  return rt_integrate_async(fe->ctx, fe->kf, fe->kf_C, 1, &fr, &T, &fe->K, fe->sigma_w);
 }
 
 int emit_keyframe(rgbid_frontend* fe) {
@@ -178,8 +186,10 @@ int emit_keyframe(rgbid_frontend* fe) {
   return RGBID_OK;
 }
 
-// track — src/pipeline.cpp:140-191
-int track(rgbid_frontend* fe, const FramePtr& frame, double t) {
+// track — src/pipeline.cpp:140-191.  The reference-covisibility counts are
+// enqueued into counts_dev[0..3]; the switch is applied by finish_frame.
+int track(rgbid_frontend* fe, const FramePtr& frame, double t, bool* check_ref,
+          PoseD* T_W_k_out) {
   const PoseD init = pose_compose(fe->T_ref_prev, fe->velocity);
   const rgbid_pose init_c = to_c(init);
   rgbid_align_result res;
@@ -213,13 +223,45 @@ int track(rgbid_frontend* fe, const FramePtr& frame, double t) {
   e.keyframe_id = -1;
   fe->traj.push_back(e);
   fe->T_ref_prev = T_ref_k;
+  *T_W_k_out = T_W_k;
+  *check_ref = !lost;
   if (!lost) {  // reference switching keeps the photometric baseline short
     const rgbid_pose T_k_ref = to_c(pose_inverse(T_ref_k));
+    return rt_covis_enqueue(fe->ctx, fe->reference->f, frame->f, &T_k_ref, &fe->K, fe->sigma_w,
+                            fe->counts_dev);
+  }
+  return RGBID_OK;
+}
+
+// fuse_and_maybe_switch — src/pipeline.cpp:193-225, first half: buffer, one drain
+// step, keyframe-covisibility counts into counts_dev[4..7]
+int fuse_enqueue(rgbid_frontend* fe, const FramePtr& frame, double t) {
+  const rgbid_frame_estimate last = fe->traj.back();
+  const PoseD T_W_last = pose_from(last.T_W_k.R, last.T_W_k.t);
+  if (fe->buffer.size() >= (size_t)fe->cfg.buffer_capacity) fe->buffer.pop_front();
+  fe->buffer.push_back(Buffered{frame, T_W_last, t});
+  const int rc = drain_buffer_step(fe);
+  if (rc) return rc;
+  const PoseD T_frame_kf = pose_compose(pose_inverse(T_W_last), fe->T_W_kf);
+  const rgbid_pose T_kf_frame = to_c(pose_inverse(T_frame_kf));
+  return rt_covis_enqueue(fe->ctx, fe->kf_source->f, frame->f, &T_kf_frame, &fe->K, fe->sigma_w,
+                          fe->counts_dev + 4);
+}
+
+// the host wait of the frame: both covisibility ratios, then the reference switch
+// (track, src/pipeline.cpp:182-190) and the keyframe switch (fuse_and_maybe_switch,
+// :206-225) in the reference's order -- the first never feeds the second
+int finish_frame(rgbid_frontend* fe, const FramePtr& frame, double t, bool check_ref,
+                 const PoseD& T_W_k) {
+  cudaStream_t st = (cudaStream_t)rgbid_ctx_stream(fe->ctx);
+  if (cudaMemcpyAsync(fe->counts_host, fe->counts_dev, 8 * sizeof(unsigned long long),
+                      cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess)
+    return RGBID_E_CUDA;
+  if (check_ref) {
     double ratio = 0.0;
     int empty = 0;
-    const int rc2 = rgbid_covisibility_ratio(fe->ctx, fe->reference->f, frame->f, &T_k_ref, &fe->K,
-                                             fe->sigma_w, &ratio, &empty, nullptr);
-    if (rc2) return rc2;
+    rt_covis_ratio(fe->counts_host, &ratio, &empty);
     if (ratio < fe->cfg.reference_covisibility) {
       fe->reference = frame;
       fe->T_W_ref = T_W_k;
@@ -227,26 +269,13 @@ int track(rgbid_frontend* fe, const FramePtr& frame, double t) {
       fe->cov_ref_prev = zero6();
     }
   }
-  return RGBID_OK;
-}
-
-// fuse_and_maybe_switch — src/pipeline.cpp:193-225
-int fuse_and_maybe_switch(rgbid_frontend* fe, const FramePtr& frame, double t) {
   const rgbid_frame_estimate last = fe->traj.back();
   const PoseD T_W_last = pose_from(last.T_W_k.R, last.T_W_k.t);
-  if (fe->buffer.size() >= (size_t)fe->cfg.buffer_capacity) fe->buffer.pop_front();
-  fe->buffer.push_back(Buffered{frame, T_W_last, t});
-  int rc = drain_buffer_step(fe);
-  if (rc) return rc;
-  const PoseD T_frame_kf = pose_compose(pose_inverse(T_W_last), fe->T_W_kf);
-  const rgbid_pose T_kf_frame = to_c(pose_inverse(T_frame_kf));
   double ratio = 0.0;
   int empty = 0;
-  rc = rgbid_covisibility_ratio(fe->ctx, fe->kf_source->f, frame->f, &T_kf_frame, &fe->K,
-                                fe->sigma_w, &ratio, &empty, nullptr);
-  if (rc) return rc;
+  rt_covis_ratio(fe->counts_host + 4, &ratio, &empty);
   if (!last.lost && ratio < fe->cfg.keyframe_covisibility) {
-    rc = emit_keyframe(fe);
+    int rc = emit_keyframe(fe);
     if (rc) return rc;
     rc = start_keyframe(fe, frame, t);
     if (rc) return rc;
@@ -300,8 +329,12 @@ int rgbid_frontend_create(rgbid_ctx* ctx, const rgbid_intrinsics* K,
     delete fe;
     return rc;
   }
-  if (cudaMalloc(&fe->kf_C, sizeof(double) * fe->w * fe->h) != cudaSuccess) {
+  if (cudaMalloc(&fe->kf_C, sizeof(double) * fe->w * fe->h) != cudaSuccess ||
+      cudaMalloc(&fe->counts_dev, 8 * sizeof(unsigned long long)) != cudaSuccess ||
+      cudaMallocHost(&fe->counts_host, 8 * sizeof(unsigned long long)) != cudaSuccess) {
     rgbid_frame_destroy(ctx, fe->kf);
+    cudaFree(fe->kf_C);
+    cudaFree(fe->counts_dev);
     delete fe;
     return RGBID_E_OOM;
   }
@@ -315,8 +348,11 @@ int rgbid_frontend_destroy(rgbid_frontend* fe) {
   fe->reference.reset();
   fe->kf_source.reset();
   fe->buffer.clear();
+  for (auto* f : fe->pool) rgbid_frame_destroy(fe->ctx, f);
   rgbid_frame_destroy(fe->ctx, fe->kf);
   cudaFree(fe->kf_C);
+  cudaFree(fe->counts_dev);
+  cudaFreeHost(fe->counts_host);
   delete fe;
   return RGBID_OK;
 }
@@ -326,14 +362,17 @@ int rgbid_frontend_process(rgbid_frontend* fe, const double* I, const double* W,
                            rgbid_frame_estimate* est) {
   if (!fe || !W) return RGBID_E_ARG;
   rgbid_frame* f = nullptr;
-  int rc = rgbid_frame_create(fe->ctx, fe->w, fe->h, &f);
-  if (rc) return rc;
-  rc = rgbid_frame_upload(fe->ctx, f, I, W);
-  if (rc) {
-    rgbid_frame_destroy(fe->ctx, f);
-    return rc;
+  int rc = RGBID_OK;
+  if (!fe->pool.empty()) {  // a recycled device frame: no allocation in steady state
+    f = fe->pool.back();
+    fe->pool.pop_back();
+  } else {
+    rc = rgbid_frame_create(fe->ctx, fe->w, fe->h, &f);
+    if (rc) return rc;
   }
-  FramePtr frame(new FrameRef{fe->ctx, f});
+  FramePtr frame(new FrameRef{&fe->pool, f});
+  rc = rt_frame_upload_async(fe->ctx, f, I, W);  // stream-ordered before the align
+  if (rc) return rc;
   if (!fe->has_prev) {  // bootstrap: the first frame anchors the world frame
     fe->reference = frame;
     fe->T_W_ref = identity();
@@ -349,8 +388,11 @@ int rgbid_frontend_process(rgbid_frontend* fe, const double* I, const double* W,
     fe->keyframe_frame_index.push_back(0);
     rc = start_keyframe(fe, frame, t);
   } else {
-    rc = track(fe, frame, t);
-    if (!rc) rc = fuse_and_maybe_switch(fe, frame, t);
+    bool check_ref = false;
+    PoseD T_W_k;
+    rc = track(fe, frame, t, &check_ref, &T_W_k);
+    if (!rc) rc = fuse_enqueue(fe, frame, t);
+    if (!rc) rc = finish_frame(fe, frame, t, check_ref, T_W_k);
   }
   if (rc) return rc;
   if (est) *est = fe->traj.back();

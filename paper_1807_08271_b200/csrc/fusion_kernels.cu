@@ -7,6 +7,9 @@
 //  k_covisibility   count_visible — src/fusion.cpp:26-50 (both directions, exact
 //                   integer counts via 64-bit atomics).
 //  k_correct_depth  correct_inverse_depth + depth_poly — src/camera.cpp:54-81
+//  k_rectify        inverse_warp with f_w = K distort(K^-1 p) — src/warping.cpp:8-18,
+//                   src/camera.cpp:11-22,41-45 (distorted-sensor frames, config 4, k != 0)
+//  k_undistort      undistort — src/camera.cpp:24-39 (per point, fixed-point iteration)
 //  k_splat/k_gather forward_register — src/warping.cpp:20-74 (z-buffer splat via
 //                   64-bit atomicMax on order-preserving keys: the max is
 //                   independent of write order, as SPEC:316-317 requires)
@@ -227,6 +230,82 @@ void launch_covisibility(const CovisDir& d0, const CovisDir& d1, int w, int h, d
   KScope ks_("covisibility", s);
   k_covisibility<<<dim3((w * h + 255) / 256, 2), 256, 0, s>>>(d0, d1, w, h, 3.0 * sigma_w,
                                                               counts_dev);
+}
+
+// ---------------------------------------------------------------------------
+// Brown distortion of a normalized point — src/camera.cpp:11-22, expression order
+// as written (z is not needed by any caller)
+__device__ __forceinline__ void distort_d(const rgbid_intrinsics& K, double x, double y, double& ox,
+                                          double& oy) {
+  const double r2 = x * x + y * y;
+  const double r4 = r2 * r2;
+  const double r6 = r4 * r2;
+  const double radial = K.k[0] * r2 + K.k[1] * r4 + K.k[4] * r6;
+  ox = (1.0 + radial) * x;
+  oy = (1.0 + radial) * y;
+  ox += 2.0 * K.k[2] * x * y + K.k[3] * (r2 + 2.0 * x * x);
+  oy += 2.0 * K.k[3] * x * y + K.k[2] * (r2 + 2.0 * y * y);
+}
+
+// rectification of a distorted-sensor image pair (I and W of one frame, blockIdx.y):
+// out(p) = bilinear(src, f_w(p)), f_w(p) = project(K, ((x - cx) / fx, (y - cy) / fy, 1))
+__global__ void k_rectify(const double* __restrict__ I, const double* __restrict__ W, int w, int h,
+                          rgbid_intrinsics K, double* __restrict__ oI, double* __restrict__ oW) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= w * h) return;
+  const int y = i / w, x = i - y * w;
+  const double mx = (x - K.cx) / K.fx, my = (y - K.cy) / K.fy;
+  double dx, dy;
+  distort_d(K, mx, my, dx, dy);
+  const double qx = K.fx * dx + K.cx, qy = K.fy * dy + K.cy;
+  const double* src = blockIdx.y ? W : I;
+  double* out = blockIdx.y ? oW : oI;
+  out[i] = bilinear_f(src, w, h, qx, qy);
+}
+
+void launch_rectify(const double* I, const double* W, int w, int h, const rgbid_intrinsics& K,
+                    double* oI, double* oW, cudaStream_t s) {
+  KScope ks_("rectify", s);
+  k_rectify<<<dim3((w * h + 255) / 256, 2), 256, 0, s>>>(I, W, w, h, K, oI, oW);
+}
+
+// undistort — src/camera.cpp:24-39: fixed-point iteration m_u -= distort(m_u) - m_d,
+// at most 50 steps, |err|_inf < 1e-10; ok = 0 is the reference's std::nullopt
+__global__ void k_undistort(const double* __restrict__ md, long long n, rgbid_intrinsics K,
+                            double* __restrict__ mu, uint8_t* __restrict__ ok) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double tx = md[2 * i], ty = md[2 * i + 1];
+  bool dist = false;
+  for (int k = 0; k < 5; ++k) dist |= K.k[k] != 0.0;  // Intrinsics::has_distortion
+  double ux = tx, uy = ty;
+  uint8_t good = 0;
+  if (!dist) {
+    good = 1;
+  } else {
+    for (int it = 0; it < 50 && !good; ++it) {
+      double dx, dy;
+      distort_d(K, ux, uy, dx, dy);
+      const double ex = dx - tx, ey = dy - ty;
+      ux -= ex;
+      uy -= ey;
+      if (dmax_std(fabs(ex), fabs(ey)) < 1e-10) good = 1;
+    }
+    if (!good) {
+      double dx, dy;
+      distort_d(K, ux, uy, dx, dy);
+      if (dmax_std(fabs(dx - tx), fabs(dy - ty)) < 1e-10) good = 1;
+    }
+  }
+  ok[i] = good;
+  mu[2 * i] = good ? ux : 0.0;
+  mu[2 * i + 1] = good ? uy : 0.0;
+}
+
+void launch_undistort(const double* md, long long n, const rgbid_intrinsics& K, double* mu,
+                      uint8_t* ok, cudaStream_t s) {
+  KScope ks_("undistort", s);
+  k_undistort<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(md, n, K, mu, ok);
 }
 
 // ---------------------------------------------------------------------------

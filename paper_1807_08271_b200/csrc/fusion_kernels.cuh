@@ -36,6 +36,10 @@ void launch_forward_register(const double* WA, int w, int h, const RegisterMats&
                              unsigned long long* inter, int iw, int ih, int wb, int hb,
                              double* out, cudaStream_t s);
 void launch_render(const SynthView& v, double* I, double* W, cudaStream_t s);
+void launch_rectify(const double* I, const double* W, int w, int h, const rgbid_intrinsics& K,
+                    double* oI, double* oW, cudaStream_t s);
+void launch_undistort(const double* md, long long n, const rgbid_intrinsics& K, double* mu,
+                      uint8_t* ok, cudaStream_t s);
 void launch_decode_frame(const uint8_t* bgr, const uint16_t* depth, int n, double scale, double* I,
                          double* W, cudaStream_t s);
 

@@ -23,6 +23,7 @@
 #include "align_kernels.cuh"
 #include "fusion_kernels.cuh"
 #include "map_kernels.cuh"
+#include "runtime_internal.cuh"
 
 using namespace rgbid_b200;
 
@@ -1322,22 +1323,9 @@ int rgbid_integrate_frame(rgbid_ctx* ctx, double* kf_W, double* kf_C, const doub
 int rgbid_integrate_frames(rgbid_ctx* ctx, rgbid_frame* kf, double* kf_C_dev, int k,
                            const rgbid_frame* const* frames, const rgbid_pose* T,
                            const rgbid_intrinsics* K, double sigma_w) {
-  if (!ctx || !kf || !kf_C_dev || k < 0 || (k > 0 && (!frames || !T)) || !K) return RGBID_E_ARG;
-  if (k == 0) return RGBID_OK;
+  if (!ctx) return RGBID_E_ARG;
   LaunchScope ls(ctx);
-  std::vector<FuseFrame> hf(k);
-  for (int i = 0; i < k; ++i) {
-    if (frames[i]->w != kf->w || frames[i]->h != kf->h) return RGBID_E_ARG;
-    hf[i].W = frames[i]->W;
-    hf[i].wm = warp_mats(pose_of(&T[i]), K->fx, K->fy, K->cx, K->cy);
-  }
-  FuseFrame* df;
-  int rc = scratch_buf(ctx, "integrate_frames", k, &df);
-  if (rc) return rc;
-  H2D(df, hf.data(), sizeof(FuseFrame) * k);
-  launch_integrate(df, k, kf->W, kf_C_dev, kf->w, kf->h, sigma_w, ctx->stream);
-  kf->pyr_levels = 0;
-  rc = check_launch(ctx);
+  const int rc = rt_integrate_async(ctx, kf, kf_C_dev, k, frames, T, K, sigma_w);
   if (rc) return rc;
   CK(cudaStreamSynchronize(ctx->stream));
   return RGBID_OK;
@@ -1347,40 +1335,19 @@ int rgbid_covisibility_ratio(rgbid_ctx* ctx, const rgbid_frame* a, const rgbid_f
                              const rgbid_pose* T_BA, const rgbid_intrinsics* K, double sigma_w,
                              double* ratio, int* empty, long long* counts) {
   if (!ctx || !a || !b || !T_BA || !K || !ratio) return RGBID_E_ARG;
-  if (a->w != b->w || a->h != b->h) return RGBID_E_ARG;
   LaunchScope ls(ctx);
-  const M3 Km = K_mat(K->fx, K->fy, K->cx, K->cy), Kinv = m3_inv(Km);
-  auto dir = [&](const rgbid_frame* A, const rgbid_frame* B, const PoseD& T) {
-    CovisDir d;
-    d.WA = A->W;
-    d.WB = B->W;
-    const M3 Rt = m3_mul(m3_mul(Km, T.R), Kinv);
-    const V3 tt = m3_mulv(Km, T.t);
-    for (int i = 0; i < 9; ++i) d.Rt[i] = Rt.m[i / 3][i % 3];
-    for (int i = 0; i < 3; ++i) d.tt[i] = tt.v[i];
-    return d;
-  };
-  const PoseD T = pose_of(T_BA);
-  const CovisDir d0 = dir(a, b, T), d1 = dir(b, a, pose_inverse(T));
   unsigned long long* dc;
   int rc = scratch_buf(ctx, "covis", 4, &dc);
   if (rc) return rc;
-  launch_covisibility(d0, d1, a->w, a->h, sigma_w, dc, ctx->stream);
-  rc = check_launch(ctx);
+  rc = rt_covis_enqueue(ctx, a, b, T_BA, K, sigma_w, dc);
   if (rc) return rc;
   unsigned long long hc[4];
   D2H(hc, dc, sizeof(hc));
   CK(cudaStreamSynchronize(ctx->stream));
   if (counts)
     for (int i = 0; i < 4; ++i) counts[i] = (long long)hc[i];
-  // covisibility_ratio — src/fusion.cpp:56-66
-  *ratio = 0.0;
   int e = 0;
-  if (hc[0] == 0 || hc[2] == 0) {
-    e = 1;
-  } else {
-    *ratio = dmin_std((double)hc[1] / (double)hc[0], (double)hc[3] / (double)hc[2]);
-  }
+  rt_covis_ratio(hc, ratio, &e);
   if (empty) *empty = e;
   return RGBID_OK;
 }
@@ -1512,6 +1479,59 @@ int rgbid_correct_inverse_depth(rgbid_ctx* ctx, const double* Wm, int w, int h,
   rc = check_launch(ctx);
   if (rc) return rc;
   D2H(out, dd + N, sizeof(double) * N);
+  CK(cudaStreamSynchronize(ctx->stream));
+  return RGBID_OK;
+}
+
+// inverse_warp of both maps of a distorted-sensor frame with f_w = K distort(K^-1 p)
+// (src/warping.cpp:8-18, src/camera.cpp:11-22,41-45), device-resident
+int rgbid_rectify_frame(rgbid_ctx* ctx, const rgbid_frame* src, const rgbid_intrinsics* K,
+                        rgbid_frame* dst) {
+  if (!ctx || !src || !K || !dst || src == dst || src->w != dst->w || src->h != dst->h ||
+      K->width != src->w || K->height != src->h)
+    return RGBID_E_ARG;
+  LaunchScope ls(ctx);
+  launch_rectify(src->I, src->W, src->w, src->h, *K, dst->I, dst->W, ctx->stream);
+  dst->pyr_levels = 0;
+  dst->pyr_lane = -1;
+  const int rc = check_launch(ctx);
+  if (rc) return rc;
+  CK(cudaStreamSynchronize(ctx->stream));
+  return RGBID_OK;
+}
+
+int rgbid_rectify(rgbid_ctx* ctx, const double* src, int w, int h, const rgbid_intrinsics* K,
+                  double* out) {
+  if (!ctx || !src || !K || !out || w <= 0 || h <= 0) return RGBID_E_ARG;
+  LaunchScope ls(ctx);
+  const size_t N = (size_t)w * h;
+  double* d;
+  int rc = scratch_buf(ctx, "rectify", 2 * N, &d);
+  if (rc) return rc;
+  H2D(d, src, sizeof(double) * N);
+  launch_rectify(d, d, w, h, *K, d + N, d + N, ctx->stream);  // both grid rows: same map
+  rc = check_launch(ctx);
+  if (rc) return rc;
+  D2H(out, d + N, sizeof(double) * N);
+  CK(cudaStreamSynchronize(ctx->stream));
+  return RGBID_OK;
+}
+
+int rgbid_undistort_points(rgbid_ctx* ctx, const double* m_d, long long n,
+                           const rgbid_intrinsics* K, double* m_u, unsigned char* ok) {
+  if (!ctx || n < 0 || (n > 0 && (!m_d || !m_u || !ok)) || !K) return RGBID_E_ARG;
+  if (n == 0) return RGBID_OK;
+  LaunchScope ls(ctx);
+  double* d;
+  int rc = scratch_buf(ctx, "undistort", (size_t)4 * n + (n + 7) / 8, &d);
+  if (rc) return rc;
+  uint8_t* dok = reinterpret_cast<uint8_t*>(d + 4 * n);
+  H2D(d, m_d, sizeof(double) * 2 * n);
+  launch_undistort(d, n, *K, d + 2 * n, dok, ctx->stream);
+  rc = check_launch(ctx);
+  if (rc) return rc;
+  D2H(m_u, d + 2 * n, sizeof(double) * 2 * n);
+  D2H(ok, dok, (size_t)n);
   CK(cudaStreamSynchronize(ctx->stream));
   return RGBID_OK;
 }
@@ -1760,3 +1780,76 @@ int rgbid_frame_invalidate(rgbid_frame* f) {
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// stream-ordered building blocks (runtime_internal.cuh)
+namespace rgbid_b200 {
+
+int rt_frame_upload_async(rgbid_ctx* ctx, rgbid_frame* f, const double* I, const double* W) {
+  if (!ctx || !f || !W) return RGBID_E_ARG;
+  const size_t N = (size_t)f->w * f->h;
+  if (I)
+    H2D(f->I, I, sizeof(double) * N);
+  else
+    CK(cudaMemsetAsync(f->I, 0xff, sizeof(double) * N, ctx->stream));  // NaN holes
+  H2D(f->W, W, sizeof(double) * N);
+  f->pyr_levels = 0;
+  f->pyr_lane = -1;
+  return RGBID_OK;
+}
+
+int rt_covis_enqueue(rgbid_ctx* ctx, const rgbid_frame* a, const rgbid_frame* b,
+                     const rgbid_pose* T_BA, const rgbid_intrinsics* K, double sigma_w,
+                     unsigned long long* counts_dev) {
+  if (!ctx || !a || !b || !T_BA || !K || !counts_dev) return RGBID_E_ARG;
+  if (a->w != b->w || a->h != b->h) return RGBID_E_ARG;
+  LaunchScope ls(ctx);
+  // host setup — src/fusion.cpp:29-32 (R~ = K R K^-1, t~ = K t per direction)
+  const M3 Km = K_mat(K->fx, K->fy, K->cx, K->cy), Kinv = m3_inv(Km);
+  auto dir = [&](const rgbid_frame* A, const rgbid_frame* B, const PoseD& T) {
+    CovisDir d;
+    d.WA = A->W;
+    d.WB = B->W;
+    const M3 Rt = m3_mul(m3_mul(Km, T.R), Kinv);
+    const V3 tt = m3_mulv(Km, T.t);
+    for (int i = 0; i < 9; ++i) d.Rt[i] = Rt.m[i / 3][i % 3];
+    for (int i = 0; i < 3; ++i) d.tt[i] = tt.v[i];
+    return d;
+  };
+  const PoseD T = pose_of(T_BA);
+  const CovisDir d0 = dir(a, b, T), d1 = dir(b, a, pose_inverse(T));
+  launch_covisibility(d0, d1, a->w, a->h, sigma_w, counts_dev, ctx->stream);
+  return check_launch(ctx);
+}
+
+void rt_covis_ratio(const unsigned long long* hc, double* ratio, int* empty) {
+  *ratio = 0.0;
+  *empty = 0;
+  if (hc[0] == 0 || hc[2] == 0)
+    *empty = 1;
+  else
+    *ratio = dmin_std((double)hc[1] / (double)hc[0], (double)hc[3] / (double)hc[2]);
+}
+
+int rt_integrate_async(rgbid_ctx* ctx, rgbid_frame* kf, double* kf_C_dev, int k,
+                       const rgbid_frame* const* frames, const rgbid_pose* T,
+                       const rgbid_intrinsics* K, double sigma_w) {
+  if (!ctx || !kf || !kf_C_dev || k < 0 || (k > 0 && (!frames || !T)) || !K) return RGBID_E_ARG;
+  if (k == 0) return RGBID_OK;
+  LaunchScope ls(ctx);
+  std::vector<FuseFrame> hf(k);
+  for (int i = 0; i < k; ++i) {
+    if (frames[i]->w != kf->w || frames[i]->h != kf->h) return RGBID_E_ARG;
+    hf[i].W = frames[i]->W;
+    hf[i].wm = warp_mats(pose_of(&T[i]), K->fx, K->fy, K->cx, K->cy);
+  }
+  FuseFrame* df;
+  int rc = scratch_buf(ctx, "integrate_frames", k, &df);
+  if (rc) return rc;
+  H2D(df, hf.data(), sizeof(FuseFrame) * k);  // pageable: staged before return
+  launch_integrate(df, k, kf->W, kf_C_dev, kf->w, kf->h, sigma_w, ctx->stream);
+  kf->pyr_levels = 0;
+  return check_launch(ctx);
+}
+
+}  // namespace rgbid_b200

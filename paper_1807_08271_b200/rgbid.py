@@ -764,6 +764,37 @@ def forward_register(W_A, T_BA: Pose, K_A: Intrinsics, K_B: Intrinsics,
 # --------------------------------------------------------------------------- synthetic inputs
 
 
+def rectify(img: np.ndarray, K: Intrinsics, ctx: Optional[Context] = None) -> np.ndarray:
+    """inverse_warp(img, f_w = K distort(K^-1 p)) — src/warping.cpp:8-18 with the
+    distorted-sensor map of src/camera.cpp:11-22,41-45, evaluated on the device."""
+    ctx = ctx or default_context()
+    img = np.ascontiguousarray(img, dtype=np.float64)
+    h, w = img.shape
+    out = np.empty_like(img)
+    ctx.check(ctx.lib.rgbid_rectify(ctx.h, dptr(img), w, h, C.byref(K.to_c()), dptr(out)), "rectify")
+    return out
+
+
+def rectify_frame(src: "DeviceFrame", K: Intrinsics, dst: "DeviceFrame"):
+    """Both maps of a device frame through rectify (device-resident)."""
+    src.ctx.check(src.ctx.lib.rgbid_rectify_frame(src.ctx.h, src.h, C.byref(K.to_c()), dst.h),
+                  "rectify_frame")
+    return dst
+
+
+def undistort_points(m_d, K: Intrinsics, ctx: Optional[Context] = None):
+    """undistort (src/camera.cpp:24-39) of n normalized points: (m_u [n, 2], ok [n])."""
+    ctx = ctx or default_context()
+    m_d = np.ascontiguousarray(m_d, dtype=np.float64).reshape(-1, 2)
+    n = len(m_d)
+    m_u = np.empty_like(m_d)
+    ok = np.zeros(n, dtype=np.uint8)
+    ctx.check(ctx.lib.rgbid_undistort_points(ctx.h, dptr(m_d), n, C.byref(K.to_c()), dptr(m_u),
+                                             ok.ctypes.data_as(C.POINTER(C.c_ubyte))),
+              "undistort_points")
+    return m_u, ok.astype(bool)
+
+
 def render_plane(K: Intrinsics, T_WC: Pose, n=(0.0, 0.0, 1.0), d: float = -2.0,
                  tex_scale: float = 1.0) -> FrameData:
     """tests/synthetic.hpp:31-50 (bit-identical to the reference fixture at tex_scale=1)."""
