@@ -1428,8 +1428,9 @@ int init_kernel_attributes() {
   return (e == cudaSuccess && e2 == cudaSuccess) ? 0 : 1;
 }
 
-void launch_tdist(const AlignLaunch& a, const LevelInfo& li, int phase, cudaStream_t s) {
-  if (a.nslots <= kTdistClusterMaxSlots) {  // latency mode: cluster per chain
+void launch_tdist(const AlignLaunch& a, const LevelInfo& li, int phase, cudaStream_t s, int part) {
+  if (a.nslots <= kTdistClusterMaxSlots) {  // latency mode: cluster per chain (no gather)
+    if (part == 1) return;
     KScope ks_("tdist_cluster", s);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(2 * kTdistCluster, a.nslots);
@@ -1447,11 +1448,12 @@ void launch_tdist(const AlignLaunch& a, const LevelInfo& li, int phase, cudaStre
     cudaLaunchKernelEx(&cfg, k_tdist_cluster, a.io, a.st, li, phase);
     return;
   }
-  {
+  if (part != 2) {
     KScope ks_("gather", s);
     k_gather<<<dim3(kGatherCTAs, 2, a.nslots), kGatherThreads, (li.ntiles + 1) * sizeof(int), s>>>(
         a.io, a.st, li, phase);
   }
+  if (part == 1) return;
   KScope ks_("tdist", s);
   // highest launch priority: the FP64-bound chains claim SMs first, the other
   // lane's memory-bound kernels fill around them

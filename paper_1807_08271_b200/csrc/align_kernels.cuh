@@ -114,7 +114,10 @@ struct AlignLaunch {
 
 // Kernel launchers (align_kernels.cu); all asynchronous on `stream`.
 void launch_warp_residuals(const AlignLaunch& a, const LevelInfo& li, int phase, cudaStream_t s);
-void launch_tdist(const AlignLaunch& a, const LevelInfo& li, int phase, cudaStream_t s);
+// K2: part 0 = gather + Student-t, 1 = gather only (K2a), 2 = Student-t only (K2b);
+// latency mode (<= kTdistClusterMaxSlots slots) has no separate gather
+void launch_tdist(const AlignLaunch& a, const LevelInfo& li, int phase, cudaStream_t s,
+                  int part = 0);
 void launch_normal_equations(const AlignLaunch& a, const LevelInfo& li, int phase, cudaStream_t s);
 void launch_solve(const AlignLaunch& a, const LevelInfo& li, const LevelInfo& li0, cudaStream_t s);
 void launch_covariance(const AlignLaunch& a, const LevelInfo& li, cudaStream_t s);

@@ -413,11 +413,21 @@ int validate_cfg(const rgbid_align_config& c, int w, int h) {
 // pair the FP64-bound Student-t kernel with a memory-bound kernel.
 using Stage = std::function<void(cudaStream_t)>;
 
+// Schedule of co-scheduled chunk pairs (read once per ctx from the environment):
+// stages per IRLS iteration (3: K1 | K2 | K3+K4, or 4: K1 | K2a | K2b | K3+K4) and the
+// stage offset D of the second chunk (its stage s runs beside the first chunk's s+D).
+int g_pair_stages = 3, g_pair_offset = 1;
+
+// The whole align (all levels + covariance pass) as a list of stages; a stage
+// is one or more dependent kernel launches on one stream.  Stages cycle over
+// the IRLS iteration's kernels so that two chunks offset by D stages pair the
+// FP64-bound Student-t kernel with a memory/latency-bound one.
 std::vector<Stage> align_stages(const AlignLaunch& a, const rgbid_intrinsics& K,
                                 const rgbid_align_config& cfg) {
   std::vector<Stage> st;
   const LevelInfo li0 = make_level(K, a.w0, a.h0, 0);
   const int levels = cfg.levels;
+  const bool split = g_pair_stages == 4;
   st.push_back([a, levels](cudaStream_t s) {
     launch_pyramid_slots(a, levels, s);  // build_pyramid (src/alignment.cpp:369)
     launch_amask(a, levels, 0, s);       // A-side validity + gradients, once per align
@@ -428,7 +438,12 @@ std::vector<Stage> align_stages(const AlignLaunch& a, const rgbid_intrinsics& K,
     const int iters = level_iters(cfg, level);
     for (int it = 0; it < iters; ++it) {
       st.push_back([a, li](cudaStream_t s) { launch_warp_residuals(a, li, 0, s); });
-      st.push_back([a, li](cudaStream_t s) { launch_tdist(a, li, 0, s); });
+      if (split) {
+        st.push_back([a, li](cudaStream_t s) { launch_tdist(a, li, 0, s, 1); });
+        st.push_back([a, li](cudaStream_t s) { launch_tdist(a, li, 0, s, 2); });
+      } else {
+        st.push_back([a, li](cudaStream_t s) { launch_tdist(a, li, 0, s); });
+      }
       st.push_back([a, li, li0](cudaStream_t s) {
         launch_normal_equations(a, li, 0, s);
         launch_solve(a, li, li0, s);
@@ -483,27 +498,33 @@ void enqueue_align_group(const std::vector<cudaStream_t>& sj, const std::vector<
   cudaStreamWaitEvent(sj[0], ev[(G - 1) * n + n - 1], 0);  // join
 }
 
-// Two chunks in one launch sequence: stage s of B after stage s of A, stage
-// s+2 of A after stage s of B -> the pairs {A_{s+1}, B_s} run concurrently.
+// Two chunks in one launch sequence, B lagging D stages behind A: B's stage i
+// waits for A's stage i + D - 1, A's stage j for B's stage j - D - 1, so A's stage
+// i + D runs beside B's stage i.
 void enqueue_align_pair(cudaStream_t sA, cudaStream_t sB, const AlignLaunch& a,
                         const AlignLaunch& b, const rgbid_intrinsics& K,
                         const rgbid_align_config& cfg, std::vector<cudaEvent_t>& ev) {
   const std::vector<Stage> A = align_stages(a, K, cfg), B = align_stages(b, K, cfg);
-  const size_t n = A.size();
-  while (ev.size() < 2 * n + 1) {
+  const int n = (int)A.size(), D = std::max(1, g_pair_offset);
+  while ((int)ev.size() < 2 * n + 1) {
     cudaEvent_t e;
     cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
     ev.push_back(e);
   }
   cudaEventRecord(ev[2 * n], sA);  // fork B off A's stream (capture origin)
   cudaStreamWaitEvent(sB, ev[2 * n], 0);
-  for (size_t i = 0; i < n; ++i) {
-    if (i >= 2) cudaStreamWaitEvent(sA, ev[n + i - 2], 0);
-    A[i](sA);
-    cudaEventRecord(ev[i], sA);
-    cudaStreamWaitEvent(sB, ev[i], 0);
-    B[i](sB);
-    cudaEventRecord(ev[n + i], sB);
+  for (int t = 0; t < n + D - 1; ++t) {
+    if (t < n) {
+      if (t - D - 1 >= 0) cudaStreamWaitEvent(sA, ev[n + t - D - 1], 0);
+      A[t](sA);
+      cudaEventRecord(ev[t], sA);
+    }
+    const int i = t - (D - 1);
+    if (i >= 0 && i < n) {
+      cudaStreamWaitEvent(sB, ev[std::min(i + D - 1, n - 1)], 0);
+      B[i](sB);
+      cudaEventRecord(ev[n + i], sB);
+    }
   }
   cudaStreamWaitEvent(sA, ev[2 * n - 1], 0);  // join
 }
@@ -897,6 +918,8 @@ int rgbid_ctx_create(int device, rgbid_ctx** out) {
   }
   const char* g = std::getenv("RGBID_NO_GRAPHS");
   ctx->use_graphs = !(g && g[0] == '1');
+  if (const char* e = std::getenv("RGBID_PAIR_STAGES")) g_pair_stages = atoi(e) == 4 ? 4 : 3;
+  if (const char* e = std::getenv("RGBID_PAIR_OFFSET")) g_pair_offset = std::max(1, atoi(e));
   *out = ctx;
   return RGBID_OK;
 }

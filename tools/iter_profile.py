@@ -8,7 +8,7 @@ n = 512
 A = [rg.DeviceFrame(640, 480, ctx) for _ in range(n)]
 B = [rg.DeviceFrame(640, 480, ctx) for _ in range(n)]
 for i in range(n):
-    rg.synth_pair_device(A[i], B[i], K, i, 1)
+    rg.synth_pair_device(A[i], B[i], K, i, 1 + (i & 1))
 cfg = rg.AlignmentConfig(levels=4, iterations=[10, 5, 4])
 rg.align_batch(A, B, K, config=cfg, ctx=ctx)
 lib = ctx.lib
