@@ -251,6 +251,16 @@ def host_pairs(n, variant, seed0=0):
         return K, list(ex.map(one, range(n)))
 
 
+def rgbid_libraries_loaded():
+    """The repo's native libraries mapped into this process (/proc/self/maps): the
+    reference arm must show oracle/ libraries only, never the CUDA library."""
+    try:
+        paths = {ln.split()[-1] for ln in open("/proc/self/maps") if ln.strip().endswith(".so")}
+    except OSError:
+        return []
+    return sorted(os.path.relpath(p, ROOT) for p in paths if p.startswith(ROOT) and "rgbid" in p)
+
+
 def input_digest(pairs):
     import hashlib
     h = hashlib.sha256()
@@ -334,7 +344,8 @@ def run_reference(args, rank, world):
               f"covariance on {cores} threads, one pair per thread at a time")
     cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample,
            "cpu_model": cpu_model(), "latency": lat,
-           "ok": sum(1 for r in res if r.status == 0)}
+           "ok": sum(1 for r in res if r.status == 0),
+           "libraries_loaded": rgbid_libraries_loaded()}
     line = {
         "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,

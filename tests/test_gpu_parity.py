@@ -566,3 +566,30 @@ def test_inverse_warp_bitwise(ctx):
                     for y in range(15)])
     assert bitwise_equal(rg.inverse_warp(src, f_vec, 22, 15, ctx), ref)
     assert bitwise_equal(rg.inverse_warp(src, f_sca, 22, 15, ctx), ref)
+
+
+@pytest.mark.parametrize("case", ["tight_core", "tiny_scale", "two_clusters", "heavy_tail_low_nu"])
+def test_student_t_stress_samples(ctx, orc, case):
+    """The device location/scale update uses sum w d^2 = c2 (m - c1 sum 1/q), which
+    cancels when most d^2 << c1 = nu sigma^2: samples whose bulk
+    is far tighter than the scale the outliers impose, a scale near the 1e-8 floor,
+    two separated clusters, and a t(1.2) tail that drives nu into the bisection.
+    GPU vs the oracle (the reference's sequential sums) at the 1e-6 bar."""
+    rng = np.random.default_rng({"tight_core": 11, "tiny_scale": 12, "two_clusters": 13,
+                                 "heavy_tail_low_nu": 14}[case])
+    n = 19200
+    if case == "tight_core":
+        r = np.where(rng.random(n) < 0.97, rng.normal(0.01, 1e-6, n), rng.normal(0.0, 1.0, n))
+    elif case == "tiny_scale":
+        r = 0.5 + rng.normal(0.0, 3e-8, n)
+    elif case == "two_clusters":
+        r = np.where(rng.random(n) < 0.7, rng.normal(-0.2, 1e-4, n), rng.normal(0.3, 1e-4, n))
+    else:
+        r = 0.02 * rng.standard_t(1.2, size=n)
+    for nu in (5.0, 2.5, 10.0):
+        g = rg.estimate_location_scale(r, nu, ctx)
+        o = orc.estimate_location_scale(r, nu)
+        assert g.mu == pytest.approx(o[0], rel=1e-6, abs=1e-12 + 1e-6 * o[1])
+        assert g.sigma == pytest.approx(o[1], rel=1e-6)
+    mu, s, _ = orc.estimate_location_scale(r, 5.0)
+    assert rg.estimate_nu(r, mu, s, ctx) == pytest.approx(orc.estimate_nu(r, mu, s), rel=1e-6)

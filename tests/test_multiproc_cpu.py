@@ -104,3 +104,6 @@ def test_gpus_flag_relaunches_one_rank_per_gpu():
     line = json.loads(lines[0])
     assert line["n_gpus"] == 2 and line["impl"] == "reference"
     assert line["cpu_baseline"]["ok"] == 2
+    # the reference arm never maps the CUDA library (inputs from oracle/_build/librgbid_synth.so)
+    libs = line["cpu_baseline"]["libraries_loaded"]
+    assert libs and all(p.startswith("oracle/") for p in libs), libs
