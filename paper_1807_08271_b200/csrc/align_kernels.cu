@@ -782,9 +782,6 @@ struct LogProd {
 #define RGBID_QBODY 4
 #endif
 constexpr int kQBody = RGBID_QBODY;  // samples per fraction
-#ifndef RGBID_QBODY_UNROLL
-#define RGBID_QBODY_UNROLL 3
-#endif
 
 // sum_i 1/q_i = N/D (and sum_i x_i/q_i = NV/D) over BW samples, pairwise tree
 template <int BW, bool WV>
@@ -846,10 +843,6 @@ __device__ __forceinline__ void q_sums(const Sample& S, double mu, double c1, do
   LogProd P;
   bool bad = false;
   int k = 0;
-  // latency mode (~10 samples per thread): the bodies' trees and reciprocals overlap
-  // when unrolled; the FP64-bound batch kernels gain nothing from it (round 1)
-  constexpr int kUnroll = NT == kTdistClusterThreads ? RGBID_QBODY_UNROLL : 1;
-#pragma unroll kUnroll
   for (; k + BW - 1 < S.kfull; k += BW)  // branch-free bodies
     q_body<NT, BW, WV, WL, false>(S, v, k, mu, c1, sr, sv, P, bad);
   const int kend = (S.m_local + NT - 1) / NT;
