@@ -14,9 +14,10 @@ def summarize(path, min_slots=64):
     agg = collections.defaultdict(lambda: [0, 0.0])
     for r in rows[1:]:
         dims = [int(x) for x in re.findall(r"\d+", r[gi])]
-        if max(dims[1:]) < min_slots:
-            continue
         name = r[ki].split("(")[0].replace("void ", "").replace("rgbid_b200::", "")
+        per_slot = name in ("k_solve", "k_covariance")  # grid.x = slots
+        if (dims[0] if per_slot else max(dims[1:])) < min_slots:
+            continue
         agg[(name, r[gi])][0] += 1
         agg[(name, r[gi])][1] += float(r[vi].replace(",", "")) * scale.get(r[ui], 1e-6)
     tot = sum(v[1] for v in agg.values())
