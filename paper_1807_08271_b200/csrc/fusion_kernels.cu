@@ -266,7 +266,8 @@ __global__ void k_rectify(const double* __restrict__ I, const double* __restrict
 void launch_rectify(const double* I, const double* W, int w, int h, const rgbid_intrinsics& K,
                     double* oI, double* oW, cudaStream_t s) {
   KScope ks_("rectify", s);
-  k_rectify<<<dim3((w * h + 255) / 256, 2), 256, 0, s>>>(I, W, w, h, K, oI, oW);
+  // one grid row per map; W == nullptr: I only
+  k_rectify<<<dim3((w * h + 255) / 256, W ? 2 : 1), 256, 0, s>>>(I, W, w, h, K, oI, oW);
 }
 
 // undistort — src/camera.cpp:24-39: fixed-point iteration m_u -= distort(m_u) - m_d,

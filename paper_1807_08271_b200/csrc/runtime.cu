@@ -1532,7 +1532,7 @@ int rgbid_rectify(rgbid_ctx* ctx, const double* src, int w, int h, const rgbid_i
   int rc = scratch_buf(ctx, "rectify", 2 * N, &d);
   if (rc) return rc;
   H2D(d, src, sizeof(double) * N);
-  launch_rectify(d, d, w, h, *K, d + N, d + N, ctx->stream);  // both grid rows: same map
+  launch_rectify(d, nullptr, w, h, *K, d + N, nullptr, ctx->stream);
   rc = check_launch(ctx);
   if (rc) return rc;
   D2H(out, d + N, sizeof(double) * N);
