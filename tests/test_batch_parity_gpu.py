@@ -182,3 +182,21 @@ def test_host_streaming_calls_complete_previous_lanes(ctx, K, cfg, pairs):
     ref = _batch(ctx, K, cfg, A, B, range(n1 + n2), slots=n1 + n2)
     assert done1 == [_key(r) for r in ref[:n1]]
     assert [bytes(r) for r in r2] == [_key(r) for r in ref[n1:]]
+
+
+@pytest.mark.parametrize("variant", [0, 1, 2])
+def test_device_scene_equals_host_scene(ctx, K, variant):
+    """bench.py times device-rendered pairs and checks parity on host-rendered ones:
+    the same scene model (synth_scene.cuh) -- identical hole patterns (integer hashing)
+    and values equal up to libm's last bits (CUDA vs glibc sin/cos/log)."""
+    for i in (3, 4):
+        A, B = rg.DeviceFrame(640, 480, ctx), rg.DeviceFrame(640, 480, ctx)
+        T_dev = rg.synth_pair_device(A, B, K, i, variant)
+        IA, WA, IB, WB, T_host = O.synth_pair_host(K.to_c(), i, variant)
+        fa, fb = A.download(), B.download()
+        assert bytes(T_dev.to_c()) == bytes(T_host)
+        for g, h in ((fa.intensity, IA), (fa.inverse_depth, WA), (fb.intensity, IB),
+                     (fb.inverse_depth, WB)):
+            assert np.array_equal(np.isnan(g), np.isnan(h))
+            m = ~np.isnan(h)
+            assert np.abs(g[m] - h[m]).max() <= 1e-12
