@@ -72,6 +72,15 @@ __device__ __forceinline__ double div_rcp(double a, double b, double r) {
   return fma(e, r, q);
 }
 
+// a / b correctly rounded: one IEEE reciprocal + the Markstein correction where the
+// operands are in the range rgbid_selftest_division checks bit for bit, else a / b
+__device__ __forceinline__ double div_safe(double a, double b) {
+  const double mb = fabs(b), ma = fabs(a);
+  if (mb > 1e-290 && mb < 1e290 && ma < 1e290 && (ma > 1e-280 || a == 0.0))
+    return div_rcp(a, b, __drcp_rn(b));
+  return a / b;
+}
+
 // bilinear — inc/image.hpp:51-62
 __device__ __forceinline__ double bilinear(const double* __restrict__ img, int w, int h, double x,
                                            double y) {
@@ -131,7 +140,7 @@ __device__ __forceinline__ void warp_px(const WarpMats& m, const double* __restr
   oI = inb ? ri : CUDART_NAN;
   const bool v2 = inb && valid(w_meas) && w_meas > 0.0;
   const double rz = red3(m.Rt_AB[6] * px, m.Rt_AB[7] * py, m.Rt_AB[8] * 1.0);
-  const double za = rz / (v2 ? w_meas : 1.0) + m.tt_AB[2];
+  const double za = div_safe(rz, v2 ? w_meas : 1.0) + m.tt_AB[2];
   const bool v3 = v2 && za > 1e-12;
   oW = v3 ? __drcp_rn(za) : CUDART_NAN;  // == 1.0 / za
 }
@@ -173,7 +182,7 @@ __device__ __forceinline__ void warp_px_iw(const WarpMats& m, const double2* __r
   oI = inb ? ri : CUDART_NAN;
   const bool v2 = inb && valid(w_meas) && w_meas > 0.0;
   const double rz = red3(m.Rt_AB[6] * px, m.Rt_AB[7] * py, m.Rt_AB[8] * 1.0);
-  const double za = rz / (v2 ? w_meas : 1.0) + m.tt_AB[2];
+  const double za = div_safe(rz, v2 ? w_meas : 1.0) + m.tt_AB[2];
   const bool v3 = v2 && za > 1e-12;
   oW = v3 ? __drcp_rn(za) : CUDART_NAN;  // == 1.0 / za
 }
@@ -208,7 +217,9 @@ __device__ __forceinline__ bool gradient_at(const double* img, int w, int h, int
   return true;
 }
 
-// 2x2 NaN-aware mean — inc/image.hpp:73-91 (tap order (0,0),(1,0),(0,1),(1,1))
+// 2x2 NaN-aware mean — inc/image.hpp:73-91 (tap order (0,0),(1,0),(0,1),(1,1)).
+// sum / n for n = 1, 2, 4 is the exact product sum * (1/n) (a power of two: the same
+// correctly rounded value), so only n = 3 (a hole next to the block) divides.
 __device__ __forceinline__ double ds4(double a, double b, double c, double d) {
   double sum = 0.0;
   int n = 0;
@@ -216,7 +227,8 @@ __device__ __forceinline__ double ds4(double a, double b, double c, double d) {
   if (valid(b)) sum += b, ++n;
   if (valid(c)) sum += c, ++n;
   if (valid(d)) sum += d, ++n;
-  return n > 0 ? sum / n : CUDART_NAN;
+  if (n == 3) return sum / 3.0;
+  return n == 4 ? sum * 0.25 : n == 2 ? sum * 0.5 : n == 1 ? sum : CUDART_NAN;
 }
 
 // ---------------------------------------------------------------------------
@@ -250,7 +262,7 @@ __global__ void __launch_bounds__(k1_threads<L>(), RGBID_K1_THREADS_PER_SM / k1_
                                                            const SlotState* __restrict__ st,
                                                            LevelInfo li, int w0, int h0, int phase) {
   static_assert(L >= 1, "level 0 uses k_warp_residuals_l0");
-  const int slot = blockIdx.y;
+  const int slot = blockIdx.z;  // grid (segment, level row, slot): no tile-index division
   const SlotState& S = st[slot];
   if (!slot_active(S, L, phase)) return;
   __shared__ WarpMats wm;
@@ -260,11 +272,10 @@ __global__ void __launch_bounds__(k1_threads<L>(), RGBID_K1_THREADS_PER_SM / k1_
   const double* __restrict__ WAw = phase ? o.fWA : o.WA[0];
   const double* __restrict__ IAl = phase ? o.fIA : o.IA[L];
   const uint8_t* __restrict__ am = o.amask[L];
-  __syncthreads();
 
   const int tid = threadIdx.x;
-  const int tile = blockIdx.x;
-  const int yl = tile / li.nseg, seg = tile - yl * li.nseg;
+  const int seg = blockIdx.x, yl = blockIdx.y;
+  const int tile = yl * li.nseg + seg;
   const int xl0 = seg * li.tx;
   const int nx = min(li.tx, li.w - xl0);
   // Level-1 block of the tile: cw = nx * 2^(L-1) columns (<= 128, one per thread) x
@@ -275,8 +286,14 @@ __global__ void __launch_bounds__(k1_threads<L>(), RGBID_K1_THREADS_PER_SM / k1_
   constexpr int CW = k1_cw<L>(), NG = k1_ng<L>();  // thread columns x row groups
   int cw = nx << (L - 1), ch = 1 << (L - 1);
   const int col = tid % CW, grp = tid / CW;
+  const int x = (xl0 << L) + 2 * col;
+  // the first quad's W_A values in flight while the warp matrices arrive
+  double wa0[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+    wa0[q] = col < cw ? __ldg(WAw + ((yl << L) + 2 * grp + (q >> 1)) * w0 + x + (q & 1)) : 0.0;
+  __syncthreads();
   if (col < cw) {
-    const int x = (xl0 << L) + 2 * col;
 #pragma unroll
     for (int rr = 0; rr < (1 << (L - 1)) / NG; ++rr) {
       const int r = rr * NG + grp;
@@ -285,7 +302,8 @@ __global__ void __launch_bounds__(k1_threads<L>(), RGBID_K1_THREADS_PER_SM / k1_
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const int xx = x + (q & 1), yy = y + (q >> 1);
-        warp_px_iw(wm, o.IWB, w0, h0, xx, yy, __ldg(WAw + yy * w0 + xx), vi[q], vw[q], d0, d1);
+        const double w_a = rr == 0 ? wa0[q] : __ldg(WAw + yy * w0 + xx);
+        warp_px_iw(wm, o.IWB, w0, h0, xx, yy, w_a, vi[q], vw[q], d0, d1);
       }
       sI[r * cw + col] = ds4(vi[0], vi[1], vi[2], vi[3]);
       sW[r * cw + col] = ds4(vw[0], vw[1], vw[2], vw[3]);
@@ -356,7 +374,7 @@ __global__ void __launch_bounds__(128, RGBID_K1L0_MINB) k_warp_residuals_l0(cons
                                                                 const SlotState* __restrict__ st,
                                                                 LevelInfo li, int w0, int h0,
                                                                 int phase) {
-  const int slot = blockIdx.y;
+  const int slot = blockIdx.z;  // grid (segment, row, slot): no tile-index division
   const SlotState& S = st[slot];
   if (!slot_active(S, 0, phase)) return;
   __shared__ WarpMats wm;
@@ -366,12 +384,24 @@ __global__ void __launch_bounds__(128, RGBID_K1L0_MINB) k_warp_residuals_l0(cons
   const double* __restrict__ WAw = phase ? o.fWA : o.WA[0];
   const double* __restrict__ IA0 = phase ? o.fIA : o.IA[0];
   const uint8_t* __restrict__ am = o.amask[0];
-  __syncthreads();
   const int tid = threadIdx.x;
-  const int tile = blockIdx.x;
-  const int yl = tile / li.nseg, seg = tile - yl * li.nseg;
+  const int seg = blockIdx.x, yl = blockIdx.y;
+  const int tile = yl * li.nseg + seg;
   const int xl0 = seg * li.tx;
   const int nx = min(li.tx, li.w - xl0);
+  // the pixels' A-side values in flight while the warp matrices arrive
+  double wa[2], iav[2];
+  unsigned amv[2];
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int lx = tid + 128 * q;
+    const int idx = yl * w0 + xl0 + lx;
+    const bool in = lx < nx;
+    wa[q] = in ? __ldg(WAw + idx) : 0.0;
+    iav[q] = in ? __ldg(IA0 + idx) : 0.0;
+    amv[q] = in ? __ldg(am + idx) : 0u;
+  }
+  __syncthreads();
   bool jet[2], dep[2];
 #pragma unroll
   for (int q = 0; q < 2; ++q) {
@@ -379,10 +409,10 @@ __global__ void __launch_bounds__(128, RGBID_K1L0_MINB) k_warp_residuals_l0(cons
     jet[q] = dep[q] = false;
     if (lx < nx) {
       const int idx = yl * w0 + xl0 + lx;
-      const unsigned a = __ldg(am + idx);
-      const double ia = __ldg(IA0 + idx);
+      const unsigned a = amv[q];
+      const double ia = iav[q];
       double ib, wb, d0, d1;
-      warp_px_iw(wm, o.IWB, w0, h0, xl0 + lx, yl, __ldg(WAw + idx), ib, wb, d0, d1);
+      warp_px_iw(wm, o.IWB, w0, h0, xl0 + lx, yl, wa[q], ib, wb, d0, d1);
       o.ibw[idx] = make_double2(ib - ia, wb);  // r_I (src/alignment.cpp:222), w_b: K2, K3
       jet[q] = (a & 1u) && valid(ib);
       dep[q] = jet[q] && (a & 2u) && valid(wb) && wb > 0.0;
@@ -539,7 +569,7 @@ static const char* kLevelNames[2][kMaxLevels] = {
 
 void launch_warp_residuals(const AlignLaunch& a, const LevelInfo& li, int phase, cudaStream_t s) {
   KScope ks_(kLevelNames[phase ? 1 : 0][li.level], s);
-  dim3 grid(li.ntiles, a.nslots);
+  dim3 grid(li.nseg, li.h, a.nslots);  // tile = row * nseg + segment
   switch (li.level) {
     case 0: k_warp_residuals_l0<<<grid, 128, 0, s>>>(a.io, a.st, li, a.w0, a.h0, phase); break;
     case 1: k_warp_residuals<1><<<grid, k1_threads<1>(), 0, s>>>(a.io, a.st, li, a.w0, a.h0, phase); break;

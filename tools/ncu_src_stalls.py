@@ -16,13 +16,15 @@ def main(rep, kreg, cubin, mangled, top=30):
     hi = next(i for i, r in enumerate(rows) if len(r) > 3 and r[0] == "Address")
     h = rows[hi]
     si, ni = h.index("Warp Stall Sampling (All Samples)"), h.index("Source")
+    ei = h.index("Instructions Executed") if "Instructions Executed" in h else None
     sass = []
     for r in rows[hi + 1:]:
-        if len(r) <= si:
+        if len(r) <= max(si, ei or 0):
             continue
         if r[0] == "Address":  # a second function / section: stop at the first
             break
-        sass.append((r[ni].strip(), float(r[si] or 0)))
+        sass.append((r[ni].strip(), float(r[si] or 0),
+                     float(r[ei] or 0) if ei is not None else 0.0))
     dis = subprocess.run(["nvdisasm", "-g", "-c", cubin], capture_output=True, text=True).stdout
     parts = re.split(r"\n\s*\.text\.(\S+):", dis)
     body = next(parts[i + 1] for i in range(1, len(parts), 2) if mangled in parts[i])
@@ -39,11 +41,22 @@ def main(rep, kreg, cubin, mangled, top=30):
     mism = sum(1 for i in range(n) if sass[i][0].split()[0].lstrip("@!P0123456789UT ") [:4] !=
                lines[i][1].split()[0].lstrip("@!P0123456789UT ")[:4])
     agg = collections.Counter()
+    ins = collections.Counter()
+    ops = collections.Counter()
     for i in range(n):
         agg[lines[i][0]] += sass[i][1]
+        ins[lines[i][0]] += sass[i][2]
+        ops[sass[i][0].split()[0].lstrip("@!P0123456789UT").split(".")[0] if not sass[i][0].startswith("@")
+            else sass[i][0].split()[1].split(".")[0]] += sass[i][2]
     tot = sum(agg.values()) or 1
     srcs = {}
     print(f"# {len(sass)} SASS rows vs {len(lines)} disassembled, opcode mismatches {mism}")
+    itot = sum(ins.values()) or 1
+    print("# executed warp instructions by opcode: " + ", ".join(
+        f"{k} {v / itot * 100:.1f}%" for k, v in ops.most_common(24)))
+    print("# executed warp instructions by source line (top):")
+    for (f, l), v in ins.most_common(25):
+        print(f"#   {v / itot * 100:5.1f}% {f}:{l}")
     for (f, l), v in agg.most_common(top):
         if f not in srcs:
             try:
