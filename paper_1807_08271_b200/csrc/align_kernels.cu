@@ -287,11 +287,14 @@ __global__ void __launch_bounds__(k1_threads<L>(), RGBID_K1_THREADS_PER_SM / k1_
   int cw = nx << (L - 1), ch = 1 << (L - 1);
   const int col = tid % CW, grp = tid / CW;
   const int x = (xl0 << L) + 2 * col;
-  // the first quad's W_A values in flight while the warp matrices arrive
+  // one quad per thread (levels 1-2): its W_A values in flight while the warp
+  // matrices arrive (at level 3 the extra registers cost more than they save)
+  constexpr bool kHoist = (1 << (L - 1)) / NG == 1;
   double wa0[4];
 #pragma unroll
   for (int q = 0; q < 4; ++q)
-    wa0[q] = col < cw ? __ldg(WAw + ((yl << L) + 2 * grp + (q >> 1)) * w0 + x + (q & 1)) : 0.0;
+    wa0[q] = kHoist && col < cw ? __ldg(WAw + ((yl << L) + 2 * grp + (q >> 1)) * w0 + x + (q & 1))
+                                : 0.0;
   __syncthreads();
   if (col < cw) {
 #pragma unroll
@@ -302,7 +305,7 @@ __global__ void __launch_bounds__(k1_threads<L>(), RGBID_K1_THREADS_PER_SM / k1_
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const int xx = x + (q & 1), yy = y + (q >> 1);
-        const double w_a = rr == 0 ? wa0[q] : __ldg(WAw + yy * w0 + xx);
+        const double w_a = kHoist ? wa0[q] : __ldg(WAw + yy * w0 + xx);
         warp_px_iw(wm, o.IWB, w0, h0, xx, yy, w_a, vi[q], vw[q], d0, d1);
       }
       sI[r * cw + col] = ds4(vi[0], vi[1], vi[2], vi[3]);
