@@ -598,14 +598,10 @@ void launch_warp_residuals(const AlignLaunch& a, const LevelInfo& li, int phase,
 // has two halves used alternately (the caller's parity flips per call), so one
 // barrier per reduction suffices: a half is rewritten only two calls later,
 // after every thread has passed the intervening barrier.
-// values per reduction, at most (the latency-mode location pass carries 10)
-constexpr int kMomNV = 10;
-
 template <int NV, int NT>
 __device__ __forceinline__ void block_allsum(double (&v)[NV], double* scratch2, int& parity) {
-  static_assert(NV <= kMomNV, "scratch halves hold kMomNV values per warp");
   constexpr int NW = NT / 32;
-  double* scratch = scratch2 + parity * (NW * kMomNV);
+  double* scratch = scratch2 + parity * (NW * 2);
   parity ^= 1;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
 #pragma unroll
@@ -701,8 +697,7 @@ __device__ __forceinline__ void cluster_allsum(double (&v)[NV], Sample& S) {
   for (int off = 16; off > 0; off >>= 1)
 #pragma unroll
     for (int i = 0; i < NV; ++i) v[i] += __shfl_xor_sync(0xffffffffu, v[i], off);
-  static_assert(NV <= kMomNV, "slot halves hold kMomNV values per warp");
-  double* buf = S.cbuf + p * (NP * kMomNV);
+  double* buf = S.cbuf + p * (NP * 2);
   uint64_t* mb = S.cmbar + p;
   if (threadIdx.x == 0) {
     const unsigned a = (unsigned)__cvta_generic_to_shared(mb);
@@ -913,37 +908,6 @@ __device__ __forceinline__ void q_sums(const Sample& S, double mu, double c1, do
   }
 }
 
-// Latency mode: the location pass with the Taylor moments of the scale pass.  The
-// scale pass needs S(mu') = sum 1/((v - mu')^2 + c1) at the NEW location mu' = mu + dl.
-// With d = v - mu, q = d^2 + c1, r = 1/q:
-//   1/((d - dl)^2 + c1) = r + 2 d r^2 dl + (4 d^2 r^3 - r^2) dl^2
-//                         + (8 d^3 r^4 - 4 d r^3) dl^3 + (r^3 - 12 d^2 r^4 + 16 d^4 r^5) dl^4 + R5,
-// |R5| <= r (2 |d| r |dl|)^5 <= r (|dl| / sqrt(c1))^5.  The pass accumulates
-// {sum r, sum r v} and the eight moments; when |dl| < 1e-3 sqrt(c1) the series gives
-// S(mu') to ~1e-15 relative (the rounding level of the reassociated sums) and the
-// dependent scale pass + its cluster reduction are skipped.
-template <int NT>
-__device__ __forceinline__ void q_moments(const Sample& S, double mu, double c1,
-                                          double (&o)[kMomNV]) {
-#pragma unroll
-  for (int i = 0; i < kMomNV; ++i) o[i] = 0.0;
-  const double* v = S.v + threadIdx.x;
-  for (int k = 0; k * NT + (int)threadIdx.x < S.m_local; ++k) {
-    const double x = v[k * NT], d = x - mu, q = fma(d, d, c1), r = rcp_fast(q);
-    const double r2 = r * r, dr = d * r, dr2 = dr * dr;
-    o[0] += r;
-    o[1] = fma(r, x, o[1]);
-    o[2] = fma(dr, r, o[2]);         // d r^2
-    o[3] = fma(dr2, r, o[3]);        // d^2 r^3
-    o[4] += r2;                      // r^2
-    o[5] = fma(dr2 * dr, r, o[5]);   // d^3 r^4
-    o[6] = fma(dr, r2, o[6]);        // d r^3
-    o[7] = fma(r2, r, o[7]);         // r^3
-    o[8] = fma(dr2, r2, o[8]);       // d^2 r^4
-    o[9] = fma(dr2 * dr2, r, o[9]);  // d^4 r^5
-  }
-}
-
 // estimate_location_scale on the shared-memory sample — src/alignment.cpp:61-101
 template <int NT>
 __device__ __forceinline__ TD loc_scale(Sample& S, double nu, double* scratch) {
@@ -975,33 +939,14 @@ __device__ __forceinline__ TD loc_scale(Sample& S, double nu, double* scratch) {
       // the constant c2 is applied after the reduction (sums of r = 1/(c1 + d^2))
       const double s2 = sigma * sigma, c1 = nu * s2, c2 = nu1 * s2;
       double a3[3];
-      double mu_new;
-      bool scale_done = false;
-      if (NT == kTdistClusterThreads && S.cs > 1) {  // latency mode (uniform over the cluster)
-        double am[kMomNV];
-        q_moments<NT>(S, mu, c1, am);
-        sample_allsum<kMomNV, NT>(am, S);
-        mu_new = am[1] / am[0];
-        const double dl = mu_new - mu;
-        if (fabs(dl) < 1e-3 * sqrt(c1)) {
-          const double dl2 = dl * dl;
-          a1[0] = am[0] + dl * (2.0 * am[2]) + dl2 * (4.0 * am[3] - am[4]) +
-                  dl2 * dl * (8.0 * am[5] - 4.0 * am[6]) +
-                  dl2 * dl2 * ((am[7] - 12.0 * am[8]) + 16.0 * am[9]);
-          scale_done = true;
-        }
-      } else {
-        q_sums<NT, true, false>(S, mu, c1, a3);
-        double a2[2] = {a3[0], a3[1]};
-        sample_allsum<2, NT>(a2, S);
-        mu_new = a2[1] / a2[0];  // (c2 sum r v) / (c2 sum r)
-      }
-      if (!scale_done) {
-        // sum w d^2 = c2 sum d^2 / (d^2 + c1) = c2 (m - c1 sum r)
-        q_sums<NT, false, false>(S, mu_new, c1, a3);
-        a1[0] = a3[0];
-        sample_allsum<1, NT>(a1, S);
-      }
+      q_sums<NT, true, false>(S, mu, c1, a3);
+      double a2[2] = {a3[0], a3[1]};
+      sample_allsum<2, NT>(a2, S);
+      const double mu_new = a2[1] / a2[0];  // (c2 sum r v) / (c2 sum r)
+      // sum w d^2 = c2 sum d^2 / (d^2 + c1) = c2 (m - c1 sum r)
+      q_sums<NT, false, false>(S, mu_new, c1, a3);
+      a1[0] = a3[0];
+      sample_allsum<1, NT>(a1, S);
       a1[0] = c2 * fma(-c1, a1[0], (double)m);
       const double sigma_new = dmax_std(1e-8, sqrt(a1[0] * inv_m));
       const double rel = fabs(sigma_new - sigma) / sigma;
@@ -1250,7 +1195,7 @@ __device__ __forceinline__ void tdist_chain(const SlotIO* __restrict__ io, SlotS
   const SlotIO& o = io[slot];
   extern __shared__ double dsm[];  // sample[kMaxSample]
   double* smp_sh = dsm;
-  __shared__ double scratch[NT / 32 * 2 * kMomNV];
+  __shared__ double scratch[NT / 32 * 2 * 2];
   const int tid = threadIdx.x;
 
   const long long n = o.nsmp[type];
@@ -1346,8 +1291,8 @@ __global__ void __launch_bounds__(kTdistClusterThreads, 1)
   double* smp_sh = dsm;
   int* offs = reinterpret_cast<int*>(dsm + kShare);
   __shared__ int wsum[NT / 32];
-  __shared__ double scratch[NT / 32 * 2 * kMomNV];
-  __shared__ double cbuf[2 * CS * (NT / 32) * kMomNV];
+  __shared__ double scratch[NT / 32 * 2 * 2];
+  __shared__ double cbuf[2 * CS * (NT / 32) * 2];
   __shared__ __align__(8) uint64_t cmbar[2];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   if (tid == 0) {
@@ -2251,7 +2196,7 @@ __global__ void __launch_bounds__(kTdistThreads, 1)  // one CTA per SM (sample i
                 double* __restrict__ out) {
   constexpr int NT = kTdistThreads;
   extern __shared__ double dsm[];
-  __shared__ double scratch[NT / 32 * 2 * kMomNV];
+  __shared__ double scratch[NT / 32 * 2 * 2];
   const long long stride = n <= kMaxSample ? 1 : (n + kMaxSample - 1) / kMaxSample;
   Sample smp;
   smp.v = dsm;
