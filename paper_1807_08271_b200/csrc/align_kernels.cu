@@ -612,10 +612,13 @@ __device__ __forceinline__ void block_allsum(double (&v)[NV], double* scratch2, 
 #pragma unroll
     for (int i = 0; i < NV; ++i) scratch[wid * NV + i] = v[i];
   __syncthreads();
+  // lane l takes warp l % NW's partial (what a 5-round butterfly over zero-padded lanes
+  // holds after its rounds xor >= NW, which only add zeros), so log2(NW) rounds finish
+  // the same sum (the same additions in the same order, up to the sign of an exact zero)
 #pragma unroll
-  for (int i = 0; i < NV; ++i) v[i] = lane < NW ? scratch[lane * NV + i] : 0.0;
+  for (int i = 0; i < NV; ++i) v[i] = scratch[(lane % NW) * NV + i];
 #pragma unroll
-  for (int off = 16; off > 0; off >>= 1)
+  for (int off = NW / 2; off > 0; off >>= 1)
 #pragma unroll
     for (int i = 0; i < NV; ++i) v[i] += __shfl_xor_sync(0xffffffffu, v[i], off);
 }
