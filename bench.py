@@ -763,7 +763,7 @@ def main():
             dist.barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        e2e_steps = max(1, min(args.steps, 3))
+        e2e_steps = max(1, args.steps)  # streamed like the timed steps: pipeline fill amortised
         for k in range(e2e_steps):
             e2e_step(k)
         ctx.check(ctx.lib.rgbid_align_batch_host_wait(ctx.h), "align_batch_host_wait")
