@@ -745,7 +745,7 @@ def main():
         res = [(abi.AlignResult_t * n_local)() for _ in range(2)]
         cfg_c_, K_c_ = cfg.to_c(), K.to_c()
 
-        E2E_CHUNK = int(os.environ.get("RGBID_E2E_CHUNK", str(min(512, max(1, n_local // 2)))))
+        E2E_CHUNK = int(os.environ.get("RGBID_E2E_CHUNK", str(min(1024, max(1, n_local // 2)))))
 
         def e2e_step(k):
             # streaming form: step k's first uploads overlap step k-1's last chunks;
