@@ -200,3 +200,31 @@ def test_device_scene_equals_host_scene(ctx, K, variant):
             assert np.array_equal(np.isnan(g), np.isnan(h))
             m = ~np.isnan(h)
             assert np.abs(g[m] - h[m]).max() <= 1e-12
+
+
+def test_coscheduled_batch_with_failing_pairs(ctx, K, cfg, pairs, frames):
+    """A co-scheduled batch in which some pairs fail: an all-hole frame (no jets ->
+    DegenerateAlignmentError with a zero spectrum) and a noiseless pair (the reference's
+    own rank-deficiency throw at 4 levels).  Their statuses match the reference build and
+    every other pair is bit-identical to the same pair aligned in a clean batch."""
+    A, B = frames
+    hole = np.full((480, 640), np.nan)
+    IAc, WAc, IBc, WBc, _ = O.synth_pair_host(K.to_c(), 7, 0)  # clean: degenerate at 4 levels
+    bad = [(hole, hole, pairs[1][2], pairs[1][3]), (IAc, WAc, IBc, WBc)]
+    badA = [rg.DeviceFrame.from_frame(rg.FrameData(p[0], p[1]), ctx) for p in bad]
+    badB = [rg.DeviceFrame.from_frame(rg.FrameData(p[2], p[3]), ctx) for p in bad]
+    idx = list(range(20))
+    fa = [A[i] for i in idx]
+    fb = [B[i] for i in idx]
+    fa[3], fb[3] = badA[0], badB[0]
+    fa[14], fb[14] = badA[1], badB[1]
+    with _env(RGBID_BATCH_SLOTS=10):
+        res = rg.align_batch(fa, fb, K, config=cfg, ctx=ctx)
+    ref = O.Oracle("REF" if O.available("REF") else "C").align_many(
+        bad, K.to_c(), None, cfg.to_c(), threads=2)
+    assert res[3].status == ref[0].status == 1 and not any(res[3].spectrum[:])
+    assert res[14].status == ref[1].status
+    clean = _batch(ctx, K, cfg, A, B, idx, slots=20)
+    for i in idx:
+        if i not in (3, 14):
+            assert _key(res[i]) == _key(clean[i]), i
