@@ -1701,163 +1701,10 @@ __global__ void __launch_bounds__(kTPB, RGBID_K3_MMA_MINB) k_normal_eq_mma(const
   }
 }
 
-// K3 variant: lane pairs with FMA accumulation (RGBID_K3_PAIR).  Lanes 2j and 2j+1 both
-// compute the jets of pixel j and split the 28 products w x_a x_b (a >= b, x = (J, r))
-// by the row a: the even lane owns a in {0, 5, 6} (14 sums), the odd lane a in {1..4}
-// (14 sums) -- exactly the products a full 8x8 FP64 MMA spends 64 slots on, in 14
-// registers per lane.
-#ifndef RGBID_K3_PAIR
-#define RGBID_K3_PAIR 0
-#endif
-template <int A0, int A1, int A2, int A3>
-__device__ __forceinline__ void pair_accum(double (&acc)[14], const double (&x)[7], double w) {
-  int q = 0;
-  const int rows[4] = {A0, A1, A2, A3};
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int a = rows[i];
-    if (a < 0) continue;
-    const double wa = w * x[a];
-#pragma unroll
-    for (int b = 0; b <= a; ++b) {
-      acc[q] = fma(wa, x[b], acc[q]);
-      ++q;
-    }
-  }
-}
-
-__global__ void __launch_bounds__(kTPB, RGBID_K3_MMA_MINB) k_normal_eq_pair(const SlotIO* __restrict__ io,
-                                                         const SlotState* __restrict__ st,
-                                                         LevelInfo li, int phase,
-                                                         double lambda_n_min) {
-  const int slot = blockIdx.y;
-  const SlotState& S = st[slot];
-  if (!slot_active(S, li.level, phase)) return;  // uniform over the CTA
-  const SlotIO& o = io[slot];
-  const double* __restrict__ WA = phase ? o.fWA : o.WA[li.level];
-  const uint8_t* __restrict__ am = o.amask[li.level];
-  const double2* __restrict__ ag = reinterpret_cast<const double2*>(o.agrad[li.level]);
-  const double2* __restrict__ ibwp = o.ibw;
-  __shared__ double cst[kTPB / 32][2][14];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, odd = lane & 1;
-  const double muI = S.tI.mu, isgI = 1.0 / S.tI.sigma, nuI = dmax_std(S.tI.nu, S.tW.nu);
-  const double muW = S.tW.mu, isgW = 1.0 / S.tW.sigma, nuW = S.tW.nu;
-  const double nuI1 = nuI + 1.0, nuW1 = nuW + 1.0;
-  const double is2i = isgI * isgI, is2w = isgW * isgW;
-  const int w = li.w;
-  const double* Ki = li.Kinv;
-  const int N = li.w * li.h;
-  double acc[14];
-#pragma unroll
-  for (int i = 0; i < 14; ++i) acc[i] = 0.0;
-  // the CTA's 2048 pixels: 16 per warp and iteration (pixel = lane / 2)
-#pragma unroll 1
-  for (int p = 0; p < 2 * kPixK3; ++p) {
-    const int k0i = blockIdx.x * kPixK3 * kTPB + (p * (kTPB / 32) + wid) * 16 + (lane >> 1);
-    const bool inr = k0i < N;
-    const int k = inr ? k0i : 0;
-    const unsigned a = __ldg(am + k);
-    const double2 rw = __ldg(ibwp + k);  // {r_I = i_b - i_a, w_b} (K1)
-    const double r_I = rw.x, w_b = rw.y;
-    const double w_a = __ldg(WA + k);
-    const double2 gI = __ldg(ag + 2 * k), gW = __ldg(ag + 2 * k + 1);
-    const bool jet = inr && (a & 1u) && valid(r_I);  // bit0 implies valid(i_a)
-    const bool dep = jet && (a & 2u) && valid(w_b) && w_b > 0.0;
-    const int y = k / w, x = k - y * w;
-    const double px = x, py = y;
-    const double ax = li.cx - px, ay = li.cy - py;
-    const double iwa = rcp_fast(w_a);
-    const double k0 = red3(Ki[0] * px, Ki[1] * py, Ki[2]), k1 = red3(Ki[3] * px, Ki[4] * py, Ki[5]),
-                 k2 = red3(Ki[6] * px, Ki[7] * py, Ki[8]);
-    const double X0 = k0 * iwa, X1 = k1 * iwa, X2 = k2 * iwa;
-    {  // photometric row
-      const double s0 = w_a * gI.x, s1 = w_a * gI.y;
-      const double u0 = s0 * li.fx, u1 = s1 * li.fy, u2 = s0 * ax + s1 * ay;
-      const double xi_ = (r_I - muI) * isgI;
-      const double wi = jet ? nuI1 * rcp_fast(fma(xi_, xi_, nuI)) * is2i : 0.0;
-      const double xr[7] = {jet ? u0 : 0.0, jet ? u1 : 0.0, jet ? u2 : 0.0,
-                            jet ? X1 * u2 - X2 * u1 : 0.0, jet ? X2 * u0 - X0 * u2 : 0.0,
-                            jet ? X0 * u1 - X1 * u0 : 0.0, jet ? r_I : 0.0};
-      if (odd)
-        pair_accum<1, 2, 3, 4>(acc, xr, wi);
-      else
-        pair_accum<0, 5, 6, -1>(acc, xr, wi);
-    }
-    {  // geometric row
-      const double g0 = gW.x * li.fx, g1 = gW.y * li.fy, g2 = gW.x * ax + gW.y * ay;
-      const double s0 = w_a * g0, s1 = w_a * g1, s2 = w_a * (g2 + w_b);
-      double lambda = 1.0;
-      {
-        const double n0 = g0 * iwa, n1 = g1 * iwa, n2 = g2 * iwa + 1.0;
-        const double nn2 = n0 * n0 + n1 * n1 + n2 * n2;
-        if (!(nn2 < 1e-24)) {
-          const double rr2 = k0 * k0 + k1 * k1 + k2 * k2;
-          double c = (n0 * k0 + n1 * k1 + n2 * k2) * rsqrt(nn2 * rr2);
-          if (n2 < 0) c = -c;
-          lambda = dmax_std(lambda_n_min, c);
-        }
-      }
-      const double rW = w_b - w_a;
-      const double xw_ = (rW - muW) * isgW;
-      const double ww = dep ? lambda * nuW1 * rcp_fast(fma(xw_, xw_, nuW)) * is2w : 0.0;
-      const double xr[7] = {dep ? s0 : 0.0, dep ? s1 : 0.0, dep ? s2 : 0.0,
-                            dep ? X1 * s2 - X2 * s1 : 0.0, dep ? X2 * s0 - X0 * s2 : 0.0,
-                            dep ? X0 * s1 - X1 * s0 : 0.0, dep ? rW : 0.0};
-      if (odd)
-        pair_accum<1, 2, 3, 4>(acc, xr, ww);
-      else
-        pair_accum<0, 5, 6, -1>(acc, xr, ww);
-    }
-  }
-  // warp: sum the lanes of the same parity (xor 2, 4, 8, 16), then the warps in order
-#pragma unroll
-  for (int off = 2; off < 32; off <<= 1)
-#pragma unroll
-    for (int i = 0; i < 14; ++i) acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], off);
-  if (lane < 2)
-#pragma unroll
-    for (int i = 0; i < 14; ++i) cst[wid][lane][i] = acc[i];
-  __syncthreads();
-  if (threadIdx.x < kNPart) {  // partial q in k_normal_eq's order: lower H row-major, b, cost
-    const int q = threadIdx.x;
-    int r, c;
-    if (q < 21) {
-      r = 0;
-      while ((r + 1) * (r + 2) / 2 <= q) ++r;
-      c = q - r * (r + 1) / 2;
-    } else if (q < 27) {
-      r = 6;
-      c = q - 21;
-    } else {
-      r = 6;
-      c = 6;
-    }
-    // owner lane parity and slot of product (r, c): even lane rows {0, 5, 6}, odd {1..4}
-    int par, idx;
-    if (r == 0) {
-      par = 0, idx = 0;
-    } else if (r == 5) {
-      par = 0, idx = 1 + c;
-    } else if (r == 6) {
-      par = 0, idx = 7 + c;
-    } else {
-      par = 1, idx = (r * (r + 1)) / 2 - 1 + c;  // rows 1..4 from slot 0
-    }
-    double t = 0.0;
-#pragma unroll
-    for (int wv = 0; wv < kTPB / 32; ++wv) t += cst[wv][par][idx];
-    o.part[(size_t)blockIdx.x * kNPart + q] = t;
-  }
-}
-
 void launch_normal_equations(const AlignLaunch& a, const LevelInfo& li, int phase, cudaStream_t s) {
   KScope ks_(phase ? "normal_eq_cov" : kNeNames[li.level], s);
-  if (RGBID_K3_PAIR)
-    k_normal_eq_pair<<<dim3(li.ntiles3, a.nslots), kTPB, 0, s>>>(a.io, a.st, li, phase,
-                                                                 a.lambda_n_min);
-  else
-    k_normal_eq_mma<<<dim3(li.ntiles3, a.nslots), kTPB, 0, s>>>(a.io, a.st, li, phase,
-                                                                a.lambda_n_min);
+  k_normal_eq_mma<<<dim3(li.ntiles3, a.nslots), kTPB, 0, s>>>(a.io, a.st, li, phase,
+                                                              a.lambda_n_min);
 }
 
 // fixed-order reduction of the per-tile partials into H (full, mirrored), b, cost
