@@ -369,15 +369,20 @@ __global__ void __launch_bounds__(k1_threads<L>(), RGBID_K1_THREADS_PER_SM / k1_
 }
 
 // Level-0 K1: 128 threads per 256-pixel tile, two independent pixels per thread
-// (x and x + 128) so their dependent load chains (W_A -> gathers) overlap.
+// (x and x + 128) so their dependent load chains (W_A -> gathers) overlap; a CTA
+// takes the same segment of RGBID_K1L0_ROWS consecutive rows (one tile per 128
+// threads), so the per-CTA setup -- slot check, warp matrices, barriers -- is shared.
 #ifndef RGBID_K1L0_MINB
 #define RGBID_K1L0_MINB 12
 #endif
-__global__ void __launch_bounds__(128, RGBID_K1L0_MINB) k_warp_residuals_l0(const SlotIO* __restrict__ io,
-                                                                const SlotState* __restrict__ st,
-                                                                LevelInfo li, int w0, int h0,
-                                                                int phase) {
-  const int slot = blockIdx.z;  // grid (segment, row, slot): no tile-index division
+#ifndef RGBID_K1L0_ROWS
+#define RGBID_K1L0_ROWS 1
+#endif
+constexpr int kK1L0Rows = RGBID_K1L0_ROWS;
+__global__ void __launch_bounds__(128 * kK1L0Rows, RGBID_K1L0_MINB / kK1L0Rows)
+    k_warp_residuals_l0(const SlotIO* __restrict__ io, const SlotState* __restrict__ st,
+                        LevelInfo li, int w0, int h0, int phase) {
+  const int slot = blockIdx.z;  // grid (segment, row group, slot): no tile-index division
   const SlotState& S = st[slot];
   if (!slot_active(S, 0, phase)) return;
   __shared__ WarpMats wm;
@@ -387,11 +392,11 @@ __global__ void __launch_bounds__(128, RGBID_K1L0_MINB) k_warp_residuals_l0(cons
   const double* __restrict__ WAw = phase ? o.fWA : o.WA[0];
   const double* __restrict__ IA0 = phase ? o.fIA : o.IA[0];
   const uint8_t* __restrict__ am = o.amask[0];
-  const int tid = threadIdx.x;
-  const int seg = blockIdx.x, yl = blockIdx.y;
+  const int half = threadIdx.x >> 7, tid = threadIdx.x & 127;
+  const int seg = blockIdx.x, yl = blockIdx.y * kK1L0Rows + half;
   const int tile = yl * li.nseg + seg;
   const int xl0 = seg * li.tx;
-  const int nx = min(li.tx, li.w - xl0);
+  const int nx = yl < li.h ? min(li.tx, li.w - xl0) : 0;
   // the pixels' A-side values in flight while the warp matrices arrive
   double wa[2], iav[2];
   unsigned amv[2];
@@ -421,26 +426,26 @@ __global__ void __launch_bounds__(128, RGBID_K1L0_MINB) k_warp_residuals_l0(cons
       dep[q] = jet[q] && (a & 2u) && valid(wb) && wb > 0.0;
     }
   }
-  __shared__ int wcnt[2][8];
+  __shared__ int wcnt[kK1L0Rows][2][8];
   const int lane = tid & 31, wid = tid >> 5;
 #pragma unroll
   for (int q = 0; q < 2; ++q) {
     const unsigned bj = __ballot_sync(0xffffffffu, jet[q]), bd = __ballot_sync(0xffffffffu, dep[q]);
-    if (lane == 0) {
+    if (lane == 0 && yl < li.h) {
       const int word = wid + 4 * q;  // pixels [32 word, 32 word + 32) of the tile
-      wcnt[0][word] = __popc(bj);
-      wcnt[1][word] = __popc(bd);
+      wcnt[half][0][word] = __popc(bj);
+      wcnt[half][1][word] = __popc(bd);
       o.bitsI[tile * kWordsPerTile + word] = bj;
       o.bitsW[tile * kWordsPerTile + word] = bd;
     }
   }
   __syncthreads();
-  if (tid == 0) {
+  if (tid == 0 && yl < li.h) {
     int tI = 0, tW = 0;
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
-      tI += wcnt[0][k];
-      tW += wcnt[1][k];
+      tI += wcnt[half][0][k];
+      tW += wcnt[half][1][k];
     }
     o.cntI[tile] = tI;
     o.cntW[tile] = tW;
@@ -574,7 +579,10 @@ void launch_warp_residuals(const AlignLaunch& a, const LevelInfo& li, int phase,
   KScope ks_(kLevelNames[phase ? 1 : 0][li.level], s);
   dim3 grid(li.nseg, li.h, a.nslots);  // tile = row * nseg + segment
   switch (li.level) {
-    case 0: k_warp_residuals_l0<<<grid, 128, 0, s>>>(a.io, a.st, li, a.w0, a.h0, phase); break;
+    case 0:
+      k_warp_residuals_l0<<<dim3(li.nseg, (li.h + kK1L0Rows - 1) / kK1L0Rows, a.nslots),
+                            128 * kK1L0Rows, 0, s>>>(a.io, a.st, li, a.w0, a.h0, phase);
+      break;
     case 1: k_warp_residuals<1><<<grid, k1_threads<1>(), 0, s>>>(a.io, a.st, li, a.w0, a.h0, phase); break;
     case 2: k_warp_residuals<2><<<grid, k1_threads<2>(), 0, s>>>(a.io, a.st, li, a.w0, a.h0, phase); break;
     case 3: k_warp_residuals<3><<<grid, k1_threads<3>(), 0, s>>>(a.io, a.st, li, a.w0, a.h0, phase); break;
