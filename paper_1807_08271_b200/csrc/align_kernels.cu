@@ -376,7 +376,7 @@ __global__ void __launch_bounds__(k1_threads<L>(), RGBID_K1_THREADS_PER_SM / k1_
 #define RGBID_K1L0_MINB 12
 #endif
 #ifndef RGBID_K1L0_ROWS
-#define RGBID_K1L0_ROWS 1
+#define RGBID_K1L0_ROWS 1  // 2 and 4 rows per CTA measured 2.5% / 14% slower per launch
 #endif
 constexpr int kK1L0Rows = RGBID_K1L0_ROWS;
 __global__ void __launch_bounds__(128 * kK1L0Rows, RGBID_K1L0_MINB / kK1L0Rows)
