@@ -228,3 +228,31 @@ def test_coscheduled_batch_with_failing_pairs(ctx, K, cfg, pairs, frames):
     for i in idx:
         if i not in (3, 14):
             assert _key(res[i]) == _key(clean[i]), i
+
+
+@pytest.mark.parametrize("size,levels", [((333, 251, 250.0), 3), ((160, 120, 120.0), 1),
+                                         ((320, 240, 240.0), 5), ((640, 480, 480.0), 6)])
+def test_coscheduled_ragged_sizes_and_level_counts(ctx, size, levels):
+    """Ragged image sizes and 1-6 pyramid levels through co-scheduled chunk pairs
+    (9-slot chunks: the batch Student-t kernels), against the oracle per pair."""
+    Kr = rg.simple_intrinsics(*size)
+    n = 18
+    ps = [O.synth_pair_host(Kr.to_c(), 100 + i, 1 + (i & 1))[:4] for i in range(n)]
+    A = [rg.DeviceFrame.from_frame(rg.FrameData(p[0], p[1]), ctx) for p in ps]
+    B = [rg.DeviceFrame.from_frame(rg.FrameData(p[2], p[3]), ctx) for p in ps]
+    c = rg.AlignmentConfig(levels=levels)
+    with _env(RGBID_BATCH_SLOTS=9):
+        res = rg.align_batch(A, B, Kr, config=c, ctx=ctx)
+    ref = O.Oracle("C").align_many(ps, Kr.to_c(), None, c.to_c(), threads=os.cpu_count() or 1)
+    n_ok = 0
+    for g, o in zip(res, ref):
+        assert g.status == o.status
+        if o.status != 0:
+            continue
+        n_ok += 1
+        Tg, To = rg.Pose.from_c(g.T_AB), rg.Pose.from_c(o.T_AB)
+        assert np.abs(Tg.t - To.t).max() < 1e-5
+        assert np.linalg.norm(rg.so3_log(Tg.R @ To.R.T)) < 1e-5
+        assert [g.level_log[k].iterations for k in range(levels)] == \
+            [o.level_log[k].iterations for k in range(levels)]
+    assert n_ok >= n // 2
