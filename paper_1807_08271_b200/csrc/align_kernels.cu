@@ -826,6 +826,10 @@ struct LogProd {
 #define RGBID_QBODY 4
 #endif
 constexpr int kQBody = RGBID_QBODY;  // samples per fraction
+#ifndef RGBID_QUNROLL
+#define RGBID_QUNROLL 2
+#endif
+constexpr int kQUnroll = RGBID_QUNROLL;  // bodies per loop trip
 
 // sum_i 1/q_i = N/D (and sum_i x_i/q_i = NV/D) over BW samples, pairwise tree
 template <int BW, bool WV>
@@ -887,6 +891,7 @@ __device__ __forceinline__ void q_sums(const Sample& S, double mu, double c1, do
   LogProd P;
   bool bad = false;
   int k = 0;
+#pragma unroll kQUnroll
   for (; k + BW - 1 < S.kfull; k += BW)  // branch-free bodies
     q_body<NT, BW, WV, WL, false>(S, v, k, mu, c1, sr, sv, P, bad);
   const int kend = (S.m_local + NT - 1) / NT;
@@ -1010,24 +1015,66 @@ __device__ __forceinline__ double stationarity(Sample& S, double mu, double sigm
   return ((C + log(c2)) - a[0] * inv_m) - c2 * (a[1] * inv_m);
 }
 
-// solve_nu — src/alignment.cpp:131-157
+// solve_nu — src/alignment.cpp:131-157.  The reference's 30 bisection steps on
+// [2, 10] only ever evaluate f on the grid nu_k = 2 + k 2^-27 (k in [0, 2^30], every
+// value exact in fp64) and end in the cell [nu_k, nu_k+1] whose ends satisfy
+// f(lo) f(nu_k) > 0 and f(lo) f(nu_k+1) <= 0 (the same test, zeros and NaNs included);
+// they return its midpoint.  For a stationarity with one sign change over the grid
+// (the ML condition of the Student-t dof is monotone) that cell is unique, so any
+// search over the grid that closes it returns the same nu: here regula falsi on the
+// grid index, Illinois-weighted, falling back to a bisection step whenever the bracket
+// did not halve twice in a row.  ~8-10 stationarity passes instead of 32.
+// RGBID_NU_BISECT=1 builds the reference's plain bisection (for A/B).
+#ifndef RGBID_NU_BISECT
+#define RGBID_NU_BISECT 0
+#endif
 template <int NT>
 __device__ __forceinline__ double solve_nu(Sample& S, double mu, double sigma, double* scratch) {
-  double lo = 2.0, hi = 10.0;
-  double flo = stationarity<NT>(S, mu, sigma, lo, scratch);
-  const double fhi = stationarity<NT>(S, mu, sigma, hi, scratch);
-  if (flo * fhi > 0.0) return fhi > 0.0 ? hi : lo;
-  for (int it = 0; it < 30; ++it) {
-    const double mid = 0.5 * (lo + hi);
-    const double fmid = stationarity<NT>(S, mu, sigma, mid, scratch);
-    if (flo * fmid <= 0.0) {
-      hi = mid;
+  const double flo0 = stationarity<NT>(S, mu, sigma, 2.0, scratch);
+  const double fhi0 = stationarity<NT>(S, mu, sigma, 10.0, scratch);
+  if (flo0 * fhi0 > 0.0) return fhi0 > 0.0 ? 10.0 : 2.0;
+  constexpr double h = 0x1p-27;  // (10 - 2) / 2^30
+  int klo = 0, khi = 1 << 30;
+  double flo = flo0;
+  // bisect: the reference's steps verbatim (A/B builds, and after any NaN: the
+  // bisection's path through NaNs depends on where it meets them)
+  bool bisect = RGBID_NU_BISECT || isnan(flo0) || isnan(fhi0);
+  double gl = flo0, gh = fhi0;  // interpolation values (Illinois-scaled)
+  int last = 0, slow = 0;       // side retained last (-1 lo, +1 hi); steps without halving
+  while (khi - klo > 1) {
+    const int width = khi - klo;
+    int k;
+    const double t = gl / (gl - gh);
+    if (bisect || slow >= 2 || !(t >= 0.0 && t <= 1.0)) {  // also NaN / inf values
+      k = klo + (width >> 1);
+      slow = 0;
     } else {
-      lo = mid;
-      flo = fmid;
+      const double ke = (double)klo + t * (double)width;
+      k = (int)fmin(fmax(rint(ke), (double)(klo + 1)), (double)(khi - 1));
     }
+    const double fk = stationarity<NT>(S, mu, sigma, 2.0 + (double)k * h, scratch);
+    if (!bisect && isnan(fk)) {  // restart as the plain bisection
+      bisect = true;
+      klo = 0;
+      khi = 1 << 30;
+      flo = flo0;
+      continue;
+    }
+    if (flo * fk <= 0.0) {  // the reference's test (src/alignment.cpp:147)
+      khi = k;
+      gh = fk;
+      if (last == -1) gl *= 0.5;  // lo retained twice: Illinois
+      last = -1;
+    } else {
+      klo = k;
+      flo = fk;
+      gl = fk;
+      if (last == 1) gh *= 0.5;
+      last = 1;
+    }
+    slow = 2 * (khi - klo) > width ? slow + 1 : 0;
   }
-  return 0.5 * (lo + hi);
+  return 2.0 + (double)(klo + khi) * (0.5 * h);  // 0.5 (lo + hi), exact
 }
 
 // estimate_nu — src/alignment.cpp:109-127

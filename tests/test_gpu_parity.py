@@ -593,3 +593,31 @@ def test_student_t_stress_samples(ctx, orc, case):
         assert g.sigma == pytest.approx(o[1], rel=1e-6)
     mu, s, _ = orc.estimate_location_scale(r, 5.0)
     assert rg.estimate_nu(r, mu, s, ctx) == pytest.approx(orc.estimate_nu(r, mu, s), rel=1e-6)
+
+
+def test_solve_nu_grid_search_matches_bisection(ctx, orc):
+    """solve_nu (src/alignment.cpp:131-157): the reference bisects [2, 10] 30 times, so
+    its nu is the midpoint of the grid cell [2 + k 2^-27, 2 + (k+1) 2^-27] where the
+    stationarity changes sign.  The device finds that cell by regula falsi on the grid
+    index (~10 passes instead of 32): same nu unless the root sits within rounding
+    noise of a grid point.  200 samples of varied shape, size and tail weight, most
+    with an interior root (the full search), against the oracle's bisection."""
+    rng = np.random.default_rng(2024)
+    exact, interior, worst = 0, 0, 0.0
+    cases = 200
+    for i in range(cases):
+        n = int(rng.choice([40, 700, 5000, 19200, 45000]))
+        nu_true = float(rng.uniform(1.5, 14.0))
+        scale = float(10.0 ** rng.uniform(-4, 0))
+        r = float(rng.normal(0, 0.1)) + scale * rng.standard_t(nu_true, size=n)
+        if i % 5 == 0:  # contamination: a broad outlier component
+            k = max(1, n // 10)
+            r[rng.choice(n, size=k, replace=False)] = rng.normal(0, 30 * scale, size=k)
+        mu, s, _ = orc.estimate_location_scale(r, 5.0)
+        g, o = rg.estimate_nu(r, mu, s, ctx), orc.estimate_nu(r, mu, s)
+        exact += g == o
+        interior += 2.0 < o < 10.0
+        worst = max(worst, abs(g - o))
+    assert interior >= cases // 2, interior
+    assert worst <= 1e-6, worst
+    assert exact >= int(0.9 * cases), f"{exact} of {cases} bit-identical"

@@ -28,12 +28,13 @@ ui = h.index("Metric Unit")
 scale = {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "ns": 1e-6, "us": 1e-3, "ms": 1.0}
 agg = collections.defaultdict(lambda: [0, 0.0])
 for r in rows[1:]:
-    if not any(t in r[gi] for t in ("512", "1024")):
+    if r[ki].startswith(("k_render", "void k_render")):  # the input synthesis
         continue
     k = (r[ki].split("(")[0][:40], r[gi])
     agg[k][0] += 1
     agg[k][1] += float(r[vi].replace(",", "")) * scale.get(r[ui], 1e-6)
-for (k, g), (n, ms) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
+print(f"   total {sum(ms for _, ms in agg.values()):.3f} ms")
+for (k, g), (n, ms) in sorted(agg.items(), key=lambda kv: -kv[1][1])[:12]:
     print(f"   {k:42s} {g:16s} {n:4d} {ms:9.3f} ms  {ms / n * 1e3:9.1f} us/launch")
 PY
 done
