@@ -62,6 +62,63 @@ KScope::~KScope() {
 
 __device__ __forceinline__ bool valid(double v) { return isfinite(v); }
 
+// ---------------------------------------------------------------------------
+// Active-slot lists.  A converged slot (done_level == level) or a failed one
+// skips the rest of the level, but its CTAs in the remaining launches of the
+// graph would still be scheduled and exit: ~77 ns per CTA per SM whatever they do
+// (tools/micro/empty_ctas.cu), i.e. 0.77 ms for the 1.47M CTAs of a 1024-slot
+// level-0 K1 even when only 17 slots are left (bench level-0 iteration 10).
+// k_active_slots compacts the slots still iterating, in slot order, before each
+// K1, and picks the body of the iteration's K1 and K3 graph switch nodes: the
+// same kernel over ceil(nslots / 2^k) slot rows, the smallest that covers the
+// list (row j works on list entry j; rows past the count exit).
+__device__ __forceinline__ int active_slot(const int* act, int j) {
+  return act ? (j < act[0] ? act[1 + j] : -1) : j;
+}
+
+__global__ void __launch_bounds__(1024) k_active_slots(const SlotState* __restrict__ st, int nslots,
+                                                       int level, int phase, int* __restrict__ act,
+                                                       cudaGraphConditionalHandle h0,
+                                                       cudaGraphConditionalHandle h1, int nbodies) {
+  __shared__ int wsum[32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int base = 0;
+  for (int s0 = 0; s0 < nslots; s0 += 1024) {
+    const int s = s0 + (int)threadIdx.x;
+    const bool on = s < nslots && slot_active(st[s], level, phase);
+    const unsigned b = __ballot_sync(0xffffffffu, on);
+    if (lane == 0) wsum[wid] = __popc(b);
+    __syncthreads();
+    int before = 0, total = 0;
+    for (int k = 0; k < 32; ++k) {
+      before += k < wid ? wsum[k] : 0;
+      total += wsum[k];
+    }
+    if (on) act[1 + base + before + __popc(b & ((1u << lane) - 1u))] = s;
+    base += total;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    act[0] = base;
+    if (nbodies > 0) {  // body k: ceil(nslots / 2^k) rows; none for an empty list
+      int k = 0;
+      while (k + 1 < nbodies && ((nslots + (2 << k) - 1) >> (k + 1)) >= base) ++k;
+      const unsigned v = base == 0 ? (unsigned)nbodies : (unsigned)k;
+      cudaGraphSetConditional(h0, v);
+      cudaGraphSetConditional(h1, v);
+    }
+  }
+}
+
+void launch_active_slots(const AlignLaunch& a, int level, int phase, cudaStream_t s,
+                         const SlotSwitch* sw) {
+  if (!a.act) return;
+  KScope ks_("active_slots", s);
+  k_active_slots<<<1, 1024, 0, s>>>(a.st, a.nslots, level, phase, a.act, sw ? sw->h[0] : 0,
+                                    sw ? sw->h[1] : 0, sw ? sw->nbodies : 0);
+}
+
+
 // Correctly rounded a / b from r = RN(1/b) (Markstein): q = RN(a r),
 // e = a - b q (exact with FMA), RN(q + e r) == RN(a / b) for normal operands.
 // Used where several quotients share a divisor; bit-identity with IEEE division
@@ -260,9 +317,12 @@ template <int L>
 #endif
 __global__ void __launch_bounds__(k1_threads<L>(), RGBID_K1_THREADS_PER_SM / k1_threads<L>()) k_warp_residuals(const SlotIO* __restrict__ io,
                                                            const SlotState* __restrict__ st,
-                                                           LevelInfo li, int w0, int h0, int phase) {
+                                                           LevelInfo li, int w0, int h0, int phase,
+                                                           const int* __restrict__ act) {
   static_assert(L >= 1, "level 0 uses k_warp_residuals_l0");
-  const int slot = blockIdx.z;  // grid (segment, level row, slot): no tile-index division
+  // grid (segment, level row, slot row): no tile-index division
+  const int slot = active_slot(act, blockIdx.z);
+  if (slot < 0) return;
   const SlotState& S = st[slot];
   if (!slot_active(S, L, phase)) return;
   __shared__ WarpMats wm;
@@ -381,8 +441,10 @@ __global__ void __launch_bounds__(k1_threads<L>(), RGBID_K1_THREADS_PER_SM / k1_
 constexpr int kK1L0Rows = RGBID_K1L0_ROWS;
 __global__ void __launch_bounds__(128 * kK1L0Rows, RGBID_K1L0_MINB / kK1L0Rows)
     k_warp_residuals_l0(const SlotIO* __restrict__ io, const SlotState* __restrict__ st,
-                        LevelInfo li, int w0, int h0, int phase) {
-  const int slot = blockIdx.z;  // grid (segment, row group, slot): no tile-index division
+                        LevelInfo li, int w0, int h0, int phase, const int* __restrict__ act) {
+  // grid (segment, row group, slot row): no tile-index division
+  const int slot = active_slot(act, blockIdx.z);
+  if (slot < 0) return;
   const SlotState& S = st[slot];
   if (!slot_active(S, 0, phase)) return;
   __shared__ WarpMats wm;
@@ -575,19 +637,22 @@ static const char* kLevelNames[2][kMaxLevels] = {
     {"warp_residuals_cov", "warp_residuals_cov", "warp_residuals_cov", "warp_residuals_cov",
      "warp_residuals_cov", "warp_residuals_cov"}};
 
-void launch_warp_residuals(const AlignLaunch& a, const LevelInfo& li, int phase, cudaStream_t s) {
+void launch_warp_residuals(const AlignLaunch& a, const LevelInfo& li, int phase, cudaStream_t s,
+                           int rows) {
   KScope ks_(kLevelNames[phase ? 1 : 0][li.level], s);
-  dim3 grid(li.nseg, li.h, a.nslots);  // tile = row * nseg + segment
+  const int rows0 = (li.h + kK1L0Rows - 1) / kK1L0Rows;
+  dim3 grid(li.nseg, li.h, rows > 0 ? rows : a.nslots);  // tile = row * nseg + segment
+  const int* act = a.act;
   switch (li.level) {
     case 0:
-      k_warp_residuals_l0<<<dim3(li.nseg, (li.h + kK1L0Rows - 1) / kK1L0Rows, a.nslots),
-                            128 * kK1L0Rows, 0, s>>>(a.io, a.st, li, a.w0, a.h0, phase);
+      k_warp_residuals_l0<<<dim3(li.nseg, rows0, grid.z), 128 * kK1L0Rows, 0, s>>>(
+          a.io, a.st, li, a.w0, a.h0, phase, act);
       break;
-    case 1: k_warp_residuals<1><<<grid, k1_threads<1>(), 0, s>>>(a.io, a.st, li, a.w0, a.h0, phase); break;
-    case 2: k_warp_residuals<2><<<grid, k1_threads<2>(), 0, s>>>(a.io, a.st, li, a.w0, a.h0, phase); break;
-    case 3: k_warp_residuals<3><<<grid, k1_threads<3>(), 0, s>>>(a.io, a.st, li, a.w0, a.h0, phase); break;
-    case 4: k_warp_residuals<4><<<grid, k1_threads<4>(), 0, s>>>(a.io, a.st, li, a.w0, a.h0, phase); break;
-    case 5: k_warp_residuals<5><<<grid, k1_threads<5>(), 0, s>>>(a.io, a.st, li, a.w0, a.h0, phase); break;
+    case 1: k_warp_residuals<1><<<grid, k1_threads<1>(), 0, s>>>(a.io, a.st, li, a.w0, a.h0, phase, act); break;
+    case 2: k_warp_residuals<2><<<grid, k1_threads<2>(), 0, s>>>(a.io, a.st, li, a.w0, a.h0, phase, act); break;
+    case 3: k_warp_residuals<3><<<grid, k1_threads<3>(), 0, s>>>(a.io, a.st, li, a.w0, a.h0, phase, act); break;
+    case 4: k_warp_residuals<4><<<grid, k1_threads<4>(), 0, s>>>(a.io, a.st, li, a.w0, a.h0, phase, act); break;
+    case 5: k_warp_residuals<5><<<grid, k1_threads<5>(), 0, s>>>(a.io, a.st, li, a.w0, a.h0, phase, act); break;
     default: return;
   }
 }
@@ -1646,8 +1711,10 @@ __device__ __forceinline__ void stage_row(double* r, bool ok, double j0, double 
 __global__ void __launch_bounds__(kTPB, RGBID_K3_MMA_MINB) k_normal_eq_mma(const SlotIO* __restrict__ io,
                                                         const SlotState* __restrict__ st,
                                                         LevelInfo li, int phase,
-                                                        double lambda_n_min) {
-  const int slot = blockIdx.y;
+                                                        double lambda_n_min,
+                                                        const int* __restrict__ act) {
+  const int slot = active_slot(act, blockIdx.y);
+  if (slot < 0) return;
   const SlotState& S = st[slot];
   if (!slot_active(S, li.level, phase)) return;  // uniform over the CTA
   const SlotIO& o = io[slot];
@@ -1756,10 +1823,11 @@ __global__ void __launch_bounds__(kTPB, RGBID_K3_MMA_MINB) k_normal_eq_mma(const
   }
 }
 
-void launch_normal_equations(const AlignLaunch& a, const LevelInfo& li, int phase, cudaStream_t s) {
+void launch_normal_equations(const AlignLaunch& a, const LevelInfo& li, int phase, cudaStream_t s,
+                             int rows) {
   KScope ks_(phase ? "normal_eq_cov" : kNeNames[li.level], s);
-  k_normal_eq_mma<<<dim3(li.ntiles3, a.nslots), kTPB, 0, s>>>(a.io, a.st, li, phase,
-                                                              a.lambda_n_min);
+  k_normal_eq_mma<<<dim3(li.ntiles3, rows > 0 ? rows : a.nslots), kTPB, 0, s>>>(
+      a.io, a.st, li, phase, a.lambda_n_min, a.act);
 }
 
 // fixed-order reduction of the per-tile partials into H (full, mirrored), b, cost

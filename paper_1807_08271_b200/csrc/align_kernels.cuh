@@ -110,15 +110,35 @@ struct AlignLaunch {
   int w0, h0;
   double eps;
   double lambda_n_min;
+  // device [1 + nslots]: count, then the slots still iterating in slot order
+  // (k_active_slots, before each K1); nullptr = every CTA row maps one slot
+  int* act = nullptr;
+  bool graph_switch = true;  // captured graphs pick K1 / K3 grids by switch nodes
 };
 
+// Batches above this size run K1 / K3 over a compact active-slot list, their grids
+// picked per iteration on the device by graph switch nodes (k_active_slots).
+constexpr int kActiveListMinSlots = 16;
+inline bool use_active_list(int nslots) { return nslots > kActiveListMinSlots; }
+struct SlotSwitch {
+  cudaGraphConditionalHandle h[2] = {0, 0};  // the iteration's K1 and K3 switch nodes
+  int nbodies = 0;                           // body k: ceil(nslots / 2^k) slot rows
+};
+// compaction of the slots still active at (level, phase) into a.act, setting the
+// switch values of *sw (no-op without a list)
+void launch_active_slots(const AlignLaunch& a, int level, int phase, cudaStream_t s,
+                         const SlotSwitch* sw);
+
 // Kernel launchers (align_kernels.cu); all asynchronous on `stream`.
-void launch_warp_residuals(const AlignLaunch& a, const LevelInfo& li, int phase, cudaStream_t s);
+// rows: slot rows of the grid (0 = one per slot)
+void launch_warp_residuals(const AlignLaunch& a, const LevelInfo& li, int phase, cudaStream_t s,
+                           int rows = 0);
 // K2: part 0 = gather + Student-t, 1 = gather only (K2a), 2 = Student-t only (K2b);
 // latency mode (<= kTdistClusterMaxSlots slots) has no separate gather
 void launch_tdist(const AlignLaunch& a, const LevelInfo& li, int phase, cudaStream_t s,
                   int part = 0);
-void launch_normal_equations(const AlignLaunch& a, const LevelInfo& li, int phase, cudaStream_t s);
+void launch_normal_equations(const AlignLaunch& a, const LevelInfo& li, int phase, cudaStream_t s,
+                             int rows = 0);
 void launch_solve(const AlignLaunch& a, const LevelInfo& li, const LevelInfo& li0, cudaStream_t s);
 void launch_covariance(const AlignLaunch& a, const LevelInfo& li, cudaStream_t s);
 void launch_downsample2(const double* I, const double* W, int w, int h, double* oI, double* oW,

@@ -15,6 +15,7 @@
 #include <cstring>
 #include <functional>
 #include <map>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -62,6 +63,7 @@ struct Lane {
   uint8_t* ws_u8 = nullptr;
   SlotIO* d_io = nullptr;
   SlotState* d_st = nullptr;
+  int* d_act = nullptr;  // active-slot list [1 + slots] (k_active_slots)
   std::vector<SlotIO> h_io;
   SlotState* h_st_pinned = nullptr;
   std::map<std::string, CachedGraph> graphs;
@@ -87,6 +89,7 @@ struct rgbid_ctx {
   rgbid_iter_trace* d_trace = nullptr;
   std::vector<rgbid_iter_trace> last_trace;
   bool use_graphs = true;
+  bool graph_switch = true;  // K1 / K3 slot rows chosen by graph switch nodes
   std::vector<cudaEvent_t> pair_events;  // stage events of co-scheduled chunk pairs
   // scratch device buffers for the one-shot host APIs
   std::map<std::string, std::pair<void*, size_t>> scratch;
@@ -284,12 +287,14 @@ void free_lane_ws(Lane& L) {
   if (L.ws_u8) cudaFree(L.ws_u8);
   if (L.d_io) cudaFree(L.d_io);
   if (L.d_st) cudaFree(L.d_st);
+  if (L.d_act) cudaFree(L.d_act);
   if (L.h_st_pinned) cudaFreeHost(L.h_st_pinned);
   L.ws_f64 = nullptr;
   L.ws_i32 = nullptr;
   L.ws_u8 = nullptr;
   L.d_io = nullptr;
   L.d_st = nullptr;
+  L.d_act = nullptr;
   L.h_st_pinned = nullptr;
   L.cap_slots = 0;
 }
@@ -317,6 +322,7 @@ int ensure_workspace(rgbid_ctx* ctx, Lane& L, int nslots, int w, int h) {
   CK(cudaMalloc(&L.ws_u8, slot_u8(w, h) * nslots));
   CK(cudaMalloc(&L.d_io, sizeof(SlotIO) * nslots));
   CK(cudaMalloc(&L.d_st, sizeof(SlotState) * nslots));
+  CK(cudaMalloc(&L.d_act, sizeof(int) * (nslots + 1)));
   CK(cudaMallocHost(&L.h_st_pinned, sizeof(SlotState) * nslots));
   if (!ctx->d_trace) CK(cudaMalloc(&ctx->d_trace, sizeof(rgbid_iter_trace) * kTraceMax));
   L.cap_slots = nslots;
@@ -407,6 +413,71 @@ int validate_cfg(const rgbid_align_config& c, int w, int h) {
   return RGBID_OK;
 }
 
+// Graph switch nodes for the slot-row count of K1 / K3 (k_active_slots picks the
+// body per iteration on the device).  Outside a stream capture (direct launches,
+// profiling) the kernels run one row per slot over the same list.
+int switch_bodies(int nslots) {  // bodies k = 0.. with ceil(nslots / 2^k) >= 8 rows
+  int nb = 1;
+  while (nb < 8 && ((nslots + (1 << nb) - 1) >> nb) >= 8) ++nb;
+  return nb;
+}
+
+void switch_begin(cudaStream_t s, const AlignLaunch& a, SlotSwitch& sw) {
+  sw = SlotSwitch{};
+  if (!a.act || !a.graph_switch) return;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaGraph_t g = nullptr;
+  if (cudaStreamGetCaptureInfo(s, &cs, nullptr, &g, nullptr, nullptr) != cudaSuccess ||
+      cs != cudaStreamCaptureStatusActive)
+    return;
+  for (auto& h : sw.h)  // default body 0 (the full grid)
+    if (cudaGraphConditionalHandleCreate(&h, g, 0u, cudaGraphCondAssignDefault) != cudaSuccess)
+      return;
+  sw.nbodies = switch_bodies(a.nslots);
+}
+
+// launch(stream, rows) as switch node `idx` of sw in the capture on s, one body per
+// row count; a plain launch over all slots when not capturing
+void launch_switched(cudaStream_t s, const AlignLaunch& a, const SlotSwitch& sw, int idx,
+                     const std::function<void(cudaStream_t, int)>& launch) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaGraph_t g = nullptr;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t nd = 0;
+  if (sw.nbodies == 0 || cudaStreamGetCaptureInfo(s, &cs, nullptr, &g, &deps, &nd) != cudaSuccess ||
+      cs != cudaStreamCaptureStatusActive) {
+    launch(s, 0);
+    return;
+  }
+  cudaGraphNodeParams cp = {};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = sw.h[idx];
+  cp.conditional.type = cudaGraphCondTypeSwitch;
+  cp.conditional.size = (unsigned)sw.nbodies;
+  cudaGraphNode_t node;
+  std::vector<cudaGraphNode_t> dv(deps, deps + nd);
+  if (cudaGraphAddNode(&node, g, dv.empty() ? nullptr : dv.data(), dv.size(), &cp) != cudaSuccess) {
+    launch(s, 0);
+    return;
+  }
+  static thread_local std::map<int, cudaStream_t> scratch;  // body captures, per device
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaStream_t& t = scratch[dev];
+  if (!t) cudaStreamCreateWithFlags(&t, cudaStreamNonBlocking);
+  long long* cnt = g_launch_counter;
+  const long long c0 = cnt ? *cnt : 0;
+  for (int k = 0; k < sw.nbodies; ++k) {
+    cudaStreamBeginCaptureToGraph(t, cp.conditional.phGraph_out[k], nullptr, nullptr, 0,
+                                  cudaStreamCaptureModeThreadLocal);
+    launch(t, (a.nslots + (1 << k) - 1) >> k);
+    cudaGraph_t body;
+    cudaStreamEndCapture(t, &body);
+  }
+  if (cnt) *cnt = c0 + 1;  // one body runs per graph launch
+  cudaStreamUpdateCaptureDependencies(s, &node, 1, cudaStreamSetCaptureDependencies);
+}
+
 // The whole align (all levels + covariance pass) as a list of stages; a stage
 // is one or more dependent kernel launches on one stream.  Stages cycle
 // K1 | K2 | K3+K4 per IRLS iteration so that two chunks offset by one stage
@@ -437,15 +508,25 @@ std::vector<Stage> align_stages(const AlignLaunch& a, const rgbid_intrinsics& K,
     const LevelInfo li = make_level(K, a.w0, a.h0, level);
     const int iters = level_iters(cfg, level);
     for (int it = 0; it < iters; ++it) {
-      st.push_back([a, li](cudaStream_t s) { launch_warp_residuals(a, li, 0, s); });
+      // the slots this iteration still works on, and the K1 / K3 grids that cover them
+      auto sw = std::make_shared<SlotSwitch>();
+      st.push_back([a, li, sw](cudaStream_t s) {
+        switch_begin(s, a, *sw);
+        launch_active_slots(a, li.level, 0, s, sw.get());
+        launch_switched(s, a, *sw, 0, [a, li](cudaStream_t t, int rows) {
+          launch_warp_residuals(a, li, 0, t, rows);
+        });
+      });
       if (split) {
         st.push_back([a, li](cudaStream_t s) { launch_tdist(a, li, 0, s, 1); });
         st.push_back([a, li](cudaStream_t s) { launch_tdist(a, li, 0, s, 2); });
       } else {
         st.push_back([a, li](cudaStream_t s) { launch_tdist(a, li, 0, s); });
       }
-      st.push_back([a, li, li0](cudaStream_t s) {
-        launch_normal_equations(a, li, 0, s);
+      st.push_back([a, li, li0, sw](cudaStream_t s) {
+        launch_switched(s, a, *sw, 1, [a, li](cudaStream_t t, int rows) {
+          launch_normal_equations(a, li, 0, t, rows);
+        });
         launch_solve(a, li, li0, s);
       });
     }
@@ -456,6 +537,7 @@ std::vector<Stage> align_stages(const AlignLaunch& a, const rgbid_intrinsics& K,
   st.push_back([a, li0, ss, si, sd](cudaStream_t s) {
     launch_bilateral_pair(a, ss, si, sd, s);
     launch_amask(a, 1, 1, s);
+    launch_active_slots(a, 0, 1, s, nullptr);  // every slot still OK: full grids
     launch_warp_residuals(a, li0, 1, s);
   });
   st.push_back([a, li0](cudaStream_t s) { launch_tdist(a, li0, 1, s); });
@@ -669,6 +751,8 @@ int prepare_chunk(rgbid_ctx* ctx, Lane& L, int n, const rgbid_frame* const* fa,
   a.h0 = h;
   a.eps = cfg.convergence_eps;
   a.lambda_n_min = cfg.lambda_n_min;
+  a.act = use_active_list(nslots) ? L.d_act : nullptr;
+  a.graph_switch = ctx->graph_switch;
 
   *out_a = a;
   // remember what finish_chunk / the pyramid bookkeeping need
@@ -920,6 +1004,9 @@ int rgbid_ctx_create(int device, rgbid_ctx** out) {
   ctx->use_graphs = !(g && g[0] == '1');
   if (const char* e = std::getenv("RGBID_PAIR_STAGES")) g_pair_stages = atoi(e) == 4 ? 4 : 3;
   if (const char* e = std::getenv("RGBID_PAIR_OFFSET")) g_pair_offset = std::max(1, atoi(e));
+  // graph switch nodes for the K1 / K3 slot rows (RGBID_GRAPH_SWITCH=0: none -- ncu
+  // cannot profile the kernel nodes of a graph that has conditional nodes)
+  if (const char* e = std::getenv("RGBID_GRAPH_SWITCH")) ctx->graph_switch = atoi(e) != 0;
   *out = ctx;
   return RGBID_OK;
 }

@@ -256,3 +256,33 @@ def test_coscheduled_ragged_sizes_and_level_counts(ctx, size, levels):
         assert [g.level_log[k].iterations for k in range(levels)] == \
             [o.level_log[k].iterations for k in range(levels)]
     assert n_ok >= n // 2
+
+
+def test_active_slot_lists_and_switch_nodes(K, pairs, frames):
+    """Chunks of > 16 slots run K1 / K3 over a compact list of the slots still
+    iterating, their grids picked per iteration by graph switch nodes (runtime.cu
+    launch_switched, k_active_slots).  With long iteration caps most of each level is
+    tail (few slots left), and with two failing pairs some slots leave the list
+    early: results stay bit-identical to 10-slot chunks (no list) and to the same
+    lists without switch nodes (RGBID_GRAPH_SWITCH=0, read at context creation)."""
+    A, B = frames
+    hole = np.full((480, 640), np.nan)
+    fa, fb = list(A), list(B)
+    ctx = rg.Context(0)
+    badA = rg.DeviceFrame.from_frame(rg.FrameData(hole, hole), ctx)
+    fa[5], fb[5] = badA, B[5]  # no jets at all: fails in the first iteration
+    long_cfg = rg.AlignmentConfig(levels=LEVELS, iterations=[30, 12, 12, 12])
+    with _env(RGBID_BATCH_SLOTS=20):
+        lists = rg.align_batch(fa, fb, K, config=long_cfg, ctx=ctx)
+    with _env(RGBID_BATCH_SLOTS=10):
+        plain = rg.align_batch(fa, fb, K, config=long_cfg, ctx=ctx)
+    with _env(RGBID_GRAPH_SWITCH=0):
+        ctx2 = rg.Context(0)
+    with _env(RGBID_BATCH_SLOTS=20):
+        noswitch = rg.align_batch(fa, fb, K, config=long_cfg, ctx=ctx2)
+    assert lists[5].status == 1
+    assert sum(r.status == 0 for r in lists) >= N_PAIRS - 3
+    its = [sum(r.level_log[k].iterations for k in range(LEVELS)) for r in lists if r.status == 0]
+    assert min(its) < max(its)  # slots leave the list at different iterations
+    for a, b, c in zip(lists, plain, noswitch):
+        assert _key(a) == _key(b) == _key(c)

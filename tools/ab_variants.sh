@@ -8,7 +8,7 @@ for v in "$@"; do
   if [ "$v" = cur ]; then lib=paper_1807_08271_b200/_lib/librgbid_b200.so; else lib=build/$v/librgbid_b200.so; fi
   RGBID_LIB=$lib python bench.py --steps 3 --warmup 2 --no-e2e --no-cpu --no-extra \
     > gpurun_out/ab_${tag}_$v.json 2> gpurun_out/ab_${tag}_$v.err
-  RGBID_LIB=$lib ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+  RGBID_GRAPH_SWITCH=0 RGBID_LIB=$lib ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file gpurun_out/ab_${tag}_$v.csv python tools/prof_run.py --pairs 512 --levels 4 --iters 2 \
     > gpurun_out/ab_${tag}_$v.log 2>&1
 done
