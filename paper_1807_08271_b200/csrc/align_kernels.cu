@@ -1678,31 +1678,20 @@ __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double
 // stages its 32 pixel rows x = (J, r, 0) and w in shared memory and accumulates
 // C += sum_k w_k x_k x_k^T with 8 MMAs per row type, so the 8x8 system (H, the
 // J^T W r column, the cost) lives in two fp64 registers per lane instead of 28 --
-// the register file no longer caps occupancy.  Invalid rows are zeroed (w and x).
-#ifndef RGBID_K3_XS
-#define RGBID_K3_XS 9
-#endif
-// one staged row x = (J, r, 0) and its weight w (zeros for an invalid row)
-__device__ __forceinline__ void stage_row(double* r, bool ok, double j0, double j1, double j2,
-                                          double j3, double j4, double j5, double res, double w) {
-  if (RGBID_K3_XS == 10) {
-    double2* r2 = reinterpret_cast<double2*>(r);
-    r2[0] = ok ? make_double2(j0, j1) : make_double2(0.0, 0.0);
-    r2[1] = ok ? make_double2(j2, j3) : make_double2(0.0, 0.0);
-    r2[2] = ok ? make_double2(j4, j5) : make_double2(0.0, 0.0);
-    r2[3] = make_double2(ok ? res : 0.0, 0.0);
-    r2[4] = make_double2(ok ? w : 0.0, 0.0);
-  } else {
-    r[0] = ok ? j0 : 0.0;
-    r[1] = ok ? j1 : 0.0;
-    r[2] = ok ? j2 : 0.0;
-    r[3] = ok ? j3 : 0.0;
-    r[4] = ok ? j4 : 0.0;
-    r[5] = ok ? j5 : 0.0;
-    r[6] = ok ? res : 0.0;
-    r[7] = 0.0;
-    r[8] = ok ? w : 0.0;
-  }
+// the register file no longer caps occupancy.  Invalid rows are zeroed at their
+// inputs (gradients, residual, w_a, w_b), so every staged component is an exact 0.
+// one staged row x = (J, r, 0) and its weight w
+__device__ __forceinline__ void stage_row(double* r, double j0, double j1, double j2, double j3,
+                                          double j4, double j5, double res, double w) {
+  r[0] = j0;
+  r[1] = j1;
+  r[2] = j2;
+  r[3] = j3;
+  r[4] = j4;
+  r[5] = j5;
+  r[6] = res;
+  r[7] = 0.0;
+  r[8] = w;
 }
 
 #ifndef RGBID_K3_MMA_MINB
@@ -1725,7 +1714,7 @@ __global__ void __launch_bounds__(kTPB, RGBID_K3_MMA_MINB) k_normal_eq_mma(const
   // staged row: 8 components + w; a stride of 9 doubles keeps the per-lane row stores
   // conflict-free (the operand loads see 2-way conflicts).  A stride of 10 with 16-byte
   // stores (conflict-free both ways) measured 3.5% slower per launch.
-  constexpr int XS = RGBID_K3_XS;
+  constexpr int XS = 9;
   __shared__ __align__(16) double xs[kTPB / 32][32 * XS];
   __shared__ double cst[kTPB / 32][64];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -1755,14 +1744,21 @@ __global__ void __launch_bounds__(kTPB, RGBID_K3_MMA_MINB) k_normal_eq_mma(const
     const int k = inr ? k0i : 0;
     const unsigned a = __ldg(am + k);
     const double2 rw = __ldcs(ibwp + k);  // {r_I = i_b - i_a, w_b} (K1)
-    const double r_I = rw.x, w_b = rw.y;
-    const double w_a = __ldg(WA + k);
-    const double2 gI = __ldg(ag + 2 * k), gW = __ldg(ag + 2 * k + 1);
+    const double r_I = rw.x, w_b_ = rw.y;
+    const double w_a_ = __ldg(WA + k);
+    const double2 gI_ = __ldg(ag + 2 * k), gW_ = __ldg(ag + 2 * k + 1);
     const bool jet = inr && (a & 1u) && valid(r_I);  // bit0 implies valid(i_a)
-    const bool dep = jet && (a & 2u) && valid(w_b) && w_b > 0.0;
+    const bool dep = jet && (a & 2u) && valid(w_b_) && w_b_ > 0.0;
     const int y = k / w, x = k - y * w;
     const double px = x, py = y;
     const double ax = li.cx - px, ay = li.cy - py;
+    // invalid rows zeroed at their inputs (gradients, residual, w_a, w_b): every
+    // staged component is then an exact 0 and the weight finite -- 16 selects per
+    // pixel instead of 32 at the staging
+    const double w_a = jet ? w_a_ : 1.0;
+    const double2 gI = make_double2(jet ? gI_.x : 0.0, jet ? gI_.y : 0.0);
+    const double2 gW = make_double2(dep ? gW_.x : 0.0, dep ? gW_.y : 0.0);
+    const double w_b = dep ? w_b_ : 0.0;
     const double iwa = rcp_fast(w_a);  // H is tolerance-checked: MUFU + Newton, no IEEE divide
     const double k0 = red3(Ki[0] * px, Ki[1] * py, Ki[2]), k1 = red3(Ki[3] * px, Ki[4] * py, Ki[5]),
                  k2 = red3(Ki[6] * px, Ki[7] * py, Ki[8]);
@@ -1770,10 +1766,10 @@ __global__ void __launch_bounds__(kTPB, RGBID_K3_MMA_MINB) k_normal_eq_mma(const
     {  // photometric row
       const double s0 = w_a * gI.x, s1 = w_a * gI.y;
       const double u0 = s0 * li.fx, u1 = s1 * li.fy, u2 = s0 * ax + s1 * ay;
-      const double rI = r_I;
+      const double rI = jet ? r_I : 0.0;
       const double xi_ = (rI - muI) * isgI;
       const double wi = nuI1 * rcp_fast(fma(xi_, xi_, nuI)) * is2i;
-      stage_row(xw + lane * XS, jet, u0, u1, u2, X1 * u2 - X2 * u1, X2 * u0 - X0 * u2,
+      stage_row(xw + lane * XS, u0, u1, u2, X1 * u2 - X2 * u1, X2 * u0 - X0 * u2,
                 X0 * u1 - X1 * u0, rI, wi);
     }
     mma_rows();
@@ -1791,10 +1787,10 @@ __global__ void __launch_bounds__(kTPB, RGBID_K3_MMA_MINB) k_normal_eq_mma(const
           lambda = dmax_std(lambda_n_min, c);
         }
       }
-      const double rW = w_b - w_a;
+      const double rW = dep ? w_b - w_a : 0.0;
       const double xw_ = (rW - muW) * isgW;
       const double ww = lambda * nuW1 * rcp_fast(fma(xw_, xw_, nuW)) * is2w;
-      stage_row(xw + lane * XS, dep, s0, s1, s2, X1 * s2 - X2 * s1, X2 * s0 - X0 * s2,
+      stage_row(xw + lane * XS, s0, s1, s2, X1 * s2 - X2 * s1, X2 * s0 - X0 * s2,
                 X0 * s1 - X1 * s0, rW, ww);
     }
     mma_rows();
