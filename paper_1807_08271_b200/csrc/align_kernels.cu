@@ -71,7 +71,8 @@ __device__ __forceinline__ bool valid(double v) { return isfinite(v); }
 // k_active_slots compacts the slots still iterating, in slot order, before each
 // K1, and picks the body of the iteration's K1 and K3 graph switch nodes: the
 // same kernel over ceil(nslots / 2^k) slot rows, the smallest that covers the
-// list (row j works on list entry j; rows past the count exit).
+// list (row j works on list entry j; rows past the count exit).  Body 0 is the
+// plain one-row-per-slot grid (no list loads ahead of the slot check).
 __device__ __forceinline__ int active_slot(const int* act, int j) {
   return act ? (j < act[0] ? act[1 + j] : -1) : j;
 }
@@ -642,7 +643,7 @@ void launch_warp_residuals(const AlignLaunch& a, const LevelInfo& li, int phase,
   KScope ks_(kLevelNames[phase ? 1 : 0][li.level], s);
   const int rows0 = (li.h + kK1L0Rows - 1) / kK1L0Rows;
   dim3 grid(li.nseg, li.h, rows > 0 ? rows : a.nslots);  // tile = row * nseg + segment
-  const int* act = a.act;
+  const int* act = rows > 0 ? a.act : nullptr;  // rows = 0: one row per slot, no list
   switch (li.level) {
     case 0:
       k_warp_residuals_l0<<<dim3(li.nseg, rows0, grid.z), 128 * kK1L0Rows, 0, s>>>(
@@ -1823,7 +1824,7 @@ void launch_normal_equations(const AlignLaunch& a, const LevelInfo& li, int phas
                              int rows) {
   KScope ks_(phase ? "normal_eq_cov" : kNeNames[li.level], s);
   k_normal_eq_mma<<<dim3(li.ntiles3, rows > 0 ? rows : a.nslots), kTPB, 0, s>>>(
-      a.io, a.st, li, phase, a.lambda_n_min, a.act);
+      a.io, a.st, li, phase, a.lambda_n_min, rows > 0 ? a.act : nullptr);
 }
 
 // fixed-order reduction of the per-tile partials into H (full, mirrored), b, cost

@@ -415,7 +415,7 @@ int validate_cfg(const rgbid_align_config& c, int w, int h) {
 
 // Graph switch nodes for the slot-row count of K1 / K3 (k_active_slots picks the
 // body per iteration on the device).  Outside a stream capture (direct launches,
-// profiling) the kernels run one row per slot over the same list.
+// profiling) the kernels run one row per slot with their own slot check.
 int switch_bodies(int nslots) {  // bodies k = 0.. with ceil(nslots / 2^k) >= 8 rows
   int nb = 1;
   while (nb < 8 && ((nslots + (1 << nb) - 1) >> nb) >= 8) ++nb;
@@ -437,7 +437,8 @@ void switch_begin(cudaStream_t s, const AlignLaunch& a, SlotSwitch& sw) {
 }
 
 // launch(stream, rows) as switch node `idx` of sw in the capture on s, one body per
-// row count; a plain launch over all slots when not capturing
+// row count (rows = 0: one row per slot, no list); a plain launch over all slots
+// when not capturing
 void launch_switched(cudaStream_t s, const AlignLaunch& a, const SlotSwitch& sw, int idx,
                      const std::function<void(cudaStream_t, int)>& launch) {
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
@@ -470,7 +471,7 @@ void launch_switched(cudaStream_t s, const AlignLaunch& a, const SlotSwitch& sw,
   for (int k = 0; k < sw.nbodies; ++k) {
     cudaStreamBeginCaptureToGraph(t, cp.conditional.phGraph_out[k], nullptr, nullptr, 0,
                                   cudaStreamCaptureModeThreadLocal);
-    launch(t, (a.nslots + (1 << k) - 1) >> k);
+    launch(t, k == 0 ? 0 : (a.nslots + (1 << k) - 1) >> k);  // body 0: every slot, no list
     cudaGraph_t body;
     cudaStreamEndCapture(t, &body);
   }
@@ -537,7 +538,6 @@ std::vector<Stage> align_stages(const AlignLaunch& a, const rgbid_intrinsics& K,
   st.push_back([a, li0, ss, si, sd](cudaStream_t s) {
     launch_bilateral_pair(a, ss, si, sd, s);
     launch_amask(a, 1, 1, s);
-    launch_active_slots(a, 0, 1, s, nullptr);  // every slot still OK: full grids
     launch_warp_residuals(a, li0, 1, s);
   });
   st.push_back([a, li0](cudaStream_t s) { launch_tdist(a, li0, 1, s); });
