@@ -1308,6 +1308,9 @@ __global__ void __launch_bounds__(kGatherThreads)
 // threads hold the sample in shared memory, ~38 samples per thread: NT = 512 for
 // the 19200-sample cap (one CTA per SM, all 128 registers per thread), smaller
 // CTAs -- several per SM -- for coarse levels whose pixel count caps the sample.
+#ifndef RGBID_TDIST_BULK
+#define RGBID_TDIST_BULK 1  // sample into shared memory by cp.async.bulk (0: per-thread loads)
+#endif
 template <int NT>
 __device__ __forceinline__ void tdist_chain(const SlotIO* __restrict__ io, SlotState* __restrict__ st,
                                             LevelInfo li, int phase) {
@@ -1317,7 +1320,7 @@ __device__ __forceinline__ void tdist_chain(const SlotIO* __restrict__ io, SlotS
   TPH_T(tk0);
   TPH_CNT(10, 1);
   const SlotIO& o = io[slot];
-  extern __shared__ double dsm[];  // sample[kMaxSample]
+  extern __shared__ __align__(16) double dsm[];  // sample[kMaxSample]
   double* smp_sh = dsm;
   __shared__ double scratch[NT / 32 * 2 * 2];
   const int tid = threadIdx.x;
@@ -1338,6 +1341,47 @@ __device__ __forceinline__ void tdist_chain(const SlotIO* __restrict__ io, SlotS
   smp.scratch = scratch;
   smp.parity = 0;
   const double* gs = o.smp + (size_t)type * kMaxSample;
+#if RGBID_TDIST_BULK
+  // the compact sample (written by K2a, L2-resident) into shared memory by bulk
+  // async copies: warp 0 issues kBulkParts pieces on one mbarrier, the odd last
+  // sample (a piece must be a multiple of 16 B) by a plain load
+  {
+    __shared__ __align__(8) uint64_t mbar;
+    const unsigned mb = (unsigned)__cvta_generic_to_shared(&mbar);
+    const unsigned bytes = (unsigned)(smp.m & ~1) * 8u;
+    if (tid == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb));
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(bytes)
+                   : "memory");
+    }
+    __syncwarp();
+    constexpr int kBulkParts = 8;
+    const unsigned part = ((bytes / kBulkParts) + 15u) & ~15u;
+    if (tid < kBulkParts && bytes > 0) {
+      const unsigned off = tid * part;
+      if (off < bytes) {
+        const unsigned n = min(part, bytes - off);
+        const unsigned dst = (unsigned)__cvta_generic_to_shared(smp_sh) + off;
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+            "l"(reinterpret_cast<const char*>(gs) + off), "r"(n), "r"(mb)
+            : "memory");
+      }
+    }
+    if (tid == 0 && (smp.m & 1)) smp_sh[smp.m - 1] = gs[smp.m - 1];
+    __syncthreads();  // mbarrier initialised and armed before anyone waits
+    unsigned done = 0;
+    do {
+      asm volatile(
+          "{ .reg .pred P; mbarrier.try_wait.parity.shared::cta.b64 P, [%1], 0;"
+          " selp.u32 %0, 1, 0, P; }"
+          : "=r"(done)
+          : "r"(mb)
+          : "memory");
+    } while (!done);
+  }
+#else
   for (int s = tid; s < smp.m; s += 4 * NT) {
     double x[4];
 #pragma unroll
@@ -1347,6 +1391,7 @@ __device__ __forceinline__ void tdist_chain(const SlotIO* __restrict__ io, SlotS
     for (int u = 0; u < 4; ++u)
       if (s + u * NT < smp.m) smp_sh[s + u * NT] = x[u];
   }
+#endif
   __syncthreads();
 
   // build_system's Student-t part — src/alignment.cpp:305-317
