@@ -73,8 +73,10 @@ __device__ __forceinline__ bool valid(double v) { return isfinite(v); }
 // same kernel over ceil(nslots / 2^k) slot rows, the smallest that covers the
 // list (row j works on list entry j; rows past the count exit).  Body 0 is the
 // plain one-row-per-slot grid (no list loads ahead of the slot check).
+// slot of grid row j: list entry j (-1 past the count) or, without a list, j itself
+template <bool LIST>
 __device__ __forceinline__ int active_slot(const int* act, int j) {
-  return act ? (j < act[0] ? act[1 + j] : -1) : j;
+  return LIST ? (j < act[0] ? act[1 + j] : -1) : j;
 }
 
 __global__ void __launch_bounds__(1024) k_active_slots(const SlotState* __restrict__ st, int nslots,
@@ -311,7 +313,7 @@ __host__ __device__ constexpr int k1_ng() {
 template <int L>
 __host__ __device__ constexpr int k1_threads() { return k1_cw<L>() * k1_ng<L>(); }
 
-template <int L>
+template <int L, bool LIST>
 #ifndef RGBID_K1_THREADS_PER_SM
 #define RGBID_K1_THREADS_PER_SM 1536  // 40 registers: occupancy over L1-cached spills (-16% vs 64
                                       // registers; 1536 best with the interleaved {I, W} taps)
@@ -322,7 +324,7 @@ __global__ void __launch_bounds__(k1_threads<L>(), RGBID_K1_THREADS_PER_SM / k1_
                                                            const int* __restrict__ act) {
   static_assert(L >= 1, "level 0 uses k_warp_residuals_l0");
   // grid (segment, level row, slot row): no tile-index division
-  const int slot = active_slot(act, blockIdx.z);
+  const int slot = active_slot<LIST>(act, blockIdx.z);
   if (slot < 0) return;
   const SlotState& S = st[slot];
   if (!slot_active(S, L, phase)) return;
@@ -440,11 +442,12 @@ __global__ void __launch_bounds__(k1_threads<L>(), RGBID_K1_THREADS_PER_SM / k1_
 #define RGBID_K1L0_ROWS 1  // 2 and 4 rows per CTA measured 2.5% / 14% slower per launch
 #endif
 constexpr int kK1L0Rows = RGBID_K1L0_ROWS;
+template <bool LIST>
 __global__ void __launch_bounds__(128 * kK1L0Rows, RGBID_K1L0_MINB / kK1L0Rows)
     k_warp_residuals_l0(const SlotIO* __restrict__ io, const SlotState* __restrict__ st,
                         LevelInfo li, int w0, int h0, int phase, const int* __restrict__ act) {
   // grid (segment, row group, slot row): no tile-index division
-  const int slot = active_slot(act, blockIdx.z);
+  const int slot = active_slot<LIST>(act, blockIdx.z);
   if (slot < 0) return;
   const SlotState& S = st[slot];
   if (!slot_active(S, 0, phase)) return;
@@ -643,19 +646,30 @@ void launch_warp_residuals(const AlignLaunch& a, const LevelInfo& li, int phase,
   KScope ks_(kLevelNames[phase ? 1 : 0][li.level], s);
   const int rows0 = (li.h + kK1L0Rows - 1) / kK1L0Rows;
   dim3 grid(li.nseg, li.h, rows > 0 ? rows : a.nslots);  // tile = row * nseg + segment
-  const int* act = rows > 0 ? a.act : nullptr;  // rows = 0: one row per slot, no list
+  const int* act = a.act;
+  const bool list = rows > 0 && act;  // rows = 0: one row per slot, no list
+#define K1L(L)                                                                                  \
+  (list ? k_warp_residuals<L, true><<<grid, k1_threads<L>(), 0, s>>>(a.io, a.st, li, a.w0, a.h0, \
+                                                                     phase, act)               \
+        : k_warp_residuals<L, false><<<grid, k1_threads<L>(), 0, s>>>(a.io, a.st, li, a.w0,     \
+                                                                      a.h0, phase, act))
   switch (li.level) {
-    case 0:
-      k_warp_residuals_l0<<<dim3(li.nseg, rows0, grid.z), 128 * kK1L0Rows, 0, s>>>(
-          a.io, a.st, li, a.w0, a.h0, phase, act);
+    case 0: {
+      const dim3 g0(li.nseg, rows0, grid.z);
+      if (list)
+        k_warp_residuals_l0<true><<<g0, 128 * kK1L0Rows, 0, s>>>(a.io, a.st, li, a.w0, a.h0, phase, act);
+      else
+        k_warp_residuals_l0<false><<<g0, 128 * kK1L0Rows, 0, s>>>(a.io, a.st, li, a.w0, a.h0, phase, act);
       break;
-    case 1: k_warp_residuals<1><<<grid, k1_threads<1>(), 0, s>>>(a.io, a.st, li, a.w0, a.h0, phase, act); break;
-    case 2: k_warp_residuals<2><<<grid, k1_threads<2>(), 0, s>>>(a.io, a.st, li, a.w0, a.h0, phase, act); break;
-    case 3: k_warp_residuals<3><<<grid, k1_threads<3>(), 0, s>>>(a.io, a.st, li, a.w0, a.h0, phase, act); break;
-    case 4: k_warp_residuals<4><<<grid, k1_threads<4>(), 0, s>>>(a.io, a.st, li, a.w0, a.h0, phase, act); break;
-    case 5: k_warp_residuals<5><<<grid, k1_threads<5>(), 0, s>>>(a.io, a.st, li, a.w0, a.h0, phase, act); break;
+    }
+    case 1: K1L(1); break;
+    case 2: K1L(2); break;
+    case 3: K1L(3); break;
+    case 4: K1L(4); break;
+    case 5: K1L(5); break;
     default: return;
   }
+#undef K1L
 }
 
 // ---------------------------------------------------------------------------
@@ -1743,12 +1757,13 @@ __device__ __forceinline__ void stage_row(double* r, double j0, double j1, doubl
 #ifndef RGBID_K3_MMA_MINB
 #define RGBID_K3_MMA_MINB 3
 #endif
+template <bool LIST>
 __global__ void __launch_bounds__(kTPB, RGBID_K3_MMA_MINB) k_normal_eq_mma(const SlotIO* __restrict__ io,
                                                         const SlotState* __restrict__ st,
                                                         LevelInfo li, int phase,
                                                         double lambda_n_min,
                                                         const int* __restrict__ act) {
-  const int slot = active_slot(act, blockIdx.y);
+  const int slot = active_slot<LIST>(act, blockIdx.y);
   if (slot < 0) return;
   const SlotState& S = st[slot];
   if (!slot_active(S, li.level, phase)) return;  // uniform over the CTA
@@ -1868,8 +1883,11 @@ __global__ void __launch_bounds__(kTPB, RGBID_K3_MMA_MINB) k_normal_eq_mma(const
 void launch_normal_equations(const AlignLaunch& a, const LevelInfo& li, int phase, cudaStream_t s,
                              int rows) {
   KScope ks_(phase ? "normal_eq_cov" : kNeNames[li.level], s);
-  k_normal_eq_mma<<<dim3(li.ntiles3, rows > 0 ? rows : a.nslots), kTPB, 0, s>>>(
-      a.io, a.st, li, phase, a.lambda_n_min, rows > 0 ? a.act : nullptr);
+  const dim3 grid(li.ntiles3, rows > 0 ? rows : a.nslots);
+  if (rows > 0 && a.act)
+    k_normal_eq_mma<true><<<grid, kTPB, 0, s>>>(a.io, a.st, li, phase, a.lambda_n_min, a.act);
+  else
+    k_normal_eq_mma<false><<<grid, kTPB, 0, s>>>(a.io, a.st, li, phase, a.lambda_n_min, nullptr);
 }
 
 // fixed-order reduction of the per-tile partials into H (full, mirrored), b, cost
