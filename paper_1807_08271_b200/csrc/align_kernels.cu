@@ -1486,6 +1486,7 @@ __global__ void __launch_bounds__(kTdistClusterThreads, 1)
                    : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  TPH_T(tg0);
   const int nt = li.ntiles;
   const int per = (nt + NT - 1) / NT;
   const int b0 = min(nt, tid * per), b1 = min(nt, b0 + per);
@@ -1511,6 +1512,7 @@ __global__ void __launch_bounds__(kTdistClusterThreads, 1)
   }
   if (tid == 0) offs[nt] = total;
   __syncthreads();
+  TPH_ADD(12, tg0);
   const long long n = total;
   const long long stride = n <= kMaxSample ? 1 : (n + kMaxSample - 1) / kMaxSample;
   Sample smp;
@@ -1562,6 +1564,7 @@ __global__ void __launch_bounds__(kTdistClusterThreads, 1)
     }
   }
   __syncthreads();
+  TPH_ADD(13, tg0);
   for (int k = tid; k < smp.m_local; k += 4 * NT) {  // values, four loads in flight
     long long ix[4];
     double bb[4], aa[4];
@@ -1586,6 +1589,7 @@ __global__ void __launch_bounds__(kTdistClusterThreads, 1)
   smp.memo_nu = -1.0;
   smp.scratch = scratch;
   smp.parity = 0;
+  TPH_ADD(14, tg0);
   TPH_ADD(0, tk0);
   cl.sync();  // every CTA's share (and cbuf) ready before the first cluster reduction
   TD t = loc_scale<NT>(smp, 5.0, scratch);

@@ -21,7 +21,8 @@ e1.record(s); e1.synchronize()
 L.rgbid_debug_tdist_phases(buf, 1)
 ctas = buf[10]
 print(f"align {e0.elapsed_time(e1):.3f} ms, iterations {r.total_iterations}, tdist CTAs {ctas}")
-names = {0: "gather", 1: "loc_scale", 4: "stationarity", 8: "allsum", 7: "kernel"}
+names = {0: "gather", 12: "gather: tile-count scan (cumulative)", 13: "gather: + search/walk",
+         14: "gather: + value loads", 1: "loc_scale", 4: "stationarity", 8: "allsum", 7: "kernel"}
 for k, v in names.items():
     print(f"  {v}: {buf[k] / ctas / 1.95e3:.1f} us per CTA, x launches {ctas/16:.0f} = {buf[k]/16/1.95e6:.3f} ms")
 ctx.set_profiling(True); ctx.reset_stats()
