@@ -416,6 +416,8 @@ int validate_cfg(const rgbid_align_config& c, int w, int h) {
 // Graph switch nodes for the slot-row count of K1 / K3 (k_active_slots picks the
 // body per iteration on the device).  Outside a stream capture (direct launches,
 // profiling) the kernels run one row per slot with their own slot check.
+thread_local bool g_switch_capture_failed = false;  // a switch body could not be captured
+
 int switch_bodies(int nslots) {  // bodies k = 0.. with ceil(nslots / 2^k) >= 8 rows
   int nb = 1;
   while (nb < 8 && ((nslots + (1 << nb) - 1) >> nb) >= 8) ++nb;
@@ -469,14 +471,19 @@ void launch_switched(cudaStream_t s, const AlignLaunch& a, const SlotSwitch& sw,
   long long* cnt = g_launch_counter;
   const long long c0 = cnt ? *cnt : 0;
   for (int k = 0; k < sw.nbodies; ++k) {
-    cudaStreamBeginCaptureToGraph(t, cp.conditional.phGraph_out[k], nullptr, nullptr, 0,
-                                  cudaStreamCaptureModeThreadLocal);
+    if (!t || cudaStreamBeginCaptureToGraph(t, cp.conditional.phGraph_out[k], nullptr, nullptr, 0,
+                                            cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+      g_switch_capture_failed = true;  // never launch a body for real: fail the graph
+      continue;
+    }
     launch(t, k == 0 ? 0 : (a.nslots + (1 << k) - 1) >> k);  // body 0: every slot, no list
     cudaGraph_t body;
-    cudaStreamEndCapture(t, &body);
+    if (cudaStreamEndCapture(t, &body) != cudaSuccess) g_switch_capture_failed = true;
   }
   if (cnt) *cnt = c0 + 1;  // one body runs per graph launch
-  cudaStreamUpdateCaptureDependencies(s, &node, 1, cudaStreamSetCaptureDependencies);
+  if (cudaStreamUpdateCaptureDependencies(s, &node, 1, cudaStreamSetCaptureDependencies) !=
+      cudaSuccess)
+    g_switch_capture_failed = true;
 }
 
 // The whole align (all levels + covariance pass) as a list of stages; a stage
@@ -815,6 +822,12 @@ int launch_prepared(rgbid_ctx* ctx, Lane& L, const AlignLaunch& a, Lane* LB,
       cg.launches = ctx->launches - before;
       ctx->launches = before;
       CK(cudaStreamEndCapture(L.stream, &g));
+      if (g_switch_capture_failed) {
+        g_switch_capture_failed = false;
+        cudaGraphDestroy(g);
+        ctx->err = "capture of a graph switch-node body failed";
+        return RGBID_E_CUDA;
+      }
       CK(cudaGraphInstantiateWithFlags(&cg.exec, g, cudaGraphInstantiateFlagUseNodePriority));
       cudaGraphDestroy(g);
       it = L.graphs.emplace(key, cg).first;
@@ -872,6 +885,12 @@ int launch_group(rgbid_ctx* ctx, int G, const AlignLaunch* aj, const rgbid_intri
       cg.launches = ctx->launches - before;
       ctx->launches = before;
       CK(cudaStreamEndCapture(L.stream, &g));
+      if (g_switch_capture_failed) {
+        g_switch_capture_failed = false;
+        cudaGraphDestroy(g);
+        ctx->err = "capture of a graph switch-node body failed";
+        return RGBID_E_CUDA;
+      }
       CK(cudaGraphInstantiateWithFlags(&cg.exec, g, cudaGraphInstantiateFlagUseNodePriority));
       cudaGraphDestroy(g);
       it = L.graphs.emplace(key, cg).first;
