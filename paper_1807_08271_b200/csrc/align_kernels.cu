@@ -1938,17 +1938,30 @@ __global__ void __launch_bounds__(kTPB) k_solve(const SlotIO* __restrict__ io,
   __shared__ double sh[(kTPB / 32) * kNPart];
   __shared__ double H[36], b[6], cost;
   reduce_partials(io[slot].part, li.ntiles3, H, b, &cost, sh);
-  if (threadIdx.x != 0) return;
-  for (int i = 0; i < 36; ++i) S.H[i] = H[i];
-  if (rank_deficient6(H)) {
+  // the rank test (warp 1) runs beside the solve and pose update (warp 0): the
+  // serial 6x6 chains overlap instead of adding up; the update is kept only if H
+  // passed (src/alignment.cpp:391-394)
+  __shared__ int deficient;
+  __syncthreads();  // H, b, cost from thread 0
+  const int t = threadIdx.x;
+  if (t >= 64 && t < 100) S.H[t - 64] = H[t - 64];
+  if (t == 32) deficient = rank_deficient6(H) ? 1 : 0;
+  double xi[6];
+  PoseD T;
+  WarpMats wmn;
+  if (t == 0) {
+    ldlt_solve6(H, b, xi);
+    T = pose_update(xi, pose_from(S.R, S.t));
+    wmn = warp_mats(T, fx0, fy0, cx0, cy0);
+  }
+  __syncthreads();
+  if (t != 0) return;
+  if (deficient) {
     S.status = RGBID_E_DEGENERATE;
     return;
   }
-  double xi[6];
-  ldlt_solve6(H, b, xi);
-  const PoseD T = pose_update(xi, pose_from(S.R, S.t));
   pose_to(T, S.R, S.t);
-  S.wm = warp_mats(T, fx0, fy0, cx0, cy0);
+  S.wm = wmn;
   const int L = li.level;
   S.iters[L] += 1;
   S.cost[L] = cost;
