@@ -1703,7 +1703,8 @@ void launch_tdist(const AlignLaunch& a, const LevelInfo& li, int phase, cudaStre
 }
 
 // ---------------------------------------------------------------------------
-// K3: jets + robust weights + 28 fp64 sums per tile (kPixK3 pixels per thread).
+// K3: jets + robust weights + 28 fp64 sums per tile (PIX pixels per thread: kPixK3 in
+// batches, 1 in latency mode).
 // Jets restate src/alignment.cpp:212-244 with the structure of A = K - p e_z^T and
 // M = [I | -[X_A]x] folded in: J = (u, X_A x u) with u = w_a g A; the weights are
 // src/alignment.cpp:324,329-330.  Tolerance-level (not bitwise) w.r.t. the
@@ -1761,7 +1762,7 @@ __device__ __forceinline__ void stage_row(double* r, double j0, double j1, doubl
 #ifndef RGBID_K3_MMA_MINB
 #define RGBID_K3_MMA_MINB 3
 #endif
-template <bool LIST>
+template <bool LIST, int PIX>
 __global__ void __launch_bounds__(kTPB, RGBID_K3_MMA_MINB) k_normal_eq_mma(const SlotIO* __restrict__ io,
                                                         const SlotState* __restrict__ st,
                                                         LevelInfo li, int phase,
@@ -1803,8 +1804,8 @@ __global__ void __launch_bounds__(kTPB, RGBID_K3_MMA_MINB) k_normal_eq_mma(const
     __syncwarp();
   };
 #pragma unroll 1
-  for (int p = 0; p < kPixK3; ++p) {
-    const int k0i = (blockIdx.x * kPixK3 + p) * kTPB + threadIdx.x;
+  for (int p = 0; p < PIX; ++p) {
+    const int k0i = (blockIdx.x * PIX + p) * kTPB + threadIdx.x;
     const bool inr = k0i < N;
     const int k = inr ? k0i : 0;
     const unsigned a = __ldg(am + k);
@@ -1888,10 +1889,14 @@ void launch_normal_equations(const AlignLaunch& a, const LevelInfo& li, int phas
                              int rows) {
   KScope ks_(phase ? "normal_eq_cov" : kNeNames[li.level], s);
   const dim3 grid(li.ntiles3, rows > 0 ? rows : a.nslots);
-  if (rows > 0 && a.act)
-    k_normal_eq_mma<true><<<grid, kTPB, 0, s>>>(a.io, a.st, li, phase, a.lambda_n_min, a.act);
+  if (li.pix3 == 1)  // latency mode: one pixel per thread, no list
+    k_normal_eq_mma<false, 1><<<grid, kTPB, 0, s>>>(a.io, a.st, li, phase, a.lambda_n_min, nullptr);
+  else if (rows > 0 && a.act)
+    k_normal_eq_mma<true, kPixK3><<<grid, kTPB, 0, s>>>(a.io, a.st, li, phase, a.lambda_n_min,
+                                                         a.act);
   else
-    k_normal_eq_mma<false><<<grid, kTPB, 0, s>>>(a.io, a.st, li, phase, a.lambda_n_min, nullptr);
+    k_normal_eq_mma<false, kPixK3><<<grid, kTPB, 0, s>>>(a.io, a.st, li, phase, a.lambda_n_min,
+                                                          nullptr);
 }
 
 // fixed-order reduction of the per-tile partials into H (full, mirrored), b, cost

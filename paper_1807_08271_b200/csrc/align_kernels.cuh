@@ -32,9 +32,10 @@ constexpr int kTdistClusterMaxSlots = 8; // batches up to this size use the clus
 #endif
 constexpr int kTdistClusterThreads = RGBID_TDIST_CLUSTER_THREADS;
 constexpr int kPixK3 = 8;           // pixels per thread in the normal-equation kernel
-// K3 tiles: kTPB * kPixK3 consecutive level pixels
-__host__ __device__ constexpr int k3_tiles(int w, int h) {
-  return (w * h + kTPB * kPixK3 - 1) / (kTPB * kPixK3);
+// K3 tiles: kTPB * pix consecutive level pixels (pix = kPixK3 for batches, 1 in
+// latency mode: one pixel per thread, 8x the CTAs for one slot)
+__host__ __device__ constexpr int k3_tiles(int w, int h, int pix = kPixK3) {
+  return (w * h + kTPB * pix - 1) / (kTPB * pix);
 }
 
 // K1 tiling of level l: tile = (level row, segment of tx level pixels).
@@ -50,7 +51,8 @@ struct LevelInfo {
   int w, h;          // level image size (w0 >> l, h0 >> l)
   int tx, nseg;      // K1 tiling
   int ntiles;        // K1 tiles = h * nseg
-  int ntiles3;       // K3 tiles of kTPB * kPixK3 consecutive pixels
+  int ntiles3;       // K3 tiles of kTPB * pix3 consecutive pixels
+  int pix3;          // K3 pixels per thread (kPixK3, or 1 in latency mode)
   double fx, fy, cx, cy;
   double Kinv[9];    // level K^-1 (host m3_inv, bit-identical to the oracle)
 };

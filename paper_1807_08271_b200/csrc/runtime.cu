@@ -233,6 +233,7 @@ LevelInfo make_level(const rgbid_intrinsics& K0, int w0, int h0, int level) {
   li.nseg = (li.w + li.tx - 1) / li.tx;
   li.ntiles = li.nseg * li.h;
   li.ntiles3 = k3_tiles(li.w, li.h);
+  li.pix3 = kPixK3;
   rgbid_intrinsics k;
   level_intrinsics(K0, level, &k);
   li.fx = k.fx;
@@ -273,7 +274,7 @@ size_t pyr_pixels(int w, int h) {
 }
 size_t slot_f64(int w, int h) {
   const size_t N = (size_t)w * h;
-  const size_t part = (size_t)k3_tiles(w, h) * kNPart;
+  const size_t part = (size_t)k3_tiles(w, h, 1) * kNPart;  // latency mode: 1 pixel per thread
   // ... + K2 samples + interleaved frame B (16-byte aligned: the total stays even)
   const size_t f = 4 * N + 4 * pyr_pixels(w, h) + part + 2 * (size_t)kMaxSample;
   return ((f + 1) & ~(size_t)1) + 2 * N;
@@ -504,7 +505,16 @@ int g_pair_stages = 4, g_pair_offset = 2;  // 4 stages, offset 2: +0.8% over 3 /
 std::vector<Stage> align_stages(const AlignLaunch& a, const rgbid_intrinsics& K,
                                 const rgbid_align_config& cfg) {
   std::vector<Stage> st;
-  const LevelInfo li0 = make_level(K, a.w0, a.h0, 0);
+  // latency mode (<= kTdistClusterMaxSlots slots): K3 with one pixel per thread
+  auto level = [&](int l) {
+    LevelInfo li = make_level(K, a.w0, a.h0, l);
+    if (a.nslots <= kTdistClusterMaxSlots) {
+      li.pix3 = 1;
+      li.ntiles3 = k3_tiles(li.w, li.h, 1);
+    }
+    return li;
+  };
+  const LevelInfo li0 = level(0);
   const int levels = cfg.levels;
   const bool split = g_pair_stages == 4;
   st.push_back([a, levels](cudaStream_t s) {
@@ -512,9 +522,9 @@ std::vector<Stage> align_stages(const AlignLaunch& a, const rgbid_intrinsics& K,
     launch_amask(a, levels, 0, s);       // A-side validity + gradients, once per align
     launch_interleave_B(a, s);           // B as {I, W} pairs for K1's bilinear taps
   });
-  for (int level = cfg.levels - 1; level >= 0; --level) {
-    const LevelInfo li = make_level(K, a.w0, a.h0, level);
-    const int iters = level_iters(cfg, level);
+  for (int lv = cfg.levels - 1; lv >= 0; --lv) {
+    const LevelInfo li = level(lv);
+    const int iters = level_iters(cfg, lv);
     for (int it = 0; it < iters; ++it) {
       // the slots this iteration still works on, and the K1 / K3 grids that cover them
       auto sw = std::make_shared<SlotSwitch>();
