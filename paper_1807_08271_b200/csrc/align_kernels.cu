@@ -718,7 +718,7 @@ struct TD {
 // Phase counters for the Student-t chain (thread 0 of each CTA; instrumented
 // builds only: RGBID_NVFLAGS=-DRGBID_TDIST_TRACE, read by tools/tdist_phases.py)
 #ifdef RGBID_TDIST_TRACE
-__device__ unsigned long long g_tph[16];
+__device__ unsigned long long g_tph[24];
 #define TPH_T(v) const unsigned long long v = clock64()
 #define TPH_ADD(i, t0) \
   if (threadIdx.x == 0) atomicAdd(&g_tph[i], (unsigned long long)(clock64() - (t0)))
@@ -1621,7 +1621,7 @@ extern "C" int rgbid_debug_tdist_phases(unsigned long long* out, int reset) {
   cudaDeviceSynchronize();
   cudaMemcpyFromSymbol(out, g_tph, sizeof(g_tph));
   if (reset) {
-    static const unsigned long long z[16] = {};
+    static const unsigned long long z[24] = {};
     cudaMemcpyToSymbol(g_tph, z, sizeof(z));
   }
   return 0;
@@ -1881,7 +1881,7 @@ __global__ void __launch_bounds__(kTPB, RGBID_K3_MMA_MINB) k_normal_eq_mma(const
     double t = 0.0;
 #pragma unroll
     for (int wv = 0; wv < kTPB / 32; ++wv) t += cst[wv][r * 8 + c];
-    o.part[(size_t)blockIdx.x * kNPart + q] = t;
+    o.part[(size_t)q * li.ntiles3 + blockIdx.x] = t;  // value-major: K4 reads coalesced
   }
 }
 
@@ -1907,7 +1907,7 @@ __device__ void reduce_partials(const double* part, int ntiles, double* H, doubl
   for (int i = 0; i < kNPart; ++i) acc[i] = 0.0;
   for (int t = threadIdx.x; t < ntiles; t += kTPB)
 #pragma unroll
-    for (int i = 0; i < kNPart; ++i) acc[i] += part[(size_t)t * kNPart + i];
+    for (int i = 0; i < kNPart; ++i) acc[i] += part[(size_t)i * ntiles + t];
   __shared__ double tot[kNPart];
   block_sum_to<kTPB>(acc, tot, sh);
   __syncthreads();
@@ -1933,6 +1933,7 @@ __global__ void __launch_bounds__(kTPB) k_solve(const SlotIO* __restrict__ io,
   const int slot = blockIdx.x;
   SlotState& S = st[slot];
   if (!slot_active(S, li.level, 0)) return;
+  TPH_T(ts0);
   if (S.nI < 6) {  // jets.size() < 6 -> DegenerateAlignmentError(zero spectrum)
     if (threadIdx.x == 0) {
       S.status = RGBID_E_DEGENERATE;
@@ -1943,6 +1944,7 @@ __global__ void __launch_bounds__(kTPB) k_solve(const SlotIO* __restrict__ io,
   __shared__ double sh[(kTPB / 32) * kNPart];
   __shared__ double H[36], b[6], cost;
   reduce_partials(io[slot].part, li.ntiles3, H, b, &cost, sh);
+  TPH_ADD(16, ts0);
   // the rank test (warp 1) runs beside the solve and pose update (warp 0): the
   // serial 6x6 chains overlap instead of adding up; the update is kept only if H
   // passed (src/alignment.cpp:391-394)
@@ -1955,9 +1957,15 @@ __global__ void __launch_bounds__(kTPB) k_solve(const SlotIO* __restrict__ io,
   PoseD T;
   WarpMats wmn;
   if (t == 0) {
+    TPH_T(ts1);
     ldlt_solve6(H, b, xi);
+    TPH_ADD(17, ts1);
+    TPH_T(ts2);
     T = pose_update(xi, pose_from(S.R, S.t));
+    TPH_ADD(18, ts2);
+    TPH_T(ts3);
     wmn = warp_mats(T, fx0, fy0, cx0, cy0);
+    TPH_ADD(19, ts3);
   }
   __syncthreads();
   if (t != 0) return;
@@ -1995,6 +2003,8 @@ __global__ void __launch_bounds__(kTPB) k_solve(const SlotIO* __restrict__ io,
   }
   const double xn = sqrt(red3(xi[0] * xi[0], xi[1] * xi[1], xi[2] * xi[2]) +
                          red3(xi[3] * xi[3], xi[4] * xi[4], xi[5] * xi[5]));
+  TPH_ADD(20, ts0);
+  TPH_CNT(21, 1);
   if (xn < eps) S.done_level = L;
   (void)w0;
   (void)h0;

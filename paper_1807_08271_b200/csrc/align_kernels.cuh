@@ -76,7 +76,7 @@ struct SlotIO {
   int* cntW;
   unsigned* bitsI;               // per K1 tile validity bitmask [ntiles][kWordsPerTile]
   unsigned* bitsW;
-  double* part;                  // K3 partial sums [ntiles3][kNPart]
+  double* part;                  // K3 partial sums [kNPart][ntiles3] (value-major)
   double* smp;                   // K2 systematic samples [2][kMaxSample] (r_I, r_W; k_gather)
   int* nsmp;                     // K2 valid residual counts [2] (k_gather)
   int build_pyr;                 // 1: this slot builds frame A's pyramid levels >= 1

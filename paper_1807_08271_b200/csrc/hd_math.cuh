@@ -13,8 +13,10 @@
 
 #ifdef __CUDACC__
 #define HD __host__ __device__ __forceinline__
+#define HD_UNROLL _Pragma("unroll")
 #else
 #define HD inline
+#define HD_UNROLL
 #endif
 
 namespace rgbid_b200 {
@@ -180,47 +182,69 @@ HD WarpMats warp_mats(const PoseD& T_AB, double fx, double fy, double cx, double
 // ---- 6x6 numerics (Eigen conventions; same algorithms as the oracle) -------
 
 // Eigen ldlt_inplace<Lower> with diagonal pivoting + solve (src/alignment.cpp:393).
+// Every loop has compile-time bounds and the pivot swaps are unrolled over the
+// candidate rows, so all indices are static and the factor stays in registers
+// (no local-memory round trips on the single thread that runs it): the same
+// operations in the same order as the textbook loop, hence the same bits.
 HD void ldlt_solve6(const double Hin[36], const double b[6], double x[6]) {
   double m[6][6], temp[6];
   int tr[6];
+  HD_UNROLL
   for (int i = 0; i < 6; ++i)
+    HD_UNROLL
     for (int j = 0; j < 6; ++j) m[i][j] = Hin[i * 6 + j];
+  bool stop = false;
+  HD_UNROLL
   for (int k = 0; k < 6; ++k) {
+    if (stop) {  // a zero first pivot: identity permutation, factor abandoned
+      tr[k] = k;
+      continue;
+    }
     int big = k;
     double bigv = fabs(m[k][k]);
+    HD_UNROLL
     for (int i = k + 1; i < 6; ++i)
       if (fabs(m[i][i]) > bigv) {
         bigv = fabs(m[i][i]);
         big = i;
       }
     tr[k] = big;
-    if (k != big) {
+    HD_UNROLL
+    for (int c = k + 1; c < 6; ++c) {
+      if (big != c) continue;
+      HD_UNROLL
       for (int j = 0; j < k; ++j) {
         const double t = m[k][j];
-        m[k][j] = m[big][j];
-        m[big][j] = t;
+        m[k][j] = m[c][j];
+        m[c][j] = t;
       }
-      for (int i = big + 1; i < 6; ++i) {
+      HD_UNROLL
+      for (int i = c + 1; i < 6; ++i) {
         const double t = m[i][k];
-        m[i][k] = m[i][big];
-        m[i][big] = t;
+        m[i][k] = m[i][c];
+        m[i][c] = t;
       }
       double t = m[k][k];
-      m[k][k] = m[big][big];
-      m[big][big] = t;
-      for (int i = k + 1; i < big; ++i) {
+      m[k][k] = m[c][c];
+      m[c][c] = t;
+      HD_UNROLL
+      for (int i = k + 1; i < c; ++i) {
         t = m[i][k];
-        m[i][k] = m[big][i];
-        m[big][i] = t;
+        m[i][k] = m[c][i];
+        m[c][i] = t;
       }
     }
     if (k > 0) {
+      HD_UNROLL
       for (int j = 0; j < k; ++j) temp[j] = m[j][j] * m[k][j];
       double acc = 0.0;
+      HD_UNROLL
       for (int j = 0; j < k; ++j) acc += m[k][j] * temp[j];
       m[k][k] -= acc;
+      HD_UNROLL
       for (int i = k + 1; i < 6; ++i) {
         double s = 0.0;
+        HD_UNROLL
         for (int j = 0; j < k; ++j) s += m[i][j] * temp[j];
         m[i][k] -= s;
       }
@@ -228,28 +252,44 @@ HD void ldlt_solve6(const double Hin[36], const double b[6], double x[6]) {
     const double akk = m[k][k];
     const bool valid = fabs(akk) > 0.0;
     if (k == 0 && !valid) {
-      for (int j = 0; j < 6; ++j) tr[j] = j;
-      break;
+      tr[0] = 0;
+      stop = true;
+      continue;
     }
     if (k < 5 && valid)
+      HD_UNROLL
       for (int i = k + 1; i < 6; ++i) m[i][k] /= akk;
   }
+  HD_UNROLL
   for (int i = 0; i < 6; ++i) x[i] = b[i];
-  for (int k = 0; k < 6; ++k) {
-    const double t = x[k];
-    x[k] = x[tr[k]];
-    x[tr[k]] = t;
-  }
+  HD_UNROLL
+  for (int k = 0; k < 6; ++k)
+    HD_UNROLL
+    for (int c = k + 1; c < 6; ++c)
+      if (tr[k] == c) {
+        const double t = x[k];
+        x[k] = x[c];
+        x[c] = t;
+      }
+  HD_UNROLL
   for (int i = 0; i < 6; ++i)
+    HD_UNROLL
     for (int j = 0; j < i; ++j) x[i] -= m[i][j] * x[j];
+  HD_UNROLL
   for (int i = 0; i < 6; ++i) x[i] = fabs(m[i][i]) > 2.2250738585072014e-308 ? x[i] / m[i][i] : 0.0;
+  HD_UNROLL
   for (int i = 5; i >= 0; --i)
+    HD_UNROLL
     for (int j = i + 1; j < 6; ++j) x[i] -= m[j][i] * x[j];
-  for (int k = 5; k >= 0; --k) {
-    const double t = x[k];
-    x[k] = x[tr[k]];
-    x[tr[k]] = t;
-  }
+  HD_UNROLL
+  for (int k = 5; k >= 0; --k)
+    HD_UNROLL
+    for (int c = k + 1; c < 6; ++c)
+      if (tr[k] == c) {
+        const double t = x[k];
+        x[k] = x[c];
+        x[c] = t;
+      }
 }
 
 // Rank test of src/alignment.cpp:342-353 without an eigensolver:
@@ -258,21 +298,28 @@ HD void ldlt_solve6(const double Hin[36], const double b[6], double x[6]) {
 // reference's "< 1e-9" only on exact ties).
 HD bool rank_deficient6(const double H[36]) {
   double s[6];
+  HD_UNROLL
   for (int i = 0; i < 6; ++i) {
     if (!(H[i * 6 + i] > 0.0)) return true;
     s[i] = 1.0 / sqrt(H[i * 6 + i]);
   }
   double a[6][6];
+  HD_UNROLL
   for (int i = 0; i < 6; ++i)
+    HD_UNROLL
     for (int j = 0; j < 6; ++j) a[i][j] = (s[i] * H[i * 6 + j]) * s[j] - (i == j ? 1e-9 : 0.0);
+  HD_UNROLL
   for (int j = 0; j < 6; ++j) {
     double d = a[j][j];
+    HD_UNROLL
     for (int k = 0; k < j; ++k) d -= a[j][k] * a[j][k];
     if (!(d > 0.0)) return true;
     d = sqrt(d);
     a[j][j] = d;
+    HD_UNROLL
     for (int i = j + 1; i < 6; ++i) {
       double t = a[i][j];
+      HD_UNROLL
       for (int k = 0; k < j; ++k) t -= a[i][k] * a[j][k];
       a[i][j] = t / d;
     }

@@ -10,7 +10,7 @@ A, B = rg.DeviceFrame(640, 480, ctx), rg.DeviceFrame(640, 480, ctx)
 rg.synth_pair_device(A, B, K, 0, 1)
 cfg = rg.AlignmentConfig(levels=4)
 s = torch.cuda.ExternalStream(ctx.stream_ptr)
-buf = (C.c_ulonglong * 16)()
+buf = (C.c_ulonglong * 24)()
 for _ in range(3):
     rg.align(A, B, K, config=cfg, ctx=ctx)
 L.rgbid_debug_tdist_phases(buf, 1)
@@ -25,6 +25,11 @@ names = {0: "gather", 12: "gather: tile-count scan (cumulative)", 13: "gather: +
          14: "gather: + value loads", 1: "loc_scale", 4: "stationarity", 8: "allsum", 7: "kernel"}
 for k, v in names.items():
     print(f"  {v}: {buf[k] / ctas / 1.95e3:.1f} us per CTA, x launches {ctas/16:.0f} = {buf[k]/16/1.95e6:.3f} ms")
+ns = max(buf[21], 1)
+print(f"k_solve ({ns} launches), thread 0, us per launch:")
+for k, v in {16: "reduce partials", 17: "ldlt_solve6", 18: "pose_update", 19: "warp_mats",
+             20: "whole kernel (from the slot check)"}.items():
+    print(f"  {v}: {buf[k] / ns / 1.95e3:.2f}")
 ctx.set_profiling(True); ctx.reset_stats()
 rg.align(A, B, K, config=cfg, ctx=ctx); ctx.synchronize()
 st = ctx.kernel_stats(); ctx.set_profiling(False)

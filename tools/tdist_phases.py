@@ -17,7 +17,7 @@ A = [rg.DeviceFrame(640, 480, ctx) for _ in range(n)]
 B = [rg.DeviceFrame(640, 480, ctx) for _ in range(n)]
 for i in range(n):
     rg.synth_pair_device(A[i], B[i], K, i, 1)
-buf = (C.c_ulonglong * 16)()
+buf = (C.c_ulonglong * 24)()
 names = {0: "gather", 1: "loc_scale", 4: "stationarity", 6: "stat_pass", 8: "allsum", 7: "kernel",
          3: "ls_iters(count)", 9: "allsums(count)", 2: "ls_calls(count)", 5: "stat_calls(count)"}
 for lv in range(-1, 4):
