@@ -767,6 +767,10 @@ struct Sample {
   // -> same result (e.g. the final refit repeating estimate_nu's, src/alignment.cpp:117,316)
   double memo_nu;
   TD memo;
+  // the sample's mean and root-mean-square deviation (the start of every
+  // estimate_location_scale call, src/alignment.cpp:65-71): computed once per chain
+  bool have_mom;
+  double mu0, sigma0;
 };
 
 // Cluster-wide sum (latency mode): every warp's lane d pushes the warp's partials
@@ -1015,16 +1019,21 @@ __device__ __forceinline__ TD loc_scale(Sample& S, double nu, double* scratch) {
   TPH_CNT(2, 1);
   const double inv_m = 1.0 / (double)m;
   double a1[1];
-  sample_sum<NT>(S, a1, [](double v, double (&a)[1]) { a[0] += v; });
-  sample_allsum<1, NT>(a1, S);
-  const double mu0 = a1[0] / (double)m;
-  sample_sum<NT>(S, a1, [mu0](double v, double (&a)[1]) {
-    const double d = v - mu0;
-    a[0] = fma(d, d, a[0]);
-  });
-  sample_allsum<1, NT>(a1, S);
-  double mu = mu0;
-  double sigma = sqrt(a1[0] / (double)m);
+  if (!S.have_mom) {
+    sample_sum<NT>(S, a1, [](double v, double (&a)[1]) { a[0] += v; });
+    sample_allsum<1, NT>(a1, S);
+    const double mu0 = a1[0] / (double)m;
+    sample_sum<NT>(S, a1, [mu0](double v, double (&a)[1]) {
+      const double d = v - mu0;
+      a[0] = fma(d, d, a[0]);
+    });
+    sample_allsum<1, NT>(a1, S);
+    S.mu0 = mu0;
+    S.sigma0 = sqrt(a1[0] / (double)m);
+    S.have_mom = true;
+  }
+  double mu = S.mu0;
+  double sigma = S.sigma0;
   TD out;
   if (sigma < 1e-8) {
     out = TD{mu, 1e-8, nu};
@@ -1352,6 +1361,7 @@ __device__ __forceinline__ void tdist_chain(const SlotIO* __restrict__ io, SlotS
   smp.cred = 0;
   smp.rank = 0;
   smp.memo_nu = -1.0;
+  smp.have_mom = false;
   smp.scratch = scratch;
   smp.parity = 0;
   const double* gs = o.smp + (size_t)type * kMaxSample;
@@ -1587,6 +1597,7 @@ __global__ void __launch_bounds__(kTdistClusterThreads, 1)
   smp.cred = 0;
   smp.rank = rank;
   smp.memo_nu = -1.0;
+  smp.have_mom = false;
   smp.scratch = scratch;
   smp.parity = 0;
   TPH_ADD(14, tg0);
@@ -2427,6 +2438,7 @@ __global__ void __launch_bounds__(kTdistThreads, 1)  // one CTA per SM (sample i
   smp.cred = 0;
   smp.rank = 0;
   smp.memo_nu = -1.0;
+  smp.have_mom = false;
   smp.scratch = scratch;
   smp.parity = 0;
   for (int s = threadIdx.x; s < smp.m; s += NT) dsm[s] = r[(long long)s * stride];
