@@ -237,8 +237,13 @@ __device__ __forceinline__ void warp_px_iw(const WarpMats& m, const double2* __r
                 t11 = __ldg(IWB + i00 + dy + dx);
   const double a00 = t00.x, a10 = t10.x, a01 = t01.x, a11 = t11.x;
   const double b00 = t00.y, b10 = t10.y, b01 = t01.y, b11 = t11.y;
-  const double ri = bilin_fix(gy * (gx * a00 + fx * a10) + fy * (gx * a01 + fx * a11), a00, a10, a01, a11);
-  const double w_meas = bilin_fix(gy * (gx * b00 + fx * b10) + fy * (gx * b01 + fx * b11), b00, b10, b01, b11);
+  // the formula alone: it is non-finite exactly when the reference's result is a
+  // hole (an invalid tap) or has overflowed, and K1's consumers (the validity tests,
+  // the NaN-skipping downsample, K2's sample of valid residuals, K3's zeroed rows)
+  // treat both alike -- only the payload of an invalid value differs (bilin_fix
+  // keeps the reference's for the C-ABI warp maps)
+  const double ri = gy * (gx * a00 + fx * a10) + fy * (gx * a01 + fx * a11);
+  const double w_meas = gy * (gx * b00 + fx * b10) + fy * (gx * b01 + fx * b11);
   oI = inb ? ri : CUDART_NAN;
   const bool v2 = inb && valid(w_meas) && w_meas > 0.0;
   const double rz = red3(m.Rt_AB[6] * px, m.Rt_AB[7] * py, m.Rt_AB[8] * 1.0);
