@@ -247,7 +247,8 @@ __device__ __forceinline__ void warp_px_iw(const WarpMats& m, const double2* __r
   oI = inb ? ri : CUDART_NAN;
   const bool v2 = inb && valid(w_meas) && w_meas > 0.0;
   const double rz = red3(m.Rt_AB[6] * px, m.Rt_AB[7] * py, m.Rt_AB[8] * 1.0);
-  const double za = div_safe(rz, v2 ? w_meas : 1.0) + m.tt_AB[2];
+  const double za = rz / (v2 ? w_meas : 1.0) + m.tt_AB[2];  // IEEE division (the library's
+                                                             // sequence beats div_safe here)
   const bool v3 = v2 && za > 1e-12;
   oW = v3 ? __drcp_rn(za) : CUDART_NAN;  // == 1.0 / za
 }
