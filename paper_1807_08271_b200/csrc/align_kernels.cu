@@ -321,8 +321,9 @@ __host__ __device__ constexpr int k1_threads() { return k1_cw<L>() * k1_ng<L>();
 
 template <int L, bool LIST>
 #ifndef RGBID_K1_THREADS_PER_SM
-#define RGBID_K1_THREADS_PER_SM 1536  // 40 registers: occupancy over L1-cached spills (-16% vs 64
-                                      // registers; 1536 best with the interleaved {I, W} taps)
+#define RGBID_K1_THREADS_PER_SM 2048  // 32 registers, a full SM of threads: -4..7% per launch vs
+                                      // 1536 (40 registers) since the warp lost its tap fix-up;
+                                      // 1024 (64 registers) +8%
 #endif
 __global__ void __launch_bounds__(k1_threads<L>(), RGBID_K1_THREADS_PER_SM / k1_threads<L>()) k_warp_residuals(const SlotIO* __restrict__ io,
                                                            const SlotState* __restrict__ st,
