@@ -2109,7 +2109,11 @@ __constant__ double c_exp2_32[32] = {
 __device__ __forceinline__ double exp2_32_lane() { return c_exp2_32[threadIdx.x & 31]; }
 
 __device__ __forceinline__ double exp_le0(double x, double tlane) {
-  x = fmax(x, -746.0);                                 // maxNum: NaN -> -746
+  // arguments below -708 (and NaN: an invalid tap) give exp(-708) ~ 3e-308 instead
+  // of the tiny or zero true value: a weight that small is absorbed by any sum that
+  // holds the centre tap's weight 1 (and multiplies a 0 value for an invalid tap),
+  // and 2^m is then one normal power of two
+  x = x > -708.0 ? x : -708.0;
   const double kMagic = 6755399441055744.0;            // 1.5 * 2^52: round to integer
   const double kd = fma(x, 46.16624130844683, kMagic);  // x * 32 / ln2
   const int n = __double2loint(kd);
@@ -2123,10 +2127,8 @@ __device__ __forceinline__ double exp_le0(double x, double tlane) {
   pl = fma(r, pl, 1.0);
   const double em1 = r * pl;  // e^r - 1
   const double t = __shfl_sync(0xffffffffu, tlane, n & 31);
-  const int m = n >> 5, m1 = m >> 1, m2 = m - m1;  // 2^m = 2^m2 * 2^m1, both normal
-  const double s1 = __longlong_as_double((long long)(m1 + 1023) << 52);
-  const double s2 = __longlong_as_double((long long)(m2 + 1023) << 52);
-  return fma(t, em1, t) * s2 * s1;
+  const double sc = __longlong_as_double((long long)((n >> 5) + 1023) << 52);  // 2^m, m >= -1022
+  return fma(t, em1, t) * sc;
 }
 
 // bilateral_filter — src/alignment.cpp:252-277, tiled.  The tap weight
