@@ -378,10 +378,10 @@ def algorithmic_bytes(results):
 # ncu-measured per full-res pixel constants of the warp_residuals family
 # (profiles/r01_k1_ncu_v14.txt): fp64 flop = dadd + dmul + 2 dfma per pixel warped
 # (level 0 / covariance pass: 112; levels >= 1 add the in-tile downsample: ~122-124),
-# and DRAM bytes per slot-iteration at level 0 (read + write of one 128-slot launch,
-# profiles/r02_ncu_full_l0_kernels.txt).
+# and DRAM bytes per slot-iteration at level 0 (read + write of one 64-slot launch,
+# profiles/r02_ncu_full_final.txt).
 K1_FLOP_PER_PX = {0: 112.0, 1: 121.4, 2: 123.8, 3: 124.5}
-K1_TRAFFIC_L0 = (1.297798e9 + 0.621426e9) / 128
+K1_TRAFFIC_L0 = (0.646615e9 + 0.295246e9) / 64
 FP64_STEP_PROFILE = os.path.join(ROOT, "profiles", "r02_fp64_flops.json")
 
 
@@ -662,7 +662,7 @@ def main():
         # ncu dram read+write per slot-iteration of the level-0 launch vs SURVEY 8(d)'s
         # algorithmic B_it(0) = 5M: no wasted re-reads
         "traffic": K1_TRAFFIC_L0, "traffic_algorithmic": 5 * M_BYTES,
-        "traffic_unit": "bytes per slot-iteration at level 0 (profiles/r02_ncu_full_l0_kernels.txt)",
+        "traffic_unit": "bytes per slot-iteration at level 0 (profiles/r02_ncu_full_final.txt)",
         "frac": ((warp_bytes / (warp_ms / 1e3)) / 1e9) / peak if warp_ms else None,
         "kernel_share_of_step": warp_ms / prof_total if prof_total else None,
         "dominant_kernel": dom[0], "dominant_share": dom[1] / prof_total if prof_total else None,
