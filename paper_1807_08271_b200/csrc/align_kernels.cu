@@ -2112,7 +2112,7 @@ __device__ __forceinline__ double exp_le0(double x, double tlane) {
   // arguments below -708 (and NaN: an invalid tap) give exp(-708) ~ 3e-308 instead
   // of the tiny or zero true value: a weight that small is absorbed by any sum that
   // holds the centre tap's weight 1 (and multiplies a 0 value for an invalid tap),
-  // and 2^m is then one normal power of two
+  // and t 2^m below is then a normal double
   x = x > -708.0 ? x : -708.0;
   const double kMagic = 6755399441055744.0;            // 1.5 * 2^52: round to integer
   const double kd = fma(x, 46.16624130844683, kMagic);  // x * 32 / ln2
@@ -2127,8 +2127,10 @@ __device__ __forceinline__ double exp_le0(double x, double tlane) {
   pl = fma(r, pl, 1.0);
   const double em1 = r * pl;  // e^r - 1
   const double t = __shfl_sync(0xffffffffu, tlane, n & 31);
-  const double sc = __longlong_as_double((long long)((n >> 5) + 1023) << 52);  // 2^m, m >= -1022
-  return fma(t, em1, t) * sc;
+  // t 2^m (m = n >> 5 >= -1022, t in [1, 2): a normal double) by adding m to t's
+  // exponent field -- no scale multiply
+  const double ts = __hiloint2double(__double2hiint(t) + ((n >> 5) << 20), __double2loint(t));
+  return fma(ts, em1, ts);
 }
 
 // bilateral_filter — src/alignment.cpp:252-277, tiled.  The tap weight
