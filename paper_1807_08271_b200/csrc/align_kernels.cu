@@ -532,7 +532,11 @@ __global__ void __launch_bounds__(128 * kK1L0Rows, RGBID_K1L0_MINB / kK1L0Rows)
 // Tiled: a 32 x 8 pixel tile per CTA with its 1-pixel halo of I_A and W_A staged
 // in shared memory (coalesced row loads, NaN outside the image = the reference's
 // out-of-bounds hole), so every 3 x 3 stencil read is a shared load.
-constexpr int kPTW = 32, kPTH = 8, kPRW = kPTW + 2, kPRH = kPTH + 2;
+#ifndef RGBID_PREP_ROWS
+#define RGBID_PREP_ROWS 4  // tile rows per thread (32 x 8 threads)
+#endif
+constexpr int kPTT = 8;                                   // thread rows
+constexpr int kPTW = 32, kPTH = kPTT * RGBID_PREP_ROWS, kPRW = kPTW + 2, kPRH = kPTH + 2;
 
 // gradient_at on the staged tile (same tests and expressions)
 __device__ __forceinline__ bool grad_sm(const double* t, int i, double& gx, double& gy) {
@@ -559,7 +563,7 @@ __device__ __forceinline__ bool grad_sm(const double* t, int i, double& gx, doub
   return true;
 }
 
-__global__ void __launch_bounds__(kPTW * kPTH) k_prep_A(const SlotIO* __restrict__ io,
+__global__ void __launch_bounds__(kPTW * kPTT) k_prep_A(const SlotIO* __restrict__ io,
                                                          const SlotState* __restrict__ st,
                                                          int level, int w, int h, int phase) {
   const int slot = blockIdx.z;
@@ -569,28 +573,38 @@ __global__ void __launch_bounds__(kPTW * kPTH) k_prep_A(const SlotIO* __restrict
   const double* WA = phase ? o.fWA : o.WA[level];
   __shared__ double tI[kPRW * kPRH], tW[kPRW * kPRH];
   const int x0 = blockIdx.x * kPTW, y0 = blockIdx.y * kPTH, t = threadIdx.x;
-  for (int i = t; i < kPRW * kPRH; i += kPTW * kPTH) {
-    const int ry = i / kPRW, rx = i - ry * kPRW;
-    const int gx = x0 - 1 + rx, gy = y0 - 1 + ry;
-    const bool in = gx >= 0 && gx < w && gy >= 0 && gy < h;
-    const size_t k = (size_t)gy * w + gx;
-    tI[i] = in ? __ldg(IA + k) : CUDART_NAN;
-    tW[i] = in ? __ldg(WA + k) : CUDART_NAN;
+  constexpr int NT = kPTW * kPTT;
+  constexpr int kLoads = (kPRW * kPRH + NT - 1) / NT;
+#pragma unroll
+  for (int j = 0; j < kLoads; ++j) {  // the halo'd tile, all loads of a thread in flight
+    const int i = t + j * NT;
+    if (i < kPRW * kPRH) {
+      const int ry = i / kPRW, rx = i - ry * kPRW;
+      const int gx = x0 - 1 + rx, gy = y0 - 1 + ry;
+      const bool in = gx >= 0 && gx < w && gy >= 0 && gy < h;
+      const size_t k = (size_t)gy * w + gx;
+      tI[i] = in ? __ldg(IA + k) : CUDART_NAN;
+      tW[i] = in ? __ldg(WA + k) : CUDART_NAN;
+    }
   }
   __syncthreads();
-  const int tx = t % kPTW, ty = t / kPTW, x = x0 + tx, y = y0 + ty;
-  if (x >= w || y >= h) return;
-  const int i = (ty + 1) * kPRW + tx + 1;
-  const size_t k = (size_t)y * w + x;
-  const double w_a = tW[i], i_a = tI[i];
-  double g[4] = {0.0, 0.0, 0.0, 0.0};
-  unsigned m = 0;
-  if (valid(w_a) && w_a > 0.0 && valid(i_a) && grad_sm(tI, i, g[0], g[1])) m |= 1u;
-  if (grad_sm(tW, i, g[2], g[3])) m |= 2u;
-  o.amask[level][k] = (uint8_t)m;
-  double2* gp = reinterpret_cast<double2*>(o.agrad[level] + 4 * k);
-  gp[0] = make_double2(g[0], g[1]);
-  gp[1] = make_double2(g[2], g[3]);
+  const int tx = t % kPTW, x = x0 + tx;
+#pragma unroll
+  for (int rr = 0; rr < RGBID_PREP_ROWS; ++rr) {
+    const int ty = t / kPTW + rr * kPTT, y = y0 + ty;
+    if (x >= w || y >= h) continue;
+    const int i = (ty + 1) * kPRW + tx + 1;
+    const size_t k = (size_t)y * w + x;
+    const double w_a = tW[i], i_a = tI[i];
+    double g[4] = {0.0, 0.0, 0.0, 0.0};
+    unsigned m = 0;
+    if (valid(w_a) && w_a > 0.0 && valid(i_a) && grad_sm(tI, i, g[0], g[1])) m |= 1u;
+    if (grad_sm(tW, i, g[2], g[3])) m |= 2u;
+    o.amask[level][k] = (uint8_t)m;
+    double2* gp = reinterpret_cast<double2*>(o.agrad[level] + 4 * k);
+    gp[0] = make_double2(g[0], g[1]);
+    gp[1] = make_double2(g[2], g[3]);
+  }
 }
 
 // frame B interleaved {I, W} for K1's taps, once per align
@@ -613,7 +627,7 @@ void launch_amask(const AlignLaunch& a, int levels, int phase, cudaStream_t s) {
   for (int l = 0; l < levels; ++l) {
     const int w = a.w0 >> l, h = a.h0 >> l;
     KScope ks_("prep_A", s);
-    k_prep_A<<<dim3((w + kPTW - 1) / kPTW, (h + kPTH - 1) / kPTH, a.nslots), kPTW * kPTH, 0, s>>>(
+    k_prep_A<<<dim3((w + kPTW - 1) / kPTW, (h + kPTH - 1) / kPTH, a.nslots), kPTW * kPTT, 0, s>>>(
         a.io, a.st, l, w, h, phase);
   }
 }
