@@ -613,14 +613,22 @@ __global__ void k_interleave_B(const SlotIO* __restrict__ io, const SlotState* _
   const int slot = blockIdx.y;
   if (st[slot].status != RGBID_OK) return;
   const SlotIO& o = io[slot];
-  const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k < n) o.IWB[k] = make_double2(__ldg(o.IB + k), __ldg(o.WB + k));
+  // two pixels per thread: 16-byte loads of I_B and W_B where the pair is aligned
+  const int k = 2 * (blockIdx.x * blockDim.x + threadIdx.x);
+  if (k + 1 < n && ((reinterpret_cast<size_t>(o.IB) | reinterpret_cast<size_t>(o.WB)) & 15) == 0) {
+    const double2 i2 = __ldg(reinterpret_cast<const double2*>(o.IB + k));
+    const double2 w2 = __ldg(reinterpret_cast<const double2*>(o.WB + k));
+    o.IWB[k] = make_double2(i2.x, w2.x);
+    o.IWB[k + 1] = make_double2(i2.y, w2.y);
+  } else {
+    for (int j = k; j < min(k + 2, n); ++j) o.IWB[j] = make_double2(__ldg(o.IB + j), __ldg(o.WB + j));
+  }
 }
 
 void launch_interleave_B(const AlignLaunch& a, cudaStream_t s) {
   KScope ks_("interleave_B", s);
   const int n = a.w0 * a.h0;
-  k_interleave_B<<<dim3((n + 255) / 256, a.nslots), 256, 0, s>>>(a.io, a.st, n);
+  k_interleave_B<<<dim3((n + 511) / 512, a.nslots), 256, 0, s>>>(a.io, a.st, n);
 }
 
 void launch_amask(const AlignLaunch& a, int levels, int phase, cudaStream_t s) {
