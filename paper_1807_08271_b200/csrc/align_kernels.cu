@@ -210,7 +210,7 @@ __device__ __forceinline__ void warp_px(const WarpMats& m, const double* __restr
 // loads instead of eight 8-byte loads (-11% per level-0 launch).  Written branch-free (predicates + clamped, always-issued tap loads) so that
 // several pixels unrolled in one thread overlap their gathers.
 __device__ __forceinline__ void warp_px_iw(const WarpMats& m, const double2* __restrict__ IWB,
-                                           int wb, int hb, int x,
+                                           int wb, int hb, double bx1, double by1, int x,
                                         int y, double w_a, double& oI, double& oW, double& mx,
                                         double& my) {
   const bool v0 = valid(w_a) && w_a > 0.0;
@@ -226,7 +226,9 @@ __device__ __forceinline__ void warp_px_iw(const WarpMats& m, const double2* __r
   const double px = div_rcp(xb0, z, rz2), py = div_rcp(xb1, z, rz2);
   mx = v1 ? px : CUDART_NAN;
   my = v1 ? py : CUDART_NAN;
-  const bool inb = v1 && (px >= 0.0 && px <= wb - 1.0 && py >= 0.0 && py <= hb - 1.0);
+  // the bounds test as one predicate expression (no short-circuit branch) against
+  // w - 1 and h - 1 as kernel-parameter doubles (constant-bank operands)
+  const bool inb = v1 & (px >= 0.0) & (px <= bx1) & (py >= 0.0) & (py <= by1);
   const double sx = inb ? px : 0.0, sy = inb ? py : 0.0;
   const int x0 = (int)floor(sx), y0 = (int)floor(sy);
   const int dx = x0 + 1 < wb ? 1 : 0;  // x1 = min(x0 + 1, w - 1)
@@ -376,7 +378,7 @@ __global__ void __launch_bounds__(k1_threads<L>(), RGBID_K1_THREADS_PER_SM / k1_
       for (int q = 0; q < 4; ++q) {
         const int xx = x + (q & 1), yy = y + (q >> 1);
         const double w_a = kHoist ? wa0[q] : __ldg(WAw + yy * w0 + xx);
-        warp_px_iw(wm, o.IWB, w0, h0, xx, yy, w_a, vi[q], vw[q], d0, d1);
+        warp_px_iw(wm, o.IWB, w0, h0, li.bx1, li.by1, xx, yy, w_a, vi[q], vw[q], d0, d1);
       }
       sI[r * cw + col] = ds4(vi[0], vi[1], vi[2], vi[3]);
       sW[r * cw + col] = ds4(vw[0], vw[1], vw[2], vw[3]);
@@ -493,7 +495,7 @@ __global__ void __launch_bounds__(128 * kK1L0Rows, RGBID_K1L0_MINB / kK1L0Rows)
       const unsigned a = amv[q];
       const double ia = iav[q];
       double ib, wb, d0, d1;
-      warp_px_iw(wm, o.IWB, w0, h0, xl0 + lx, yl, wa[q], ib, wb, d0, d1);
+      warp_px_iw(wm, o.IWB, w0, h0, li.bx1, li.by1, xl0 + lx, yl, wa[q], ib, wb, d0, d1);
       o.ibw[idx] = make_double2(ib - ia, wb);  // r_I (src/alignment.cpp:222), w_b: K2, K3
       jet[q] = (a & 1u) && valid(ib);
       dep[q] = jet[q] && (a & 2u) && valid(wb) && wb > 0.0;

@@ -55,6 +55,7 @@ struct LevelInfo {
   int pix3;          // K3 pixels per thread (kPixK3, or 1 in latency mode)
   double fx, fy, cx, cy;
   double Kinv[9];    // level K^-1 (host m3_inv, bit-identical to the oracle)
+  double bx1, by1;   // full-res frame B bounds w0 - 1, h0 - 1 (K1's bilinear test)
 };
 
 constexpr int kWordsPerTile = 8;  // K1 tile <= 256 level pixels -> 8 ballot words per type

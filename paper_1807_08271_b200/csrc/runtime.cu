@@ -234,6 +234,8 @@ LevelInfo make_level(const rgbid_intrinsics& K0, int w0, int h0, int level) {
   li.ntiles = li.nseg * li.h;
   li.ntiles3 = k3_tiles(li.w, li.h);
   li.pix3 = kPixK3;
+  li.bx1 = w0 - 1.0;
+  li.by1 = h0 - 1.0;
   rgbid_intrinsics k;
   level_intrinsics(K0, level, &k);
   li.fx = k.fx;
