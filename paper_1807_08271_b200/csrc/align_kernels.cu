@@ -321,6 +321,19 @@ __host__ __device__ constexpr int k1_ng() {
 template <int L>
 __host__ __device__ constexpr int k1_threads() { return k1_cw<L>() * k1_ng<L>(); }
 
+// downsample2 applied K times to the 2^K x 2^K block of level-1 values at (r, c) of
+// the staged tile (pitch cw), taps (0,0),(1,0),(0,1),(1,1) at every stage
+template <int K>
+__device__ __forceinline__ double ds_tree(const double* t, int cw, int r, int c) {
+  if constexpr (K == 0) {
+    return t[r * cw + c];
+  } else {
+    constexpr int hk = 1 << (K - 1);
+    return ds4(ds_tree<K - 1>(t, cw, r, c), ds_tree<K - 1>(t, cw, r, c + hk),
+               ds_tree<K - 1>(t, cw, r + hk, c), ds_tree<K - 1>(t, cw, r + hk, c + hk));
+  }
+}
+
 template <int L, bool LIST>
 #ifndef RGBID_K1_THREADS_PER_SM
 #define RGBID_K1_THREADS_PER_SM 2048  // 32 registers, a full SM of threads: -4..7% per launch vs
@@ -356,7 +369,7 @@ __global__ void __launch_bounds__(k1_threads<L>(), RGBID_K1_THREADS_PER_SM / k1_
   // order (0,0),(1,0),(0,1),(1,1) (inc/image.hpp:77-85).
   __shared__ double sI[512], sW[512];
   constexpr int CW = k1_cw<L>(), NG = k1_ng<L>();  // thread columns x row groups
-  int cw = nx << (L - 1), ch = 1 << (L - 1);
+  const int cw = nx << (L - 1);
   const int col = tid % CW, grp = tid / CW;
   const int x = (xl0 << L) + 2 * col;
   // one quad per thread (levels 1-2): its W_A values in flight while the warp
@@ -385,40 +398,19 @@ __global__ void __launch_bounds__(k1_threads<L>(), RGBID_K1_THREADS_PER_SM / k1_
     }
   }
   __syncthreads();
-  // remaining downsample stages in shared memory (level 1 -> L)
-#pragma unroll
-  for (int s = 1; s < L; ++s) {
-    const int ow = cw >> 1;
-    constexpr int kMaxOh = (L >= 2) ? (1 << (L - 2)) : 1;
-    const int oh = ch >> 1;
-    double oi[kMaxOh], owv[kMaxOh];
-    if (tid < ow) {
-#pragma unroll
-      for (int r = 0; r < kMaxOh; ++r)
-        if (r < oh) {
-          const int i0 = (2 * r) * cw + 2 * tid, i1 = i0 + cw;
-          oi[r] = ds4(sI[i0], sI[i0 + 1], sI[i1], sI[i1 + 1]);
-          owv[r] = ds4(sW[i0], sW[i0 + 1], sW[i1], sW[i1 + 1]);
-        }
-    }
-    __syncthreads();
-    if (tid < ow) {
-#pragma unroll
-      for (int r = 0; r < kMaxOh; ++r)
-        if (r < oh) {
-          sI[r * ow + tid] = oi[r];
-          sW[r * ow + tid] = owv[r];
-        }
-    }
-    __syncthreads();
-    cw = ow;
-    ch = oh;
+  // remaining downsample stages (level 1 -> L) by the level-L pixel's own thread, in
+  // registers from the staged level-1 values, in the reference's tap order at every
+  // stage: no further block barrier
+  double vI = 0.0, vW = 0.0;
+  if (tid < nx) {
+    vI = ds_tree<L - 1>(sI, cw, 0, tid << (L - 1));
+    vW = ds_tree<L - 1>(sW, cw, 0, tid << (L - 1));
   }
 
   bool jet = false, dep = false;
   if (tid < nx) {
     const int idx = yl * li.w + xl0 + tid;
-    const double ib = sI[tid], wb = sW[tid];
+    const double ib = vI, wb = vW;
     o.ibw[idx] = make_double2(ib - __ldg(IAl + idx), wb);  // r_I (src/alignment.cpp:222), w_b
     const unsigned a = __ldg(am + idx);
     jet = (a & 1u) && valid(ib);
