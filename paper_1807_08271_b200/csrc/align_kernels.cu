@@ -926,9 +926,10 @@ struct LogProd {
 // (the FP64 MUFU reciprocal issues at a quarter of the DFMA rate; 8 per fraction
 // measured 1.5% slower in the batch kernel, 10% in latency mode), all terms
 // positive except r v's numerators.  D also feeds the running log-product, so
-// sum(log q) costs one log per thread.  A thread with any D outside
-// [1e-250, 1e250] (only for |v - mu| > 1e30 or c1 < 1e-31) redoes its share
-// with exact per-sample division and logs.
+// sum(log q) costs one log per thread.  A thread whose sums show an out-of-range
+// fraction (a non-finite or zero sum of positive terms, or a non-normal log
+// product: only for |v - mu| beyond ~1e38 or q below ~1e-77) redoes its share with
+// exact per-sample division and logs.
 #ifndef RGBID_QBODY
 #define RGBID_QBODY 4
 #endif
@@ -978,9 +979,6 @@ __device__ __forceinline__ void q_body(const Sample& S, const double* v, int k, 
   }
   double D, NR, NV;
   frac_tree<BW, WV>(q, x, D, NR, NV);
-  // D within ~[1.4e-250, 5.5e250] on the exponent bits (integer pipe, biased exponents
-  // 193..1853); NaN, inf, zero and negative D all fall outside
-  bad |= ((unsigned)__double2hiint(D) >> 20) - 193u > 1660u;
   const double inv = rcp_fast(D);
   sr = fma(NR, inv, sr);
   if (WV) sv = fma(NV, inv, sv);
@@ -1009,6 +1007,10 @@ __device__ __forceinline__ void q_sums(const Sample& S, double mu, double c1, do
     for (int u = 0; u < BW; ++u) npad += (k + u) * NT + (int)threadIdx.x < S.m_local ? 0 : 1;
     sr -= (double)npad;
   }
+  // out-of-range fractions show in the thread's sums: an overflowing or vanishing D
+  // (|v - mu| beyond ~1e38 or q below ~1e-77) leaves a non-finite or zero sum of
+  // strictly positive terms; anything less extreme stays within rounding
+  bad |= !(sr > 0.0 && sr < 1.0e300) || (WV && !isfinite(sv));
   if (bad) {  // exact per-sample division for this thread's share
     sr = sv = 0.0;
     for (int kk = 0; kk * NT < S.m_local; ++kk)

@@ -568,15 +568,17 @@ def test_inverse_warp_bitwise(ctx):
     assert bitwise_equal(rg.inverse_warp(src, f_sca, 22, 15, ctx), ref)
 
 
-@pytest.mark.parametrize("case", ["tight_core", "tiny_scale", "two_clusters", "heavy_tail_low_nu"])
+@pytest.mark.parametrize("case", ["tight_core", "tiny_scale", "two_clusters", "heavy_tail_low_nu",
+                                  "huge_scale"])
 def test_student_t_stress_samples(ctx, orc, case):
     """The device location/scale update uses sum w d^2 = c2 (m - c1 sum 1/q), which
     cancels when most d^2 << c1 = nu sigma^2: samples whose bulk
     is far tighter than the scale the outliers impose, a scale near the 1e-8 floor,
-    two separated clusters, and a t(1.2) tail that drives nu into the bisection.
+    two separated clusters, a t(1.2) tail that drives nu into the bisection, and
+    residuals of ~1e40 whose 4-sample fractions overflow (the exact per-sample path).
     GPU vs the oracle (the reference's sequential sums) at the 1e-6 bar."""
     rng = np.random.default_rng({"tight_core": 11, "tiny_scale": 12, "two_clusters": 13,
-                                 "heavy_tail_low_nu": 14}[case])
+                                 "heavy_tail_low_nu": 14, "huge_scale": 15}[case])
     n = 19200
     if case == "tight_core":
         r = np.where(rng.random(n) < 0.97, rng.normal(0.01, 1e-6, n), rng.normal(0.0, 1.0, n))
@@ -584,6 +586,8 @@ def test_student_t_stress_samples(ctx, orc, case):
         r = 0.5 + rng.normal(0.0, 3e-8, n)
     elif case == "two_clusters":
         r = np.where(rng.random(n) < 0.7, rng.normal(-0.2, 1e-4, n), rng.normal(0.3, 1e-4, n))
+    elif case == "huge_scale":  # q ~ 1e80: a 4-sample fraction's D overflows -> exact path
+        r = 1e40 * rng.standard_t(3.0, size=n)
     else:
         r = 0.02 * rng.standard_t(1.2, size=n)
     for nu in (5.0, 2.5, 10.0):
